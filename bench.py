@@ -1,0 +1,334 @@
+"""Headline benchmark: MLFFT Toeplitz matvec/s and GMRES solve time at
+30x30, N_b = 128, complex128 (BASELINE.json configs[1]), with the HBM
+roofline fraction of the dominant kernel.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one MLFFT matvec (pad -> 2-D DFT -> per-bin 128x128 product ->
+inverse DFT -> crop) of one dense seeded vector against the resident
+spectral operator.  The spectral blocks (944 MB) exceed the 126 MB L2, so
+every step streams them from HBM (no L2 flush needed).  N > 1 runs one
+independent replica per GPU (the single-RHS path does not shard; DESIGN.md
+"replicas only"); value = total matvecs over all ranks / max-over-ranks time.
+
+``--impl reference`` times the reference algorithm's CPU implementation on
+the host cores: the numpy restatement in ``oracle/`` (the reference itself
+is pure Python and is not installed on the GPU box), on the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+NY = NX = 30
+NB = 128
+DIM = NY * NX * NB
+METRIC = "MLFFT Toeplitz matvec/s & GMRES solve time, 30x30, N_b=128; % HBM roofline"
+UNIT = "matvec/s"
+
+
+def algorithmic_bytes(bins: int, nb: int = NB, dim: int = DIM, s: int = 16) -> dict:
+    """Per-matvec algorithmic HBM bytes: D read once + u in + v out."""
+    return {"matvec": bins * nb * nb * s + 2 * dim * s,
+            "kernel": bins * nb * nb * s + 2 * bins * nb * s,   # per-bin product: D + u_hat + v_hat
+            "matvec_min_embedding": (2 * NY - 1) * (2 * NX - 1) * nb * nb * s + 2 * dim * s}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the GPU is busy."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, val in zip(names, r[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def measured_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cpu_baseline(max_seconds: float = 20.0) -> dict:
+    """Oracle (numpy restatement of the reference, pocketfft + OpenBLAS) on the host cores."""
+    import oracle
+    from paper_2506_20350_b200.problems import dense_rhs, seeded_stacked4
+
+    cores = os.cpu_count() or 1
+    s4 = seeded_stacked4(NY, NX, NB, seed=0)
+    d = oracle.precompute_spectral(s4)
+    del s4
+    dims = (NY, NX, NB, 2 * NY - 1, 2 * NX - 1)
+    u = dense_rhs(DIM, seed=1)[:, None]
+    oracle.matvec(d, dims, u)  # warm-up (FFT plans, pools)
+    times = []
+    t_end = time.perf_counter() + max_seconds
+    while time.perf_counter() < t_end and len(times) < 200:
+        t0 = time.perf_counter()
+        oracle.matvec(d, dims, u)
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    return {"value": 1.0 / best, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{len(times)} cfg2 matvecs (best-of, after warm-up) of oracle/mlfft.py "
+                      f"(numpy pocketfft + OpenBLAS, {cores} threads), precompute excluded",
+            "mean_s": float(np.mean(times))}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    from paper_2506_20350_b200.problems import dense_rhs, seeded_stacked4
+
+    s4 = seeded_stacked4(NY, NX, NB, seed=0)
+    d = oracle.precompute_spectral(s4)
+    del s4
+    dims = (NY, NX, NB, 2 * NY - 1, 2 * NX - 1)
+    u = dense_rhs(DIM, seed=1)[:, None]
+    for _ in range(args.warmup):
+        oracle.matvec(d, dims, u)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.matvec(d, dims, u)
+    dt = time.perf_counter() - t0
+    value = args.steps / dt
+    cores = os.cpu_count() or 1
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (BASELINE seeded generator)",
+            "config": {"workload": "cfg2: 30x30 array, N_b=128, single RHS, (2N-1)^2 embedding (reference)",
+                       "n_bins": (2 * NY - 1) * (2 * NX - 1), "dim": DIM},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{args.steps} timed matvecs of oracle/mlfft.py on {cores} host threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_20350_b200.problems import dense_rhs, seeded_stacked4, system_from_generator, unit_feed_rhs
+    from paper_2506_20350_b200.solvers import BorderedOperator, GmresConfig, build_pk, solve_multi_rhs_vectorized
+    from paper_2506_20350_b200.toeplitz import generator_from_stacked, matvec
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    s4 = seeded_stacked4(NY, NX, NB, seed=0)
+    sys_ = system_from_generator(generator_from_stacked(s4))
+    t0 = time.perf_counter()
+    op = BorderedOperator.from_system(sys_)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    spec = op.spectral
+    del s4
+    u = torch.from_numpy(dense_rhs(DIM, seed=1)[:, None]).to(dev)
+    v = torch.empty_like(u)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+
+    # ---- device-resident matvecs (value)
+    for _ in range(args.warmup):
+        v = matvec(spec, u)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        v = matvec(spec, u)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    t_dev = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+    ms_max = float(t_dev.item())
+    value = world * args.steps / (ms_max * 1e-3)
+
+    # ---- dominant kernel alone (per-bin product), CUDA events on its stream
+    hat_in = torch.randn((spec.bins, NB, 1), dtype=torch.complex128, device=dev)
+    hat_out = torch.empty_like(hat_in)
+    for _ in range(3):
+        spec.spectral_apply(hat_in, hat_out)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nk = max(args.steps, 20)
+    k0.record(stream)
+    for _ in range(nk):
+        spec.spectral_apply(hat_in, hat_out)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    k_ms = k0.elapsed_time(k1) / nk
+
+    # ---- end to end through the public API, pinned host buffers
+    u_host = torch.from_numpy(dense_rhs(DIM, seed=1)[:, None]).pin_memory()
+    for _ in range(max(2, args.warmup // 2)):
+        matvec(spec, u_host)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record(stream)
+    n_e2e = args.steps
+    for _ in range(n_e2e):
+        out_host = matvec(spec, u_host)
+    x1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = x0.elapsed_time(x1)
+    t_e2e = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    e2e_value = world * n_e2e / (float(t_e2e.item()) * 1e-3)
+
+    # ---- GMRES(50) to 1e-8, none and PK (BASELINE cfg2)
+    gm = {}
+    b = unit_feed_rhs(NY, NX, NB)[:, None]
+    bt = torch.from_numpy(b).to(dev)
+    pk = build_pk(sys_)
+    for tag, p in (("none", None), ("pk", pk)):
+        solve_multi_rhs_vectorized(op, p, bt, GmresConfig(tol=1e-8, restart=50))  # warm (fold, workspace)
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        x, rep = solve_multi_rhs_vectorized(op, p, bt, GmresConfig(tol=1e-8, restart=50))
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gm[tag] = {"iterations": rep.iterations, "solve_ms": g0.elapsed_time(g1),
+                   "final_residual": rep.final_residual, "reference_iterations": 31 if tag == "none" else 30}
+    clocks = sampler.stop()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = measured_peaks()
+    by = algorithmic_bytes(spec.bins)
+    achieved_k = by["kernel"] / (k_ms * 1e-3) / 1e9
+    achieved_mv = by["matvec"] * (args.steps / (ms * 1e-3)) / 1e9
+    traffic = None
+    prof = os.path.join(REPO, "profiles", "binprod_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (BASELINE seeded generator, seed 0; dense default_rng(1) vector)",
+        "config": {"workload": "cfg2: 30x30 array, N_b=128, single RHS, 60x60 circulant (3600 bins)",
+                   "parallelism": f"replicas x{world}", "l2_policy": "inputs larger than L2 (944 MB spectral blocks)",
+                   "matvec_hbm_frac": achieved_mv / peak, "matvec_GBps": achieved_mv,
+                   "algorithmic_bytes_per_matvec": by["matvec"],
+                   "algorithmic_bytes_min_embedding": by["matvec_min_embedding"],
+                   "setup_s": t_setup,
+                   "gmres": gm},
+        "roofline": {"bound": "hbm", "achieved": achieved_k, "peak": peak, "unit": "GB/s", "frac": achieved_k / peak,
+                     "traffic": traffic, "kernel": "binprod_cm_kernel (per-bin D_k u_k)", "kernel_ms": k_ms,
+                     "bytes_per_launch": by["kernel"], "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": DIM * 16, "d2h_bytes_per_step": DIM * 16,
+                "path": "toeplitz.matvec(op, pinned CPU tensor) -> pinned CPU tensor"},
+        "gpu_launches": 5 * args.steps,
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

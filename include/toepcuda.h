@@ -1,0 +1,173 @@
+/*
+ * libtoepcuda — C ABI of the B200-native MLFFT block-Toeplitz hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no torch types.
+ * Each entry point replaces one function of the reference Python API
+ * (toepsolve, /root/reference/pkg/src/toepsolve); the replaced function is
+ * cited (file:line) above each declaration.  The Python host mirror
+ * (paper_2506_20350_b200/) binds these with ctypes.
+ *
+ * Conventions
+ *   - complex128 = interleaved {double re, im}; complex64 = {float re, im}.
+ *   - A "stacked vector" / column block is (n, w) row-major, n = n2*n1*n0,
+ *     row index (i2*n1 + i1)*n0 + b, exactly the reference layout
+ *     (toeplitz.py:256-269).
+ *   - All device pointers belong to the current CUDA device; `stream` is a
+ *     cudaStream_t (NULL = legacy default stream).  Calls are asynchronous
+ *     on `stream` unless stated otherwise.
+ *   - Every function returns a status code; toep_last_error() gives the
+ *     thread-local message of the last failure.
+ */
+#ifndef TOEPCUDA_H
+#define TOEPCUDA_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TOEP_API __attribute__((visibility("default")))
+#else
+#define TOEP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes -> Python exceptions (paper_2506_20350_b200/_lib.py). */
+#define TOEP_OK 0
+#define TOEP_ERR_SHAPE 1          /* errors.ShapeError            (errors.py:8)  */
+#define TOEP_ERR_ARG 2            /* ValueError                                  */
+#define TOEP_ERR_SINGULAR 3       /* errors.SingularMatrix        (errors.py:24) */
+#define TOEP_ERR_SINGULAR_BLOCK 4 /* errors.SingularBlock         (errors.py:28) */
+#define TOEP_ERR_SINGULAR_DENOM 5 /* errors.SingularDenominator   (errors.py:32) */
+#define TOEP_ERR_NOCONV 6         /* errors.NoConvergence         (errors.py:76) */
+#define TOEP_ERR_CUDA 7           /* errors.CudaError (RuntimeError)             */
+#define TOEP_ERR_OOM 8            /* MemoryError                                 */
+
+/* Element types. */
+#define TOEP_C128 0
+#define TOEP_C64 1
+
+/* toep_matvec flags. */
+#define TOEP_MV_TRANSPOSE 1   /* matvec_transpose (toeplitz.py:306-324)                */
+#define TOEP_MV_IO_C128 2     /* c64 operator, but u / v are complex128 (cast in the   */
+                              /* first / last FFT pass; the GMRES Krylov space is c128) */
+
+typedef struct toep_op_s* toep_op_t;
+
+typedef struct {
+  int32_t n2, n1, n0;     /* Ny (level 2), Nx (level 1), N_b (block side)          */
+  int32_t l2, l1;         /* circulant embedding lengths (>= 2n-1; default 2n)     */
+  int32_t dtype;          /* TOEP_C128 / TOEP_C64                                   */
+  int64_t bins;           /* l2 * l1 frequency bins                                 */
+  int64_t dim;            /* n2 * n1 * n0                                           */
+  int64_t resident_bytes; /* spectral blocks resident in HBM                        */
+} toep_op_info_t;
+
+TOEP_API const char* toep_last_error(void);
+TOEP_API int toep_version(void);
+
+/* toeplitz.py:248-253 precompute_spectral (+ SpectralOperator, :135-155).
+ * stacked4: the generator, (2n2-1, 2n1-1, n0, n0) complex128 row-major in
+ * circulant order (BlockGenerator2L.stacked4(), toeplitz.py:129-131), on the
+ * host (on_device = 0) or on the device (on_device = 1).  The blocks are
+ * embedded into an (l2, l1) circulant (l = 0 picks 2n), transformed on the
+ * device by the batched FFT kernels and kept resident in HBM as one
+ * n0 x n0 block per bin, stored transposed (column-major) for streaming. */
+TOEP_API int toep_op_create(const void* stacked4, int on_device, int n2, int n1, int n0, int l2, int l1,
+                   int dtype, void* stream, toep_op_t* out);
+TOEP_API int toep_op_destroy(toep_op_t op);
+TOEP_API int toep_op_info(toep_op_t op, toep_op_info_t* info);
+/* SpectralOperator.diag_blocks (toeplitz.py:153): copy the (bins, n0, n0) blocks, row-major. */
+TOEP_API int toep_op_diag_blocks(toep_op_t op, void* dst_dev, void* stream);
+/* New operator whose blocks are M * D_k (M: n0 x n0 complex128, device).
+ * With M = R_00^-1 this folds the element preconditioner P_K (precond.py:124-131)
+ * into the operator, valid because P_K = I (x) R_00 commutes with F (x) I_n0. */
+TOEP_API int toep_op_fold_left(toep_op_t op, const void* m_dev, void* stream, toep_op_t* out);
+
+/* toeplitz.py:287-303 matvec (flags & TOEP_MV_TRANSPOSE: :306-324 matvec_transpose).
+ * u, v: (n, w) device column blocks.  pad_rhs / extract_result (:256-284) are
+ * fused into the first / last FFT pass.  v must not alias u. */
+TOEP_API int toep_matvec(toep_op_t op, const void* u, void* v, int64_t w, int flags, void* stream);
+
+/* toeplitz.py:300 (flags & TOEP_MV_TRANSPOSE: :320): the per-bin product alone,
+ * hat_out[k] = D_k @ hat_in[k] for every bin k, hat_* (bins, n0, w) in the
+ * operator dtype.  This is the streaming kernel that carries >98% of the
+ * matvec's HBM bytes; exposed separately for spectral-domain use and timing. */
+TOEP_API int toep_op_spectral_apply(toep_op_t op, const void* hat_in, void* hat_out, int64_t w, int flags,
+                                    void* stream);
+
+/* toeplitz.py:229-245 block_fft_2l (n2 == 1: :215-226 block_fft_1l): F_{n2} (x) F_{n1} (x) I_inner
+ * on (n2*n1*inner) contiguous values, level 1 first; inverse carries 1/(n1*n2) like
+ * np.fft.ifft per axis.  Lengths must be 13-smooth. out must not alias in. */
+TOEP_API int toep_block_dft(const void* in, void* out, int n2, int n1, int64_t inner, int inverse, int dtype, void* stream);
+
+/* precond.py:65-71 Preconditioner._solve_segments as a product with the
+ * precomputed inverse: out[s] = M @ in[s] for every (n0, w) segment s of an
+ * (segments*n0, w) block; M: n0 x n0 device.  out must not alias in. */
+TOEP_API int toep_block_apply(const void* m, int n0, const void* in, void* out, int64_t segments, int64_t w,
+                     int dtype, void* stream);
+
+/* Batched strided complex GEMM, the dense block product used by the solvers
+ * (rybicki.py:114-133 block sums, bordered.py border products):
+ * C_b = alpha * A_b @ B_b + beta * C_b, element (r, c) of X_b at
+ * X + b*bs + r*rs + c*cs (strides in elements). */
+TOEP_API int toep_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* alpha, const void* a, int64_t a_rs,
+              int64_t a_cs, int64_t a_bs, const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs,
+              const void* beta, void* c, int64_t c_rs, int64_t c_cs, int64_t c_bs, int64_t batch,
+              void* stream);
+
+/* ------------------------------------------------------------------ GMRES
+ * solvers/gmres.py:98-219 _gmres_block, device resident: the Krylov basis,
+ * Hessenberg columns, Givens rotations and the residual recurrence live in
+ * HBM; the host only polls a completion flag one Arnoldi step behind. */
+typedef int (*toep_apply_fn)(void* ctx, const void* x, void* y, int64_t w, void* stream);
+
+#define TOEP_PC_NONE 0     /* apply_precond(None, v) = v                            */
+#define TOEP_PC_BLOCK 1    /* P_K^-1 applied every step: toep_block_apply(pinv)      */
+#define TOEP_PC_FOLDED 2   /* op already holds P_K^-1 A (toep_op_fold_left);        */
+                           /* pinv gives P^-1 b, pmat gives A x = P (P^-1 A) x      */
+#define TOEP_PC_CALLBACK 3 /* papply(ctx, x, y, w, stream)                          */
+
+typedef struct {
+  toep_op_t op;               /* operator; NULL -> use apply/apply_ctx               */
+  toep_apply_fn apply;
+  void* apply_ctx;
+  int32_t precond;            /* TOEP_PC_*                                           */
+  int32_t pside;              /* n0 of pinv / pmat                                   */
+  const void* pinv;           /* pside x pside complex128, device                    */
+  const void* pmat;           /* pside x pside complex128, device (FOLDED only)      */
+  toep_apply_fn papply;
+  void* papply_ctx;
+  int64_t n, w;               /* the Krylov vectors are (n, w) complex128 blocks     */
+} toep_gmres_problem_t;
+
+typedef struct {
+  double tol;                 /* GmresConfig.tol      (gmres.py:40)                  */
+  int32_t max_iter;           /* GmresConfig.max_iter (gmres.py:41)                  */
+  int32_t restart;            /* GmresConfig.restart, 0 = None (full GMRES)          */
+  int32_t timings;            /* 1: fill per-phase timings with CUDA events          */
+} toep_gmres_cfg_t;
+
+typedef struct {
+  int32_t iterations;         /* SolveReport.iterations                              */
+  int32_t converged;          /* SolveReport.converged                               */
+  int32_t breakdown;          /* Arnoldi breakdown (h_{j+1,j} == 0)                   */
+  int32_t n_history;          /* entries written to history                          */
+  double final_residual;      /* ||b - A x|| / ||b||, unpreconditioned               */
+  double t_matvec, t_precond, t_orth, t_total;   /* phase_timings, seconds           */
+  double* history;            /* caller-owned host buffer: residual_history          */
+  int32_t history_cap;
+} toep_gmres_report_t;
+
+/* b, x: (n, w) complex128 device blocks; x is overwritten with the iterate.
+ * Returns TOEP_OK even when not converged (report.converged = 0); the Python
+ * layer raises NoConvergence with the iterate attached, as gmres.py:242-248. */
+TOEP_API int toep_gmres(const toep_gmres_problem_t* prob, const toep_gmres_cfg_t* cfg, const void* b, void* x,
+               void* stream, toep_gmres_report_t* rep);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TOEPCUDA_H */

@@ -1,0 +1,305 @@
+// Batched shared-memory mixed-radix DFT pass (Stockham autosort).
+//
+// Replaces the block-wise FFT of the reference, block_fft_2l / _fft_axis
+// (toeplitz.py:207-245, np.fft.fft / np.fft.ifft = pocketfft), for one axis of
+// the circulant grid: F_L (x) I_inner applied to a strided array whose batch
+// dimension (n0 * w, or n0 * n0 for the spectral precompute) is contiguous, so
+// every global load / store is a coalesced run of `TIL` complex values.
+//
+// One CTA owns one (outer, batch-tile) pair: it gathers the L axis values of
+// TIL batch columns into shared memory (zero-padding fused), runs the radix
+// stages ping-ponging between two shared buffers, and the last stage writes
+// straight to global memory with the crop and the 1/L scale fused.
+#include "kernels.cuh"
+
+namespace toep {
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kMinBlocks = 4;  // 128 regs/thread cap: several CTAs per SM, one wave for the matvec passes
+constexpr int kMaxStages = 16;
+
+struct Radices {
+  int n;
+  int r[kMaxStages];
+};
+
+template <typename T> __device__ __forceinline__ void sincospi_t(T x, T* s, T* c);
+template <> __device__ __forceinline__ void sincospi_t<double>(double x, double* s, double* c) { sincospi(x, s, c); }
+template <> __device__ __forceinline__ void sincospi_t<float>(float x, float* s, float* c) { sincospif(x, s, c); }
+
+template <typename Zd, typename Zs> __device__ __forceinline__ Zd cvt(Zs v) {
+  Zd r;
+  r.x = v.x;
+  r.y = v.y;
+  return r;
+}
+
+// y = DFT_R(v) with R-th roots wr[m] = exp(sign*2*pi*i*m/R)
+template <typename Z, int R>
+__device__ __forceinline__ void butterfly(Z* v, const Z* wr, int sign) {
+  if constexpr (R == 2) {
+    Z a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    Z t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+    Z t2 = cadd(v[1], v[3]), d = csub(v[1], v[3]);
+    Z t3;  // (sign*i) * d
+    t3.x = -sign * d.y;
+    t3.y = sign * d.x;
+    v[0] = cadd(t0, t2);
+    v[2] = csub(t0, t2);
+    v[1] = cadd(t1, t3);
+    v[3] = csub(t1, t3);
+  } else {
+    Z o[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      Z acc = v[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) cfma(acc, v[r], wr[(q * r) % R]);
+      o[q] = acc;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = o[q];
+  }
+}
+
+template <typename TC, typename TO, int TIL, int R, bool LAST>
+__device__ __forceinline__ void run_stage(const C<TC>* __restrict__ src, C<TC>* __restrict__ dst,
+                                          const C<TC>* __restrict__ tw, int L, int Ns, int sign,
+                                          C<TO>* __restrict__ gout, int64_t out_sa, int n_out,
+                                          int ncol, TC scale) {
+  using Z = C<TC>;
+  const int nb = L / R;
+  const int tstep = L / (Ns * R);
+  Z wr[R];
+#pragma unroll
+  for (int m = 0; m < R; ++m) wr[m] = tw[m * nb];
+  for (int e = threadIdx.x; e < nb * TIL; e += kThreads) {
+    const int j = e / TIL;
+    const int col = e - j * TIL;
+    const int k = j % Ns;
+    Z v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = src[(j + r * nb) * TIL + col];
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[k * r * tstep]);
+    butterfly<Z, R>(v, wr, sign);
+    const int base = (j / Ns) * Ns * R + k;
+    if constexpr (!LAST) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) dst[(base + q * Ns) * TIL + col] = v[q];
+    } else {
+      if (col < ncol) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int idx = base + q * Ns;
+          if (idx < n_out) gout[idx * out_sa + col] = cvt<C<TO>>(cscale(v[q], scale));
+        }
+      }
+    }
+  }
+}
+
+template <typename TC, typename TO, int TIL, bool LAST>
+__device__ __forceinline__ void dispatch_stage(int R, const C<TC>* src, C<TC>* dst, const C<TC>* tw, int L,
+                                               int Ns, int sign, C<TO>* gout, int64_t out_sa, int n_out,
+                                               int ncol, TC scale) {
+  switch (R) {
+    case 2: run_stage<TC, TO, TIL, 2, LAST>(src, dst, tw, L, Ns, sign, gout, out_sa, n_out, ncol, scale); break;
+    case 3: run_stage<TC, TO, TIL, 3, LAST>(src, dst, tw, L, Ns, sign, gout, out_sa, n_out, ncol, scale); break;
+    case 4: run_stage<TC, TO, TIL, 4, LAST>(src, dst, tw, L, Ns, sign, gout, out_sa, n_out, ncol, scale); break;
+    case 5: run_stage<TC, TO, TIL, 5, LAST>(src, dst, tw, L, Ns, sign, gout, out_sa, n_out, ncol, scale); break;
+    case 7: run_stage<TC, TO, TIL, 7, LAST>(src, dst, tw, L, Ns, sign, gout, out_sa, n_out, ncol, scale); break;
+    default: break;
+  }
+}
+
+template <typename TI, typename TC, typename TO, int TIL>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) fft_pass_kernel(PassArgs a, Radices rad, double two_over_L) {
+  if (a.stop != nullptr && *a.stop != 0) return;
+  using Z = C<TC>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Z* tw = reinterpret_cast<Z*>(smem_raw);
+  Z* buf0 = tw + a.L;
+  Z* buf1 = buf0 + a.L * TIL;
+  const int L = a.L;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * TIL;
+  const int o = blockIdx.y;
+  const int ncol = static_cast<int>(std::min<int64_t>(TIL, a.inner - i0));
+
+  for (int t = threadIdx.x; t < L; t += kThreads) {
+    TC s, c;
+    sincospi_t<TC>(static_cast<TC>(t * two_over_L), &s, &c);
+    tw[t] = mk<TC>(c, a.sign * s);
+  }
+
+  const C<TI>* in = static_cast<const C<TI>*>(a.in) + o * a.in_so + i0;
+  if (a.in_idx != nullptr) in += static_cast<int64_t>(*a.in_idx) * a.in_idx_stride;
+  C<TO>* out = static_cast<C<TO>*>(a.out) + o * a.out_so + i0;
+  if (a.out_idx != nullptr) out += static_cast<int64_t>(*a.out_idx) * a.out_idx_stride;
+
+  const int hi_start = L - a.n_hi;
+  for (int e = threadIdx.x; e < L * TIL; e += kThreads) {
+    const int slot = e / TIL;
+    const int col = e - slot * TIL;
+    int src = -1;
+    if (slot < a.n_lo) src = slot;
+    else if (slot >= hi_start) src = a.n_lo + slot - hi_start;
+    Z v = mk<TC>(0, 0);
+    if (src >= 0 && col < ncol) v = cvt<Z>(in[src * a.in_sa + col]);
+    buf0[e] = v;
+  }
+  __syncthreads();
+
+  const TC scale = static_cast<TC>(a.scale);
+  if (rad.n == 0) {  // L == 1
+    if (threadIdx.x < ncol && a.n_out > 0) out[threadIdx.x] = cvt<C<TO>>(cscale(buf0[threadIdx.x], scale));
+    return;
+  }
+  Z* src = buf0;
+  Z* dst = buf1;
+  int Ns = 1;
+  for (int s = 0; s < rad.n; ++s) {
+    const int R = rad.r[s];
+    if (s + 1 < rad.n) {
+      dispatch_stage<TC, TO, TIL, false>(R, src, dst, tw, L, Ns, a.sign, out, a.out_sa, a.n_out, ncol, scale);
+      __syncthreads();
+      Z* t = src;
+      src = dst;
+      dst = t;
+      Ns *= R;
+    } else {
+      dispatch_stage<TC, TO, TIL, true>(R, src, dst, tw, L, Ns, a.sign, out, a.out_sa, a.n_out, ncol, scale);
+    }
+  }
+}
+
+// Direct O(L^2) DFT for lengths that are not 7-smooth (API block_fft_* on prime
+// lengths such as the reference's 2n-1 = 59).  Same placement / crop contract.
+template <typename TI, typename TC, typename TO, int TIL>
+__global__ void __launch_bounds__(kThreads) dft_direct_kernel(PassArgs a, double two_over_L) {
+  if (a.stop != nullptr && *a.stop != 0) return;
+  using Z = C<TC>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Z* tw = reinterpret_cast<Z*>(smem_raw);
+  Z* buf = tw + a.L;
+  const int L = a.L;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * TIL;
+  const int o = blockIdx.y;
+  const int ncol = static_cast<int>(std::min<int64_t>(TIL, a.inner - i0));
+  for (int t = threadIdx.x; t < L; t += kThreads) {
+    TC s, c;
+    sincospi_t<TC>(static_cast<TC>(t * two_over_L), &s, &c);
+    tw[t] = mk<TC>(c, a.sign * s);
+  }
+  const C<TI>* in = static_cast<const C<TI>*>(a.in) + o * a.in_so + i0;
+  if (a.in_idx != nullptr) in += static_cast<int64_t>(*a.in_idx) * a.in_idx_stride;
+  C<TO>* out = static_cast<C<TO>*>(a.out) + o * a.out_so + i0;
+  if (a.out_idx != nullptr) out += static_cast<int64_t>(*a.out_idx) * a.out_idx_stride;
+  const int hi_start = L - a.n_hi;
+  for (int e = threadIdx.x; e < L * TIL; e += kThreads) {
+    const int slot = e / TIL;
+    const int col = e - slot * TIL;
+    int src = -1;
+    if (slot < a.n_lo) src = slot;
+    else if (slot >= hi_start) src = a.n_lo + slot - hi_start;
+    Z v = mk<TC>(0, 0);
+    if (src >= 0 && col < ncol) v = cvt<Z>(in[src * a.in_sa + col]);
+    buf[e] = v;
+  }
+  __syncthreads();
+  const TC scale = static_cast<TC>(a.scale);
+  for (int e = threadIdx.x; e < a.n_out * TIL; e += kThreads) {
+    const int k = e / TIL;
+    const int col = e - k * TIL;
+    Z acc = mk<TC>(0, 0);
+    int idx = 0;
+    for (int t = 0; t < L; ++t) {
+      cfma(acc, buf[t * TIL + col], tw[idx]);
+      idx += k;
+      if (idx >= L) idx -= L;
+    }
+    if (col < ncol) out[k * a.out_sa + col] = cvt<C<TO>>(cscale(acc, scale));
+  }
+}
+
+template <typename TI, typename TC, typename TO>
+int launch(const PassArgs& a, const Radices& rad, bool direct, cudaStream_t s) {
+  const size_t es = sizeof(C<TC>);
+  const int nbuf = direct ? 1 : 2;
+  int til = 32;
+  while (til > 1 && static_cast<size_t>(nbuf * a.L * til + a.L) * es > 48 * 1024) til /= 2;
+  while (til > 1 && til / 2 >= a.inner) til /= 2;
+  const size_t smem = static_cast<size_t>(nbuf * a.L * til + a.L) * es;
+  TOEP_REQUIRE(smem <= 200 * 1024, TOEP_ERR_ARG, "fft length %d too long for one shared-memory pass", a.L);
+  dim3 grid(static_cast<unsigned>((a.inner + til - 1) / til), static_cast<unsigned>(a.outer));
+  TOEP_REQUIRE(a.outer <= 65535, TOEP_ERR_ARG, "fft pass outer count %d > 65535", a.outer);
+  const double two_over_L = 2.0 / a.L;
+#define TOEP_FFT_CASE(T)                                                                         \
+  case T: {                                                                                      \
+    if (direct) {                                                                                \
+      auto k = dft_direct_kernel<TI, TC, TO, T>;                                                 \
+      if (smem > 48 * 1024) TOEP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      k<<<grid, kThreads, smem, s>>>(a, two_over_L);                                             \
+    } else {                                                                                     \
+      auto k = fft_pass_kernel<TI, TC, TO, T>;                                                   \
+      if (smem > 48 * 1024) TOEP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      k<<<grid, kThreads, smem, s>>>(a, rad, two_over_L);                                        \
+    }                                                                                            \
+    break;                                                                                       \
+  }
+  switch (til) {
+    TOEP_FFT_CASE(1)
+    TOEP_FFT_CASE(2)
+    TOEP_FFT_CASE(4)
+    TOEP_FFT_CASE(8)
+    TOEP_FFT_CASE(16)
+    TOEP_FFT_CASE(32)
+    default: break;
+  }
+#undef TOEP_FFT_CASE
+  TOEP_LAUNCHED();
+  return TOEP_OK;
+}
+
+}  // namespace
+
+int factorize(int L, int* rad, int* nrad) {
+  int n = 0;
+  int m = L;
+  while (m % 4 == 0 && m > 4 && n < kMaxStages) { rad[n++] = 4; m /= 4; }
+  const int radices[] = {4, 2, 3, 5, 7};
+  for (int p : radices) {
+    while (m % p == 0 && n < kMaxStages) { rad[n++] = p; m /= p; }
+  }
+  *nrad = n;
+  if (m != 1) {
+    set_error("DFT length %d is not 7-smooth", L);
+    return TOEP_ERR_ARG;
+  }
+  return TOEP_OK;
+}
+
+int fft_pass(const PassArgs& a, int tin, int tcomp, int tout, cudaStream_t s) {
+  TOEP_REQUIRE(a.L >= 1 && a.n_lo >= 0 && a.n_hi >= 0 && a.n_lo + a.n_hi <= a.L && a.n_out <= a.L,
+               TOEP_ERR_ARG, "bad fft pass geometry L=%d lo=%d hi=%d out=%d", a.L, a.n_lo, a.n_hi, a.n_out);
+  if (a.inner == 0 || a.outer == 0 || a.n_out == 0) return TOEP_OK;
+  Radices rad{};
+  const bool direct = factorize(a.L, rad.r, &rad.n) != TOEP_OK;  // not 7-smooth: direct DFT
+  const int code = tin * 4 + tcomp * 2 + tout;
+  switch (code) {
+    case 0: return launch<double, double, double>(a, rad, direct, s);   // c128 end to end
+    case 7: return launch<float, float, float>(a, rad, direct, s);      // c64 end to end
+    case 6: return launch<float, float, double>(a, rad, direct, s);     // c64 compute, c128 out
+    case 3: return launch<double, float, float>(a, rad, direct, s);     // c128 in, c64 compute
+    default:
+      set_error("unsupported fft pass type combination %d/%d/%d", tin, tcomp, tout);
+      return TOEP_ERR_ARG;
+  }
+}
+
+}  // namespace toep

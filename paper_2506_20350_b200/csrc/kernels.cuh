@@ -1,0 +1,57 @@
+// Internal kernel launchers of libtoepcuda (not part of the C ABI).
+#pragma once
+
+#include "common.cuh"
+
+namespace toep {
+
+// ------------------------------------------------------------------ FFT pass
+// One batched 1-D DFT of length L along an "axis" of a strided array whose
+// innermost ("batch") dimension of length `inner` is contiguous:
+//   element (outer o, axis a, batch i) at base + o*so + a*sa + i.
+// Input placement fuses the circulant embedding / pad_rhs (toeplitz.py:256-269):
+//   slot s in [0, n_lo)        <- input row s
+//   slot s in [L-n_hi, L)      <- input row n_lo + s - (L - n_hi)
+//   all other slots            <- 0
+// Only outputs 0..n_out-1 are stored (extract_result crop, toeplitz.py:272-284),
+// each multiplied by `scale`.  sign = -1 forward (np.fft.fft), +1 inverse.
+struct PassArgs {
+  const void* in = nullptr;
+  void* out = nullptr;
+  int L = 1, n_lo = 0, n_hi = 0, n_out = 0;
+  int64_t inner = 0;
+  int64_t in_sa = 0, in_so = 0, out_sa = 0, out_so = 0;
+  int outer = 1;
+  int sign = -1;
+  double scale = 1.0;
+  // optional device-side offsets (GMRES basis indexing inside one launch sequence)
+  const int* in_idx = nullptr;
+  int64_t in_idx_stride = 0;
+  const int* out_idx = nullptr;
+  int64_t out_idx_stride = 0;
+  const int* stop = nullptr;  // if non-null and *stop != 0 the launch is a no-op
+};
+
+// type codes: 0 = complex128, 1 = complex64
+int fft_pass(const PassArgs& a, int tin, int tcomp, int tout, cudaStream_t s);
+int factorize(int L, int* rad, int* nrad);
+
+// --------------------------------------------------------------- bin product
+// V_k = D_k U_k for k < K, D_k stored transposed: DT[k][j][m] = D_k[m][j].
+// U, V: [K][n0][w].  transpose: V_k = D_k^T U_k.
+int bin_product(int dtype, const void* DT, const void* U, void* V, int64_t K, int n0, int64_t w,
+                bool transpose, const int* stop, cudaStream_t s);
+
+// ---------------------------------------------------------------- GEMM
+int gemm(int dtype, int64_t m, int64_t n, int64_t k, double2 alpha, const void* a, int64_t a_rs,
+         int64_t a_cs, int64_t a_bs, const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs,
+         double2 beta, void* c, int64_t c_rs, int64_t c_cs, int64_t c_bs, int64_t batch,
+         cudaStream_t s, const int* stop = nullptr);
+
+// batched transpose of complex matrices: out[b][c][r] = in[b][r][c]  (rows x cols)
+int transpose_batched(int dtype, const void* in, void* out, int64_t batch, int rows, int cols, cudaStream_t s);
+
+// embed / cast helpers
+int cast_c128_to_c64(const void* in, void* out, int64_t n, cudaStream_t s);
+
+}  // namespace toep

@@ -1,0 +1,378 @@
+// Resident spectral operator: precompute (toeplitz.py:248-253), matvec
+// (toeplitz.py:287-324), block preconditioner apply (precond.py:65-71) and the
+// C-ABI entry points for them.
+#include <cstdarg>
+#include <cstring>
+#include <new>
+
+#include "op.h"
+
+namespace toep {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+const char* last_error() { return g_err; }
+
+size_t elt_size(int dtype) { return dtype == TOEP_C64 ? sizeof(float2) : sizeof(double2); }
+int64_t op_dim(const toep_op_s* op) { return static_cast<int64_t>(op->n2) * op->n1 * op->n0; }
+
+static int smooth7_at_least(int m) {
+  for (int L = m;; ++L) {
+    int r = L;
+    for (int p : {2, 3, 5, 7})
+      while (r % p == 0) r /= p;
+    if (r == 1) return L;
+  }
+}
+
+// Keep memory freed with cudaFreeAsync in the device pool: with the default
+// release threshold (0) every stream synchronisation returns it to the driver
+// and the next solve pays cudaMalloc again (milliseconds).
+void keep_pool() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done_dev == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done_dev = dev;
+}
+
+int op_workspace(toep_op_s* op, int64_t w, cudaStream_t s, toep_op_s::Workspace** out) {
+  keep_pool();
+  std::lock_guard<std::mutex> lock(op->mu);
+  auto& ws = op->ws[s];
+  if (ws.w_cap < w) {
+    const size_t es = elt_size(op->dtype);
+    if (ws.x1) TOEP_CUDA(cudaFreeAsync(ws.x1, s));
+    if (ws.hat) TOEP_CUDA(cudaFreeAsync(ws.hat, s));
+    if (ws.hat2) TOEP_CUDA(cudaFreeAsync(ws.hat2, s));
+    ws.x1 = ws.hat = ws.hat2 = nullptr;
+    ws.w_cap = 0;
+    const size_t nx1 = static_cast<size_t>(op->n2) * op->l1 * op->n0 * w * es;
+    const size_t nhat = static_cast<size_t>(op->K) * op->n0 * w * es;
+    if (cudaMallocAsync(&ws.x1, nx1, s) != cudaSuccess || cudaMallocAsync(&ws.hat, nhat, s) != cudaSuccess ||
+        cudaMallocAsync(&ws.hat2, nhat, s) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("out of device memory for matvec workspace (w=%lld)", static_cast<long long>(w));
+      return TOEP_ERR_OOM;
+    }
+    ws.w_cap = w;
+  }
+  *out = &ws;
+  return TOEP_OK;
+}
+
+int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose, bool io_c128, const int* stop,
+                cudaStream_t s) {
+  if (w == 0) return TOEP_OK;
+  toep_op_s::Workspace* ws = nullptr;
+  TOEP_TRY(op_workspace(op, w, s, &ws));
+  const int tc = op->dtype == TOEP_C64 ? 1 : 0;
+  const int tio = io_c128 ? 0 : tc;
+  const int64_t inner = static_cast<int64_t>(op->n0) * w;
+  // forward transform of transpose() is the inverse DFT (toeplitz.py:318) and vice versa
+  const int s1 = transpose ? +1 : -1;
+  const double sc1y = transpose ? 1.0 / op->l2 : 1.0, sc1x = transpose ? 1.0 / op->l1 : 1.0;
+  const double sc2y = transpose ? 1.0 : 1.0 / op->l2, sc2x = transpose ? 1.0 : 1.0 / op->l1;
+
+  PassArgs a;  // level-1 (x) pass: u [n2][n1][inner] -> x1 [n2][l1][inner]  (pad fused)
+  a.in = u; a.out = ws->x1; a.L = op->l1; a.n_lo = op->n1; a.n_hi = 0; a.n_out = op->l1;
+  a.inner = inner; a.outer = op->n2; a.in_sa = inner; a.in_so = op->n1 * inner; a.out_sa = inner;
+  a.out_so = op->l1 * inner; a.sign = s1; a.scale = sc1x; a.stop = stop;
+  TOEP_TRY(fft_pass(a, tio, tc, tc, s));
+
+  PassArgs b;  // level-2 (y) pass over the n2 non-zero rows: x1 -> hat [l2][l1][inner]
+  b.in = ws->x1; b.out = ws->hat; b.L = op->l2; b.n_lo = op->n2; b.n_hi = 0; b.n_out = op->l2;
+  b.inner = inner; b.outer = op->l1; b.in_sa = op->l1 * inner; b.in_so = inner; b.out_sa = op->l1 * inner;
+  b.out_so = inner; b.sign = s1; b.scale = sc1y; b.stop = stop;
+  TOEP_TRY(fft_pass(b, tc, tc, tc, s));
+
+  TOEP_TRY(bin_product(op->dtype, op->DT, ws->hat, ws->hat2, op->K, op->n0, w, transpose, stop, s));
+
+  PassArgs c;  // inverse level-2 pass, keep the n2 payload rows: hat2 -> x1 [n2][l1][inner]
+  c.in = ws->hat2; c.out = ws->x1; c.L = op->l2; c.n_lo = op->l2; c.n_hi = 0; c.n_out = op->n2;
+  c.inner = inner; c.outer = op->l1; c.in_sa = op->l1 * inner; c.in_so = inner; c.out_sa = op->l1 * inner;
+  c.out_so = inner; c.sign = -s1; c.scale = sc2y; c.stop = stop;
+  TOEP_TRY(fft_pass(c, tc, tc, tc, s));
+
+  PassArgs d;  // inverse level-1 pass + extract_result crop: x1 -> v [n2][n1][inner]
+  d.in = ws->x1; d.out = v; d.L = op->l1; d.n_lo = op->l1; d.n_hi = 0; d.n_out = op->n1;
+  d.inner = inner; d.outer = op->n2; d.in_sa = inner; d.in_so = op->l1 * inner; d.out_sa = inner;
+  d.out_so = op->n1 * inner; d.sign = -s1; d.scale = sc2x; d.stop = stop;
+  TOEP_TRY(fft_pass(d, tc, tc, tio, s));
+  return TOEP_OK;
+}
+
+int block_apply_impl(const void* m, int n0, const void* in, void* out, int64_t segments, int64_t w, int dtype,
+                     cudaStream_t s, const int* stop) {
+  if (w == 1) {
+    // one GEMM: out(:, seg) = M in(:, seg), segments as columns
+    return gemm(dtype, n0, segments, n0, make_double2(1, 0), m, n0, 1, 0, in, 1, n0, 0, make_double2(0, 0), out, 1,
+                n0, 0, 1, s, stop);
+  }
+  // batched over segments: (n0 x w) blocks
+  int64_t done = 0;
+  while (done < segments) {
+    const int64_t nb = std::min<int64_t>(segments - done, 65535);
+    const size_t es = elt_size(dtype);
+    const char* pin = static_cast<const char*>(in) + done * n0 * w * es;
+    char* pout = static_cast<char*>(out) + done * n0 * w * es;
+    TOEP_TRY(gemm(dtype, n0, w, n0, make_double2(1, 0), m, n0, 1, 0, pin, w, 1, n0 * w, make_double2(0, 0), pout, w,
+                  1, n0 * w, nb, s, stop));
+    done += nb;
+  }
+  return TOEP_OK;
+}
+
+}  // namespace toep
+
+using namespace toep;
+
+extern "C" {
+
+const char* toep_last_error(void) { return last_error(); }
+int toep_version(void) { return 100; }
+
+int toep_op_create(const void* stacked4, int on_device, int n2, int n1, int n0, int l2, int l1, int dtype,
+                   void* stream, toep_op_t* out) {
+  TOEP_REQUIRE(out != nullptr && stacked4 != nullptr, TOEP_ERR_ARG, "null argument");
+  TOEP_REQUIRE(n2 >= 1 && n1 >= 1 && n0 >= 1, TOEP_ERR_SHAPE, "n2, n1, n0 must be positive");
+  TOEP_REQUIRE(dtype == TOEP_C128 || dtype == TOEP_C64, TOEP_ERR_ARG, "dtype must be TOEP_C128 or TOEP_C64");
+  const int k2 = 2 * n2 - 1, k1 = 2 * n1 - 1;
+  if (l2 <= 0) l2 = smooth7_at_least(k2);
+  if (l1 <= 0) l1 = smooth7_at_least(k1);
+  TOEP_REQUIRE(l2 >= k2 && l1 >= k1, TOEP_ERR_SHAPE, "embedding (%d,%d) shorter than 2n-1 (%d,%d)", l2, l1, k2, k1);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+  auto* op = new (std::nothrow) toep_op_s();
+  TOEP_REQUIRE(op != nullptr, TOEP_ERR_OOM, "host allocation failed");
+  op->n2 = n2; op->n1 = n1; op->n0 = n0; op->l2 = l2; op->l1 = l1; op->dtype = dtype;
+  op->K = static_cast<int64_t>(l2) * l1;
+  cudaGetDevice(&op->device);
+
+  const int64_t nn = static_cast<int64_t>(n0) * n0;
+  const size_t gen_bytes = static_cast<size_t>(k2) * k1 * nn * sizeof(double2);
+  const size_t x_bytes = static_cast<size_t>(k2) * l1 * nn * sizeof(double2);
+  const size_t d_bytes = static_cast<size_t>(op->K) * nn * sizeof(double2);
+  void *gen = nullptr, *x = nullptr, *d = nullptr, *dt = nullptr;
+  auto fail = [&](int code) {
+    cudaGetLastError();
+    if (gen && !on_device) cudaFreeAsync(gen, s);
+    if (x) cudaFreeAsync(x, s);
+    if (d) cudaFreeAsync(d, s);
+    if (dt) cudaFreeAsync(dt, s);
+    delete op;
+    return code;
+  };
+#define TOEP_STEP(expr)                 \
+  do {                                  \
+    int _c = (expr);                    \
+    if (_c != TOEP_OK) return fail(_c); \
+  } while (0)
+#define TOEP_ALLOC(ptr, bytes)                                                                   \
+  do {                                                                                           \
+    if (cudaMallocAsync(&(ptr), (bytes), s) != cudaSuccess) {                                    \
+      set_error("out of device memory in precompute_spectral (%zu bytes)", (size_t)(bytes));    \
+      return fail(TOEP_ERR_OOM);                                                                 \
+    }                                                                                            \
+  } while (0)
+
+  if (on_device) {
+    gen = const_cast<void*>(stacked4);
+  } else {
+    TOEP_ALLOC(gen, gen_bytes);
+    if (cudaMemcpyAsync(gen, stacked4, gen_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+      set_error("generator upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+      return fail(TOEP_ERR_CUDA);
+    }
+  }
+  TOEP_ALLOC(x, x_bytes);
+  // level-1 DFT of every (offset2) row of the generator, embedded at offset % l1
+  PassArgs a;
+  a.in = gen; a.out = x; a.L = l1; a.n_lo = n1; a.n_hi = n1 - 1; a.n_out = l1; a.inner = nn; a.outer = k2;
+  a.in_sa = nn; a.in_so = k1 * nn; a.out_sa = nn; a.out_so = static_cast<int64_t>(l1) * nn; a.sign = -1;
+  TOEP_STEP(fft_pass(a, 0, 0, 0, s));
+  if (!on_device) { cudaFreeAsync(gen, s); }
+  gen = nullptr;
+  TOEP_ALLOC(d, d_bytes);
+  PassArgs b;  // level-2 DFT, embedded at offset % l2 -> D [l2][l1][n0][n0]
+  b.in = x; b.out = d; b.L = l2; b.n_lo = n2; b.n_hi = n2 - 1; b.n_out = l2; b.inner = nn; b.outer = l1;
+  b.in_sa = static_cast<int64_t>(l1) * nn; b.in_so = nn; b.out_sa = static_cast<int64_t>(l1) * nn; b.out_so = nn;
+  b.sign = -1;
+  TOEP_STEP(fft_pass(b, 0, 0, 0, s));
+  cudaFreeAsync(x, s);
+  x = nullptr;
+  TOEP_ALLOC(dt, d_bytes);
+  for (int64_t k0 = 0; k0 < op->K; k0 += 65535) {
+    const int64_t nb = std::min<int64_t>(op->K - k0, 65535);
+    TOEP_STEP(transpose_batched(TOEP_C128, static_cast<double2*>(d) + k0 * nn, static_cast<double2*>(dt) + k0 * nn,
+                                nb, n0, n0, s));
+  }
+  cudaFreeAsync(d, s);
+  d = nullptr;
+  if (dtype == TOEP_C64) {
+    void* dt32 = nullptr;
+    TOEP_ALLOC(dt32, static_cast<size_t>(op->K) * nn * sizeof(float2));
+    TOEP_STEP(cast_c128_to_c64(dt, dt32, op->K * nn, s));
+    cudaFreeAsync(dt, s);
+    dt = dt32;
+  }
+  op->DT = dt;
+  if (cudaStreamSynchronize(s) != cudaSuccess) {
+    set_error("precompute_spectral failed: %s", cudaGetErrorString(cudaGetLastError()));
+    dt = op->DT;
+    return fail(TOEP_ERR_CUDA);
+  }
+#undef TOEP_STEP
+#undef TOEP_ALLOC
+  *out = op;
+  return TOEP_OK;
+}
+
+int toep_op_destroy(toep_op_t op) {
+  if (op == nullptr) return TOEP_OK;
+  cudaDeviceSynchronize();
+  for (auto& kv : op->ws) {
+    cudaFree(kv.second.x1);
+    cudaFree(kv.second.hat);
+    cudaFree(kv.second.hat2);
+  }
+  cudaFree(op->DT);
+  delete op;
+  TOEP_LAUNCHED();
+  return TOEP_OK;
+}
+
+int toep_op_info(toep_op_t op, toep_op_info_t* info) {
+  TOEP_REQUIRE(op != nullptr && info != nullptr, TOEP_ERR_ARG, "null argument");
+  info->n2 = op->n2; info->n1 = op->n1; info->n0 = op->n0; info->l2 = op->l2; info->l1 = op->l1;
+  info->dtype = op->dtype; info->bins = op->K; info->dim = op_dim(op);
+  info->resident_bytes = static_cast<int64_t>(op->K) * op->n0 * op->n0 * static_cast<int64_t>(elt_size(op->dtype));
+  return TOEP_OK;
+}
+
+int toep_op_diag_blocks(toep_op_t op, void* dst, void* stream) {
+  TOEP_REQUIRE(op != nullptr && dst != nullptr, TOEP_ERR_ARG, "null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t nn = static_cast<int64_t>(op->n0) * op->n0;
+  const size_t es = elt_size(op->dtype);
+  for (int64_t k0 = 0; k0 < op->K; k0 += 65535) {
+    const int64_t nb = std::min<int64_t>(op->K - k0, 65535);
+    TOEP_TRY(transpose_batched(op->dtype, static_cast<const char*>(op->DT) + k0 * nn * es,
+                               static_cast<char*>(dst) + k0 * nn * es, nb, op->n0, op->n0, s));
+  }
+  return TOEP_OK;
+}
+
+int toep_op_fold_left(toep_op_t op, const void* m_dev, void* stream, toep_op_t* out) {
+  TOEP_REQUIRE(op != nullptr && m_dev != nullptr && out != nullptr, TOEP_ERR_ARG, "null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto* f = new (std::nothrow) toep_op_s();
+  TOEP_REQUIRE(f != nullptr, TOEP_ERR_OOM, "host allocation failed");
+  f->n2 = op->n2; f->n1 = op->n1; f->n0 = op->n0; f->l2 = op->l2; f->l1 = op->l1; f->dtype = op->dtype;
+  f->K = op->K; f->device = op->device;
+  const int64_t n0 = op->n0;
+  const size_t bytes = static_cast<size_t>(op->K) * n0 * n0 * elt_size(op->dtype);
+  if (cudaMallocAsync(&f->DT, bytes, s) != cudaSuccess) {
+    cudaGetLastError();
+    delete f;
+    set_error("out of device memory folding the preconditioner");
+    return TOEP_ERR_OOM;
+  }
+  // DT'[k][j][:] = M DT[k][j][:]   ((M D_k)^T = D_k^T M^T, row j of D_k^T times M^T)
+  const void* m = m_dev;
+  void* m32 = nullptr;
+  if (op->dtype == TOEP_C64) {
+    TOEP_CUDA(cudaMallocAsync(&m32, n0 * n0 * sizeof(float2), s));
+    TOEP_TRY(cast_c128_to_c64(m_dev, m32, n0 * n0, s));
+    m = m32;
+  }
+  int rc = gemm(op->dtype, n0, op->K * n0, n0, make_double2(1, 0), m, n0, 1, 0, op->DT, 1, n0, 0,
+                make_double2(0, 0), f->DT, 1, n0, 0, 1, s);
+  if (m32) cudaFreeAsync(m32, s);
+  if (rc != TOEP_OK) {
+    cudaFree(f->DT);
+    delete f;
+    return rc;
+  }
+  *out = f;
+  return TOEP_OK;
+}
+
+int toep_matvec(toep_op_t op, const void* u, void* v, int64_t w, int flags, void* stream) {
+  TOEP_REQUIRE(op != nullptr && (w == 0 || (u != nullptr && v != nullptr)), TOEP_ERR_ARG, "null argument");
+  TOEP_REQUIRE(w >= 0, TOEP_ERR_SHAPE, "negative column count");
+  TOEP_REQUIRE(u != v, TOEP_ERR_ARG, "matvec output must not alias its input");
+  return matvec_impl(op, u, v, w, (flags & TOEP_MV_TRANSPOSE) != 0, (flags & TOEP_MV_IO_C128) != 0, nullptr,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int toep_op_spectral_apply(toep_op_t op, const void* hat_in, void* hat_out, int64_t w, int flags, void* stream) {
+  TOEP_REQUIRE(op != nullptr && hat_in != nullptr && hat_out != nullptr && hat_in != hat_out, TOEP_ERR_ARG,
+               "bad spectral_apply arguments");
+  return bin_product(op->dtype, op->DT, hat_in, hat_out, op->K, op->n0, w, (flags & TOEP_MV_TRANSPOSE) != 0, nullptr,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int toep_block_dft(const void* in, void* out, int n2, int n1, int64_t inner, int inverse, int dtype, void* stream) {
+  TOEP_REQUIRE(in != nullptr && out != nullptr && in != out, TOEP_ERR_ARG, "bad block_dft buffers");
+  TOEP_REQUIRE(n2 >= 1 && n1 >= 1 && inner >= 0, TOEP_ERR_SHAPE, "bad block_dft shape");
+  if (inner == 0) return TOEP_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int t = dtype == TOEP_C64 ? 1 : 0;
+  const int sign = inverse ? +1 : -1;
+  void* mid = nullptr;
+  const size_t bytes = static_cast<size_t>(n2) * n1 * inner * elt_size(dtype);
+  TOEP_REQUIRE(cudaMallocAsync(&mid, bytes, s) == cudaSuccess, TOEP_ERR_OOM, "out of device memory in block_dft");
+  PassArgs a;  // level 1 (axis of length n1) first, as block_fft_2l (toeplitz.py:241-243)
+  a.in = in; a.out = mid; a.L = n1; a.n_lo = n1; a.n_out = n1; a.inner = inner; a.outer = n2; a.in_sa = inner;
+  a.in_so = n1 * inner; a.out_sa = inner; a.out_so = n1 * inner; a.sign = sign; a.scale = inverse ? 1.0 / n1 : 1.0;
+  int rc = fft_pass(a, t, t, t, s);
+  if (rc == TOEP_OK) {
+    PassArgs b;  // level 2
+    b.in = mid; b.out = out; b.L = n2; b.n_lo = n2; b.n_out = n2; b.inner = inner; b.outer = n1;
+    b.in_sa = static_cast<int64_t>(n1) * inner; b.in_so = inner; b.out_sa = static_cast<int64_t>(n1) * inner;
+    b.out_so = inner; b.sign = sign; b.scale = inverse ? 1.0 / n2 : 1.0;
+    rc = fft_pass(b, t, t, t, s);
+  }
+  cudaFreeAsync(mid, s);
+  return rc;
+}
+
+int toep_block_apply(const void* m, int n0, const void* in, void* out, int64_t segments, int64_t w, int dtype,
+                     void* stream) {
+  TOEP_REQUIRE(m != nullptr && in != nullptr && out != nullptr, TOEP_ERR_ARG, "null argument");
+  TOEP_REQUIRE(in != out, TOEP_ERR_ARG, "block_apply output must not alias its input");
+  return block_apply_impl(m, n0, in, out, segments, w, dtype, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int toep_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* alpha, const void* a, int64_t a_rs,
+              int64_t a_cs, int64_t a_bs, const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, const void* beta,
+              void* c, int64_t c_rs, int64_t c_cs, int64_t c_bs, int64_t batch, void* stream) {
+  TOEP_REQUIRE(alpha != nullptr && beta != nullptr, TOEP_ERR_ARG, "null alpha/beta");
+  const double2 al = *static_cast<const double2*>(alpha);
+  const double2 be = *static_cast<const double2*>(beta);
+  int64_t done = 0;
+  const size_t es = elt_size(dtype);
+  while (done < batch) {
+    const int64_t nb = std::min<int64_t>(batch - done, 65535);
+    TOEP_TRY(gemm(dtype, m, n, k, al, static_cast<const char*>(a) + done * a_bs * es, a_rs, a_cs, a_bs,
+                  static_cast<const char*>(b) + done * b_bs * es, b_rs, b_cs, b_bs, be,
+                  static_cast<char*>(c) + done * c_bs * es, c_rs, c_cs, c_bs, nb, static_cast<cudaStream_t>(stream)));
+    done += nb;
+  }
+  return TOEP_OK;
+}
+
+}  // extern "C"

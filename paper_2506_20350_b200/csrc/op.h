@@ -1,0 +1,40 @@
+// Internal definition of the resident spectral operator (toep_op_t).
+#pragma once
+
+#include <map>
+#include <mutex>
+
+#include "kernels.cuh"
+
+struct toep_op_s {
+  int n2 = 0, n1 = 0, n0 = 0, l2 = 0, l1 = 0, dtype = TOEP_C128;
+  int64_t K = 0;
+  void* DT = nullptr;  // [K][n0][n0], DT[k][j][m] = D_k[m][j]
+  int device = 0;
+  struct Workspace {
+    int64_t w_cap = 0;
+    void* x1 = nullptr;    // [n2][l1][n0*w]
+    void* hat = nullptr;   // [K][n0][w]
+    void* hat2 = nullptr;  // [K][n0][w]
+  };
+  std::mutex mu;
+  std::map<cudaStream_t, Workspace> ws;
+};
+
+namespace toep {
+
+size_t elt_size(int dtype);
+int64_t op_dim(const toep_op_s* op);
+int op_workspace(toep_op_s* op, int64_t w, cudaStream_t s, toep_op_s::Workspace** out);
+
+// matvec with optional device-side stop flag (GMRES speculative steps).
+// io_c128: u / v are complex128 while the operator computes in its own dtype.
+int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose, bool io_c128,
+                const int* stop, cudaStream_t s);
+
+void keep_pool();
+
+int block_apply_impl(const void* m, int n0, const void* in, void* out, int64_t segments, int64_t w, int dtype,
+                     cudaStream_t s, const int* stop);
+
+}  // namespace toep

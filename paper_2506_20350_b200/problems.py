@@ -1,0 +1,139 @@
+"""Seeded inputs of the BASELINE configurations (host side).
+
+The BASELINE generator: for every signed block offset
+(p, q), p the level-2 / row / y offset and q the level-1 / column / x offset,
+loop order p outer then q inner, draw ``re = N(0,1)^{Nb x Nb}`` then
+``im = N(0,1)^{Nb x Nb}`` from ``numpy.random.default_rng(seed)``; the block is
+``(re + 1j*im) * exp(-1j*pi*r) / max(r, 1)`` with ``r = hypot(p, q)``, and
+``T(0,0) += Nb * I``.  This is the same stream the reference's test helper
+``random_complex`` (``pkg/tests/helpers.py:14-15``) consumes, so
+``embed_2l(blocks, Ny, Nx, Nb)`` of the reference accepts the result unchanged.
+
+The blocks are returned directly in the reference's circulant storage order
+``stacked[p % (2Ny-1), q % (2Nx-1)]`` (``toeplitz.py:59-61,193-204``), which is
+what both the device operator and the oracle consume.  The whole stream is
+drawn in one call per level-2 offset: numpy's Generator fills arrays in C order,
+so one ``(2Nx-1, 2, Nb, Nb)`` draw equals the per-block re/im draws of the loop.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = [
+    "ConfigSpec",
+    "CONFIGS",
+    "seeded_stacked4",
+    "unit_feed_rhs",
+    "dense_rhs",
+    "BorderedSystem",
+    "system_from_generator",
+    "seeded_system",
+]
+
+
+@dataclass(frozen=True)
+class ConfigSpec:
+    name: str
+    ny: int
+    nx: int
+    nb: int
+    note: str = ""
+
+    @property
+    def dim(self) -> int:
+        return self.ny * self.nx * self.nb
+
+
+CONFIGS = {
+    "cfg1": ConfigSpec("cfg1", 4, 4, 32, "parity, GMRES(30) to 1e-8"),
+    "cfg2": ConfigSpec("cfg2", 30, 30, 128, "headline: matvec/s + GMRES(50) to 1e-8"),
+    "cfg3": ConfigSpec("cfg3", 30, 30, 256, "900 RHS multi-RHS GEMM"),
+    "cfg4": ConfigSpec("cfg4", 64, 64, 128, "large single RHS, c128 + c64"),
+    "cfg5": ConfigSpec("cfg5", 16, 16, 64, "block Rybicki direct solve, 4 RHS"),
+}
+
+
+def seeded_stacked4(ny: int, nx: int, nb: int, seed: int = 0, dtype=np.complex128) -> np.ndarray:
+    """(2ny-1, 2nx-1, nb, nb) blocks in circulant order from the BASELINE generator."""
+    k2, k1 = 2 * ny - 1, 2 * nx - 1
+    rng = np.random.default_rng(seed)
+    out = np.empty((k2, k1, nb, nb), dtype=dtype)
+    qs = np.arange(-(nx - 1), nx)
+    for p in range(-(ny - 1), ny):
+        draw = rng.standard_normal((k1, 2, nb, nb))
+        r = np.hypot(float(p), qs.astype(np.float64))
+        phase = np.exp(-1j * np.pi * r)[:, None, None]
+        row = (draw[:, 0] + 1j * draw[:, 1]) * phase / np.maximum(r, 1.0)[:, None, None]
+        out[p % k2, qs % k1] = row
+        del draw, row
+    out[0, 0] += nb * np.eye(nb)
+    return out
+
+
+def unit_feed_rhs(ny: int, nx: int, nb: int, columns: str = "sum") -> np.ndarray:
+    """Unit excitation of the first basis function of each element.
+
+    ``columns="sum"``: one column exciting every element (cfg1/cfg2/cfg4);
+    ``columns="each"``: one column per element c with a 1 at row c*nb (cfg3).
+    """
+    ne = ny * nx
+    if columns == "sum":
+        b = np.zeros(ne * nb, dtype=np.complex128)
+        b[::nb] = 1.0
+        return b
+    if columns == "each":
+        b = np.zeros((ne * nb, ne), dtype=np.complex128)
+        b[np.arange(ne) * nb, np.arange(ne)] = 1.0
+        return b
+    raise ValueError(columns)
+
+
+def dense_rhs(n: int, w: int | None = None, seed: int = 1) -> np.ndarray:
+    """Complex Gaussian vector / block from ``default_rng(seed)`` (re then im)."""
+    rng = np.random.default_rng(seed)
+    shape = (n,) if w is None else (n, w)
+    re = rng.standard_normal(shape)
+    im = rng.standard_normal(shape)
+    return re + 1j * im
+
+
+@dataclass(frozen=True)
+class BorderedSystem:
+    """Bordered array system ``[[Z_A, Z_B^T], [Z_B, Z_C]]`` (problems.py:60-77 of the reference).
+
+    ``gen`` is the generator of Z_A (a ``toeplitz.BlockGenerator2L``); ``zb`` is
+    (nb, array_dim), ``zc`` (nb, nb).  The BASELINE configurations have no
+    border (nb = 0); use ``system_from_generator``.
+    """
+
+    gen: object
+    zb: np.ndarray
+    zc: np.ndarray
+    spec: object = None
+
+    @property
+    def nb(self) -> int:
+        return int(self.zb.shape[0])
+
+    @property
+    def array_dim(self) -> int:
+        return int(self.gen.dim)
+
+    @property
+    def dim(self) -> int:
+        return self.array_dim + self.nb
+
+
+def system_from_generator(gen) -> BorderedSystem:
+    """Border-free system around a generator (nb = 0)."""
+    return BorderedSystem(gen, np.zeros((0, gen.dim), dtype=np.complex128), np.zeros((0, 0), dtype=np.complex128))
+
+
+def seeded_system(ny: int, nx: int, nb: int, seed: int = 0) -> BorderedSystem:
+    """BASELINE seeded generator wrapped as an nb = 0 system."""
+    from .toeplitz import generator_from_stacked
+
+    return system_from_generator(generator_from_stacked(seeded_stacked4(ny, nx, nb, seed)))

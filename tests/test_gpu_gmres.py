@@ -1,0 +1,178 @@
+"""Device GMRES parity: the reference's test_gmres.py / test_precond.py cases and
+iteration counts / residual histories recorded from the reference on the
+BASELINE configurations (tests/golden)."""
+
+import numpy as np
+import pytest
+import scipy.linalg
+import torch
+
+from conftest import golden, random_complex, rel_err
+from paper_2506_20350_b200.errors import NoConvergence, ShapeError
+from paper_2506_20350_b200.problems import seeded_stacked4, system_from_generator, unit_feed_rhs
+from paper_2506_20350_b200.solvers import (
+    BorderedOperator,
+    GmresConfig,
+    bordered_matvec,
+    build_pk,
+    gmres,
+    identity_preconditioner,
+    solve_multi_rhs_sequential,
+    solve_multi_rhs_vectorized,
+)
+from paper_2506_20350_b200.toeplitz import assemble_dense, embed_2l, generator_from_stacked
+
+pytestmark = pytest.mark.gpu
+
+
+def dense_op(a):
+    return lambda x: a @ x
+
+
+def monotone(h):
+    return all(h[i + 1] <= h[i] for i in range(len(h) - 1))
+
+
+class TestCore:
+    def test_identity_converges_first_iteration(self):
+        b = np.array([1.0, 2.0, -1j])
+        x, rep = gmres(dense_op(np.eye(3)), None, b, GmresConfig(tol=1e-12))
+        assert rep.iterations == 1
+        assert rel_err(x, b) <= 1e-14
+
+    def test_diagonal_two_step_exactness(self):
+        x, rep = gmres(dense_op(np.diag([1.0, 2.0])), None, np.array([1.0, 1.0]), GmresConfig(tol=1e-13))
+        assert rep.iterations <= 2
+        assert np.allclose(x, [1.0, 0.5], rtol=1e-12)
+
+    def test_zero_rhs_returns_zero(self):
+        x, rep = gmres(dense_op(np.eye(3)), None, np.zeros(3), GmresConfig(tol=1e-8))
+        assert not np.any(x) and rep.converged and rep.residual_history == [0.0]
+
+    def test_no_convergence_carries_report(self):
+        rng = np.random.default_rng(0)
+        a = random_complex(rng, 30, 30) + 2 * np.eye(30)
+        b = random_complex(rng, 30)
+        with pytest.raises(NoConvergence) as err:
+            gmres(dense_op(a), None, b, GmresConfig(tol=1e-14, max_iter=3))
+        assert err.value.report.iterations == 3
+        assert err.value.solution.shape == (30,)
+        assert monotone(err.value.report.residual_history)
+
+    def test_torch_dense_operator(self):
+        rng = np.random.default_rng(2)
+        a = random_complex(rng, 25, 25) + 3 * np.eye(25)
+        b = random_complex(rng, 25)
+        at = torch.from_numpy(a).cuda()
+        x, rep = gmres(lambda v: at @ v, None, torch.from_numpy(b).cuda(), GmresConfig(tol=1e-10, max_iter=100))
+        assert isinstance(x, torch.Tensor)
+        assert rep.residual_history[0] == 1.0 and monotone(rep.residual_history)
+        assert rel_err(a @ x.cpu().numpy(), b) <= 1e-9
+
+    def test_restarted_matches_oracle(self):
+        import oracle
+
+        rng = np.random.default_rng(3)
+        for shift, tol in ((20.0, 1e-9), (6.0, 1e-9)):
+            a = random_complex(rng, 40, 40) + shift * np.eye(40)
+            b = random_complex(rng, 40)
+            cfg = GmresConfig(tol=tol, max_iter=200, restart=5)
+            try:
+                x, rep = gmres(dense_op(a), None, b, cfg)
+            except NoConvergence as exc:  # the shift-6 case stagnates, as in the reference suite
+                x, rep = exc.solution, exc.report
+            xo, info = oracle.gmres(lambda v: a @ v, None, b, tol, 200, 5)
+            assert rep.converged == info["converged"]
+            assert abs(rep.iterations - info["iterations"]) <= 1
+            n = min(len(rep.residual_history), len(info["history"]))
+            assert np.allclose(rep.residual_history[:n], info["history"][:n], rtol=1e-6, atol=1e-12)
+            if info["converged"]:
+                assert rel_err(x, xo) <= 1e-7
+
+
+def _cfg1():
+    gen = generator_from_stacked(seeded_stacked4(4, 4, 32, seed=0))
+    sys_ = system_from_generator(gen)
+    return sys_, BorderedOperator.from_system(sys_), build_pk(sys_)
+
+
+class TestBaselineCfg1:
+    @pytest.mark.parametrize("tag", ["none", "pk"])
+    def test_iterations_and_history(self, tag):
+        g = golden("cfg1")
+        sys_, op, pk = _cfg1()
+        p = pk if tag == "pk" else None
+        b = unit_feed_rhs(4, 4, 32)
+        x, rep = solve_multi_rhs_vectorized(op, p, b[:, None], GmresConfig(tol=1e-8, restart=30))
+        want = int(g[f"gm_{tag}_iters"])
+        assert abs(rep.iterations - want) <= 1
+        n = min(len(rep.residual_history), len(g[f"gm_{tag}_hist"]))
+        assert np.allclose(rep.residual_history[:n], g[f"gm_{tag}_hist"][:n], rtol=1e-6, atol=1e-13)
+        assert rel_err(x[:, 0], g[f"gm_{tag}_x"]) <= 1e-7
+        assert rep.final_residual <= 1e-7
+
+    def test_callback_path_matches_native(self):
+        g = golden("cfg1")
+        sys_, op, pk = _cfg1()
+        b = unit_feed_rhs(4, 4, 32)
+        x, rep = gmres(lambda v: bordered_matvec(op, v), pk, b, GmresConfig(tol=1e-8, restart=30))
+        assert abs(rep.iterations - int(g["gm_pk_iters"])) <= 1
+        assert rel_err(x, g["gm_pk_x"]) <= 1e-7
+
+    def test_pk_vs_dense_blockdiag(self):
+        sys_, op, pk = _cfg1()
+        rng = np.random.default_rng(1)
+        v = random_complex(rng, sys_.dim, 3)
+        dense = scipy.linalg.block_diag(*([sys_.gen.block(0, 0)] * 16))
+        assert rel_err(pk.apply(v), np.linalg.solve(dense, v)) <= 1e-12
+        assert rel_err(pk.apply_adjoint(v), np.linalg.solve(dense.conj().T, v)) <= 1e-12
+        assert pk.stored_bytes == 32 * 32 * 16
+        assert np.array_equal(identity_preconditioner(10).apply(v[:10]), v[:10])
+        with pytest.raises(ShapeError):
+            pk.apply(np.ones(5))
+
+    def test_multi_rhs_vectorized_and_sequential(self):
+        sys_, op, pk = _cfg1()
+        rng = np.random.default_rng(4)
+        v = random_complex(rng, sys_.dim, 3)
+        cfg = GmresConfig(tol=1e-6, max_iter=300)
+        dense = assemble_dense(sys_.gen)
+        xv, rv = solve_multi_rhs_vectorized(op, pk, v, cfg)
+        per_col = np.linalg.norm(dense @ xv - v, axis=0) / np.linalg.norm(v, axis=0)
+        assert per_col.max() <= 1e-4
+        assert rv.memory_estimate["krylov"] == rv.iterations * 3 * sys_.dim * 16
+        xs, reps = solve_multi_rhs_sequential(op, pk, v, cfg)
+        assert len(reps) == 3
+        assert max(np.linalg.norm(xv - xs, axis=0) / np.linalg.norm(xs, axis=0)) <= 1e-4
+        with pytest.raises(NoConvergence) as err:
+            solve_multi_rhs_sequential(op, pk, v, GmresConfig(tol=1e-14, max_iter=2))
+        assert len(err.value.reports) == 3
+
+    def test_block_diagonal_system_one_iteration(self):
+        rng = np.random.default_rng(0)
+        ne = 3
+        r0 = random_complex(rng, ne, ne) + 2 * np.eye(ne)
+        blocks = {(o2, o1): r0 if (o2, o1) == (0, 0) else np.zeros((ne, ne)) for o2 in (-1, 0, 1) for o1 in (-1, 0, 1)}
+        sys_ = system_from_generator(embed_2l(blocks, 2, 2, ne))
+        op = BorderedOperator.from_system(sys_)
+        b = random_complex(rng, sys_.dim)
+        x, rep = gmres(lambda u: bordered_matvec(op, u), build_pk(sys_), b, GmresConfig(tol=1e-12))
+        assert rep.iterations == 1
+        assert rel_err(x, np.linalg.solve(scipy.linalg.block_diag(*[r0] * 4), b)) <= 1e-12
+
+
+@pytest.mark.slow
+class TestBaselineCfg2:
+    @pytest.mark.parametrize("tag", ["none", "pk"])
+    def test_iterations(self, tag):
+        g = golden("cfg2")
+        gen = generator_from_stacked(seeded_stacked4(30, 30, 128, seed=0))
+        sys_ = system_from_generator(gen)
+        op = BorderedOperator.from_system(sys_)
+        p = build_pk(sys_) if tag == "pk" else None
+        b = unit_feed_rhs(30, 30, 128)
+        x, rep = solve_multi_rhs_vectorized(op, p, b[:, None], GmresConfig(tol=1e-8, restart=50))
+        assert abs(rep.iterations - int(g[f"gm_{tag}_iters"])) <= 1
+        n = min(len(rep.residual_history), len(g[f"gm_{tag}_hist"]))
+        assert np.allclose(rep.residual_history[:n], g[f"gm_{tag}_hist"][:n], rtol=1e-5, atol=1e-12)
+        assert rel_err(x[::97, 0], g[f"gm_{tag}_x_sub"]) <= 1e-6

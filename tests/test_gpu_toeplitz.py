@@ -1,0 +1,220 @@
+"""Device MLFFT matvec / block DFT parity (the reference's test_toeplitz.py cases,
+plus the golden fixtures made by running the reference)."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import golden, random_complex, rel_err
+from paper_2506_20350_b200.errors import BlockShapeMismatch, MissingOffset, ShapeError
+from paper_2506_20350_b200.problems import dense_rhs, seeded_stacked4
+from paper_2506_20350_b200.toeplitz import (
+    assemble_dense,
+    block_fft_1l,
+    block_fft_2l,
+    embed_1l,
+    embed_2l,
+    extract_result,
+    generator_from_stacked,
+    matvec,
+    matvec_transpose,
+    pad_rhs,
+    precompute_spectral,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def random_generator(rng, n2, n1, n0, symmetric=False, diag_boost=0.0):
+    blocks = {}
+    for o2 in range(-(n2 - 1), n2):
+        for o1 in range(-(n1 - 1), n1):
+            blocks[(o2, o1)] = random_complex(rng, n0, n0)
+    if symmetric:
+        blocks[(0, 0)] = blocks[(0, 0)] + blocks[(0, 0)].T
+        for key in list(blocks):
+            if key > (0, 0):
+                blocks[(-key[0], -key[1])] = blocks[key].T.copy()
+    if diag_boost:
+        blocks[(0, 0)] = blocks[(0, 0)] + diag_boost * np.eye(n0)
+    return embed_2l(blocks, n2, n1, n0)
+
+
+def naive_dft(x, inverse=False):
+    x = np.asarray(x, dtype=np.complex128)
+    n = x.shape[0]
+    sign = 1 if inverse else -1
+    j, k = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    f = np.exp(sign * 2j * np.pi * j * k / n)
+    out = np.tensordot(f, x, axes=(1, 0))
+    return out / n if inverse else out
+
+
+def dft_matrix(n, inverse=False):
+    f = naive_dft(np.eye(n))
+    return np.conj(f) / n if inverse else f
+
+
+class TestBlockDft:
+    def test_scalar_blocks_match_naive_dft(self):
+        rng = np.random.default_rng(2)
+        for n in (1, 2, 7, 12, 13, 60):
+            x = random_complex(rng, n, 3)
+            assert rel_err(block_fft_1l(x, n0=1), naive_dft(x)) <= 1e-13
+            assert rel_err(block_fft_1l(x, n0=1, direction="inverse"), naive_dft(x, inverse=True)) <= 1e-13
+
+    def test_kronecker_identity_small_grids(self):
+        rng = np.random.default_rng(6)
+        for n2 in (1, 2, 3):
+            for n1 in (1, 2, 3):
+                for n0 in (1, 2):
+                    u = random_complex(rng, n2 * n1 * n0, 2)
+                    mat = np.kron(dft_matrix(n2), np.kron(dft_matrix(n1), np.eye(n0)))
+                    assert rel_err(block_fft_2l(u, n2, n1, n0), mat @ u) <= 1e-13
+                    inv = np.kron(dft_matrix(n2, True), np.kron(dft_matrix(n1, True), np.eye(n0)))
+                    assert rel_err(block_fft_2l(u, n2, n1, n0, "inverse"), inv @ u) <= 1e-13
+
+    def test_roundtrip_and_lengths(self):
+        rng = np.random.default_rng(7)
+        for (n2, n1) in ((3, 5), (60, 60), (128, 8), (7, 9)):
+            x = random_complex(rng, n2 * n1 * 2, 3)
+            back = block_fft_2l(block_fft_2l(x, n2, n1, 2), n2, n1, 2, direction="inverse")
+            assert rel_err(back, x) <= 1e-14
+            assert rel_err(block_fft_2l(x, n2, n1, 2), oracle.block_dft_2l(x, n2, n1, 2)) <= 1e-14
+
+    def test_errors(self):
+        with pytest.raises(ShapeError):
+            block_fft_2l(np.ones((11, 1)), 2, 3, 2)
+        with pytest.raises(ValueError):
+            block_fft_2l(np.ones((12, 1)), 2, 3, 2, direction="sideways")
+        with pytest.raises(ShapeError):
+            block_fft_1l(np.ones((7, 1)), n0=2)
+
+
+class TestPadExtract:
+    def test_layouts(self):
+        assert np.array_equal(pad_rhs(np.array([1.0, 2.0]), 1, 2, 1), [1, 2, 0])
+        assert np.array_equal(pad_rhs(np.array([1.0, 2.0, 3.0, 4.0]), 2, 2, 1), [1, 2, 0, 3, 4, 0, 0, 0, 0])
+        v = np.zeros(15)
+        v[[0, 1, 3, 4, 6, 7]] = np.arange(1, 7)
+        assert np.array_equal(extract_result(v, 3, 2, 1), np.arange(1, 7))
+
+    def test_roundtrip(self):
+        u = random_complex(np.random.default_rng(9), 3 * 4 * 2, 5)
+        assert np.array_equal(extract_result(pad_rhs(u, 3, 4, 2), 3, 4, 2), u)
+
+
+class TestMatvec:
+    def test_identity_generator(self):
+        n2, n1, n0 = 2, 3, 4
+        blocks = {(o2, o1): np.eye(n0) if (o2, o1) == (0, 0) else np.zeros((n0, n0))
+                  for o2 in range(-(n2 - 1), n2) for o1 in range(-(n1 - 1), n1)}
+        op = precompute_spectral(embed_2l(blocks, n2, n1, n0))
+        u = random_complex(np.random.default_rng(10), n2 * n1 * n0, 2)
+        assert rel_err(matvec(op, u), u) <= 1e-14
+
+    def test_single_cell_exact(self):
+        rng = np.random.default_rng(11)
+        r0 = random_complex(rng, 4, 4)
+        op = precompute_spectral(embed_2l({(0, 0): r0}, 1, 1, 4))
+        u = random_complex(rng, 4, 3)
+        assert rel_err(matvec(op, u), r0 @ u) <= 1e-15
+
+    def test_dense_oracle_symmetric_and_transpose(self):
+        rng = np.random.default_rng(13)
+        gen = random_generator(rng, 3, 3, 2, symmetric=True)
+        dense = assemble_dense(gen)
+        op = precompute_spectral(gen)
+        u = random_complex(rng, gen.dim, 2)
+        assert rel_err(matvec(op, u), dense @ u) <= 1e-12
+        gen = random_generator(rng, 3, 2, 3)
+        op = precompute_spectral(gen)
+        u = random_complex(rng, gen.dim, 2)
+        assert rel_err(matvec_transpose(op, u), assemble_dense(gen).T @ u) <= 1e-12
+
+    def test_linearity(self):
+        rng = np.random.default_rng(15)
+        gen = random_generator(rng, 2, 3, 2)
+        op = precompute_spectral(gen)
+        u, w = random_complex(rng, gen.dim), random_complex(rng, gen.dim)
+        a, b = 1.3 - 0.7j, -2.1 + 0.4j
+        assert rel_err(matvec(op, a * u + b * w), a * matvec(op, u) + b * matvec(op, w)) <= 1e-13
+
+    def test_multi_column_consistency(self):
+        rng = np.random.default_rng(16)
+        gen = random_generator(rng, 3, 4, 5)
+        op = precompute_spectral(gen)
+        for wcols in (2, 3, 6, 9, 17, 40):
+            u = random_complex(rng, gen.dim, wcols)
+            full = matvec(op, u)
+            cols = np.column_stack([matvec(op, u[:, c]) for c in range(wcols)])
+            assert rel_err(full, cols) <= 1e-14
+            assert rel_err(full, assemble_dense(gen) @ u) <= 1e-12
+
+    def test_golden_sweep_30_generators(self):
+        g = golden("sweep")
+        for i in range(30):
+            gen = generator_from_stacked(g[f"sweep{i}_gen"])
+            op = precompute_spectral(gen)
+            assert rel_err(matvec(op, g[f"sweep{i}_u"]), g[f"sweep{i}_out"]) <= 1e-12
+
+    def test_golden_small_transpose(self):
+        g = golden("small")
+        op = precompute_spectral(generator_from_stacked(seeded_stacked4(3, 4, 6, seed=5)))
+        assert rel_err(matvec(op, g["small_u"]), g["small_mv"]) <= 1e-13
+        assert rel_err(matvec_transpose(op, g["small_u"]), g["small_mvt"]) <= 1e-13
+
+    def test_golden_cfg1(self):
+        g = golden("cfg1")
+        op = precompute_spectral(generator_from_stacked(seeded_stacked4(4, 4, 32, seed=0)))
+        assert rel_err(matvec(op, g["u"]), g["mv"]) <= 1e-12
+
+    def test_torch_in_torch_out(self):
+        g = golden("cfg1")
+        op = precompute_spectral(generator_from_stacked(seeded_stacked4(4, 4, 32, seed=0)))
+        u = torch.from_numpy(g["u"]).cuda()
+        v = matvec(op, u)
+        assert isinstance(v, torch.Tensor) and v.is_cuda and v.shape == u.shape
+        assert rel_err(v.cpu().numpy(), g["mv"]) <= 1e-12
+
+    def test_shape_error(self):
+        gen = random_generator(np.random.default_rng(18), 2, 2, 2)
+        with pytest.raises(ShapeError):
+            matvec(precompute_spectral(gen), np.ones(5))
+
+    def test_embed_errors(self):
+        with pytest.raises(MissingOffset):
+            embed_1l({0: np.eye(1)}, n1=2, n0=1)
+        with pytest.raises(BlockShapeMismatch):
+            embed_1l({0: np.eye(3)}, n1=1, n0=2)
+
+    def test_complex64_variant(self):
+        g = golden("cfg1")
+        op = precompute_spectral(generator_from_stacked(seeded_stacked4(4, 4, 32, seed=0)), dtype=torch.complex64)
+        assert rel_err(matvec(op, g["u"]), g["mv"]) <= 1e-5
+        u32 = torch.from_numpy(g["u"]).to(torch.complex64).cuda()
+        assert rel_err(matvec(op, u32).cpu().numpy(), g["mv"]) <= 1e-5
+
+
+@pytest.mark.slow
+class TestBaselineConfigs:
+    def test_cfg2_matvec_vs_reference(self):
+        g = golden("cfg2")
+        op = precompute_spectral(generator_from_stacked(seeded_stacked4(30, 30, 128, seed=0)))
+        assert (op.l2, op.l1, op.bins) == (60, 60, 3600)
+        mv = matvec(op, dense_rhs(30 * 30 * 128, seed=1))
+        assert rel_err(mv[::97], g["mv_sub"]) <= 1e-12
+        assert abs(np.linalg.norm(mv) - g["mv_norm"]) / g["mv_norm"] <= 1e-12
+
+    def test_cfg4_matvec_c128_c64(self):
+        g = golden("cfg4")
+        gen = generator_from_stacked(seeded_stacked4(64, 64, 128, seed=0))
+        u = dense_rhs(64 * 64 * 128, seed=1)
+        op = precompute_spectral(gen)
+        assert (op.l2, op.l1) == (128, 128)
+        mv = matvec(op, u)
+        assert rel_err(mv[::97], g["mv_sub"]) <= 1e-12
+        del op
+        op32 = precompute_spectral(gen, dtype=torch.complex64)
+        assert rel_err(matvec(op32, u)[::97], g["mv_sub"]) <= 1e-5
