@@ -16,6 +16,8 @@
 #include <cstring>
 
 #include "kernels.cuh"
+#include "launch.cuh"
+#include "tma.cuh"
 
 namespace toep {
 
@@ -112,45 +114,6 @@ binprod_cm_kernel(const C<T>* __restrict__ DT, const C<T>* __restrict__ U, C<T>*
 // mbarriers (complete_tx).  Warps 0-7 consume: lane l owns rows m0 + l + 32 i, each warp
 // takes RB/8 rows j of every stage, no cross-lane reduction; the 8 warp partials meet in
 // shared memory once per item.  The memory pipeline never waits for the math.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
-constexpr int kTmaConsumerWarps = 8;
-constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
-
 template <typename T, int MT, int RB, int STAGES>
 struct TmaCfg {
   using Z = C<T>;
@@ -165,7 +128,13 @@ template <typename T, int MT, int RB, int STAGES>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 binprod_tma_kernel(const C<T>* __restrict__ DT, const C<T>* __restrict__ U, C<T>* __restrict__ V, int n0,
                    int mtiles, int64_t items, const int* stop) {
-  if (stop != nullptr && *stop != 0) return;
+  // PDL: D is constant, so without a stop flag the producer starts streaming D
+  // before the forward DFT kernel has drained; consumers wait for u_hat.
+  if (stop != nullptr) {
+    pdl_wait();
+    if (*stop != 0) return;
+  }
+  pdl_trigger();
   using Z = C<T>;
   using Cfg = TmaCfg<T, MT, RB, STAGES>;
   constexpr int MPL = MT / 32;
@@ -187,7 +156,7 @@ binprod_tma_kernel(const C<T>* __restrict__ DT, const C<T>* __restrict__ U, C<T>
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kTmaConsumerWarps);
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_init_fence();
   }
   __syncthreads();
 
@@ -219,6 +188,7 @@ binprod_tma_kernel(const C<T>* __restrict__ DT, const C<T>* __restrict__ U, C<T>
     return;
   }
   // ------------------------------------------------------ consumers
+  pdl_wait();
   int stage = 0;
   uint32_t phase = 0;
   for (int64_t it = i_begin; it < i_end; ++it) {
@@ -453,14 +423,15 @@ int binprod_variant() {
     if (std::strcmp(e, "simple") == 0) return 0;
     if (std::strcmp(e, "simple8") == 0) return 1;
     if (std::strcmp(e, "tma64") == 0) return 2;
+    if (std::strcmp(e, "tmafull4") == 0) return 4;
+    if (std::strcmp(e, "tmafull3") == 0) return 5;
     return 3;
   }();
   return v;
 }
 
-template <typename T, int MT>
+template <typename T, int MT, int STAGES = 6>
 int launch_tma(const void* DT, const void* U, void* V, int64_t K, int n0, const int* stop, cudaStream_t s) {
-  constexpr int STAGES = 6;
   constexpr int RB = 32768 / (MT * sizeof(C<T>));  // 32 KB per stage
   using Cfg = TmaCfg<T, MT, RB, STAGES>;
   auto kern = binprod_tma_kernel<T, MT, RB, STAGES>;
@@ -472,10 +443,8 @@ int launch_tma(const void* DT, const void* U, void* V, int64_t K, int n0, const 
   const int mtiles = n0 / MT;
   const int64_t items = K * mtiles;
   const int grid = static_cast<int>(std::min<int64_t>(items, sm_count()));
-  kern<<<grid, kTmaThreads, Cfg::kSmem, s>>>(static_cast<const C<T>*>(DT), static_cast<const C<T>*>(U),
-                                              static_cast<C<T>*>(V), n0, mtiles, items, stop);
-  TOEP_LAUNCHED();
-  return TOEP_OK;
+  return launch_k(kern, dim3(grid), dim3(kTmaThreads), Cfg::kSmem, s, static_cast<const C<T>*>(DT),
+                  static_cast<const C<T>*>(U), static_cast<C<T>*>(V), n0, mtiles, items, stop);
 }
 
 template <typename T>
@@ -505,6 +474,8 @@ int bin_product_t(const void* DT, const void* U, void* V, int64_t K, int n0, int
   if (w == 1) {
     const int var = binprod_variant();
     if (var == 3 && n0 == 128) return launch_tma<T, 128>(DT, U, V, K, n0, stop, s);
+    if (var == 4 && n0 == 128) return launch_tma<T, 128, 4>(DT, U, V, K, n0, stop, s);
+    if (var == 5 && n0 == 128) return launch_tma<T, 128, 3>(DT, U, V, K, n0, stop, s);
     if (var >= 2 && n0 % 64 == 0 && n0 <= 256) return launch_tma<T, 64>(DT, U, V, K, n0, stop, s);
     if (var == 1) return launch_cm<T, 1, 8>(DT, U, V, K, n0, w, stop, s);
     return launch_cm<T, 1>(DT, U, V, K, n0, w, stop, s);

@@ -11,6 +11,7 @@
 // stages ping-ponging between two shared buffers, and the last stage writes
 // straight to global memory with the crop and the 1/L scale fused.
 #include "kernels.cuh"
+#include "launch.cuh"
 
 namespace toep {
 
@@ -118,8 +119,130 @@ __device__ __forceinline__ void dispatch_stage(int R, const C<TC>* src, C<TC>* d
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Compile-time plans for the embedding lengths the BASELINE grids use (7, 32, 60, 128): every
+// index, stride and trip count is a constant.  The first stage reads its radix inputs straight
+// from global memory (zero padding fused, no staging copy), intermediate stages ping-pong in
+// shared memory, the last stage writes the cropped, scaled outputs.  Launched with PDL: the
+// twiddle table is built before griddepcontrol.wait, overlapping the predecessor's tail.
+template <int... Rs> struct PlanLen;
+template <> struct PlanLen<> { static constexpr int value = 1; };
+template <int R, int... Rest> struct PlanLen<R, Rest...> { static constexpr int value = R * PlanLen<Rest...>::value; };
+
+template <typename TI, typename TC, typename TO, int TIL, int L, int Ns, int R, int... Rest>
+__device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __restrict__ gin, C<TO>* __restrict__ gout,
+                                           C<TC>* __restrict__ src, C<TC>* __restrict__ dst,
+                                           const C<TC>* __restrict__ tw, int ncol, TC scale) {
+  using Z = C<TC>;
+  constexpr bool kFirst = (Ns == 1);
+  constexpr bool kLast = sizeof...(Rest) == 0;
+  constexpr int nb = L / R;
+  constexpr int tstep = L / (Ns * R);
+  Z wr[R];
+  if constexpr (R != 2 && R != 4) {
+#pragma unroll
+    for (int m = 0; m < R; ++m) wr[m] = tw[m * nb];
+  }
+  const int hi_start = L - a.n_hi;
+#pragma unroll 2
+  for (int e = threadIdx.x; e < nb * TIL; e += kThreads) {
+    const int j = e / TIL;
+    const int col = e % TIL;
+    const int k = j % Ns;
+    Z v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if constexpr (kFirst) {
+        const int slot = j + r * nb;
+        int row = -1;
+        if (slot < a.n_lo) row = slot;
+        else if (slot >= hi_start) row = a.n_lo + slot - hi_start;
+        v[r] = mk<TC>(0, 0);
+        if (row >= 0 && col < ncol) {
+          if (a.part_count == nullptr) {
+            v[r] = cvt<Z>(gin[row * a.in_sa + col]);
+          } else {
+            const int np = a.part_count[row];
+            for (int p = 0; p < np; ++p) v[r] = cadd(v[r], cvt<Z>(gin[row * a.in_sa + p * a.part_stride + col]));
+          }
+        }
+      } else {
+        v[r] = src[(j + r * nb) * TIL + col];
+      }
+    }
+    if constexpr (!kFirst) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[k * r * tstep]);
+    }
+    butterfly<Z, R>(v, wr, a.sign);
+    const int base = (j / Ns) * Ns * R + k;
+    if constexpr (!kLast) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) dst[(base + q * Ns) * TIL + col] = v[q];
+    } else {
+      if (col < ncol) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int idx = base + q * Ns;
+          if (idx < a.n_out) gout[idx * a.out_sa + col] = cvt<C<TO>>(cscale(v[q], scale));
+        }
+      }
+    }
+  }
+  if constexpr (!kLast) {
+    __syncthreads();
+    plan_stage<TI, TC, TO, TIL, L, Ns * R, Rest...>(a, gin, gout, dst, src, tw, ncol, scale);
+  }
+}
+
+template <typename TI, typename TC, typename TO, int TIL, int... Rs>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) fft_plan_kernel(PassArgs a, double two_over_L) {
+  using Z = C<TC>;
+  constexpr int L = PlanLen<Rs...>::value;
+  __shared__ __align__(16) Z tw[L];
+  __shared__ __align__(16) Z buf[2][L * TIL];
+  pdl_trigger();
+  for (int t = threadIdx.x; t < L; t += kThreads) {
+    TC s, c;
+    sincospi_t<TC>(static_cast<TC>(t * two_over_L), &s, &c);
+    tw[t] = mk<TC>(c, a.sign * s);
+  }
+  pdl_wait();
+  if (a.stop != nullptr && *a.stop != 0) return;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * TIL;
+  const int o = blockIdx.y;
+  const int ncol = static_cast<int>(std::min<int64_t>(TIL, a.inner - i0));
+  const C<TI>* in = static_cast<const C<TI>*>(a.in) + o * a.in_so + i0;
+  if (a.in_idx != nullptr) in += static_cast<int64_t>(*a.in_idx) * a.in_idx_stride;
+  C<TO>* out = static_cast<C<TO>*>(a.out) + o * a.out_so + i0;
+  if (a.out_idx != nullptr) out += static_cast<int64_t>(*a.out_idx) * a.out_idx_stride;
+  __syncthreads();  // twiddle table
+  plan_stage<TI, TC, TO, TIL, L, 1, Rs...>(a, in, out, buf[0], buf[1], tw, ncol, static_cast<TC>(a.scale));
+}
+
+template <typename TI, typename TC, typename TO, int TIL, int... Rs>
+int launch_plan(const PassArgs& a, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((a.inner + TIL - 1) / TIL), static_cast<unsigned>(a.outer));
+  return launch_k(fft_plan_kernel<TI, TC, TO, TIL, Rs...>, grid, dim3(kThreads), 0, s, a,
+                  2.0 / PlanLen<Rs...>::value);
+}
+
+// compile-time plan for L (7, 32, 60, 128), or -1
+template <typename TI, typename TC, typename TO>
+int try_plan(const PassArgs& a, cudaStream_t s) {
+  switch (a.L) {
+    case 60: if (a.inner >= 16) return launch_plan<TI, TC, TO, 16, 4, 3, 5>(a, s); break;
+    case 128: if (a.inner >= 8) return launch_plan<TI, TC, TO, 8, 4, 4, 4, 2>(a, s); break;
+    case 32: if (a.inner >= 32) return launch_plan<TI, TC, TO, 32, 4, 4, 2>(a, s); break;
+    case 64: if (a.inner >= 16) return launch_plan<TI, TC, TO, 16, 4, 4, 4>(a, s); break;
+    default: break;
+  }
+  return -1;
+}
+
 template <typename TI, typename TC, typename TO, int TIL>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) fft_pass_kernel(PassArgs a, Radices rad, double two_over_L) {
+  pdl_wait();
   if (a.stop != nullptr && *a.stop != 0) return;
   using Z = C<TC>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -182,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fft_pass_kernel(PassArgs
 // lengths such as the reference's 2n-1 = 59).  Same placement / crop contract.
 template <typename TI, typename TC, typename TO, int TIL>
 __global__ void __launch_bounds__(kThreads) dft_direct_kernel(PassArgs a, double two_over_L) {
+  pdl_wait();
   if (a.stop != nullptr && *a.stop != 0) return;
   using Z = C<TC>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -229,6 +353,10 @@ __global__ void __launch_bounds__(kThreads) dft_direct_kernel(PassArgs a, double
 
 template <typename TI, typename TC, typename TO>
 int launch(const PassArgs& a, const Radices& rad, bool direct, cudaStream_t s) {
+  if (!direct) {
+    const int rc = try_plan<TI, TC, TO>(a, s);
+    if (rc >= 0) return rc;
+  }
   const size_t es = sizeof(C<TC>);
   const int nbuf = direct ? 1 : 2;
   int til = 32;

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "launch.cuh"
 #include "op.h"
 
 namespace toep {
@@ -66,6 +67,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 __global__ void __launch_bounds__(kThreads)
 dots_partial_kernel(const double2* __restrict__ V, int64_t ld, int m, const double2* __restrict__ w, int64_t N,
                     double2* __restrict__ partial, const int* stop) {
+  pdl_wait();
+  pdl_trigger();
   if (stop != nullptr && *stop) return;
   __shared__ double2 red[kThreads / 32][kLG];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -100,6 +103,8 @@ dots_partial_kernel(const double2* __restrict__ V, int64_t ld, int m, const doub
 __global__ void __launch_bounds__(kThreads)
 dots_final_kernel(const double2* __restrict__ partial, int nblk, double2* __restrict__ h,
                   const double2* __restrict__ h1, double2* __restrict__ hcol, const int* stop) {
+  pdl_wait();
+  pdl_trigger();
   if (stop != nullptr && *stop) return;
   __shared__ double2 red[kThreads / 32];
   const int l = blockIdx.x;
@@ -121,6 +126,8 @@ dots_final_kernel(const double2* __restrict__ partial, int nblk, double2* __rest
 __global__ void __launch_bounds__(kThreads)
 update_kernel(const double2* __restrict__ V, int64_t ld, int m_max, const int* m_dev, const double2* __restrict__ h,
               bool neg_h, double2* __restrict__ w, int64_t N, double* __restrict__ norm_partial, const int* stop) {
+  pdl_wait();
+  pdl_trigger();
   if (stop != nullptr && *stop) return;
   extern __shared__ double2 hs[];
   __shared__ double red[kThreads / 32];
@@ -157,6 +164,8 @@ update_kernel(const double2* __restrict__ V, int64_t ld, int m_max, const int* m
 
 __global__ void __launch_bounds__(kThreads)
 norm2_partial_kernel(const double2* __restrict__ x, int64_t N, double* __restrict__ partial) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[kThreads / 32];
   double nrm = 0.0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < N;
@@ -183,6 +192,8 @@ __device__ double sum_partials_warp(const double* p, int n) {
 // out = a - b   (elementwise)
 __global__ void sub_kernel(const double2* __restrict__ a, const double2* __restrict__ b, double2* __restrict__ out,
                            int64_t N) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     out[i] = csub(a[i], b[i]);
@@ -191,6 +202,8 @@ __global__ void sub_kernel(const double2* __restrict__ a, const double2* __restr
 // out = x * (*scal)  unless *stop
 __global__ void scale_kernel(const double2* __restrict__ x, double2* __restrict__ out, const double* scal, int64_t N,
                              const int* stop) {
+  pdl_wait();
+  pdl_trigger();
   if (stop != nullptr && *stop) return;
   const double s = *scal;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
@@ -200,6 +213,8 @@ __global__ void scale_kernel(const double2* __restrict__ x, double2* __restrict_
 
 // beta0 = ||pb||; history[0]
 __global__ void init_kernel(GState* st, const double* partial, int nblk, double* hist) {
+  pdl_wait();
+  pdl_trigger();
   const double s = sum_partials_warp(partial, nblk);
   if (threadIdx.x == 0) {
     const double beta0 = sqrt(s);
@@ -217,6 +232,8 @@ __global__ void init_kernel(GState* st, const double* partial, int nblk, double*
 // cycle start (gmres.py:130-144): beta = ||z||, convergence test, g[0] = beta, inv = 1/beta
 __global__ void cycle_start_kernel(GState* st, const double* partial, int nblk, double tol, double2* g,
                                    HostFlags* hf) {
+  pdl_wait();
+  pdl_trigger();
   const double s = sum_partials_warp(partial, nblk);
   if (threadIdx.x == 0) {
     const double beta = sqrt(s);
@@ -240,6 +257,8 @@ __global__ void cycle_start_kernel(GState* st, const double* partial, int nblk, 
 __global__ void givens_kernel(GState* st, const double* norm_partial, int nblk, double2* rcols, int ldr, double* cs,
                               double2* sn, double2* g, double* hist, double tol, int max_total, int cycle_len,
                               HostFlags* hf) {
+  pdl_wait();
+  pdl_trigger();
   if (st->stop) return;
   const double hn2 = sum_partials_warp(norm_partial, nblk);
   if (threadIdx.x != 0) return;
@@ -302,6 +321,8 @@ __global__ void givens_kernel(GState* st, const double* norm_partial, int nblk, 
 
 // y = R^-1 g (gmres.py:193-204), R upper triangular from the rotated columns
 __global__ void backsub_kernel(const GState* st, const double2* rcols, int ldr, const double2* g, double2* y) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x != 0) return;
   const int m = st->m;
   for (int i = m - 1; i >= 0; --i) {
@@ -381,7 +402,8 @@ struct Engine {
     return TOEP_OK;
   }
   int norm2_partials(const void* x) {
-    norm2_partial_kernel<<<nblk, kThreads, 0, s>>>(static_cast<const double2*>(x), N, norm_partial);
+    TOEP_TRY(launch_k(norm2_partial_kernel, dim3(nblk), dim3(kThreads), 0, s, static_cast<const double2*>(x), N,
+                      norm_partial));
     TOEP_LAUNCHED();
     return TOEP_OK;
   }
@@ -548,7 +570,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     if (timed) mark(1, t0);
   }
   G_TRY(e.norm2_partials(zb));
-  init_kernel<<<1, 32, 0, s>>>(st, e.norm_partial, nblk, hist);
+  G_TRY(launch_k(init_kernel, dim3(1), dim3(32), 0, s, st, e.norm_partial, nblk, hist));
   GState hst{};
   if (cudaMemcpyAsync(&hst, st, sizeof(GState), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
       cudaStreamSynchronize(s) != cudaSuccess) {
@@ -586,9 +608,9 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       G_TRY(e.apply_a(x, tmp, nullptr));
       if (timed) t0 = mark(0, t0);
       if (p->precond == TOEP_PC_FOLDED) {
-        sub_kernel<<<grid1, kThreads, 0, s>>>(pb, tmp, w, N);  // P^-1 b - (P^-1 A) x
+        G_TRY(launch_k(sub_kernel, dim3(grid1), dim3(kThreads), 0, s, pb, tmp, w, N));  // P^-1 b - (P^-1 A) x
       } else {
-        sub_kernel<<<grid1, kThreads, 0, s>>>(b, tmp, w, N);
+        G_TRY(launch_k(sub_kernel, dim3(grid1), dim3(kThreads), 0, s, b, tmp, w, N));
         bool applied = false;
         G_TRY(e.apply_p(w, tmp, &applied, nullptr));
         if (applied) cudaMemcpyAsync(w, tmp, N * sizeof(double2), cudaMemcpyDeviceToDevice, s);
@@ -598,8 +620,8 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     }
     first = false;
     G_TRY(e.norm2_partials(z));
-    cycle_start_kernel<<<1, 32, 0, s>>>(st, e.norm_partial, nblk, cfg->tol, g, hf_dev);
-    scale_kernel<<<grid1, kThreads, 0, s>>>(z, V, &st->inv, N, stop_dev);
+    G_TRY(launch_k(cycle_start_kernel, dim3(1), dim3(32), 0, s, st, e.norm_partial, nblk, cfg->tol, g, hf_dev));
+    G_TRY(launch_k(scale_kernel, dim3(grid1), dim3(kThreads), 0, s, z, V, &st->inv, N, stop_dev));
     TOEP_LAUNCHED();
 
     // ---- Arnoldi steps (gmres.py:146-190)
@@ -616,16 +638,16 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       if (timed) t0 = mark(1, t0);
       const int m = j + 1;
       // CGS2 pass 1
-      dots_partial_kernel<<<nblk, kThreads, 0, s>>>(V, N, m, wv, N, e.dot_partial, stop_dev);
-      dots_final_kernel<<<m, kThreads, 0, s>>>(e.dot_partial, nblk, dots1, nullptr, nullptr, stop_dev);
-      update_kernel<<<grid1, kThreads, upd_smem, s>>>(V, N, m, nullptr, dots1, false, wv, N, nullptr, stop_dev);
+      G_TRY(launch_k(dots_partial_kernel, dim3(nblk), dim3(kThreads), 0, s, V, N, m, wv, N, e.dot_partial, stop_dev));
+      G_TRY(launch_k(dots_final_kernel, dim3(m), dim3(kThreads), 0, s, e.dot_partial, nblk, dots1, nullptr, nullptr, stop_dev));
+      G_TRY(launch_k(update_kernel, dim3(grid1), dim3(kThreads), upd_smem, s, V, N, m, nullptr, dots1, false, wv, N, nullptr, stop_dev));
       // CGS2 pass 2 (re-orthogonalisation), Hessenberg column = h1 + h2
-      dots_partial_kernel<<<nblk, kThreads, 0, s>>>(V, N, m, wv, N, e.dot_partial, stop_dev);
-      dots_final_kernel<<<m, kThreads, 0, s>>>(e.dot_partial, nblk, dots2, dots1, rcols + (int64_t)j * ldr, stop_dev);
-      update_kernel<<<nblk, kThreads, upd_smem, s>>>(V, N, m, nullptr, dots2, false, wv, N, e.norm_partial, stop_dev);
-      givens_kernel<<<1, 32, 0, s>>>(st, e.norm_partial, nblk, rcols, ldr, cs, sn, g, hist, cfg->tol,
-                                     static_cast<int>(max_total), cycle_len, hf_dev);
-      scale_kernel<<<grid1, kThreads, 0, s>>>(wv, V + static_cast<int64_t>(j + 1) * N, &st->inv, N, stop_dev);
+      G_TRY(launch_k(dots_partial_kernel, dim3(nblk), dim3(kThreads), 0, s, V, N, m, wv, N, e.dot_partial, stop_dev));
+      G_TRY(launch_k(dots_final_kernel, dim3(m), dim3(kThreads), 0, s, e.dot_partial, nblk, dots2, dots1, rcols + (int64_t)j * ldr, stop_dev));
+      G_TRY(launch_k(update_kernel, dim3(nblk), dim3(kThreads), upd_smem, s, V, N, m, nullptr, dots2, false, wv, N, e.norm_partial, stop_dev));
+      G_TRY(launch_k(givens_kernel, dim3(1), dim3(32), 0, s, st, e.norm_partial, nblk, rcols, ldr, cs, sn, g, hist, cfg->tol,
+                                     static_cast<int>(max_total), cycle_len, hf_dev));
+      G_TRY(launch_k(scale_kernel, dim3(grid1), dim3(kThreads), 0, s, wv, V + static_cast<int64_t>(j + 1) * N, &st->inv, N, stop_dev));
       TOEP_LAUNCHED();
       if (timed) mark(2, t0);
       cudaEvent_t ev = res.event();
@@ -639,8 +661,8 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     }
     tr.mark("arnoldi steps launched");
     // ---- assemble x += V y (gmres.py:192-204)
-    backsub_kernel<<<1, 32, 0, s>>>(st, rcols, ldr, g, y);
-    update_kernel<<<grid1, kThreads, upd_smem, s>>>(V, N, cycle_len, m_dev, y, true, x, N, nullptr, nullptr);
+    G_TRY(launch_k(backsub_kernel, dim3(1), dim3(32), 0, s, st, rcols, ldr, g, y));
+    G_TRY(launch_k(update_kernel, dim3(grid1), dim3(kThreads), upd_smem, s, V, N, cycle_len, m_dev, y, true, x, N, nullptr, nullptr));
     TOEP_LAUNCHED();
     if (cudaMemcpyAsync(&hst, st, sizeof(GState), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess) {
@@ -661,7 +683,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       cudaMemcpyAsync(tmp, w, N * sizeof(double2), cudaMemcpyDeviceToDevice, s);
     }
     if (timed) mark(0, t0);
-    sub_kernel<<<grid1, kThreads, 0, s>>>(b, tmp, w, N);
+    G_TRY(launch_k(sub_kernel, dim3(grid1), dim3(kThreads), 0, s, b, tmp, w, N));
   }
   const double rn = e.host_norm(w);
   const double bn = e.host_norm(b);

@@ -1,0 +1,53 @@
+// Kernel launch helper with Programmatic Dependent Launch (PDL).
+//
+// Every kernel of the matvec / GMRES chains is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization: the next kernel's CTAs
+// are scheduled while the previous grid drains, run their prologue, and block
+// in griddepcontrol.wait until the predecessor's memory is visible.  This
+// hides the ~2-4 us launch/ramp gap at each of the many kernel boundaries of
+// a 170 us matvec and of the short Arnoldi kernels.  TOEP_PDL=0 disables it.
+#pragma once
+
+#include <cstdlib>
+#include <cstring>
+#include <utility>
+
+#include "common.cuh"
+
+namespace toep {
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TOEP_PDL");
+    return !(e != nullptr && std::strcmp(e, "0") == 0);
+  }();
+  return on;
+}
+
+// Wait until the predecessor grid (PDL) has completed and its writes are visible.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Allow the dependent grid to start launching (its CTAs still pdl_wait for us).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(std::forward<Args>(args))...);
+  if (e != cudaSuccess) {
+    set_error("kernel launch failed: %s", cudaGetErrorString(e));
+    cudaGetLastError();
+    return TOEP_ERR_CUDA;
+  }
+  return TOEP_OK;
+}
+
+}  // namespace toep

@@ -86,6 +86,37 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
   const double sc1y = transpose ? 1.0 / op->l2 : 1.0, sc1x = transpose ? 1.0 / op->l1 : 1.0;
   const double sc2y = transpose ? 1.0 : 1.0 / op->l2, sc2x = transpose ? 1.0 : 1.0 / op->l1;
 
+  if (fused_eligible(op, w, transpose)) {
+    // level-1 pass -> fused (level-2 DFT + per-bin product + inverse level-2 DFT) -> inverse level-1 pass
+    TOEP_TRY(fused_prepare(op, s));
+    {
+      std::lock_guard<std::mutex> lock(op->mu);
+      if (ws->parts == nullptr) {
+        const size_t bytes = static_cast<size_t>(op->l1) * op->fused_maxp * op->n2 * op->n0 * elt_size(op->dtype);
+        if (cudaMallocAsync(&ws->parts, bytes, s) != cudaSuccess ||
+            cudaMallocAsync(reinterpret_cast<void**>(&ws->cnt), sizeof(int) * op->l1, s) != cudaSuccess) {
+          cudaGetLastError();
+          set_error("out of device memory for fused matvec workspace");
+          return TOEP_ERR_OOM;
+        }
+        TOEP_CUDA(cudaMemsetAsync(ws->cnt, 0, sizeof(int) * op->l1, s));
+      }
+    }
+    PassArgs a;
+    a.in = u; a.out = ws->x1; a.L = op->l1; a.n_lo = op->n1; a.n_hi = 0; a.n_out = op->l1;
+    a.inner = inner; a.outer = op->n2; a.in_sa = inner; a.in_so = op->n1 * inner; a.out_sa = inner;
+    a.out_so = op->l1 * inner; a.sign = -1; a.scale = 1.0; a.stop = stop;
+    TOEP_TRY(fft_pass(a, tio, tc, tc, s));
+    // X2 [n2][l1][n0] reuses the (otherwise idle) spectral workspace
+    TOEP_TRY(fused_spectral(op, ws->x1, ws->parts, ws->hat, ws->cnt, stop, s));
+    PassArgs d;  // inverse level-1 DFT of the combined columns, crop, 1/(l1 l2)
+    d.in = ws->hat; d.out = v; d.L = op->l1; d.n_lo = op->l1; d.n_hi = 0; d.n_out = op->n1;
+    d.inner = inner; d.outer = op->n2; d.in_sa = inner; d.in_so = op->l1 * inner;
+    d.out_sa = inner; d.out_so = op->n1 * inner; d.sign = +1; d.scale = 1.0 / (static_cast<double>(op->l1) * op->l2);
+    d.stop = stop;
+    return fft_pass(d, tc, tc, tio, s);
+  }
+
   PassArgs a;  // level-1 (x) pass: u [n2][n1][inner] -> x1 [n2][l1][inner]  (pad fused)
   a.in = u; a.out = ws->x1; a.L = op->l1; a.n_lo = op->n1; a.n_hi = 0; a.n_out = op->l1;
   a.inner = inner; a.outer = op->n2; a.in_sa = inner; a.in_so = op->n1 * inner; a.out_sa = inner;
@@ -247,8 +278,11 @@ int toep_op_destroy(toep_op_t op) {
     cudaFree(kv.second.x1);
     cudaFree(kv.second.hat);
     cudaFree(kv.second.hat2);
+    cudaFree(kv.second.parts);
+    cudaFree(kv.second.cnt);
   }
   cudaFree(op->DT);
+  cudaFree(op->part_count);
   delete op;
   TOEP_LAUNCHED();
   return TOEP_OK;

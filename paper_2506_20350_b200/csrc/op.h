@@ -16,7 +16,13 @@ struct toep_op_s {
     void* x1 = nullptr;    // [n2][l1][n0*w]
     void* hat = nullptr;   // [K][n0][w]
     void* hat2 = nullptr;  // [K][n0][w]
+    void* parts = nullptr; // fused path: [l1][maxp][n2][n0] inverse level-2 partial slabs
+    int* cnt = nullptr;    // fused path: [l1] slab arrival counters
   };
+  // fused single-RHS path (fused.cu): kx-major persistent partition
+  int fused_grid = 0;
+  int fused_maxp = 0;
+  int* part_count = nullptr;  // device [l1]
   std::mutex mu;
   std::map<cudaStream_t, Workspace> ws;
 };
@@ -33,6 +39,11 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
                 const int* stop, cudaStream_t s);
 
 void keep_pool();
+
+// fused.cu
+bool fused_eligible(const toep_op_s* op, int64_t w, bool transpose);
+int fused_prepare(toep_op_s* op, cudaStream_t s);
+int fused_spectral(toep_op_s* op, const void* x1, void* parts, void* x2, int* cnt, const int* stop, cudaStream_t s);
 
 int block_apply_impl(const void* m, int n0, const void* in, void* out, int64_t segments, int64_t w, int dtype,
                      cudaStream_t s, const int* stop);

@@ -1,0 +1,56 @@
+"""Summarise ncu reports into profiles/ (run in the build container)."""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__shared_mem_per_block_dynamic", "launch__grid_size", "launch__block_size",
+        "lts__t_sectors_srcunit_tex_op_read.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum"]
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {"kernel": r[hdr.index("Kernel Name")][:120]}
+        for k in KEYS:
+            if k in hdr:
+                d[k] = r[hdr.index(k)] + " " + units[hdr.index(k)]
+        res.append(d)
+    return res
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    out = []
+    for r in rows:
+        if "Kernel Name" in r:
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            if d.get("Metric Name") == "gpu__time_duration.sum":
+                out.append((d["Kernel Name"].split("(")[0][-60:], float(d["Metric Value"])))
+    agg = {}
+    for name, t in out:
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += t
+    total = sum(v[1] for v in agg.values())
+    return {"launches": len(out), "total_ns": total,
+            "by_kernel": {k: {"count": v[0], "sum_ns": v[1], "share": v[1] / total} for k, v in
+                          sorted(agg.items(), key=lambda kv: -kv[1][1])}}
+
+
+if __name__ == "__main__":
+    kind, src = sys.argv[1], sys.argv[2]
+    print(json.dumps(raw(src) if kind == "raw" else launches(src), indent=1))
