@@ -30,6 +30,11 @@ template <typename T> __device__ __forceinline__ void sincospi_t(T x, T* s, T* c
 template <> __device__ __forceinline__ void sincospi_t<double>(double x, double* s, double* c) { sincospi(x, s, c); }
 template <> __device__ __forceinline__ void sincospi_t<float>(float x, float* s, float* c) { sincospif(x, s, c); }
 
+// output scale of a pass; a device-side input scale (lazy GMRES normalisation) folds in by linearity
+template <typename T> __device__ __forceinline__ T pass_scale(const PassArgs& a) {
+  return static_cast<T>(a.in_scale != nullptr ? a.scale * *a.in_scale : a.scale);
+}
+
 template <typename Zd, typename Zs> __device__ __forceinline__ Zd cvt(Zs v) {
   Zd r;
   r.x = v.x;
@@ -217,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fft_plan_kernel(PassArgs
   C<TO>* out = static_cast<C<TO>*>(a.out) + o * a.out_so + i0;
   if (a.out_idx != nullptr) out += static_cast<int64_t>(*a.out_idx) * a.out_idx_stride;
   __syncthreads();  // twiddle table
-  plan_stage<TI, TC, TO, TIL, L, 1, Rs...>(a, in, out, buf[0], buf[1], tw, ncol, static_cast<TC>(a.scale));
+  plan_stage<TI, TC, TO, TIL, L, 1, Rs...>(a, in, out, buf[0], buf[1], tw, ncol, pass_scale<TC>(a));
 }
 
 template <typename TI, typename TC, typename TO, int TIL, int... Rs>
@@ -278,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fft_pass_kernel(PassArgs
   }
   __syncthreads();
 
-  const TC scale = static_cast<TC>(a.scale);
+  const TC scale = pass_scale<TC>(a);
   if (rad.n == 0) {  // L == 1
     if (threadIdx.x < ncol && a.n_out > 0) out[threadIdx.x] = cvt<C<TO>>(cscale(buf0[threadIdx.x], scale));
     return;
@@ -336,7 +341,7 @@ __global__ void __launch_bounds__(kThreads) dft_direct_kernel(PassArgs a, double
     buf[e] = v;
   }
   __syncthreads();
-  const TC scale = static_cast<TC>(a.scale);
+  const TC scale = pass_scale<TC>(a);
   for (int e = threadIdx.x; e < a.n_out * TIL; e += kThreads) {
     const int k = e / TIL;
     const int col = e - k * TIL;

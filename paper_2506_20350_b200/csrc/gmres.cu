@@ -8,17 +8,27 @@
 // exit residual is the unpreconditioned ||b - A x|| / ||b||.
 //
 // Orthogonalisation is classical Gram-Schmidt with one re-orthogonalisation
-// (CGS2): two passes of (V^H w, w -= V h), each a single coalesced sweep of the
-// resident basis instead of the reference's j sequential vdot/axpy pairs
+// (CGS2) instead of the reference's j sequential vdot/axpy pairs
 // (gmres.py:155-159); CGS2 keeps the basis orthogonal to working precision
-// like MGS does, so the Hessenberg entries agree to rounding.
+// like MGS, so Hessenberg entries and residual histories agree to rounding.
+//
+// Kernel chain of one Arnoldi step (all PDL-launched, all no-ops once the
+// device stop flag is set):
+//   matvec(v_j) -> V[j+1]                       (4-5 kernels, matvec_impl)
+//   k_dots      : partials of V_{0..j}^H w       (pass 1)
+//   k_upd       : h1 = reduce(partials) [every CTA, fixed order], w -= V h1,
+//                 partials of V^H w'             (pass 2)
+//   k_upd       : h2, w -= V h2, ||w||^2 partials, H[:, j] = h1 + h2
+//   k_givens    : ||w||, rotations, g, estimate, stop flags, scale of V[j+1]
+// The basis is stored unnormalised: v_l = vs[l] * V[l].  The 1/h_{j+1,j}
+// normalisation is a device scalar consumed by the next matvec's first DFT
+// pass and by the Gram-Schmidt kernels, so no kernel rescales the vector.
 //
 // Host/device split: every scalar (Hessenberg column, rotations, g, the
 // residual history, the stop flags) lives on the device.  The host only
 // launches; after launching step j it waits for step j-1 and reads the stop
 // flag from mapped pinned memory, so the launch queue stays one step ahead
-// and no step waits on a host round trip.  Steps launched past a stop are
-// no-ops (every step kernel checks the device stop flag).
+// and no step waits on a host round trip.
 #include <chrono>
 #include <cstdlib>
 #include <vector>
@@ -33,13 +43,13 @@ constexpr int kThreads = 256;
 constexpr int kLG = 8;  // basis vectors per accumulation group
 
 struct GState {
-  int stop;       // no further Arnoldi steps in this cycle
+  int stop;       // 0 running, 1 converged / breakdown, 2 cycle exhausted
   int converged;
   int breakdown;
   int m;          // completed steps in the current cycle
   int total;      // completed steps overall
   int nhist;
-  double beta0, beta, hnext, inv;
+  double beta0, beta, hnext;
 };
 
 struct HostFlags {
@@ -63,13 +73,23 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// partial[l * nblk + cta] = sum_{i in cta} conj(V[l][i]) w[i]   for l < m
-__global__ void __launch_bounds__(kThreads)
-dots_partial_kernel(const double2* __restrict__ V, int64_t ld, int m, const double2* __restrict__ w, int64_t N,
-                    double2* __restrict__ partial, const int* stop) {
-  pdl_wait();
-  pdl_trigger();
-  if (stop != nullptr && *stop) return;
+template <typename Z>
+__device__ __forceinline__ Z block_sum(Z v, Z* red /* [kThreads/32] */) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  Z t = red[0];
+#pragma unroll
+  for (int ww = 1; ww < kThreads / 32; ++ww) t = t + red[ww];
+  __syncthreads();
+  return t;
+}
+__device__ __forceinline__ double2 operator+(double2 a, double2 b) { return cadd(a, b); }
+
+// partial[l*nblk + cta] = sum_{i in cta} conj(V_l[i]) w[i], l < m
+__device__ __forceinline__ void dots_into(const double2* __restrict__ V, int64_t ld, int m,
+                                          const double2* __restrict__ w, int64_t N, double2* __restrict__ partial) {
   __shared__ double2 red[kThreads / 32][kLG];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nblk = gridDim.x;
@@ -99,40 +119,43 @@ dots_partial_kernel(const double2* __restrict__ V, int64_t ld, int m, const doub
   }
 }
 
-// h[l] = sum_b partial[l*nblk + b]; pass 2 also writes hcol[l] = h1[l] + h[l]
 __global__ void __launch_bounds__(kThreads)
-dots_final_kernel(const double2* __restrict__ partial, int nblk, double2* __restrict__ h,
-                  const double2* __restrict__ h1, double2* __restrict__ hcol, const int* stop) {
+k_dots(const double2* __restrict__ V, int64_t ld, int m, const double2* __restrict__ w, int64_t N,
+       double2* __restrict__ partial, const int* stop) {
   pdl_wait();
   pdl_trigger();
   if (stop != nullptr && *stop) return;
-  __shared__ double2 red[kThreads / 32];
-  const int l = blockIdx.x;
-  double2 s = make_double2(0, 0);
-  for (int b = threadIdx.x; b < nblk; b += kThreads) s = cadd(s, partial[l * nblk + b]);
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double2 t = red[0];
-    for (int ww = 1; ww < kThreads / 32; ++ww) t = cadd(t, red[ww]);
-    h[l] = t;
-    if (hcol != nullptr) hcol[l] = cadd(h1[l], t);
-  }
+  dots_into(V, ld, m, w, N, partial);
 }
 
-// w[i] -= sum_l V[l][i] h[l]  (l < m, m = min(m_max, *m_dev) when m_dev != null)
-// optionally norm2 partials of the result.  neg_h: use -h (x += V y with h = y).
+// Gram-Schmidt update:  h_l = vs_l * sum_b partial[l][b]  (reduced redundantly, same order, in every CTA)
+//   w -= sum_l V_l (vs_l h_l)
+// mode 1: partials of V^H w (next pass); hout[l] = h_l (CTA 0)
+// mode 2: ||w||^2 partials; hcol[l] = hprev[l] + h_l (CTA 0)
 __global__ void __launch_bounds__(kThreads)
-update_kernel(const double2* __restrict__ V, int64_t ld, int m_max, const int* m_dev, const double2* __restrict__ h,
-              bool neg_h, double2* __restrict__ w, int64_t N, double* __restrict__ norm_partial, const int* stop) {
+k_upd(const double2* __restrict__ V, int64_t ld, int m, const double* __restrict__ vs,
+      const double2* __restrict__ partial_in, int nblk_in, double2* __restrict__ w, int64_t N, int mode,
+      double2* __restrict__ hout, const double2* __restrict__ hprev, double2* __restrict__ partial_out,
+      double* __restrict__ norm_out, const int* stop) {
   pdl_wait();
   pdl_trigger();
   if (stop != nullptr && *stop) return;
-  extern __shared__ double2 hs[];
-  __shared__ double red[kThreads / 32];
-  const int m = (m_dev != nullptr) ? min(m_max, *m_dev) : m_max;
-  for (int l = threadIdx.x; l < m; l += kThreads) hs[l] = neg_h ? make_double2(-h[l].x, -h[l].y) : h[l];
+  extern __shared__ double2 coef[];  // [m]
+  __shared__ double red_n[kThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int l = warp; l < m; l += kThreads / 32) {
+    double2 s = make_double2(0, 0);
+    for (int b = lane; b < nblk_in; b += 32) s = cadd(s, partial_in[l * nblk_in + b]);
+    s = warp_sum(s);
+    if (lane == 0) {
+      const double2 h = cscale(s, vs[l]);
+      coef[l] = cscale(h, vs[l]);
+      if (blockIdx.x == 0) {
+        if (mode == 1) hout[l] = h;
+        else hout[l] = cadd(hprev[l], h);
+      }
+    }
+  }
   __syncthreads();
   double nrm = 0.0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < N;
@@ -141,29 +164,50 @@ update_kernel(const double2* __restrict__ V, int64_t ld, int m_max, const int* m
     int l = 0;
     for (; l + 3 < m; l += 4) {
       const double2 v0 = V[l * ld + i], v1 = V[(l + 1) * ld + i], v2 = V[(l + 2) * ld + i], v3 = V[(l + 3) * ld + i];
-      cfma(acc, v0, make_double2(-hs[l].x, -hs[l].y));
-      cfma(acc, v1, make_double2(-hs[l + 1].x, -hs[l + 1].y));
-      cfma(acc, v2, make_double2(-hs[l + 2].x, -hs[l + 2].y));
-      cfma(acc, v3, make_double2(-hs[l + 3].x, -hs[l + 3].y));
+      cfma(acc, v0, make_double2(-coef[l].x, -coef[l].y));
+      cfma(acc, v1, make_double2(-coef[l + 1].x, -coef[l + 1].y));
+      cfma(acc, v2, make_double2(-coef[l + 2].x, -coef[l + 2].y));
+      cfma(acc, v3, make_double2(-coef[l + 3].x, -coef[l + 3].y));
     }
-    for (; l < m; ++l) cfma(acc, V[l * ld + i], make_double2(-hs[l].x, -hs[l].y));
+    for (; l < m; ++l) cfma(acc, V[l * ld + i], make_double2(-coef[l].x, -coef[l].y));
     w[i] = acc;
     nrm = fma(acc.x, acc.x, fma(acc.y, acc.y, nrm));
   }
-  if (norm_partial != nullptr) {
+  if (mode == 1) {
+    __syncthreads();  // this CTA's w updates are its own elements: visible to itself after the barrier
+    dots_into(V, ld, m, w, N, partial_out);
+  } else {
     nrm = warp_sum(nrm);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+    if (lane == 0) red_n[warp] = nrm;
     __syncthreads();
     if (threadIdx.x == 0) {
-      double t = red[0];
-      for (int ww = 1; ww < kThreads / 32; ++ww) t += red[ww];
-      norm_partial[blockIdx.x] = t;
+      double t = red_n[0];
+      for (int ww = 1; ww < kThreads / 32; ++ww) t += red_n[ww];
+      norm_out[blockIdx.x] = t;
     }
   }
 }
 
+// x += sum_{l < m} V_l (vs_l y_l),  m = min(m_max, *m_dev)   (gmres.py:203-204)
 __global__ void __launch_bounds__(kThreads)
-norm2_partial_kernel(const double2* __restrict__ x, int64_t N, double* __restrict__ partial) {
+k_axpy_basis(const double2* __restrict__ V, int64_t ld, int m_max, const int* m_dev, const double* __restrict__ vs,
+             const double2* __restrict__ y, double2* __restrict__ x, int64_t N) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ double2 coef[];
+  const int m = min(m_max, *m_dev);
+  for (int l = threadIdx.x; l < m; l += kThreads) coef[l] = cscale(y[l], vs[l]);
+  __syncthreads();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < N;
+       i += static_cast<int64_t>(gridDim.x) * kThreads) {
+    double2 acc = x[i];
+    for (int l = 0; l < m; ++l) cfma(acc, V[l * ld + i], coef[l]);
+    x[i] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_norm2(const double2* __restrict__ x, int64_t N, double* __restrict__ partial) {
   pdl_wait();
   pdl_trigger();
   __shared__ double red[kThreads / 32];
@@ -173,14 +217,8 @@ norm2_partial_kernel(const double2* __restrict__ x, int64_t N, double* __restric
     const double2 v = x[i];
     nrm = fma(v.x, v.x, fma(v.y, v.y, nrm));
   }
-  nrm = warp_sum(nrm);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = red[0];
-    for (int ww = 1; ww < kThreads / 32; ++ww) t += red[ww];
-    partial[blockIdx.x] = t;
-  }
+  const double t = block_sum(nrm, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
 }
 
 __device__ double sum_partials_warp(const double* p, int n) {
@@ -189,9 +227,9 @@ __device__ double sum_partials_warp(const double* p, int n) {
   return warp_sum(s);
 }
 
-// out = a - b   (elementwise)
-__global__ void sub_kernel(const double2* __restrict__ a, const double2* __restrict__ b, double2* __restrict__ out,
-                           int64_t N) {
+// out = a - b
+__global__ void k_sub(const double2* __restrict__ a, const double2* __restrict__ b, double2* __restrict__ out,
+                      int64_t N) {
   pdl_wait();
   pdl_trigger();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
@@ -199,9 +237,9 @@ __global__ void sub_kernel(const double2* __restrict__ a, const double2* __restr
     out[i] = csub(a[i], b[i]);
 }
 
-// out = x * (*scal)  unless *stop
-__global__ void scale_kernel(const double2* __restrict__ x, double2* __restrict__ out, const double* scal, int64_t N,
-                             const int* stop) {
+// out = x * (*scal), unless *stop  (normalised copy for callback operators)
+__global__ void k_scale(const double2* __restrict__ x, double2* __restrict__ out, const double* scal, int64_t N,
+                        const int* stop) {
   pdl_wait();
   pdl_trigger();
   if (stop != nullptr && *stop) return;
@@ -211,8 +249,8 @@ __global__ void scale_kernel(const double2* __restrict__ x, double2* __restrict_
     out[i] = cscale(x[i], s);
 }
 
-// beta0 = ||pb||; history[0]
-__global__ void init_kernel(GState* st, const double* partial, int nblk, double* hist) {
+// beta0 = ||P^-1 b||; history[0]
+__global__ void k_init(GState* st, const double* partial, int nblk, double* hist) {
   pdl_wait();
   pdl_trigger();
   const double s = sum_partials_warp(partial, nblk);
@@ -229,9 +267,9 @@ __global__ void init_kernel(GState* st, const double* partial, int nblk, double*
   }
 }
 
-// cycle start (gmres.py:130-144): beta = ||z||, convergence test, g[0] = beta, inv = 1/beta
-__global__ void cycle_start_kernel(GState* st, const double* partial, int nblk, double tol, double2* g,
-                                   HostFlags* hf) {
+// cycle start (gmres.py:130-144): beta = ||z||, convergence test, g[0] = beta, vs[0] = 1/beta
+__global__ void k_cycle_start(GState* st, const double* partial, int nblk, double tol, double2* g, double* vs,
+                              HostFlags* hf) {
   pdl_wait();
   pdl_trigger();
   const double s = sum_partials_warp(partial, nblk);
@@ -245,7 +283,7 @@ __global__ void cycle_start_kernel(GState* st, const double* partial, int nblk, 
     } else {
       st->stop = 0;
       g[0] = make_double2(beta, 0.0);
-      st->inv = 1.0 / beta;
+      vs[0] = 1.0 / beta;
     }
     hf->stop = st->stop;
     hf->converged = st->converged;
@@ -254,9 +292,9 @@ __global__ void cycle_start_kernel(GState* st, const double* partial, int nblk, 
 }
 
 // one Givens step on column j = st->m (gmres.py:160-189)
-__global__ void givens_kernel(GState* st, const double* norm_partial, int nblk, double2* rcols, int ldr, double* cs,
-                              double2* sn, double2* g, double* hist, double tol, int max_total, int cycle_len,
-                              HostFlags* hf) {
+__global__ void k_givens(GState* st, const double* norm_partial, int nblk, double2* rcols, int ldr, double* cs,
+                         double2* sn, double2* g, double* hist, double* vs, double tol, int max_total, int cycle_len,
+                         HostFlags* hf) {
   pdl_wait();
   pdl_trigger();
   if (st->stop) return;
@@ -264,15 +302,13 @@ __global__ void givens_kernel(GState* st, const double* norm_partial, int nblk, 
   if (threadIdx.x != 0) return;
   const int j = st->m;
   const double hnext = sqrt(hn2);
-  double2* hcol = rcols + static_cast<int64_t>(j) * ldr;  // hcol[0..j] written by dots_final pass 2
+  double2* hcol = rcols + static_cast<int64_t>(j) * ldr;  // hcol[0..j] = h1 + h2 (k_upd mode 2)
   for (int i = 0; i < j; ++i) {
     const double2 a0 = hcol[i], a1 = hcol[i + 1];
     const double c = cs[i];
     const double2 s = sn[i];
-    const double2 t0 = cadd(cscale(a0, c), cmul(s, a1));
-    const double2 t1 = cadd(cscale(cmulc(s, a0), -1.0), cscale(a1, c));
-    hcol[i] = t0;
-    hcol[i + 1] = t1;
+    hcol[i] = cadd(cscale(a0, c), cmul(s, a1));
+    hcol[i + 1] = cadd(cscale(cmulc(s, a0), -1.0), cscale(a1, c));
   }
   // _givens(hcol[j], hnext) (gmres.py:87-95)
   const double2 a = hcol[j];
@@ -310,8 +346,8 @@ __global__ void givens_kernel(GState* st, const double* norm_partial, int nblk, 
     st->breakdown = 1;
     st->stop = 1;
   } else {
-    st->inv = 1.0 / hnext;
-    if (st->m >= cycle_len || st->total >= max_total) st->stop = 2;  // cycle exhausted, basis not needed
+    vs[j + 1] = 1.0 / hnext;  // v_{j+1} = w / h_{j+1,j}, applied lazily
+    if (st->m >= cycle_len || st->total >= max_total) st->stop = 2;
   }
   hf->stop = st->stop;
   hf->total = st->total;
@@ -320,7 +356,7 @@ __global__ void givens_kernel(GState* st, const double* norm_partial, int nblk, 
 }
 
 // y = R^-1 g (gmres.py:193-204), R upper triangular from the rotated columns
-__global__ void backsub_kernel(const GState* st, const double2* rcols, int ldr, const double2* g, double2* y) {
+__global__ void k_backsub(const GState* st, const double2* rcols, int ldr, const double2* g, double2* y) {
   pdl_wait();
   pdl_trigger();
   if (threadIdx.x != 0) return;
@@ -333,7 +369,6 @@ __global__ void backsub_kernel(const GState* st, const double2* rcols, int ldr, 
     }
     double2 acc = g[i];
     for (int k = i + 1; k < m; ++k) acc = csub(acc, cmul(rcols[static_cast<int64_t>(k) * ldr + i], y[k]));
-    // acc / d
     const double den = d.x * d.x + d.y * d.y;
     y[i] = make_double2((acc.x * d.x + acc.y * d.y) / den, (acc.y * d.x - acc.x * d.y) / den);
   }
@@ -341,7 +376,7 @@ __global__ void backsub_kernel(const GState* st, const double2* rcols, int ldr, 
 
 // Per-thread host resources reused across solves: the mapped pinned flag word
 // the device writes and a pool of CUDA events (creating / freeing these per
-// solve cost milliseconds of host time).
+// solve costs milliseconds of host time).
 struct HostRes {
   HostFlags* hf = nullptr;
   HostFlags* hf_dev = nullptr;
@@ -370,44 +405,74 @@ HostRes& host_res() {
   return r;
 }
 
+// TOEP_TRACE=1: host-side timeline of a solve on stderr (launch / wait split)
+struct Trace {
+  using clk = std::chrono::steady_clock;
+  bool on = std::getenv("TOEP_TRACE") != nullptr;
+  clk::time_point t0 = clk::now(), last = t0;
+  double wait = 0.0;
+  double launch_us_sum = 0.0, launch_us_max = 0.0;
+  int steps = 0;
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = clk::now();
+    std::fprintf(stderr, "[toep_gmres] %-28s +%9.3f ms (t=%9.3f ms, waited %8.3f ms, step launch mean %.1f max %.1f us)\n",
+                 what, std::chrono::duration<double, std::milli>(now - last).count(),
+                 std::chrono::duration<double, std::milli>(now - t0).count(), wait,
+                 steps ? launch_us_sum / steps : 0.0, launch_us_max);
+    last = now;
+  }
+  // spin on the event: cudaEventSynchronize may yield the thread and wake it up
+  // hundreds of microseconds late, which starves the launch queue
+  void sync_event(cudaEvent_t ev) {
+    const auto a = clk::now();
+    while (cudaEventQuery(ev) == cudaErrorNotReady) {
+    }
+    if (on) wait += std::chrono::duration<double, std::milli>(clk::now() - a).count();
+  }
+};
+
 struct Engine {
   const toep_gmres_problem_t* p;
   cudaStream_t s;
   int64_t N;
   int nblk;
   double* norm_partial = nullptr;
-  double2* dot_partial = nullptr;
+  double2* tmp2 = nullptr;  // normalised copy for callback operators
 
-  int apply_a(const void* x, void* y, const int* stop) {
+  // y = A (scale * x); scale: optional device scalar
+  int apply_a(const double2* x, const double* scale, double2* y, const int* stop) {
     if (p->op != nullptr) {
       const bool io = p->op->dtype == TOEP_C64;
-      return matvec_impl(p->op, x, y, p->w, false, io, stop, s);
+      return matvec_impl(p->op, x, y, p->w, false, io, stop, s, scale);
     }
-    const int rc = p->apply(p->apply_ctx, x, y, p->w, s);
+    const double2* xin = x;
+    if (scale != nullptr) {
+      TOEP_TRY(launch_k(k_scale, dim3(grid1()), dim3(kThreads), 0, s, x, tmp2, scale, N, stop));
+      xin = tmp2;
+    }
+    const int rc = p->apply(p->apply_ctx, xin, y, p->w, s);
     TOEP_REQUIRE(rc == 0, TOEP_ERR_ARG, "operator callback failed (%d)", rc);
     return TOEP_OK;
   }
-  // z = P^-1 x for the per-step preconditioner (BLOCK / CALLBACK); NONE/FOLDED: no-op
-  int apply_p(const void* x, void* z, bool* applied, const int* stop) {
-    *applied = false;
-    if (p->precond == TOEP_PC_BLOCK) {
-      *applied = true;
+  bool precond_per_step() const { return p->precond == TOEP_PC_BLOCK || p->precond == TOEP_PC_CALLBACK; }
+  // z = P^-1 x (BLOCK / CALLBACK)
+  int apply_p(const double2* x, double2* z, const int* stop) {
+    if (p->precond == TOEP_PC_BLOCK)
       return block_apply_impl(p->pinv, p->pside, x, z, p->n / p->pside, p->w, TOEP_C128, s, stop);
-    }
     if (p->precond == TOEP_PC_CALLBACK) {
-      *applied = true;
       const int rc = p->papply(p->papply_ctx, x, z, p->w, s);
       TOEP_REQUIRE(rc == 0, TOEP_ERR_ARG, "preconditioner callback failed (%d)", rc);
+      return TOEP_OK;
     }
-    return TOEP_OK;
+    set_error("no per-step preconditioner");
+    return TOEP_ERR_ARG;
   }
-  int norm2_partials(const void* x) {
-    TOEP_TRY(launch_k(norm2_partial_kernel, dim3(nblk), dim3(kThreads), 0, s, static_cast<const double2*>(x), N,
-                      norm_partial));
-    TOEP_LAUNCHED();
-    return TOEP_OK;
+  int grid1() const { return static_cast<int>(std::min<int64_t>((N + kThreads - 1) / kThreads, 4 * 148)); }
+  int norm2_partials(const double2* x) {
+    return launch_k(k_norm2, dim3(nblk), dim3(kThreads), 0, s, x, N, norm_partial);
   }
-  double host_norm(const void* x) {
+  double host_norm(const double2* x) {
     std::vector<double> h(nblk);
     if (norm2_partials(x) != TOEP_OK) return -1.0;
     cudaMemcpyAsync(h.data(), norm_partial, nblk * sizeof(double), cudaMemcpyDeviceToHost, s);
@@ -415,27 +480,6 @@ struct Engine {
     double t = 0.0;
     for (double v : h) t += v;
     return std::sqrt(t);
-  }
-};
-
-// TOEP_TRACE=1: host-side timeline of a solve on stderr (launch / wait split)
-struct Trace {
-  using clk = std::chrono::steady_clock;
-  bool on = std::getenv("TOEP_TRACE") != nullptr;
-  clk::time_point t0 = clk::now(), last = t0;
-  double wait = 0.0;
-  void mark(const char* what) {
-    if (!on) return;
-    const auto now = clk::now();
-    std::fprintf(stderr, "[toep_gmres] %-28s +%9.3f ms (t=%9.3f ms, waited %8.3f ms)\n", what,
-                 std::chrono::duration<double, std::milli>(now - last).count(),
-                 std::chrono::duration<double, std::milli>(now - t0).count(), wait);
-    last = now;
-  }
-  void sync_event(cudaEvent_t ev) {
-    const auto a = clk::now();
-    cudaEventSynchronize(ev);
-    wait += std::chrono::duration<double, std::milli>(clk::now() - a).count();
   }
 };
 
@@ -450,13 +494,15 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   TOEP_REQUIRE(cfg->restart >= 0, TOEP_ERR_ARG, "restart must be >= 1 or 0 (none)");
   TOEP_REQUIRE(p->op != nullptr || p->apply != nullptr, TOEP_ERR_ARG, "no operator");
   TOEP_REQUIRE(p->n >= 1 && p->w >= 1, TOEP_ERR_SHAPE, "empty system");
-  if (p->op != nullptr) TOEP_REQUIRE(op_dim(p->op) == p->n, TOEP_ERR_SHAPE, "rhs rows %lld != operator dim %lld",
-                                     (long long)p->n, (long long)op_dim(p->op));
+  if (p->op != nullptr)
+    TOEP_REQUIRE(op_dim(p->op) == p->n, TOEP_ERR_SHAPE, "rhs rows %lld != operator dim %lld", (long long)p->n,
+                 (long long)op_dim(p->op));
   if (p->precond == TOEP_PC_BLOCK || p->precond == TOEP_PC_FOLDED)
     TOEP_REQUIRE(p->pinv != nullptr && p->pside >= 1 && (p->n % p->pside) == 0, TOEP_ERR_SHAPE,
                  "preconditioner side does not divide n");
-  if (p->precond == TOEP_PC_FOLDED) TOEP_REQUIRE(p->pmat != nullptr && p->op != nullptr, TOEP_ERR_ARG,
-                                                 "folded preconditioner needs op and pmat");
+  if (p->precond == TOEP_PC_FOLDED)
+    TOEP_REQUIRE(p->pmat != nullptr && p->op != nullptr, TOEP_ERR_ARG, "folded preconditioner needs op and pmat");
+  if (p->precond == TOEP_PC_CALLBACK) TOEP_REQUIRE(p->papply != nullptr, TOEP_ERR_ARG, "no preconditioner callback");
 
   Engine e{p, s, p->n * p->w, 0};
   int sms = 148;
@@ -465,17 +511,17 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  e.nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((e.N + kThreads - 1) / kThreads, 2 * sms)));
+  e.nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((e.N + kThreads - 1) / kThreads, sms)));
   const int64_t N = e.N;
   const int64_t max_total = std::min<int64_t>(cfg->max_iter, N);
   const int cycle_len = static_cast<int>(cfg->restart == 0 ? max_total : std::min<int64_t>(cfg->restart, max_total));
   const int ldr = cycle_len + 1;
   const int nblk = e.nblk;
+  const int grid1 = e.grid1();
 
-  // device allocations (stream ordered)
-  double2 *V = nullptr, *w = nullptr, *tmp = nullptr, *pb = nullptr, *dots1 = nullptr, *dots2 = nullptr;
-  double2 *rcols = nullptr, *sn = nullptr, *g = nullptr, *y = nullptr;
-  double *cs = nullptr, *hist = nullptr;
+  double2 *V = nullptr, *tmp = nullptr, *tmp2 = nullptr, *pb = nullptr, *h1 = nullptr;
+  double2 *rcols = nullptr, *sn = nullptr, *g = nullptr, *y = nullptr, *part1 = nullptr, *part2 = nullptr;
+  double *cs = nullptr, *hist = nullptr, *vs = nullptr;
   GState* st = nullptr;
   HostRes& res = host_res();
   res.used = 0;
@@ -483,46 +529,48 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   HostFlags* hf_dev = res.hf_dev;
   int rc = TOEP_OK;
   auto cleanup = [&]() {
-    for (void* q : {(void*)V, (void*)w, (void*)tmp, (void*)pb, (void*)dots1, (void*)dots2, (void*)rcols, (void*)sn,
-                    (void*)g, (void*)y, (void*)cs, (void*)hist, (void*)st, (void*)e.norm_partial,
-                    (void*)e.dot_partial})
+    for (void* q : {(void*)V, (void*)tmp, (void*)tmp2, (void*)pb, (void*)h1, (void*)rcols, (void*)sn, (void*)g,
+                    (void*)y, (void*)part1, (void*)part2, (void*)cs, (void*)hist, (void*)vs, (void*)st,
+                    (void*)e.norm_partial})
       if (q) cudaFreeAsync(q, s);
     cudaStreamSynchronize(s);
     res.used = 0;
   };
   TOEP_REQUIRE(hf != nullptr, TOEP_ERR_OOM, "pinned allocation failed");
-#define G_ALLOC(ptr, count)                                                                   \
-  do {                                                                                        \
+#define G_ALLOC(ptr, count)                                                                                      \
+  do {                                                                                                           \
     if (cudaMallocAsync(reinterpret_cast<void**>(&(ptr)), sizeof(*(ptr)) * (size_t)(count), s) != cudaSuccess) { \
-      cudaGetLastError();                                                                     \
-      set_error("out of device memory in gmres");                                             \
-      cleanup();                                                                              \
-      return TOEP_ERR_OOM;                                                                    \
-    }                                                                                         \
+      cudaGetLastError();                                                                                        \
+      set_error("out of device memory in gmres");                                                                \
+      cleanup();                                                                                                 \
+      return TOEP_ERR_OOM;                                                                                       \
+    }                                                                                                            \
   } while (0)
-#define G_TRY(expr)          \
-  do {                       \
-    rc = (expr);             \
-    if (rc != TOEP_OK) {     \
-      cleanup();             \
-      return rc;             \
-    }                        \
+#define G_TRY(expr)      \
+  do {                   \
+    rc = (expr);         \
+    if (rc != TOEP_OK) { \
+      cleanup();         \
+      return rc;         \
+    }                    \
   } while (0)
   G_ALLOC(V, (int64_t)(cycle_len + 1) * N);
-  G_ALLOC(w, N);
   G_ALLOC(tmp, N);
   G_ALLOC(pb, N);
-  G_ALLOC(dots1, ldr);
-  G_ALLOC(dots2, ldr);
+  G_ALLOC(tmp2, N);
+  e.tmp2 = tmp2;
+  G_ALLOC(h1, ldr);
   G_ALLOC(rcols, (int64_t)cycle_len * ldr);
   G_ALLOC(sn, cycle_len + 1);
   G_ALLOC(g, cycle_len + 2);
   G_ALLOC(y, cycle_len + 1);
   G_ALLOC(cs, cycle_len + 1);
+  G_ALLOC(vs, cycle_len + 2);
   G_ALLOC(hist, max_total + 2);
   G_ALLOC(st, 1);
   G_ALLOC(e.norm_partial, nblk);
-  G_ALLOC(e.dot_partial, (int64_t)nblk * ldr);
+  G_ALLOC(part1, (int64_t)nblk * ldr);
+  G_ALLOC(part2, (int64_t)nblk * ldr);
   hf->stop = 0;
   hf->total = 0;
   hf->converged = 0;
@@ -530,27 +578,24 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   tr.mark("allocations");
 
   const bool timed = cfg->timings != 0;
-  auto new_event = [&](cudaEvent_t* ev) { *ev = res.event(); };
   struct Phase { cudaEvent_t a, b; int kind; };
   std::vector<Phase> phases;
   auto mark = [&](int kind, cudaEvent_t a) {
-    cudaEvent_t bb;
-    new_event(&bb);
+    cudaEvent_t bb = res.event();
     cudaEventRecord(bb, s);
     phases.push_back({a, bb, kind});
     return bb;
   };
   auto start_mark = [&]() {
-    cudaEvent_t a;
-    new_event(&a);
+    cudaEvent_t a = res.event();
     cudaEventRecord(a, s);
     return a;
   };
-
-  const int grid1 = std::min<int64_t>((N + kThreads - 1) / kThreads, 4 * sms);
-  const size_t upd_smem = sizeof(double2) * ldr;
-  if (upd_smem > 48 * 1024)
-    cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem);
+  const size_t coef_smem = sizeof(double2) * ldr;
+  if (coef_smem > 48 * 1024) {
+    cudaFuncSetAttribute(k_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coef_smem);
+    cudaFuncSetAttribute(k_axpy_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coef_smem);
+  }
 
   // ---- P^-1 b, beta0 (gmres.py:104-113)
   const double2* zb = b;
@@ -560,17 +605,13 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       G_TRY(block_apply_impl(p->pinv, p->pside, b, pb, p->n / p->pside, p->w, TOEP_C128, s, nullptr));
       zb = pb;
     } else if (p->precond == TOEP_PC_CALLBACK) {
-      if (p->papply(p->papply_ctx, b, pb, p->w, s) != 0) {
-        set_error("preconditioner callback failed");
-        cleanup();
-        return TOEP_ERR_ARG;
-      }
+      G_TRY(e.apply_p(b, pb, nullptr));
       zb = pb;
     }
     if (timed) mark(1, t0);
   }
   G_TRY(e.norm2_partials(zb));
-  G_TRY(launch_k(init_kernel, dim3(1), dim3(32), 0, s, st, e.norm_partial, nblk, hist));
+  G_TRY(launch_k(k_init, dim3(1), dim3(32), 0, s, st, e.norm_partial, nblk, hist));
   GState hst{};
   if (cudaMemcpyAsync(&hst, st, sizeof(GState), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
       cudaStreamSynchronize(s) != cudaSuccess) {
@@ -601,69 +642,81 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   bool first = true;
   std::vector<cudaEvent_t> step_ev;
   while (true) {
-    // ---- cycle start (gmres.py:123-144)
-    const double2* z = zb;
+    // ---- cycle start (gmres.py:123-144): V[0] = P^-1 (b - A x), vs[0] = 1 / ||.||
+    double2* v0 = V;
     if (!first) {
       cudaEvent_t t0 = timed ? start_mark() : nullptr;
-      G_TRY(e.apply_a(x, tmp, nullptr));
+      G_TRY(e.apply_a(x, nullptr, tmp, nullptr));
       if (timed) t0 = mark(0, t0);
       if (p->precond == TOEP_PC_FOLDED) {
-        G_TRY(launch_k(sub_kernel, dim3(grid1), dim3(kThreads), 0, s, pb, tmp, w, N));  // P^-1 b - (P^-1 A) x
+        G_TRY(launch_k(k_sub, dim3(grid1), dim3(kThreads), 0, s, (const double2*)pb, (const double2*)tmp, v0, N));
+      } else if (e.precond_per_step()) {
+        G_TRY(launch_k(k_sub, dim3(grid1), dim3(kThreads), 0, s, b, (const double2*)tmp, tmp2, N));
+        G_TRY(e.apply_p(tmp2, v0, nullptr));
       } else {
-        G_TRY(launch_k(sub_kernel, dim3(grid1), dim3(kThreads), 0, s, b, tmp, w, N));
-        bool applied = false;
-        G_TRY(e.apply_p(w, tmp, &applied, nullptr));
-        if (applied) cudaMemcpyAsync(w, tmp, N * sizeof(double2), cudaMemcpyDeviceToDevice, s);
+        G_TRY(launch_k(k_sub, dim3(grid1), dim3(kThreads), 0, s, b, (const double2*)tmp, v0, N));
       }
       if (timed) mark(1, t0);
-      z = w;
+    } else {
+      cudaMemcpyAsync(v0, zb, N * sizeof(double2), cudaMemcpyDeviceToDevice, s);
     }
     first = false;
-    G_TRY(e.norm2_partials(z));
-    G_TRY(launch_k(cycle_start_kernel, dim3(1), dim3(32), 0, s, st, e.norm_partial, nblk, cfg->tol, g, hf_dev));
-    G_TRY(launch_k(scale_kernel, dim3(grid1), dim3(kThreads), 0, s, z, V, &st->inv, N, stop_dev));
-    TOEP_LAUNCHED();
+    G_TRY(e.norm2_partials(v0));
+    G_TRY(launch_k(k_cycle_start, dim3(1), dim3(32), 0, s, st, (const double*)e.norm_partial, nblk, cfg->tol, g, vs,
+                   hf_dev));
 
     // ---- Arnoldi steps (gmres.py:146-190)
     int j = 0;
     step_ev.clear();
     while (j < cycle_len && total + j < max_total) {
+      const auto t_launch0 = clk::now();
       const double2* vj = V + static_cast<int64_t>(j) * N;
+      double2* w = V + static_cast<int64_t>(j + 1) * N;  // unnormalised v_{j+1} is built in place
       cudaEvent_t t0 = timed ? start_mark() : nullptr;
-      G_TRY(e.apply_a(vj, w, stop_dev));
-      if (timed) t0 = mark(0, t0);
-      bool applied = false;
-      G_TRY(e.apply_p(w, tmp, &applied, stop_dev));
-      double2* wv = applied ? tmp : w;
-      if (timed) t0 = mark(1, t0);
+      if (e.precond_per_step()) {
+        G_TRY(e.apply_a(vj, vs + j, tmp, stop_dev));
+        if (timed) t0 = mark(0, t0);
+        G_TRY(e.apply_p(tmp, w, stop_dev));
+        if (timed) t0 = mark(1, t0);
+      } else {
+        G_TRY(e.apply_a(vj, vs + j, w, stop_dev));
+        if (timed) t0 = mark(0, t0);
+      }
       const int m = j + 1;
-      // CGS2 pass 1
-      G_TRY(launch_k(dots_partial_kernel, dim3(nblk), dim3(kThreads), 0, s, V, N, m, wv, N, e.dot_partial, stop_dev));
-      G_TRY(launch_k(dots_final_kernel, dim3(m), dim3(kThreads), 0, s, e.dot_partial, nblk, dots1, nullptr, nullptr, stop_dev));
-      G_TRY(launch_k(update_kernel, dim3(grid1), dim3(kThreads), upd_smem, s, V, N, m, nullptr, dots1, false, wv, N, nullptr, stop_dev));
-      // CGS2 pass 2 (re-orthogonalisation), Hessenberg column = h1 + h2
-      G_TRY(launch_k(dots_partial_kernel, dim3(nblk), dim3(kThreads), 0, s, V, N, m, wv, N, e.dot_partial, stop_dev));
-      G_TRY(launch_k(dots_final_kernel, dim3(m), dim3(kThreads), 0, s, e.dot_partial, nblk, dots2, dots1, rcols + (int64_t)j * ldr, stop_dev));
-      G_TRY(launch_k(update_kernel, dim3(nblk), dim3(kThreads), upd_smem, s, V, N, m, nullptr, dots2, false, wv, N, e.norm_partial, stop_dev));
-      G_TRY(launch_k(givens_kernel, dim3(1), dim3(32), 0, s, st, e.norm_partial, nblk, rcols, ldr, cs, sn, g, hist, cfg->tol,
-                                     static_cast<int>(max_total), cycle_len, hf_dev));
-      G_TRY(launch_k(scale_kernel, dim3(grid1), dim3(kThreads), 0, s, wv, V + static_cast<int64_t>(j + 1) * N, &st->inv, N, stop_dev));
-      TOEP_LAUNCHED();
+      G_TRY(launch_k(k_dots, dim3(nblk), dim3(kThreads), 0, s, (const double2*)V, N, m, (const double2*)w, N, part1,
+                     (const int*)stop_dev));
+      G_TRY(launch_k(k_upd, dim3(nblk), dim3(kThreads), coef_smem, s, (const double2*)V, N, m, (const double*)vs,
+                     (const double2*)part1, nblk, w, N, 1, h1, (const double2*)nullptr, part2, (double*)nullptr,
+                     (const int*)stop_dev));
+      G_TRY(launch_k(k_upd, dim3(nblk), dim3(kThreads), coef_smem, s, (const double2*)V, N, m, (const double*)vs,
+                     (const double2*)part2, nblk, w, N, 2, rcols + (int64_t)j * ldr, (const double2*)h1,
+                     (double2*)nullptr, e.norm_partial, (const int*)stop_dev));
+      G_TRY(launch_k(k_givens, dim3(1), dim3(32), 0, s, st, (const double*)e.norm_partial, nblk, rcols, ldr, cs, sn, g,
+                     hist, vs, cfg->tol, static_cast<int>(max_total), cycle_len, hf_dev));
       if (timed) mark(2, t0);
       cudaEvent_t ev = res.event();
       cudaEventRecord(ev, s);
       step_ev.push_back(ev);
+      if (tr.on) {
+        const double us = std::chrono::duration<double, std::micro>(clk::now() - t_launch0).count();
+        tr.launch_us_sum += us;
+        tr.launch_us_max = std::max(tr.launch_us_max, us);
+        tr.steps++;
+      }
       ++j;
-      if (j >= 2) {
-        tr.sync_event(step_ev[j - 2]);
+      // keep up to kLag steps queued ahead of the one the host last saw finish
+      constexpr int kLag = 2;
+      if (j > kLag) {
+        tr.sync_event(step_ev[j - 1 - kLag]);
         if (hf->stop) break;
       }
     }
     tr.mark("arnoldi steps launched");
     // ---- assemble x += V y (gmres.py:192-204)
-    G_TRY(launch_k(backsub_kernel, dim3(1), dim3(32), 0, s, st, rcols, ldr, g, y));
-    G_TRY(launch_k(update_kernel, dim3(grid1), dim3(kThreads), upd_smem, s, V, N, cycle_len, m_dev, y, true, x, N, nullptr, nullptr));
-    TOEP_LAUNCHED();
+    G_TRY(launch_k(k_backsub, dim3(1), dim3(32), 0, s, (const GState*)st, (const double2*)rcols, ldr,
+                   (const double2*)g, y));
+    G_TRY(launch_k(k_axpy_basis, dim3(grid1), dim3(kThreads), coef_smem, s, (const double2*)V, N, cycle_len,
+                   (const int*)m_dev, (const double*)vs, (const double2*)y, x, N));
     if (cudaMemcpyAsync(&hst, st, sizeof(GState), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess) {
       set_error("gmres cycle failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -674,18 +727,20 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     tr.mark("cycle synced");
     if (hst.converged || hst.breakdown || total >= max_total) break;
   }
+
   // ---- exit residual ||b - A x|| / ||b|| (gmres.py:209-216), unpreconditioned
   {
     cudaEvent_t t0 = timed ? start_mark() : nullptr;
-    G_TRY(e.apply_a(x, tmp, nullptr));
+    G_TRY(e.apply_a(x, nullptr, tmp, nullptr));
+    double2* ax = tmp;
     if (p->precond == TOEP_PC_FOLDED) {  // A x = P (P^-1 A x)
-      G_TRY(block_apply_impl(p->pmat, p->pside, tmp, w, p->n / p->pside, p->w, TOEP_C128, s, nullptr));
-      cudaMemcpyAsync(tmp, w, N * sizeof(double2), cudaMemcpyDeviceToDevice, s);
+      G_TRY(block_apply_impl(p->pmat, p->pside, tmp, pb, p->n / p->pside, p->w, TOEP_C128, s, nullptr));
+      ax = pb;
     }
     if (timed) mark(0, t0);
-    G_TRY(launch_k(sub_kernel, dim3(grid1), dim3(kThreads), 0, s, b, tmp, w, N));
+    G_TRY(launch_k(k_sub, dim3(grid1), dim3(kThreads), 0, s, b, (const double2*)ax, tmp, N));
   }
-  const double rn = e.host_norm(w);
+  const double rn = e.host_norm(tmp);
   const double bn = e.host_norm(b);
   tr.mark("exit residual synced");
   rep->final_residual = rn / bn;

@@ -30,6 +30,7 @@ struct PassArgs {
   const int* out_idx = nullptr;
   int64_t out_idx_stride = 0;
   const int* stop = nullptr;  // if non-null and *stop != 0 the launch is a no-op
+  const double* in_scale = nullptr;  // optional device scalar multiplying the input
   // optional: input row a is the sum of part_count[a] slabs spaced part_stride apart
   // (the per-CTA inverse level-2 partials of the fused spectral kernel)
   const int* part_count = nullptr;

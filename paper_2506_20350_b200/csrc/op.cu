@@ -74,7 +74,7 @@ int op_workspace(toep_op_s* op, int64_t w, cudaStream_t s, toep_op_s::Workspace*
 }
 
 int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose, bool io_c128, const int* stop,
-                cudaStream_t s) {
+                cudaStream_t s, const double* in_scale) {
   if (w == 0) return TOEP_OK;
   toep_op_s::Workspace* ws = nullptr;
   TOEP_TRY(op_workspace(op, w, s, &ws));
@@ -105,7 +105,7 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
     PassArgs a;
     a.in = u; a.out = ws->x1; a.L = op->l1; a.n_lo = op->n1; a.n_hi = 0; a.n_out = op->l1;
     a.inner = inner; a.outer = op->n2; a.in_sa = inner; a.in_so = op->n1 * inner; a.out_sa = inner;
-    a.out_so = op->l1 * inner; a.sign = -1; a.scale = 1.0; a.stop = stop;
+    a.out_so = op->l1 * inner; a.sign = -1; a.scale = 1.0; a.stop = stop; a.in_scale = in_scale;
     TOEP_TRY(fft_pass(a, tio, tc, tc, s));
     // X2 [n2][l1][n0] reuses the (otherwise idle) spectral workspace
     TOEP_TRY(fused_spectral(op, ws->x1, ws->parts, ws->hat, ws->cnt, stop, s));
@@ -120,7 +120,7 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
   PassArgs a;  // level-1 (x) pass: u [n2][n1][inner] -> x1 [n2][l1][inner]  (pad fused)
   a.in = u; a.out = ws->x1; a.L = op->l1; a.n_lo = op->n1; a.n_hi = 0; a.n_out = op->l1;
   a.inner = inner; a.outer = op->n2; a.in_sa = inner; a.in_so = op->n1 * inner; a.out_sa = inner;
-  a.out_so = op->l1 * inner; a.sign = s1; a.scale = sc1x; a.stop = stop;
+  a.out_so = op->l1 * inner; a.sign = s1; a.scale = sc1x; a.stop = stop; a.in_scale = in_scale;
   TOEP_TRY(fft_pass(a, tio, tc, tc, s));
 
   PassArgs b;  // level-2 (y) pass over the n2 non-zero rows: x1 -> hat [l2][l1][inner]

@@ -35,8 +35,9 @@ int op_workspace(toep_op_s* op, int64_t w, cudaStream_t s, toep_op_s::Workspace*
 
 // matvec with optional device-side stop flag (GMRES speculative steps).
 // io_c128: u / v are complex128 while the operator computes in its own dtype.
+// in_scale: optional device scalar s, computes A (s u)
 int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose, bool io_c128,
-                const int* stop, cudaStream_t s);
+                const int* stop, cudaStream_t s, const double* in_scale = nullptr);
 
 void keep_pool();
 
