@@ -498,6 +498,15 @@ int gemm(int dtype, int64_t m, int64_t n, int64_t k, double2 alpha, const void* 
          int64_t a_bs, const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, double2 beta, void* c, int64_t c_rs,
          int64_t c_cs, int64_t c_bs, int64_t batch, cudaStream_t s, const int* stop) {
   if (m == 0 || n == 0 || batch == 0) return TOEP_OK;
+  static const bool simt_only = [] {
+    const char* e = std::getenv("TOEP_ZGEMM");
+    return e != nullptr && std::strcmp(e, "simt") == 0;
+  }();
+  if (dtype == TOEP_C128 && stop == nullptr && !simt_only && m * n * k >= 32 * 32 * 32) {
+    const int rc = zgemm_tc(m, n, k, alpha, a, a_rs, a_cs, a_bs, b, b_rs, b_cs, b_bs, beta, c, c_rs, c_cs, c_bs,
+                            batch, s);
+    if (rc >= 0) return rc;
+  }
   GemmArgs g{m, n, k, alpha, beta, a, a_rs, a_cs, a_bs, b, b_rs, b_cs, b_bs, c, c_rs, c_cs, c_bs, stop};
   const int64_t gy = (m + BM - 1) / BM, gx = (n + BN - 1) / BN;
   TOEP_REQUIRE(gy <= 65535 && batch <= 65535 && gx <= 0x7fffffff, TOEP_ERR_ARG, "gemm grid too large");

@@ -53,6 +53,11 @@ int gemm(int dtype, int64_t m, int64_t n, int64_t k, double2 alpha, const void* 
          double2 beta, void* c, int64_t c_rs, int64_t c_cs, int64_t c_bs, int64_t batch,
          cudaStream_t s, const int* stop = nullptr);
 
+// DMMA tensor-core complex128 GEMM (zgemm_tc.cu); returns -1 when the stride pattern is not covered
+int zgemm_tc(int64_t m, int64_t n, int64_t k, double2 alpha, const void* a, int64_t a_rs, int64_t a_cs, int64_t a_bs,
+             const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, double2 beta, void* c, int64_t c_rs,
+             int64_t c_cs, int64_t c_bs, int64_t batch, cudaStream_t s);
+
 // batched transpose of complex matrices: out[b][c][r] = in[b][r][c]  (rows x cols)
 int transpose_batched(int dtype, const void* in, void* out, int64_t batch, int rows, int cols, cudaStream_t s);
 
