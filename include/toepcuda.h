@@ -166,6 +166,16 @@ typedef struct {
 TOEP_API int toep_gmres(const toep_gmres_problem_t* prob, const toep_gmres_cfg_t* cfg, const void* b, void* x,
                void* stream, toep_gmres_report_t* rep);
 
+/* solvers/gmres.py:304-336 solve_multi_rhs_sequential: an independent GMRES per column of
+ * the (n, w) block b, all columns advanced in lock step so each Arnoldi step is one
+ * multi-RHS matvec (per-bin complex GEMM on the FP64 tensor cores).  Requires prob->op;
+ * precond NONE / FOLDED / BLOCK.  Per-column outputs (host arrays of length w): iterations,
+ * converged, final_residual, n_history; history: host (history_rows, w) array, column c's
+ * residual_history[t] at history[t*w + c]. */
+TOEP_API int toep_gmres_batched(const toep_gmres_problem_t* prob, const toep_gmres_cfg_t* cfg, const void* b,
+                                void* x, void* stream, int32_t* iterations, int32_t* converged,
+                                double* final_residual, int32_t* n_history, double* history, int64_t history_rows);
+
 #ifdef __cplusplus
 }
 #endif

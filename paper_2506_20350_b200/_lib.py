@@ -86,6 +86,8 @@ SIGNATURES = {
                           c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp]),
     "toep_gmres": (c_int, [ctypes.POINTER(GmresProblem), ctypes.POINTER(GmresCfg), c_vp, c_vp, c_vp,
                            ctypes.POINTER(GmresReport)]),
+    "toep_gmres_batched": (c_int, [ctypes.POINTER(GmresProblem), ctypes.POINTER(GmresCfg), c_vp, c_vp, c_vp,
+                                   c_vp, c_vp, c_vp, c_vp, c_vp, c_i64]),
 }
 
 _lib = None

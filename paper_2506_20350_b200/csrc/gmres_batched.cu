@@ -1,0 +1,581 @@
+// Batched per-column GMRES: solve_multi_rhs_sequential (solvers/gmres.py:304-336) for all
+// columns at once.
+//
+// The reference solves each right-hand-side column with its own _gmres_block (n x 1).  Here
+// every column keeps its own Krylov basis, Hessenberg columns, Givens rotations, residual
+// history and stop flag, but all columns advance in lock step so that each Arnoldi step is
+// ONE multi-RHS matvec over the (n, W) block: the per-bin product becomes a complex GEMM
+// on the FP64 tensor cores (zgemm_tc, 256x256 x 256xW per bin at cfg3).  Columns that have
+// stopped (converged, breakdown or iteration cap) are frozen: their Gram-Schmidt, Givens
+// and solution updates are masked, so each column's iterate and report are those of an
+// independent solve.  Cycle boundaries coincide for all columns (same restart length).
+//
+// Per-column reductions run over row chunks: thread = column (coalesced over the W
+// contiguous columns of a row), partials [l][chunk][column] are reduced in fixed order.
+#include <chrono>
+#include <cstdlib>
+#include <vector>
+
+#include "launch.cuh"
+#include "op.h"
+
+namespace toep {
+namespace {
+
+constexpr int kCols = 64;   // columns per CTA in the row-chunked kernels
+constexpr int kLG = 8;      // basis vectors per accumulation group
+
+struct BCol {               // per-column state (arrays of length W)
+  double* beta0;
+  int* stop;                // 0 running, 1 converged/breakdown, 2 cycle exhausted / cap
+  int* conv;
+  int* brk;
+  int* m;                   // completed steps in the current cycle
+  int* total;
+  int* nhist;
+};
+
+__device__ __forceinline__ int64_t rows_begin(int chunk, int nchunks, int64_t n) {
+  return n * chunk / nchunks;
+}
+
+// partial[(l*nchunks + chunk)*W + c] = sum_{rows in chunk} conj(V_l[i, c]) w[i, c]
+__global__ void __launch_bounds__(kCols) kb_dots(const double2* const* __restrict__ Vp, int m,
+                                                 const double2* __restrict__ w, int64_t n, int W, int nchunks,
+                                                 double2* __restrict__ partial) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.y * kCols + threadIdx.x;
+  if (c >= W) return;
+  const int chunk = blockIdx.x;
+  const int64_t r0 = rows_begin(chunk, nchunks, n), r1 = rows_begin(chunk + 1, nchunks, n);
+  for (int l0 = 0; l0 < m; l0 += kLG) {
+    double2 acc[kLG];
+#pragma unroll
+    for (int g = 0; g < kLG; ++g) acc[g] = make_double2(0, 0);
+    for (int64_t i = r0; i < r1; ++i) {
+      const double2 wi = w[i * W + c];
+#pragma unroll
+      for (int g = 0; g < kLG; ++g)
+        if (l0 + g < m) cfmac(acc[g], Vp[l0 + g][i * W + c], wi);
+    }
+#pragma unroll
+    for (int g = 0; g < kLG; ++g)
+      if (l0 + g < m) partial[(static_cast<int64_t>(l0 + g) * nchunks + chunk) * W + c] = acc[g];
+  }
+}
+
+// h[l][c] = sum_chunk partial[l][chunk][c]; mode 1: hout = h; mode 2: hout = hprev + h
+__global__ void kb_reduce(const double2* __restrict__ partial, int m, int nchunks, int W, double2* __restrict__ h,
+                          const double2* __restrict__ hprev, double2* __restrict__ hcol, int ldh,
+                          const int* __restrict__ stop) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= static_cast<int64_t>(m) * W) return;
+  const int l = static_cast<int>(t / W), c = static_cast<int>(t - static_cast<int64_t>(l) * W);
+  if (stop[c]) return;
+  double2 s = make_double2(0, 0);
+  for (int ch = 0; ch < nchunks; ++ch) s = cadd(s, partial[(static_cast<int64_t>(l) * nchunks + ch) * W + c]);
+  h[static_cast<int64_t>(l) * W + c] = s;
+  if (hcol != nullptr) hcol[static_cast<int64_t>(l) * ldh + c] = cadd(hprev[static_cast<int64_t>(l) * W + c], s);
+}
+
+// w[:, c] -= sum_l V_l[:, c] h[l][c]  (active columns); mode 1: partial dots of the result,
+// mode 2: ||w[:, c]||^2 partials
+__global__ void __launch_bounds__(kCols) kb_upd(const double2* const* __restrict__ Vp, int m,
+                                                const double2* __restrict__ h, double2* __restrict__ w, int64_t n,
+                                                int W, int nchunks, int mode, double2* __restrict__ partial,
+                                                double* __restrict__ norm_part, const int* __restrict__ stop) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.y * kCols + threadIdx.x;
+  if (c >= W || stop[c]) return;
+  const int chunk = blockIdx.x;
+  const int64_t r0 = rows_begin(chunk, nchunks, n), r1 = rows_begin(chunk + 1, nchunks, n);
+  double nrm = 0.0;
+  // coefficients in register blocks of kLG (each thread owns one column): w is swept
+  // ceil(m / kLG) times, the basis once
+  for (int l0 = 0; l0 < m; l0 += kLG) {
+    double2 cl[kLG];
+#pragma unroll
+    for (int g = 0; g < kLG; ++g) {
+      const double2 hv = (l0 + g < m) ? h[static_cast<int64_t>(l0 + g) * W + c] : make_double2(0, 0);
+      cl[g] = make_double2(-hv.x, -hv.y);
+    }
+    const bool last = (l0 + kLG >= m);
+    for (int64_t i = r0; i < r1; ++i) {
+      double2 acc = w[i * W + c];
+#pragma unroll
+      for (int g = 0; g < kLG; ++g)
+        if (l0 + g < m) cfma(acc, Vp[l0 + g][i * W + c], cl[g]);
+      w[i * W + c] = acc;
+      if (last) nrm = fma(acc.x, acc.x, fma(acc.y, acc.y, nrm));
+    }
+  }
+  if (mode == 2) {
+    norm_part[static_cast<int64_t>(chunk) * W + c] = nrm;
+    return;
+  }
+  for (int l0 = 0; l0 < m; l0 += kLG) {
+    double2 a[kLG];
+#pragma unroll
+    for (int g = 0; g < kLG; ++g) a[g] = make_double2(0, 0);
+    for (int64_t i = r0; i < r1; ++i) {
+      const double2 wi = w[i * W + c];
+#pragma unroll
+      for (int g = 0; g < kLG; ++g)
+        if (l0 + g < m) cfmac(a[g], Vp[l0 + g][i * W + c], wi);
+    }
+#pragma unroll
+    for (int g = 0; g < kLG; ++g)
+      if (l0 + g < m) partial[(static_cast<int64_t>(l0 + g) * nchunks + chunk) * W + c] = a[g];
+  }
+}
+
+// ||x[:, c]||^2 partials over row chunks (all columns)
+__global__ void __launch_bounds__(kCols) kb_norm(const double2* __restrict__ x, int64_t n, int W, int nchunks,
+                                                 double* __restrict__ norm_part) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.y * kCols + threadIdx.x;
+  if (c >= W) return;
+  const int chunk = blockIdx.x;
+  const int64_t r0 = rows_begin(chunk, nchunks, n), r1 = rows_begin(chunk + 1, nchunks, n);
+  double nrm = 0.0;
+  for (int64_t i = r0; i < r1; ++i) {
+    const double2 v = x[i * W + c];
+    nrm = fma(v.x, v.x, fma(v.y, v.y, nrm));
+  }
+  norm_part[static_cast<int64_t>(chunk) * W + c] = nrm;
+}
+
+__device__ __forceinline__ double colnorm(const double* part, int nchunks, int W, int c) {
+  double s = 0.0;
+  for (int ch = 0; ch < nchunks; ++ch) s += part[static_cast<int64_t>(ch) * W + c];
+  return sqrt(s);
+}
+
+__global__ void kb_init(BCol st, const double* norm_part, int nchunks, int W, double* hist) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= W) return;
+  const double b0 = colnorm(norm_part, nchunks, W, c);
+  st.beta0[c] = b0;
+  st.stop[c] = (b0 == 0.0) ? 1 : 0;
+  st.conv[c] = 1;  // provisional; cleared at the first cycle start of a non-trivial column
+  st.brk[c] = 0;
+  st.m[c] = 0;
+  st.total[c] = 0;
+  st.nhist[c] = 1;
+  hist[c] = (b0 == 0.0) ? 0.0 : 1.0;
+}
+
+// cycle start: beta = ||z[:, c]||, test, g[0] = beta, inv for V[0] scaling
+__global__ void kb_cycle_start(BCol st, const double* norm_part, int nchunks, int W, double tol, double2* g,
+                               double* inv, int first, int* active) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= W) return;
+  if (first) {
+    if (st.beta0[c] == 0.0) { inv[c] = 0.0; return; }
+    st.conv[c] = 0;
+  } else if (st.conv[c] || st.brk[c] || st.stop[c] == 3) {
+    inv[c] = 0.0;
+    return;
+  }
+  const double beta = colnorm(norm_part, nchunks, W, c);
+  st.m[c] = 0;
+  if (beta / st.beta0[c] <= tol) {
+    st.conv[c] = 1;
+    st.stop[c] = 1;
+    inv[c] = 0.0;
+  } else {
+    st.stop[c] = 0;
+    g[c] = make_double2(beta, 0.0);
+    inv[c] = 1.0 / beta;
+    atomicAdd(active, 1);
+  }
+}
+
+// per-column Givens step (gmres.py:160-189); hcol layout [i][c] with row stride ldh
+__global__ void kb_givens(BCol st, const double* norm_part, int nchunks, int W, double2* rcols, int ldr, double* cs,
+                          double2* sn, double2* g, double* hist, double* inv, double tol, int max_total, int cycle_len,
+                          int* active) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= W) return;
+  if (st.stop[c]) {  // frozen column: its next basis vector is exactly zero (no NaN can leak)
+    inv[c] = 0.0;
+    return;
+  }
+  const double hnext = colnorm(norm_part, nchunks, W, c);
+  const int j = st.m[c];
+  double2* hcol = rcols + static_cast<int64_t>(j) * ldr * W;  // element i at hcol[i*W + c]
+  for (int i = 0; i < j; ++i) {
+    const double2 a0 = hcol[i * W + c], a1 = hcol[(i + 1) * W + c];
+    const double cc = cs[i * W + c];
+    const double2 s = sn[i * W + c];
+    hcol[i * W + c] = cadd(cscale(a0, cc), cmul(s, a1));
+    hcol[(i + 1) * W + c] = cadd(cscale(cmulc(s, a0), -1.0), cscale(a1, cc));
+  }
+  const double2 a = hcol[j * W + c];
+  const double absa = hypot(a.x, a.y);
+  const double t = hypot(absa, hnext);
+  double cr;
+  double2 s, r;
+  if (t == 0.0) {
+    cr = 1.0; s = make_double2(0, 0); r = make_double2(0, 0);
+  } else if (a.x == 0.0 && a.y == 0.0) {
+    cr = 0.0; s = make_double2(1, 0); r = make_double2(hnext, 0);
+  } else {
+    const double2 alpha = make_double2(a.x / absa, a.y / absa);
+    cr = absa / t;
+    s = cscale(alpha, hnext / t);
+    r = cscale(alpha, t);
+  }
+  hcol[j * W + c] = r;
+  cs[j * W + c] = cr;
+  sn[j * W + c] = s;
+  const double2 gj = g[j * W + c];
+  g[(j + 1) * W + c] = cscale(cmulc(s, gj), -1.0);
+  g[j * W + c] = cscale(gj, cr);
+  st.m[c] = j + 1;
+  st.total[c] += 1;
+  const double2 gn = g[(j + 1) * W + c];
+  const double est = hypot(gn.x, gn.y) / st.beta0[c];
+  hist[static_cast<int64_t>(st.nhist[c]) * W + c] = est;
+  st.nhist[c] += 1;
+  inv[c] = 0.0;
+  if (est <= tol) {
+    st.conv[c] = 1;
+    st.stop[c] = 1;
+  } else if (hnext == 0.0) {
+    st.conv[c] = 1;
+    st.brk[c] = 1;
+    st.stop[c] = 1;
+  } else {
+    inv[c] = 1.0 / hnext;
+    if (st.total[c] >= max_total) st.stop[c] = 3;
+    else if (st.m[c] >= cycle_len) st.stop[c] = 2;
+  }
+  if (st.stop[c]) atomicSub(active, 1);
+}
+
+// V_next[:, c] = w[:, c] * inv[c]  (in place), all columns (inv = 0 for frozen columns is harmless)
+__global__ void kb_scale(double2* __restrict__ x, const double* __restrict__ inv, int64_t n, int W,
+                         const double2* __restrict__ src) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t total = n * W;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(t % W);
+    x[t] = cscale(src[t], inv[c]);
+  }
+}
+
+// y = R^-1 g per column (gmres.py:193-204) for columns that ran steps this cycle
+__global__ void kb_backsub(BCol st, const double2* rcols, int ldr, const double2* g, double2* y, int W,
+                           const int* ran) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= W) return;
+  const int m = ran[c] ? st.m[c] : 0;
+  for (int i = m - 1; i >= 0; --i) {
+    const double2 d = rcols[(static_cast<int64_t>(i) * ldr + i) * W + c];
+    if (d.x == 0.0 && d.y == 0.0) {
+      y[i * W + c] = make_double2(0, 0);
+      continue;
+    }
+    double2 acc = g[i * W + c];
+    for (int k = i + 1; k < m; ++k) acc = csub(acc, cmul(rcols[(static_cast<int64_t>(k) * ldr + i) * W + c], y[k * W + c]));
+    const double den = d.x * d.x + d.y * d.y;
+    y[i * W + c] = make_double2((acc.x * d.x + acc.y * d.y) / den, (acc.y * d.x - acc.x * d.y) / den);
+  }
+  for (int i = m; i < ldr; ++i) y[i * W + c] = make_double2(0, 0);
+}
+
+// x[:, c] += sum_l V_l[:, c] y[l][c]
+__global__ void kb_axpy(const double2* const* __restrict__ Vp, int m, const double2* __restrict__ y,
+                        double2* __restrict__ x, int64_t n, int W) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t total = n * W;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(t % W);
+    double2 acc = x[t];
+    for (int l = 0; l < m; ++l) cfma(acc, Vp[l][t], y[static_cast<int64_t>(l) * W + c]);
+    x[t] = acc;
+  }
+}
+
+// mark which columns run Arnoldi steps this cycle (stop == 0 after the cycle start)
+__global__ void kb_mark_running(const BCol st, int* ran, int W) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < W) ran[c] = (st.stop[c] == 0);
+}
+
+__global__ void k_sub_b(const double2* __restrict__ a, const double2* __restrict__ b, double2* __restrict__ out,
+                        int64_t N) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = csub(a[i], b[i]);
+}
+
+}  // namespace
+
+// Batched independent-column GMRES.  rep_iters / rep_conv / rep_final: per column (host arrays,
+// length w); hist: host array (max_iter + 2) x w, column c's history at hist[t*w + c];
+// nhist per column in rep_nhist.
+int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const double2* b, double2* x,
+                      cudaStream_t s, int32_t* rep_iters, int32_t* rep_conv, double* rep_final, int32_t* rep_nhist,
+                      double* hist_host, int64_t hist_cap_rows) {
+  keep_pool();
+  TOEP_REQUIRE(p->op != nullptr, TOEP_ERR_ARG, "batched GMRES needs a resident operator");
+  TOEP_REQUIRE(p->precond == TOEP_PC_NONE || p->precond == TOEP_PC_FOLDED || p->precond == TOEP_PC_BLOCK,
+               TOEP_ERR_ARG, "batched GMRES supports none / folded / block preconditioners");
+  TOEP_REQUIRE(op_dim(p->op) == p->n, TOEP_ERR_SHAPE, "rhs rows != operator dim");
+  TOEP_REQUIRE(cfg->tol > 0 && cfg->max_iter >= 1 && cfg->restart >= 0, TOEP_ERR_ARG, "bad GMRES config");
+  const int64_t n = p->n;
+  const int W = static_cast<int>(p->w);
+  const int64_t N = n * W;
+  const int64_t max_total = std::min<int64_t>(cfg->max_iter, n);
+  const int cycle_len = static_cast<int>(cfg->restart == 0 ? max_total : std::min<int64_t>(cfg->restart, max_total));
+  const int ldr = cycle_len + 1;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int ctiles = (W + kCols - 1) / kCols;
+  const int nchunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n / 16, (4 * sms + ctiles - 1) / ctiles)));
+  const int g1 = static_cast<int>(std::min<int64_t>((N + 255) / 256, 8 * sms));
+  const int gc = (W + 127) / 128;
+  const bool per_step_pc = p->precond == TOEP_PC_BLOCK;
+  const bool io64 = p->op->dtype == TOEP_C64;
+
+  std::vector<double2*> Vh;  // basis vectors, allocated as the cycle grows
+  double2 *w = nullptr, *tmp = nullptr, *pb = nullptr, *h1 = nullptr, *h2 = nullptr, *rcols = nullptr;
+  double2 *sn = nullptr, *g = nullptr, *y = nullptr, *part = nullptr;
+  double *cs = nullptr, *hist = nullptr, *inv = nullptr, *npart = nullptr;
+  double2** Vp = nullptr;
+  int *ran = nullptr, *active = nullptr;
+  BCol st{};
+  int* active_host = nullptr;
+  int rc = TOEP_OK;
+  auto cleanup = [&]() {
+    for (auto v : Vh) cudaFreeAsync(v, s);
+    for (void* q : {(void*)w, (void*)tmp, (void*)pb, (void*)h1, (void*)h2, (void*)rcols, (void*)sn, (void*)g, (void*)y,
+                    (void*)part, (void*)cs, (void*)hist, (void*)inv, (void*)npart, (void*)Vp, (void*)ran,
+                    (void*)active, (void*)st.beta0, (void*)st.stop, (void*)st.conv, (void*)st.brk, (void*)st.m,
+                    (void*)st.total, (void*)st.nhist})
+      if (q) cudaFreeAsync(q, s);
+    cudaStreamSynchronize(s);
+  };
+#define B_ALLOC(ptr, count)                                                                                       \
+  do {                                                                                                            \
+    if (cudaMallocAsync(reinterpret_cast<void**>(&(ptr)), sizeof(*(ptr)) * (size_t)(count), s) != cudaSuccess) { \
+      cudaGetLastError();                                                                                         \
+      set_error("out of device memory in batched gmres");                                                         \
+      cleanup();                                                                                                  \
+      return TOEP_ERR_OOM;                                                                                        \
+    }                                                                                                             \
+  } while (0)
+#define B_TRY(expr)      \
+  do {                   \
+    rc = (expr);         \
+    if (rc != TOEP_OK) { \
+      cleanup();         \
+      return rc;         \
+    }                    \
+  } while (0)
+  B_ALLOC(w, N);
+  B_ALLOC(tmp, N);
+  B_ALLOC(pb, N);
+  B_ALLOC(h1, static_cast<int64_t>(ldr) * W);
+  B_ALLOC(h2, static_cast<int64_t>(ldr) * W);
+  B_ALLOC(rcols, static_cast<int64_t>(cycle_len) * ldr * W);
+  B_ALLOC(sn, static_cast<int64_t>(ldr) * W);
+  B_ALLOC(cs, static_cast<int64_t>(ldr) * W);
+  B_ALLOC(g, static_cast<int64_t>(ldr + 1) * W);
+  B_ALLOC(y, static_cast<int64_t>(ldr) * W);
+  B_ALLOC(part, static_cast<int64_t>(ldr) * nchunks * W);
+  B_ALLOC(npart, static_cast<int64_t>(nchunks) * W);
+  B_ALLOC(hist, (max_total + 2) * W);
+  B_ALLOC(inv, W);
+  B_ALLOC(ran, W);
+  B_ALLOC(active, 1);
+  B_ALLOC(Vp, ldr + 1);
+  B_ALLOC(st.beta0, W);
+  B_ALLOC(st.stop, W);
+  B_ALLOC(st.conv, W);
+  B_ALLOC(st.brk, W);
+  B_ALLOC(st.m, W);
+  B_ALLOC(st.total, W);
+  B_ALLOC(st.nhist, W);
+  if (cudaHostAlloc(reinterpret_cast<void**>(&active_host), sizeof(int), cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    cleanup();
+    set_error("pinned allocation failed");
+    return TOEP_ERR_OOM;
+  }
+  struct PinFree {
+    int* p;
+    ~PinFree() { cudaFreeHost(p); }
+  } pin_guard{active_host};
+  auto ensure_basis = [&](int count) -> int {
+    while (static_cast<int>(Vh.size()) < count) {
+      double2* v = nullptr;
+      if (cudaMallocAsync(reinterpret_cast<void**>(&v), sizeof(double2) * N, s) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("out of device memory for the Krylov basis (%d vectors of %lld complex)", count, (long long)N);
+        return TOEP_ERR_OOM;
+      }
+      Vh.push_back(v);
+      TOEP_CUDA(cudaMemcpyAsync(Vp + Vh.size() - 1, &Vh.back(), sizeof(double2*), cudaMemcpyHostToDevice, s));
+      TOEP_CUDA(cudaStreamSynchronize(s));  // the pageable source must outlive the copy
+    }
+    return TOEP_OK;
+  };
+  const dim3 gridc(nchunks, ctiles);
+
+  // ---- P^-1 b and beta0 per column
+  const double2* zb = b;
+  if (p->precond != TOEP_PC_NONE) {
+    B_TRY(block_apply_impl(p->pinv, p->pside, b, pb, n / p->pside, W, TOEP_C128, s, nullptr));
+    zb = pb;
+  }
+  B_TRY(launch_k(kb_norm, gridc, dim3(kCols), 0, s, zb, n, W, nchunks, npart));
+  B_TRY(launch_k(kb_init, dim3(gc), dim3(128), 0, s, st, (const double*)npart, nchunks, W, hist));
+  TOEP_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double2), s));
+  B_TRY(ensure_basis(1));
+
+  bool first = true;
+  while (true) {
+    // ---- cycle start: V[0] = (P^-1 (b - A x)) / beta per column
+    TOEP_CUDA(cudaMemsetAsync(active, 0, sizeof(int), s));
+    const double2* z = zb;
+    if (!first) {
+      B_TRY(matvec_impl(p->op, x, tmp, W, false, io64, nullptr, s));
+      if (p->precond == TOEP_PC_FOLDED) {
+        B_TRY(launch_k(k_sub_b, dim3(g1), dim3(256), 0, s, (const double2*)pb, (const double2*)tmp, w, N));
+      } else if (per_step_pc) {
+        B_TRY(launch_k(k_sub_b, dim3(g1), dim3(256), 0, s, b, (const double2*)tmp, tmp, N));
+        B_TRY(block_apply_impl(p->pinv, p->pside, tmp, w, n / p->pside, W, TOEP_C128, s, nullptr));
+      } else {
+        B_TRY(launch_k(k_sub_b, dim3(g1), dim3(256), 0, s, b, (const double2*)tmp, w, N));
+      }
+      z = w;
+    }
+    B_TRY(launch_k(kb_norm, gridc, dim3(kCols), 0, s, z, n, W, nchunks, npart));
+    B_TRY(launch_k(kb_cycle_start, dim3(gc), dim3(128), 0, s, st, (const double*)npart, nchunks, W, cfg->tol, g, inv,
+                   first ? 1 : 0, active));
+    B_TRY(launch_k(kb_mark_running, dim3(gc), dim3(128), 0, s, (const BCol)st, ran, W));
+    B_TRY(launch_k(kb_scale, dim3(g1), dim3(256), 0, s, Vh[0], (const double*)inv, n, W, z));
+    first = false;
+    TOEP_CUDA(cudaMemcpyAsync(active_host, active, sizeof(int), cudaMemcpyDeviceToHost, s));
+    TOEP_CUDA(cudaStreamSynchronize(s));
+    int j = 0;
+    int lagged_active = *active_host;
+    while (lagged_active > 0 && j < cycle_len) {
+      B_TRY(ensure_basis(j + 2));
+      const int m = j + 1;
+      if (per_step_pc) {
+        B_TRY(matvec_impl(p->op, Vh[j], tmp, W, false, io64, nullptr, s));
+        B_TRY(block_apply_impl(p->pinv, p->pside, tmp, w, n / p->pside, W, TOEP_C128, s, nullptr));
+      } else {
+        B_TRY(matvec_impl(p->op, Vh[j], w, W, false, io64, nullptr, s));
+      }
+      B_TRY(launch_k(kb_dots, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)w, n, W,
+                     nchunks, part));
+      const int rg = static_cast<int>((static_cast<int64_t>(m) * W + 255) / 256);
+      B_TRY(launch_k(kb_reduce, dim3(rg), dim3(256), 0, s, (const double2*)part, m, nchunks, W, h1,
+                     (const double2*)nullptr, (double2*)nullptr, 0, (const int*)st.stop));
+      B_TRY(launch_k(kb_upd, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)h1, w, n,
+                     W, nchunks, 1, part, (double*)nullptr, (const int*)st.stop));
+      B_TRY(launch_k(kb_reduce, dim3(rg), dim3(256), 0, s, (const double2*)part, m, nchunks, W, h2,
+                     (const double2*)h1, rcols + static_cast<int64_t>(j) * ldr * W, W, (const int*)st.stop));
+      B_TRY(launch_k(kb_upd, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)h2, w, n,
+                     W, nchunks, 2, (double2*)nullptr, npart, (const int*)st.stop));
+      B_TRY(launch_k(kb_givens, dim3(gc), dim3(128), 0, s, st, (const double*)npart, nchunks, W, rcols, ldr, cs, sn, g,
+                     hist, inv, cfg->tol, static_cast<int>(max_total), cycle_len, active));
+      B_TRY(launch_k(kb_scale, dim3(g1), dim3(256), 0, s, Vh[j + 1], (const double*)inv, n, W, (const double2*)w));
+      TOEP_CUDA(cudaMemcpyAsync(active_host, active, sizeof(int), cudaMemcpyDeviceToHost, s));
+      TOEP_CUDA(cudaStreamSynchronize(s));  // one multi-RHS step is tens of ms: a sync per step is free
+      lagged_active = *active_host;
+      ++j;
+    }
+    // ---- x += V y per column
+    B_TRY(launch_k(kb_backsub, dim3(gc), dim3(128), 0, s, st, (const double2*)rcols, ldr, (const double2*)g, y, W,
+                   (const int*)ran));
+    B_TRY(launch_k(kb_axpy, dim3(g1), dim3(256), 0, s, (const double2* const*)Vp, j, (const double2*)y, x, n, W));
+    // columns still needing a cycle: stop == 2 (cycle exhausted, not capped)
+    std::vector<int> hstop(W);
+    TOEP_CUDA(cudaMemcpyAsync(hstop.data(), st.stop, sizeof(int) * W, cudaMemcpyDeviceToHost, s));
+    TOEP_CUDA(cudaStreamSynchronize(s));
+    bool more = false;
+    for (int c = 0; c < W; ++c) more |= (hstop[c] == 2);
+    if (!more) break;
+  }
+  // ---- exit residuals per column: ||b - A x|| / ||b||
+  B_TRY(matvec_impl(p->op, x, tmp, W, false, io64, nullptr, s));
+  double2* ax = tmp;
+  if (p->precond == TOEP_PC_FOLDED) {
+    B_TRY(block_apply_impl(p->pmat, p->pside, tmp, pb, n / p->pside, W, TOEP_C128, s, nullptr));
+    ax = pb;
+  }
+  B_TRY(launch_k(k_sub_b, dim3(g1), dim3(256), 0, s, b, (const double2*)ax, w, N));
+  std::vector<double> nr(static_cast<size_t>(nchunks) * W), nb(static_cast<size_t>(nchunks) * W);
+  B_TRY(launch_k(kb_norm, gridc, dim3(kCols), 0, s, (const double2*)w, n, W, nchunks, npart));
+  TOEP_CUDA(cudaMemcpyAsync(nr.data(), npart, sizeof(double) * nchunks * W, cudaMemcpyDeviceToHost, s));
+  TOEP_CUDA(cudaStreamSynchronize(s));
+  B_TRY(launch_k(kb_norm, gridc, dim3(kCols), 0, s, b, n, W, nchunks, npart));
+  TOEP_CUDA(cudaMemcpyAsync(nb.data(), npart, sizeof(double) * nchunks * W, cudaMemcpyDeviceToHost, s));
+  std::vector<int> it(W), cv(W), nh(W);
+  TOEP_CUDA(cudaMemcpyAsync(it.data(), st.total, sizeof(int) * W, cudaMemcpyDeviceToHost, s));
+  TOEP_CUDA(cudaMemcpyAsync(cv.data(), st.conv, sizeof(int) * W, cudaMemcpyDeviceToHost, s));
+  TOEP_CUDA(cudaMemcpyAsync(nh.data(), st.nhist, sizeof(int) * W, cudaMemcpyDeviceToHost, s));
+  const int64_t rows = std::min<int64_t>(hist_cap_rows, max_total + 2);
+  if (hist_host != nullptr && rows > 0)
+    TOEP_CUDA(cudaMemcpyAsync(hist_host, hist, sizeof(double) * rows * W, cudaMemcpyDeviceToHost, s));
+  TOEP_CUDA(cudaStreamSynchronize(s));
+  for (int c = 0; c < W; ++c) {
+    double sr = 0.0, sb = 0.0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      sr += nr[static_cast<size_t>(ch) * W + c];
+      sb += nb[static_cast<size_t>(ch) * W + c];
+    }
+    rep_final[c] = sb > 0 ? std::sqrt(sr) / std::sqrt(sb) : 0.0;
+    rep_iters[c] = it[c];
+    rep_conv[c] = cv[c];
+    rep_nhist[c] = nh[c];
+  }
+  cleanup();
+#undef B_ALLOC
+#undef B_TRY
+  return TOEP_OK;
+}
+
+}  // namespace toep
+
+extern "C" int toep_gmres_batched(const toep_gmres_problem_t* prob, const toep_gmres_cfg_t* cfg, const void* b,
+                                  void* x, void* stream, int32_t* iterations, int32_t* converged,
+                                  double* final_residual, int32_t* n_history, double* history, int64_t history_rows) {
+  TOEP_REQUIRE(prob != nullptr && cfg != nullptr && b != nullptr && x != nullptr && iterations != nullptr &&
+                   converged != nullptr && final_residual != nullptr && n_history != nullptr,
+               TOEP_ERR_ARG, "null argument");
+  return toep::gmres_batched_run(prob, cfg, static_cast<const double2*>(b), static_cast<double2*>(x),
+                                 static_cast<cudaStream_t>(stream), iterations, converged, final_residual, n_history,
+                                 history, history_rows);
+}

@@ -295,9 +295,81 @@ def solve_multi_rhs_vectorized(op, p, rhs, cfg: GmresConfig, method: str = "vect
     return xo, report
 
 
+def _run_batched(native: SpectralOperator, pc, b: torch.Tensor, cfg: GmresConfig, method: str):
+    """All columns through toep_gmres_batched (lock-step independent solves)."""
+    n, w = b.shape
+    prob = _lib.GmresProblem()
+    keep = []
+    t_build = 0.0
+    if pc is None or (isinstance(pc, Preconditioner) and pc.kind == "none"):
+        prob.op = native.handle
+        prob.precond = _lib.TOEP_PC_NONE
+    elif pc.kind == "pk" and pc.side == native.n0:
+        t0 = time.perf_counter()
+        folded = _folded(native, pc)
+        d = pc.device_blocks()
+        torch.cuda.current_stream().synchronize()
+        t_build = time.perf_counter() - t0
+        prob.op = folded.handle
+        prob.precond = _lib.TOEP_PC_FOLDED
+        prob.pinv, prob.pmat, prob.pside = d["pinv"].data_ptr(), d["pmat"].data_ptr(), pc.side
+        keep += [folded, d]
+    else:
+        d = pc.device_blocks()
+        prob.op = native.handle
+        prob.precond = _lib.TOEP_PC_BLOCK
+        prob.pinv, prob.pside = d["pinv"].data_ptr(), pc.side
+        keep.append(d)
+    prob.n, prob.w = n, w
+    max_total = min(cfg.max_iter, n)
+    rows = max_total + 2
+    iters = np.zeros(w, dtype=np.int32)
+    conv = np.zeros(w, dtype=np.int32)
+    final = np.zeros(w, dtype=np.float64)
+    nhist = np.zeros(w, dtype=np.int32)
+    hist = np.zeros((rows, w), dtype=np.float64)
+    c = _lib.GmresCfg(float(cfg.tol), int(cfg.max_iter), int(cfg.restart or 0), 0)
+    x = torch.empty_like(b)
+    t0 = time.perf_counter()
+    _lib.check(_lib.lib().toep_gmres_batched(ctypes.byref(prob), ctypes.byref(c), b.data_ptr(), x.data_ptr(),
+                                             _lib.stream_handle(), iters.ctypes.data, conv.ctypes.data,
+                                             final.ctypes.data, nhist.ctypes.data, hist.ctypes.data, rows),
+               "gmres_batched")
+    total = time.perf_counter() - t0 + t_build
+    reports = []
+    for col in range(w):
+        rep = SolveReport(method=method, iterations=int(iters[col]), converged=bool(conv[col]),
+                          residual_history=hist[: nhist[col], col].tolist(), final_residual=float(final[col]))
+        rep.phase_timings.update(precond_build=t_build, total=total)
+        rep.memory_estimate["krylov"] = rep.iterations * n * _BYTES_PER_SCALAR
+        reports.append(rep)
+    return x, reports
+
+
 def solve_multi_rhs_sequential(op, p, rhs, cfg: GmresConfig, method: str = "sequential"):
-    """Independent GMRES per column (gmres.py:304-336)."""
+    """Independent GMRES per column (gmres.py:304-336).
+
+    With a resident operator the columns run as one lock-step batch
+    (``toep_gmres_batched``): every Arnoldi step is one multi-RHS matvec whose
+    per-bin product is a tensor-core complex GEMM; each column keeps its own
+    Krylov space, rotations, history and stop flag, so its iterate and report
+    are those of an independent solve.
+    """
     b, origin = _as_block(rhs)
+    native = _native_op(op)
+    pre = _coerce_precond(p)
+    if native is not None and (pre is None or (isinstance(pre, Preconditioner) and pre.nb == 0)):
+        if native.dim != b.shape[0]:
+            raise ShapeError(f"rhs rows {b.shape[0]} != operator dim {native.dim}")
+        x, reports = _run_batched(native, pre, b, cfg, method)
+        for rep in reports:
+            _operator_memory(op, p, rep)
+        xo = restore(x, origin)
+        failed = [c for c, r in enumerate(reports) if not r.converged]
+        if failed:
+            raise NoConvergence(f"columns {failed} did not converge within {cfg.max_iter} iterations",
+                                solution=xo, reports=reports)
+        return xo, reports
     apply_op = op
     if _native_op(op) is None and not callable(op):
         apply_op = lambda x: bordered_matvec(op, x)  # noqa: E731

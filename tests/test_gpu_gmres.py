@@ -176,3 +176,56 @@ class TestBaselineCfg2:
         n = min(len(rep.residual_history), len(g[f"gm_{tag}_hist"]))
         assert np.allclose(rep.residual_history[:n], g[f"gm_{tag}_hist"][:n], rtol=1e-5, atol=1e-12)
         assert rel_err(x[::97, 0], g[f"gm_{tag}_x_sub"]) <= 1e-6
+
+
+class TestBatchedSequential:
+    """solve_multi_rhs_sequential runs all columns as one lock-step batch; each column must
+    reproduce its own independent solve (gmres.py:304-336)."""
+
+    @pytest.mark.parametrize("tag", ["none", "pk"])
+    def test_columns_match_independent_solves(self, tag):
+        sys_, op, pk = _cfg1()
+        p = pk if tag == "pk" else None
+        rng = np.random.default_rng(5)
+        v = np.zeros((sys_.dim, 6), dtype=np.complex128)
+        v[np.arange(6) * 32, np.arange(6)] = 1.0          # unit feeds of elements 0..5
+        v[:, 5] = random_complex(rng, sys_.dim)            # one dense column
+        cfg = GmresConfig(tol=1e-8, restart=30)
+        xs, reps = solve_multi_rhs_sequential(op, p, v, cfg)
+        for c in range(6):
+            xc, rc = gmres(lambda u: bordered_matvec(op, u), p, v[:, c], cfg)
+            assert abs(reps[c].iterations - rc.iterations) <= 1
+            n = min(len(reps[c].residual_history), len(rc.residual_history))
+            assert np.allclose(reps[c].residual_history[:n], rc.residual_history[:n], rtol=1e-6, atol=1e-13)
+            assert rel_err(xs[:, c], xc) <= 1e-7
+            assert reps[c].final_residual <= 1e-7
+
+    def test_zero_column_and_cap(self):
+        sys_, op, pk = _cfg1()
+        v = np.zeros((sys_.dim, 3), dtype=np.complex128)
+        v[0, 1] = 1.0
+        v[:, 2] = 1.0
+        with pytest.raises(NoConvergence) as err:
+            solve_multi_rhs_sequential(op, None, v, GmresConfig(tol=1e-12, max_iter=4))
+        reps = err.value.reports
+        assert reps[0].converged and reps[0].iterations == 0 and reps[0].residual_history == [0.0]
+        assert reps[1].iterations == 4 and not reps[1].converged
+        assert not np.any(err.value.solution[:, 0])
+
+
+@pytest.mark.slow
+class TestBaselineCfg3:
+    @pytest.mark.parametrize("tag", ["none", "pk"])
+    def test_per_column_iterations(self, tag):
+        g = golden("cfg3")
+        gen = generator_from_stacked(seeded_stacked4(30, 30, 256, seed=0))
+        sys_ = system_from_generator(gen)
+        op = BorderedOperator.from_system(sys_)
+        p = build_pk(sys_) if tag == "pk" else None
+        cols = [int(c) for c in g["percol"]]
+        b = np.zeros((sys_.dim, len(cols)), dtype=np.complex128)
+        b[np.array(cols) * 256, np.arange(len(cols))] = 1.0
+        x, reps = solve_multi_rhs_sequential(op, p, b, GmresConfig(tol=1e-6))
+        for k, col in enumerate(cols):
+            assert abs(reps[k].iterations - int(g[f"col{col}_{tag}_iters"])) <= 1
+            assert rel_err(x[::97, k], g[f"col{col}_{tag}_x_sub"]) <= 1e-5
