@@ -176,6 +176,23 @@ TOEP_API int toep_gmres_batched(const toep_gmres_problem_t* prob, const toep_gmr
                                 void* x, void* stream, int32_t* iterations, int32_t* converged,
                                 double* final_residual, int32_t* n_history, double* history, int64_t history_rows);
 
+/* ------------------------------------------------------------ direct solve
+ * numerics.py:67-96 lu_factor / lu_solve: in-place LU with partial pivoting of an n x n
+ * row-major complex128 device matrix (ipiv: device int[n], LAPACK-style row interchanges;
+ * info: device int, > 0 when a pivot is below 1e-300), and the solve A X = B for an
+ * (n, nrhs) row-major device block B (overwritten). */
+TOEP_API int toep_lu_factor(void* a, int n, int* ipiv, int* info, void* stream);
+TOEP_API int toep_lu_solve(const void* lu, int n, const int* ipiv, void* b, int64_t nrhs, void* stream);
+
+/* rybicki.py:63-144 rybicki_solve: blocks (2N-1, s, s) complex128 device, circulant order
+ * (block (i, j) of the system = blocks[(i - j) mod (2N-1)]); y, x: (N*s, w) device blocks.
+ * Returns TOEP_ERR_SINGULAR_BLOCK (R_0) or TOEP_ERR_SINGULAR_DENOM with *fail_step = m.
+ * hook (nullable): called after every stage with device views x (N,s,w), g, h (N-1,s,s)
+ * whose first `stage` entries are valid (rybicki.py:107-108,139-141 step_hook). */
+typedef int (*toep_stage_fn)(void* ctx, int stage, const void* x, const void* g, const void* h, void* stream);
+TOEP_API int toep_rybicki(const void* blocks, int N, int s, const void* y, void* x, int64_t w, int* fail_step,
+                          toep_stage_fn hook, void* hook_ctx, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

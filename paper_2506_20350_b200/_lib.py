@@ -46,6 +46,7 @@ c_vp = ctypes.c_void_p
 c_dbl = ctypes.c_double
 
 APPLY_FN = ctypes.CFUNCTYPE(c_int, c_vp, c_vp, c_vp, c_i64, c_vp)
+STAGE_FN = ctypes.CFUNCTYPE(c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp)
 
 
 class OpInfo(ctypes.Structure):
@@ -86,6 +87,9 @@ SIGNATURES = {
                           c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp]),
     "toep_gmres": (c_int, [ctypes.POINTER(GmresProblem), ctypes.POINTER(GmresCfg), c_vp, c_vp, c_vp,
                            ctypes.POINTER(GmresReport)]),
+    "toep_lu_factor": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp]),
+    "toep_lu_solve": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_vp]),
+    "toep_rybicki": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_i64, ctypes.POINTER(c_int), c_vp, c_vp, c_vp]),
     "toep_gmres_batched": (c_int, [ctypes.POINTER(GmresProblem), ctypes.POINTER(GmresCfg), c_vp, c_vp, c_vp,
                                    c_vp, c_vp, c_vp, c_vp, c_vp, c_i64]),
 }
