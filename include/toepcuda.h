@@ -90,6 +90,18 @@ TOEP_API int toep_op_fold_left(toep_op_t op, const void* m_dev, void* stream, to
  * fused into the first / last FFT pass.  v must not alias u. */
 TOEP_API int toep_matvec(toep_op_t op, const void* u, void* v, int64_t w, int flags, void* stream);
 
+/* Multi-GPU row / kx-slab decomposition (no reference counterpart:
+ * the reference is single-process).  toep_op_slab: operator holding only the bins with
+ * level-1 frequency kx in [kx0, kx1).  toep_matvec_stage: the local steps of one distributed
+ * matvec, the caller doing the two all-to-all exchanges in between:
+ *   stage 0: level-1 forward DFT of `count` array rows, in (count, n1, n0*w) -> out (count, l1, n0*w)
+ *   stage 1: slab spectral step (level-2 DFT, per-bin product, inverse level-2 DFT, kept rows),
+ *            in/out (n2, count = slab width, n0*w)
+ *   stage 2: level-1 inverse DFT + crop + 1/(l1*l2) of `count` rows, (count, l1, n0*w) -> (count, n1, n0*w) */
+TOEP_API int toep_op_slab(toep_op_t op, int kx0, int kx1, void* stream, toep_op_t* out);
+TOEP_API int toep_matvec_stage(toep_op_t op, int stage, const void* in, void* out, int64_t w, int count,
+                               void* stream);
+
 /* toeplitz.py:300 (flags & TOEP_MV_TRANSPOSE: :320): the per-bin product alone,
  * hat_out[k] = D_k @ hat_in[k] for every bin k, hat_* (bins, n0, w) in the
  * operator dtype.  This is the streaming kernel that carries >98% of the

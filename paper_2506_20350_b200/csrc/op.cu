@@ -344,8 +344,74 @@ int toep_op_fold_left(toep_op_t op, const void* m_dev, void* stream, toep_op_t* 
   return TOEP_OK;
 }
 
+int toep_op_slab(toep_op_t op, int kx0, int kx1, void* stream, toep_op_t* out) {
+  TOEP_REQUIRE(op != nullptr && out != nullptr && op->slab_kxs == 0, TOEP_ERR_ARG, "slab of a full operator only");
+  TOEP_REQUIRE(0 <= kx0 && kx0 < kx1 && kx1 <= op->l1, TOEP_ERR_SHAPE, "slab [%d,%d) outside [0,%d)", kx0, kx1, op->l1);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto* f = new (std::nothrow) toep_op_s();
+  TOEP_REQUIRE(f != nullptr, TOEP_ERR_OOM, "host allocation failed");
+  f->n2 = op->n2; f->n1 = op->n1; f->n0 = op->n0; f->l2 = op->l2; f->l1 = op->l1; f->dtype = op->dtype;
+  f->device = op->device; f->slab_k0 = kx0; f->slab_kxs = kx1 - kx0;
+  f->K = static_cast<int64_t>(op->l2) * f->slab_kxs;
+  const size_t blk = static_cast<size_t>(op->n0) * op->n0 * elt_size(op->dtype);
+  if (cudaMallocAsync(&f->DT, f->K * blk, s) != cudaSuccess) {
+    cudaGetLastError();
+    delete f;
+    set_error("out of device memory for the spectral slab");
+    return TOEP_ERR_OOM;
+  }
+  // one row of the (ky, kx) bin grid per ky: kxs contiguous bins
+  const cudaError_t e = cudaMemcpy2DAsync(f->DT, f->slab_kxs * blk, static_cast<const char*>(op->DT) + kx0 * blk,
+                                          op->l1 * blk, f->slab_kxs * blk, op->l2, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) {
+    cudaFree(f->DT);
+    delete f;
+    set_error("slab copy failed: %s", cudaGetErrorString(e));
+    return TOEP_ERR_CUDA;
+  }
+  *out = f;
+  return TOEP_OK;
+}
+
+int toep_matvec_stage(toep_op_t op, int stage, const void* in, void* out, int64_t w, int count, void* stream) {
+  TOEP_REQUIRE(op != nullptr && in != nullptr && out != nullptr && in != out && w >= 1 && count >= 0, TOEP_ERR_ARG,
+               "bad matvec_stage arguments");
+  if (count == 0) return TOEP_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int tc = op->dtype == TOEP_C64 ? 1 : 0;
+  const int64_t inner = static_cast<int64_t>(op->n0) * w;
+  if (stage == 0 || stage == 2) {  // level-1 forward / inverse pass over `count` array rows
+    PassArgs a;
+    a.in = in; a.out = out; a.L = op->l1; a.inner = inner; a.outer = count;
+    if (stage == 0) {
+      a.n_lo = op->n1; a.n_out = op->l1; a.in_sa = inner; a.in_so = op->n1 * inner; a.out_sa = inner;
+      a.out_so = op->l1 * inner; a.sign = -1; a.scale = 1.0;
+    } else {
+      a.n_lo = op->l1; a.n_out = op->n1; a.in_sa = inner; a.in_so = op->l1 * inner; a.out_sa = inner;
+      a.out_so = op->n1 * inner; a.sign = +1; a.scale = 1.0 / op->l1;
+    }
+    return fft_pass(a, tc, tc, tc, s);
+  }
+  TOEP_REQUIRE(stage == 1, TOEP_ERR_ARG, "unknown matvec stage %d", stage);
+  const int kxs = op->slab_kxs ? op->slab_kxs : op->l1;
+  TOEP_REQUIRE(count == kxs, TOEP_ERR_SHAPE, "slab width %d != operator slab %d", count, kxs);
+  toep_op_s::Workspace* ws = nullptr;
+  TOEP_TRY(op_workspace(op, w, s, &ws));
+  PassArgs b;  // level-2 DFT of the slab columns: (n2, kxs, inner) -> (l2, kxs, inner) = bins ky*kxs + kx
+  b.in = in; b.out = ws->hat; b.L = op->l2; b.n_lo = op->n2; b.n_out = op->l2; b.inner = inner; b.outer = kxs;
+  b.in_sa = kxs * inner; b.in_so = inner; b.out_sa = kxs * inner; b.out_so = inner; b.sign = -1; b.scale = 1.0;
+  TOEP_TRY(fft_pass(b, tc, tc, tc, s));
+  TOEP_TRY(bin_product(op->dtype, op->DT, ws->hat, ws->hat2, op->K, op->n0, w, false, nullptr, s));
+  PassArgs c;  // inverse level-2 DFT, kept rows only
+  c.in = ws->hat2; c.out = out; c.L = op->l2; c.n_lo = op->l2; c.n_out = op->n2; c.inner = inner; c.outer = kxs;
+  c.in_sa = kxs * inner; c.in_so = inner; c.out_sa = kxs * inner; c.out_so = inner; c.sign = +1;
+  c.scale = 1.0 / op->l2;
+  return fft_pass(c, tc, tc, tc, s);
+}
+
 int toep_matvec(toep_op_t op, const void* u, void* v, int64_t w, int flags, void* stream) {
   TOEP_REQUIRE(op != nullptr && (w == 0 || (u != nullptr && v != nullptr)), TOEP_ERR_ARG, "null argument");
+  TOEP_REQUIRE(op->slab_kxs == 0, TOEP_ERR_ARG, "a slab operator is applied through toep_matvec_stage");
   TOEP_REQUIRE(w >= 0, TOEP_ERR_SHAPE, "negative column count");
   TOEP_REQUIRE(u != v, TOEP_ERR_ARG, "matvec output must not alias its input");
   return matvec_impl(op, u, v, w, (flags & TOEP_MV_TRANSPOSE) != 0, (flags & TOEP_MV_IO_C128) != 0, nullptr,

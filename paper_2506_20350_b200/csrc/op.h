@@ -19,6 +19,9 @@ struct toep_op_s {
     void* parts = nullptr; // fused path: [l1][maxp][n2][n0] inverse level-2 partial slabs
     int* cnt = nullptr;    // fused path: [l1] slab arrival counters
   };
+  // kx-slab operator of the multi-GPU row/slab decomposition (toep_op_slab): bins
+  // k' = ky*slab_kxs + (kx - slab_k0); 0 = full operator
+  int slab_k0 = 0, slab_kxs = 0;
   // fused single-RHS path (fused.cu): kx-major persistent partition
   int fused_grid = 0;
   int fused_maxp = 0;
