@@ -152,6 +152,11 @@ typedef struct {
   toep_apply_fn papply;
   void* papply_ctx;
   int64_t n, w;               /* the Krylov vectors are (n, w) complex128 blocks     */
+  /* distributed Krylov vectors (rows split over ranks, e.g. the slab-decomposed matvec):
+   * every inner product / norm is summed over ranks by allreduce(ctx, buf, ndoubles, stream)
+   * on a device buffer, enqueued on `stream` (NCCL all-reduce).  NULL: single process. */
+  int (*allreduce)(void* ctx, void* buf, int64_t ndoubles, void* stream);
+  void* allreduce_ctx;
 } toep_gmres_problem_t;
 
 typedef struct {

@@ -47,6 +47,7 @@ c_dbl = ctypes.c_double
 
 APPLY_FN = ctypes.CFUNCTYPE(c_int, c_vp, c_vp, c_vp, c_i64, c_vp)
 STAGE_FN = ctypes.CFUNCTYPE(c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(c_int, c_vp, c_vp, c_i64, c_vp)
 
 
 class OpInfo(ctypes.Structure):
@@ -57,7 +58,7 @@ class OpInfo(ctypes.Structure):
 class GmresProblem(ctypes.Structure):
     _fields_ = [("op", c_vp), ("apply", APPLY_FN), ("apply_ctx", c_vp), ("precond", c_i32), ("pside", c_i32),
                 ("pinv", c_vp), ("pmat", c_vp), ("papply", APPLY_FN), ("papply_ctx", c_vp),
-                ("n", c_i64), ("w", c_i64)]
+                ("n", c_i64), ("w", c_i64), ("allreduce", ALLREDUCE_FN), ("allreduce_ctx", c_vp)]
 
 
 class GmresCfg(ctypes.Structure):

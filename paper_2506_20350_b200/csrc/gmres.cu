@@ -221,6 +221,29 @@ k_norm2(const double2* __restrict__ x, int64_t N, double* __restrict__ partial) 
   if (threadIdx.x == 0) partial[blockIdx.x] = t;
 }
 
+// out[0] = sum_b part[b] (one warp, fixed order per lane + butterfly)
+__global__ void k_collapse_d(const double* __restrict__ part, int nblk, double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += 32) s += part[b];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+// out[l] = sum_b part[l*nblk + b], l < m (warp per l)
+__global__ void k_collapse_c(const double2* __restrict__ part, int m, int nblk, double2* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int l = warp; l < m; l += blockDim.x / 32) {
+    double2 s = make_double2(0, 0);
+    for (int b = lane; b < nblk; b += 32) s = cadd(s, part[l * nblk + b]);
+    s = warp_sum(s);
+    if (lane == 0) out[l] = s;
+  }
+}
+
 __device__ double sum_partials_warp(const double* p, int n) {
   double s = 0.0;
   for (int b = threadIdx.x; b < n; b += 32) s += p[b];
@@ -472,10 +495,49 @@ struct Engine {
   int norm2_partials(const double2* x) {
     return launch_k(k_norm2, dim3(nblk), dim3(kThreads), 0, s, x, N, norm_partial);
   }
+
+  // ---- distributed reductions (rows split over ranks): collapse the per-CTA partials to one
+  // value per quantity, all-reduce it over ranks, hand (buffer, 1) to the consumer kernel
+  double* nred = nullptr;    // [1]
+  double2* hred = nullptr;   // [ldr]
+  bool distributed() const { return p->allreduce != nullptr; }
+  int allreduce(void* buf, int64_t ndoubles) {
+    const int rc = p->allreduce(p->allreduce_ctx, buf, ndoubles, s);
+    TOEP_REQUIRE(rc == 0, TOEP_ERR_CUDA, "allreduce callback failed (%d)", rc);
+    return TOEP_OK;
+  }
+  // norm partials -> (ptr, count) for k_init / k_cycle_start / k_givens
+  int finish_norm(const double** ptr, int* count) {
+    if (!distributed()) {
+      *ptr = norm_partial;
+      *count = nblk;
+      return TOEP_OK;
+    }
+    TOEP_TRY(launch_k(k_collapse_d, dim3(1), dim3(32), 0, s, (const double*)norm_partial, nblk, nred));
+    TOEP_TRY(allreduce(nred, 1));
+    *ptr = nred;
+    *count = 1;
+    return TOEP_OK;
+  }
+  int finish_dots(const double2* part, int m, const double2** ptr, int* count) {
+    if (!distributed()) {
+      *ptr = part;
+      *count = nblk;
+      return TOEP_OK;
+    }
+    TOEP_TRY(launch_k(k_collapse_c, dim3(1), dim3(256), 0, s, part, m, nblk, hred));
+    TOEP_TRY(allreduce(hred, 2 * static_cast<int64_t>(m)));
+    *ptr = hred;
+    *count = 1;
+    return TOEP_OK;
+  }
   double host_norm(const double2* x) {
-    std::vector<double> h(nblk);
     if (norm2_partials(x) != TOEP_OK) return -1.0;
-    cudaMemcpyAsync(h.data(), norm_partial, nblk * sizeof(double), cudaMemcpyDeviceToHost, s);
+    const double* ptr = nullptr;
+    int cnt = 0;
+    if (finish_norm(&ptr, &cnt) != TOEP_OK) return -1.0;
+    std::vector<double> h(cnt);
+    cudaMemcpyAsync(h.data(), ptr, cnt * sizeof(double), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     double t = 0.0;
     for (double v : h) t += v;
@@ -531,7 +593,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   auto cleanup = [&]() {
     for (void* q : {(void*)V, (void*)tmp, (void*)tmp2, (void*)pb, (void*)h1, (void*)rcols, (void*)sn, (void*)g,
                     (void*)y, (void*)part1, (void*)part2, (void*)cs, (void*)hist, (void*)vs, (void*)st,
-                    (void*)e.norm_partial})
+                    (void*)e.norm_partial, (void*)e.nred, (void*)e.hred})
       if (q) cudaFreeAsync(q, s);
     cudaStreamSynchronize(s);
     res.used = 0;
@@ -571,6 +633,10 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   G_ALLOC(e.norm_partial, nblk);
   G_ALLOC(part1, (int64_t)nblk * ldr);
   G_ALLOC(part2, (int64_t)nblk * ldr);
+  if (e.distributed()) {
+    G_ALLOC(e.nred, 1);
+    G_ALLOC(e.hred, ldr);
+  }
   hf->stop = 0;
   hf->total = 0;
   hf->converged = 0;
@@ -610,8 +676,11 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     }
     if (timed) mark(1, t0);
   }
+  const double* nptr = nullptr;
+  int ncnt = 0;
   G_TRY(e.norm2_partials(zb));
-  G_TRY(launch_k(k_init, dim3(1), dim3(32), 0, s, st, e.norm_partial, nblk, hist));
+  G_TRY(e.finish_norm(&nptr, &ncnt));
+  G_TRY(launch_k(k_init, dim3(1), dim3(32), 0, s, st, nptr, ncnt, hist));
   GState hst{};
   if (cudaMemcpyAsync(&hst, st, sizeof(GState), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
       cudaStreamSynchronize(s) != cudaSuccess) {
@@ -662,8 +731,8 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     }
     first = false;
     G_TRY(e.norm2_partials(v0));
-    G_TRY(launch_k(k_cycle_start, dim3(1), dim3(32), 0, s, st, (const double*)e.norm_partial, nblk, cfg->tol, g, vs,
-                   hf_dev));
+    G_TRY(e.finish_norm(&nptr, &ncnt));
+    G_TRY(launch_k(k_cycle_start, dim3(1), dim3(32), 0, s, st, nptr, ncnt, cfg->tol, g, vs, hf_dev));
 
     // ---- Arnoldi steps (gmres.py:146-190)
     int j = 0;
@@ -683,16 +752,20 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
         if (timed) t0 = mark(0, t0);
       }
       const int m = j + 1;
+      const double2* dptr = nullptr;
+      int dcnt = 0;
       G_TRY(launch_k(k_dots, dim3(nblk), dim3(kThreads), 0, s, (const double2*)V, N, m, (const double2*)w, N, part1,
                      (const int*)stop_dev));
+      G_TRY(e.finish_dots(part1, m, &dptr, &dcnt));
       G_TRY(launch_k(k_upd, dim3(nblk), dim3(kThreads), coef_smem, s, (const double2*)V, N, m, (const double*)vs,
-                     (const double2*)part1, nblk, w, N, 1, h1, (const double2*)nullptr, part2, (double*)nullptr,
-                     (const int*)stop_dev));
+                     dptr, dcnt, w, N, 1, h1, (const double2*)nullptr, part2, (double*)nullptr, (const int*)stop_dev));
+      G_TRY(e.finish_dots(part2, m, &dptr, &dcnt));
       G_TRY(launch_k(k_upd, dim3(nblk), dim3(kThreads), coef_smem, s, (const double2*)V, N, m, (const double*)vs,
-                     (const double2*)part2, nblk, w, N, 2, rcols + (int64_t)j * ldr, (const double2*)h1,
-                     (double2*)nullptr, e.norm_partial, (const int*)stop_dev));
-      G_TRY(launch_k(k_givens, dim3(1), dim3(32), 0, s, st, (const double*)e.norm_partial, nblk, rcols, ldr, cs, sn, g,
-                     hist, vs, cfg->tol, static_cast<int>(max_total), cycle_len, hf_dev));
+                     dptr, dcnt, w, N, 2, rcols + (int64_t)j * ldr, (const double2*)h1, (double2*)nullptr,
+                     e.norm_partial, (const int*)stop_dev));
+      G_TRY(e.finish_norm(&nptr, &ncnt));
+      G_TRY(launch_k(k_givens, dim3(1), dim3(32), 0, s, st, nptr, ncnt, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
+                     static_cast<int>(max_total), cycle_len, hf_dev));
       if (timed) mark(2, t0);
       cudaEvent_t ev = res.event();
       cudaEventRecord(ev, s);

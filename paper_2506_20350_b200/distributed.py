@@ -196,6 +196,38 @@ class SlabOperator:
         return float(t.sqrt().item())
 
 
+def gmres_slab(op: SlabOperator, p, b_local, cfg):
+    """GMRES (gmres.py:98-249 semantics) on row-distributed vectors of a SlabOperator.
+
+    The device Arnoldi engine (toep_gmres) runs on every rank over the local rows; the
+    matvec is the distributed ``op.matvec_local`` (two all-to-alls), every inner product and
+    norm is all-reduced over the group on the device stream, so all ranks follow identical
+    scalar recurrences (same iterations, same stop step).  ``p``: None or an element-block
+    preconditioner (P_K, local to each row block).  Returns this rank's rows of x.
+    """
+    from .solvers.gmres import _run
+    from .errors import NoConvergence
+    from ._tensor import to_columns, restore
+
+    b, origin = to_columns(b_local)
+    if b.shape[0] != op.local_dim:
+        raise ShapeError(f"local rhs rows {b.shape[0]} != {op.local_dim}")
+    group = op.group
+    world = op.world
+
+    def allreduce(t):
+        if world > 1:
+            dist.all_reduce(t, group=group)
+
+    x, report = _run(lambda v: op.matvec_local(v), p, b, cfg, prefer_numpy=False, allreduce=allreduce)
+    report.method = "gmres-slab"
+    xo = restore(x, origin)
+    if not report.converged:
+        raise NoConvergence(f"distributed GMRES stopped after {report.iterations} iterations", solution=xo,
+                            report=report)
+    return xo, report
+
+
 class DeviceSlabStages:
     """The three local stages of SlabOperator on the device (toep_matvec_stage)."""
 

@@ -174,11 +174,40 @@ class _Callback:
             return 1
 
 
-def _run(apply_op, precond, b: torch.Tensor, cfg: GmresConfig, prefer_numpy: bool, timings: bool = True):
-    """Run toep_gmres on a device (n, w) complex128 block; returns (x, SolveReport)."""
+class _AllReduce:
+    """C callback: sum a device float64 buffer over the process group (NCCL, stream ordered)."""
+
+    def __init__(self, fn):
+        self.fn = fn
+        self.error = None
+        self.cfunc = _lib.ALLREDUCE_FN(self._call)
+
+    def _call(self, ctx, ptr, ndoubles, stream):
+        try:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            view = {"shape": (ndoubles,), "typestr": "<f8", "data": (ptr, False), "version": 3, "strides": None}
+            t = torch.as_tensor(type("V", (), {"__cuda_array_interface__": view})(), device=dev)
+            self.fn(t)
+            return 0
+        except BaseException as exc:  # noqa: BLE001
+            self.error = exc
+            return 1
+
+
+def _run(apply_op, precond, b: torch.Tensor, cfg: GmresConfig, prefer_numpy: bool, timings: bool = True,
+         allreduce=None):
+    """Run toep_gmres on a device (n, w) complex128 block; returns (x, SolveReport).
+
+    ``allreduce(t)``: optional in-place sum of a device float64 tensor over ranks, for
+    Krylov vectors distributed by rows (distributed.gmres_slab).
+    """
     n, w = b.shape
     prob = _lib.GmresProblem()
     keep = []  # keep ctypes callbacks / tensors alive for the call
+    if allreduce is not None:
+        ar = _AllReduce(allreduce)
+        prob.allreduce = ar.cfunc
+        keep.append(ar)
     native = _native_op(apply_op)
     report = SolveReport()
     t_build = 0.0

@@ -33,6 +33,23 @@ def test_device_slab_stages_match_matvec(dims, world):
     assert rel_err(got.cpu().numpy(), want.cpu().numpy()) <= 1e-12
 
 
+@pytest.mark.parametrize("tag", ["none", "pk"])
+def test_gmres_slab_world1_matches_native(tag):
+    from paper_2506_20350_b200.distributed import gmres_slab
+    from paper_2506_20350_b200.problems import system_from_generator, unit_feed_rhs
+    from paper_2506_20350_b200.solvers import BorderedOperator, GmresConfig, build_pk, solve_multi_rhs_vectorized
+
+    gen = generator_from_stacked(seeded_stacked4(4, 4, 32, seed=0))
+    sys_ = system_from_generator(gen)
+    p = build_pk(sys_) if tag == "pk" else None
+    b = unit_feed_rhs(4, 4, 32)
+    cfg = GmresConfig(tol=1e-8, restart=30)
+    x, rep = gmres_slab(SlabOperator.from_generator(gen), p, b, cfg)
+    xn, rn = solve_multi_rhs_vectorized(BorderedOperator.from_system(sys_), p, b[:, None], cfg)
+    assert abs(rep.iterations - rn.iterations) <= 1
+    assert rel_err(x, xn[:, 0]) <= 1e-7
+
+
 def test_world1_slab_operator():
     gen = generator_from_stacked(seeded_stacked4(8, 8, 64, seed=2))
     op = SlabOperator.from_generator(gen)
