@@ -87,35 +87,39 @@ __device__ __forceinline__ Z block_sum(Z v, Z* red /* [kThreads/32] */) {
 }
 __device__ __forceinline__ double2 operator+(double2 a, double2 b) { return cadd(a, b); }
 
-// partial[l*nblk + cta] = sum_{i in cta} conj(V_l[i]) w[i], l < m
+// CTA b of nblk owns the contiguous element range [c0, c1) (32-aligned starts, coalesced)
+__device__ __forceinline__ void chunk_of(int64_t N, int64_t* c0, int64_t* c1) {
+  const int64_t b = blockIdx.x, nb = gridDim.x;
+  *c0 = ((N * b / nb) / 32) * 32;
+  *c1 = (b + 1 == nb) ? N : ((N * (b + 1) / nb) / 32) * 32;
+}
+
+constexpr int kDG = 4;  // basis vectors per warp in the dot kernels
+
+// partial[l*nblk + cta] = sum_{i in chunk} conj(V_l[i]) w[i], l < m.  Each warp takes groups of
+// kDG basis vectors over the whole chunk (independent loads in flight, no block barrier).
 __device__ __forceinline__ void dots_into(const double2* __restrict__ V, int64_t ld, int m,
                                           const double2* __restrict__ w, int64_t N, double2* __restrict__ partial) {
-  __shared__ double2 red[kThreads / 32][kLG];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nblk = gridDim.x;
-  for (int l0 = 0; l0 < m; l0 += kLG) {
-    double2 acc[kLG];
+  int64_t c0, c1;
+  chunk_of(N, &c0, &c1);
+  for (int l0 = warp * kDG; l0 < m; l0 += (kThreads / 32) * kDG) {
+    double2 acc[kDG];
 #pragma unroll
-    for (int g = 0; g < kLG; ++g) acc[g] = make_double2(0, 0);
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < N;
-         i += static_cast<int64_t>(nblk) * kThreads) {
+    for (int g = 0; g < kDG; ++g) acc[g] = make_double2(0, 0);
+#pragma unroll 2
+    for (int64_t i = c0 + lane; i < c1; i += 32) {
       const double2 wi = w[i];
 #pragma unroll
-      for (int g = 0; g < kLG; ++g)
+      for (int g = 0; g < kDG; ++g)
         if (l0 + g < m) cfmac(acc[g], V[(l0 + g) * ld + i], wi);
     }
 #pragma unroll
-    for (int g = 0; g < kLG; ++g) {
+    for (int g = 0; g < kDG; ++g) {
       const double2 s = warp_sum(acc[g]);
-      if (lane == 0) red[warp][g] = s;
+      if (lane == 0 && l0 + g < m) partial[(l0 + g) * nblk + blockIdx.x] = s;
     }
-    __syncthreads();
-    if (threadIdx.x < kLG && l0 + threadIdx.x < m) {
-      double2 s = red[0][threadIdx.x];
-      for (int ww = 1; ww < kThreads / 32; ++ww) s = cadd(s, red[ww][threadIdx.x]);
-      partial[(l0 + threadIdx.x) * nblk + blockIdx.x] = s;
-    }
-    __syncthreads();
   }
 }
 
@@ -158,8 +162,9 @@ k_upd(const double2* __restrict__ V, int64_t ld, int m, const double* __restrict
   }
   __syncthreads();
   double nrm = 0.0;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < N;
-       i += static_cast<int64_t>(gridDim.x) * kThreads) {
+  int64_t c0, c1;
+  chunk_of(N, &c0, &c1);
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += kThreads) {
     double2 acc = w[i];
     int l = 0;
     for (; l + 3 < m; l += 4) {
@@ -314,25 +319,38 @@ __global__ void k_cycle_start(GState* st, const double* partial, int nblk, doubl
   }
 }
 
-// one Givens step on column j = st->m (gmres.py:160-189)
-__global__ void k_givens(GState* st, const double* norm_partial, int nblk, double2* rcols, int ldr, double* cs,
-                         double2* sn, double2* g, double* hist, double* vs, double tol, int max_total, int cycle_len,
-                         HostFlags* hf) {
-  pdl_wait();
-  pdl_trigger();
-  if (st->stop) return;
-  const double hn2 = sum_partials_warp(norm_partial, nblk);
-  if (threadIdx.x != 0) return;
+// one Givens step on column j = st->m (gmres.py:160-189), executed by one warp;
+// hn2 = ||w||^2, gsm: shared scratch of (2*16 + 8)*(j+1) bytes
+__device__ void givens_warp(GState* st, double hn2, double2* rcols, int ldr, double* cs, double2* sn, double2* g,
+                            double* hist, double* vs, double tol, int max_total, int cycle_len, HostFlags* hf,
+                            double2* gsm) {
   const int j = st->m;
-  const double hnext = sqrt(hn2);
-  double2* hcol = rcols + static_cast<int64_t>(j) * ldr;  // hcol[0..j] = h1 + h2 (k_upd mode 2)
-  for (int i = 0; i < j; ++i) {
-    const double2 a0 = hcol[i], a1 = hcol[i + 1];
-    const double c = cs[i];
-    const double2 s = sn[i];
-    hcol[i] = cadd(cscale(a0, c), cmul(s, a1));
-    hcol[i + 1] = cadd(cscale(cmulc(s, a0), -1.0), cscale(a1, c));
+  double2* hcol_g = rcols + static_cast<int64_t>(j) * ldr;  // hcol[0..j] = h1 + h2
+  // stage the column and the previous rotations in shared memory (one parallel load instead of
+  // a chain of dependent global accesses), rotate on lane 0, write the column back
+  double2* hcol = gsm;                                      // [j+1]
+  double2* snl = gsm + (j + 1);                             // [j]
+  double* csl = reinterpret_cast<double*>(snl + j);         // [j]
+  for (int i = threadIdx.x; i <= j; i += 32) hcol[i] = hcol_g[i];
+  for (int i = threadIdx.x; i < j; i += 32) {
+    snl[i] = sn[i];
+    csl[i] = cs[i];
   }
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < j; ++i) {
+      const double2 a0 = hcol[i], a1 = hcol[i + 1];
+      const double c = csl[i];
+      const double2 s = snl[i];
+      hcol[i] = cadd(cscale(a0, c), cmul(s, a1));
+      hcol[i + 1] = cadd(cscale(cmulc(s, a0), -1.0), cscale(a1, c));
+    }
+  }
+  __syncwarp();
+  for (int i = threadIdx.x; i < j; i += 32) hcol_g[i] = hcol[i];
+  __syncwarp();
+  if (threadIdx.x != 0) return;
+  const double hnext = sqrt(hn2);
   // _givens(hcol[j], hnext) (gmres.py:87-95)
   const double2 a = hcol[j];
   const double absa = hypot(a.x, a.y);
@@ -349,7 +367,7 @@ __global__ void k_givens(GState* st, const double* norm_partial, int nblk, doubl
     s = cscale(alpha, hnext / t);
     r = cscale(alpha, t);
   }
-  hcol[j] = r;
+  hcol_g[j] = r;
   cs[j] = c;
   sn[j] = s;
   const double2 gj = g[j];
@@ -376,6 +394,173 @@ __global__ void k_givens(GState* st, const double* norm_partial, int nblk, doubl
   hf->total = st->total;
   hf->converged = st->converged;
   hf->breakdown = st->breakdown;
+}
+
+__global__ void k_givens(GState* st, const double* norm_partial, int nblk, double2* rcols, int ldr, double* cs,
+                         double2* sn, double2* g, double* hist, double* vs, double tol, int max_total, int cycle_len,
+                         HostFlags* hf) {
+  pdl_wait();
+  pdl_trigger();
+  if (st->stop) return;
+  extern __shared__ double2 gsm[];
+  const double hn2 = sum_partials_warp(norm_partial, nblk);
+  givens_warp(st, hn2, rcols, ldr, cs, sn, g, hist, vs, tol, max_total, cycle_len, hf, gsm);
+}
+
+// ------------------------------------------------------------------------------------------
+// The whole CGS2 orthogonalisation + Givens step of one Arnoldi step as ONE cooperative kernel
+// (all CTAs co-resident, one per SM, 1024 threads): dots -> grid barrier -> coefficients
+// (every CTA reduces the per-CTA partials in the same order) -> update + dots -> barrier ->
+// update + norm -> barrier -> Givens on CTA 0.  Replaces 4 launches and their drain / ramp
+// gaps; 32 warps per SM keep enough L2 requests in flight for the basis sweeps.
+constexpr int kCoopThreads = 1024;
+
+struct OrthArgs {
+  const double2* V;
+  int64_t N;        // vector length = basis stride
+  int m;            // basis vectors v_0..v_{m-1}
+  const double* vs; // lazy scales
+  double2* w;       // = V_m, updated in place
+  double2* part;    // [ldr][nblk] dot partials
+  double* npart;    // [nblk]
+  double2* h1;      // [ldr]
+  GState* st;
+  double2* rcols;
+  int ldr;
+  double* cs;
+  double2* sn;
+  double2* g;
+  double* hist;
+  double* vsw;      // vs (written by Givens)
+  double tol;
+  int max_total, cycle_len;
+  HostFlags* hf;
+  unsigned* bar;    // [2] grid barrier: arrival count, generation
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned gen = *vgen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// coef[l] = vs_l * (vs_l * sum_b part[l][b]); CTA 0 stores h (mode 1) or hprev + h (mode 2)
+__device__ __forceinline__ void orth_coefs(const OrthArgs& a, double2* coef, int mode, double2* hout) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nblk = gridDim.x;
+  for (int l = warp; l < a.m; l += kCoopThreads / 32) {
+    double2 s = make_double2(0, 0);
+    for (int b = lane; b < nblk; b += 32) s = cadd(s, __ldcg(a.part + static_cast<int64_t>(l) * nblk + b));
+    s = warp_sum(s);
+    if (lane == 0) {
+      const double2 h = cscale(s, a.vs[l]);
+      coef[l] = cscale(h, a.vs[l]);
+      if (blockIdx.x == 0) hout[l] = (mode == 1) ? h : cadd(a.h1[l], h);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double orth_update(const OrthArgs& a, const double2* coef, int64_t c0, int64_t c1) {
+  double nrm = 0.0;
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += kCoopThreads) {
+    double2 acc = a.w[i];
+    int l = 0;
+    for (; l + 3 < a.m; l += 4) {
+      const double2 v0 = a.V[l * a.N + i], v1 = a.V[(l + 1) * a.N + i], v2 = a.V[(l + 2) * a.N + i],
+                    v3 = a.V[(l + 3) * a.N + i];
+      cfma(acc, v0, make_double2(-coef[l].x, -coef[l].y));
+      cfma(acc, v1, make_double2(-coef[l + 1].x, -coef[l + 1].y));
+      cfma(acc, v2, make_double2(-coef[l + 2].x, -coef[l + 2].y));
+      cfma(acc, v3, make_double2(-coef[l + 3].x, -coef[l + 3].y));
+    }
+    for (; l < a.m; ++l) cfma(acc, a.V[l * a.N + i], make_double2(-coef[l].x, -coef[l].y));
+    a.w[i] = acc;
+    nrm = fma(acc.x, acc.x, fma(acc.y, acc.y, nrm));
+  }
+  return nrm;
+}
+
+// all 1024 threads sweep the chunk (element-parallel, every basis vector), per-warp partials
+// meet in shared memory: red [32][m]
+__device__ __forceinline__ void orth_dots(const OrthArgs& a, int64_t c0, int64_t c1, double2* red) {
+  constexpr int G = 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nblk = gridDim.x;
+  for (int l0 = 0; l0 < a.m; l0 += G) {
+    double2 acc[G];
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) acc[gg] = make_double2(0, 0);
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += kCoopThreads) {
+      const double2 wi = a.w[i];
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg)
+        if (l0 + gg < a.m) cfmac(acc[gg], a.V[(l0 + gg) * a.N + i], wi);
+    }
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      const double2 s = warp_sum(acc[gg]);
+      if (lane == 0 && l0 + gg < a.m) red[warp * a.ldr + l0 + gg] = s;
+    }
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < a.m; l += kCoopThreads) {
+    double2 s = red[l];
+    for (int ww = 1; ww < kCoopThreads / 32; ++ww) s = cadd(s, red[ww * a.ldr + l]);
+    a.part[static_cast<int64_t>(l) * nblk + blockIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const int* stop) {
+  pdl_wait();
+  pdl_trigger();
+  if (*stop) return;  // uniform across the grid (written by the previous step, read-only here)
+  extern __shared__ double2 osm[];  // coef [ldr] | dot partials [32][ldr]; Givens scratch reuses it
+  __shared__ double red[kCoopThreads / 32];
+  double2* coef = osm;
+  double2* dred = osm + a.ldr;
+  int64_t c0, c1;
+  chunk_of(a.N, &c0, &c1);
+  // pass 1: h1 = V^H w
+  orth_dots(a, c0, c1, dred);
+  grid_barrier(a.bar);
+  orth_coefs(a, coef, 1, a.h1);
+  orth_update(a, coef, c0, c1);
+  __syncthreads();
+  // pass 2 (re-orthogonalisation): h2 = V^H w', H[:, j] = h1 + h2
+  orth_dots(a, c0, c1, dred);
+  grid_barrier(a.bar);
+  double2* hcol = a.rcols + static_cast<int64_t>(a.st->m) * a.ldr;
+  orth_coefs(a, coef, 2, hcol);
+  double nrm = orth_update(a, coef, c0, c1);
+  nrm = warp_sum(nrm);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = red[0];
+    for (int ww = 1; ww < kCoopThreads / 32; ++ww) t += red[ww];
+    a.npart[blockIdx.x] = t;
+  }
+  grid_barrier(a.bar);
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32) s += __ldcg(a.npart + b);
+    s = warp_sum(s);
+    givens_warp(a.st, s, a.rcols, a.ldr, a.cs, a.sn, a.g, a.hist, a.vsw, a.tol, a.max_total, a.cycle_len, a.hf, osm);
+  }
 }
 
 // y = R^-1 g (gmres.py:193-204), R upper triangular from the rotated columns
@@ -585,6 +770,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   double2 *rcols = nullptr, *sn = nullptr, *g = nullptr, *y = nullptr, *part1 = nullptr, *part2 = nullptr;
   double *cs = nullptr, *hist = nullptr, *vs = nullptr;
   GState* st = nullptr;
+  unsigned* bar = nullptr;  // grid barrier of k_orth_coop
   HostRes& res = host_res();
   res.used = 0;
   HostFlags* hf = res.hf;
@@ -593,7 +779,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   auto cleanup = [&]() {
     for (void* q : {(void*)V, (void*)tmp, (void*)tmp2, (void*)pb, (void*)h1, (void*)rcols, (void*)sn, (void*)g,
                     (void*)y, (void*)part1, (void*)part2, (void*)cs, (void*)hist, (void*)vs, (void*)st,
-                    (void*)e.norm_partial, (void*)e.nred, (void*)e.hred})
+                    (void*)e.norm_partial, (void*)e.nred, (void*)e.hred, (void*)bar})
       if (q) cudaFreeAsync(q, s);
     cudaStreamSynchronize(s);
     res.used = 0;
@@ -637,6 +823,25 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     G_ALLOC(e.nred, 1);
     G_ALLOC(e.hred, ldr);
   }
+  // single-kernel cooperative orthogonalisation when all CTAs fit co-resident
+  G_ALLOC(bar, 2);
+  TOEP_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s));
+  const size_t coop_smem = std::max(sizeof(double2) * ldr * (1 + kCoopThreads / 32),
+                                    (2 * sizeof(double2) + sizeof(double)) * ldr);
+  const int coop_grid = nblk;
+  bool use_coop = !e.distributed() && [] {
+    const char* v = std::getenv("TOEP_COOP");
+    return !(v != nullptr && v[0] == '0');
+  }();
+  if (use_coop) {
+    if (coop_smem > 48 * 1024)
+      cudaFuncSetAttribute(k_orth_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_orth_coop, kCoopThreads, coop_smem) != cudaSuccess ||
+        per_sm * sms < coop_grid)
+      use_coop = false;
+    cudaGetLastError();
+  }
   hf->stop = 0;
   hf->total = 0;
   hf->converged = 0;
@@ -658,6 +863,9 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     return a;
   };
   const size_t coef_smem = sizeof(double2) * ldr;
+  const size_t givens_smem = (2 * sizeof(double2) + sizeof(double)) * ldr;
+  if (givens_smem > 48 * 1024)
+    cudaFuncSetAttribute(k_givens, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)givens_smem);
   if (coef_smem > 48 * 1024) {
     cudaFuncSetAttribute(k_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coef_smem);
     cudaFuncSetAttribute(k_axpy_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coef_smem);
@@ -752,6 +960,18 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
         if (timed) t0 = mark(0, t0);
       }
       const int m = j + 1;
+      if (use_coop) {
+        OrthArgs oa{V, N, m, vs, w, part1, e.norm_partial, h1, st, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
+                    static_cast<int>(max_total), cycle_len, hf_dev, bar};
+        rc = launch_coop(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa, (const int*)stop_dev);
+        if (rc != TOEP_OK) {  // cooperative launch unavailable: permanent fallback to the 4-kernel chain
+          use_coop = false;
+          rc = TOEP_OK;
+        }
+      }
+      if (use_coop) {
+        // orthogonalisation + Givens done by k_orth_coop
+      } else {
       const double2* dptr = nullptr;
       int dcnt = 0;
       G_TRY(launch_k(k_dots, dim3(nblk), dim3(kThreads), 0, s, (const double2*)V, N, m, (const double2*)w, N, part1,
@@ -764,8 +984,9 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
                      dptr, dcnt, w, N, 2, rcols + (int64_t)j * ldr, (const double2*)h1, (double2*)nullptr,
                      e.norm_partial, (const int*)stop_dev));
       G_TRY(e.finish_norm(&nptr, &ncnt));
-      G_TRY(launch_k(k_givens, dim3(1), dim3(32), 0, s, st, nptr, ncnt, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
+      G_TRY(launch_k(k_givens, dim3(1), dim3(32), givens_smem, s, st, nptr, ncnt, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
                      static_cast<int>(max_total), cycle_len, hf_dev));
+      }
       if (timed) mark(2, t0);
       cudaEvent_t ev = res.event();
       cudaEventRecord(ev, s);

@@ -50,4 +50,28 @@ int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStr
   return TOEP_OK;
 }
 
+// Cooperative (all CTAs co-resident, grid barriers allowed) + PDL launch.
+template <typename... KArgs, typename... Args>
+int launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(std::forward<Args>(args))...);
+  if (e != cudaSuccess) {
+    set_error("cooperative launch failed: %s", cudaGetErrorString(e));
+    cudaGetLastError();
+    return TOEP_ERR_CUDA;
+  }
+  return TOEP_OK;
+}
+
 }  // namespace toep
