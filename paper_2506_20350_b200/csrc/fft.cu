@@ -134,7 +134,7 @@ template <int... Rs> struct PlanLen;
 template <> struct PlanLen<> { static constexpr int value = 1; };
 template <int R, int... Rest> struct PlanLen<R, Rest...> { static constexpr int value = R * PlanLen<Rest...>::value; };
 
-template <typename TI, typename TC, typename TO, int TIL, int L, int Ns, int R, int... Rest>
+template <typename TI, typename TC, typename TO, int NT, int TIL, int L, int Ns, int R, int... Rest>
 __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __restrict__ gin, C<TO>* __restrict__ gout,
                                            C<TC>* __restrict__ src, C<TC>* __restrict__ dst,
                                            const C<TC>* __restrict__ tw, int ncol, TC scale) {
@@ -150,7 +150,7 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
   }
   const int hi_start = L - a.n_hi;
 #pragma unroll 2
-  for (int e = threadIdx.x; e < nb * TIL; e += kThreads) {
+  for (int e = threadIdx.x; e < nb * TIL; e += NT) {
     const int j = e / TIL;
     const int col = e % TIL;
     const int k = j % Ns;
@@ -165,10 +165,10 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
         v[r] = mk<TC>(0, 0);
         if (row >= 0 && col < ncol) {
           if (a.part_count == nullptr) {
-            v[r] = cvt<Z>(gin[row * a.in_sa + col]);
+            v[r] = cvt<Z>(gin[row * a.in_sa + col * a.in_cs]);
           } else {
             const int np = a.part_count[row];
-            for (int p = 0; p < np; ++p) v[r] = cadd(v[r], cvt<Z>(gin[row * a.in_sa + p * a.part_stride + col]));
+            for (int p = 0; p < np; ++p) v[r] = cadd(v[r], cvt<Z>(gin[row * a.in_sa + p * a.part_stride + col * a.in_cs]));
           }
         }
       } else {
@@ -189,14 +189,14 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
 #pragma unroll
         for (int q = 0; q < R; ++q) {
           const int idx = base + q * Ns;
-          if (idx < a.n_out) gout[idx * a.out_sa + col] = cvt<C<TO>>(cscale(v[q], scale));
+          if (idx < a.n_out) gout[idx * a.out_sa + col * a.out_cs] = cvt<C<TO>>(cscale(v[q], scale));
         }
       }
     }
   }
   if constexpr (!kLast) {
     __syncthreads();
-    plan_stage<TI, TC, TO, TIL, L, Ns * R, Rest...>(a, gin, gout, dst, src, tw, ncol, scale);
+    plan_stage<TI, TC, TO, NT, TIL, L, Ns * R, Rest...>(a, gin, gout, dst, src, tw, ncol, scale);
   }
 }
 
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fft_plan_kernel(PassArgs
   C<TO>* out = static_cast<C<TO>*>(a.out) + o * a.out_so + i0;
   if (a.out_idx != nullptr) out += static_cast<int64_t>(*a.out_idx) * a.out_idx_stride;
   __syncthreads();  // twiddle table
-  plan_stage<TI, TC, TO, TIL, L, 1, Rs...>(a, in, out, buf[0], buf[1], tw, ncol, pass_scale<TC>(a));
+  plan_stage<TI, TC, TO, kThreads, TIL, L, 1, Rs...>(a, in, out, buf[0], buf[1], tw, ncol, pass_scale<TC>(a));
 }
 
 template <typename TI, typename TC, typename TO, int TIL, int... Rs>
@@ -242,6 +242,114 @@ int try_plan(const PassArgs& a, cudaStream_t s) {
     case 64: if (a.inner >= 16) return launch_plan<TI, TC, TO, 16, 4, 4, 4>(a, s); break;
     default: break;
   }
+  return -1;
+}
+
+// ------------------------------------------------------------------------------------------
+// Whole 2-D transform per batch column in one CTA: the level-1 pass writes the (n2 x l1)
+// intermediate to shared memory, the level-2 pass reads it from there (no global round trip,
+// one launch instead of two).  Used for the single-RHS matvec on grids whose shared-memory
+// footprint fits (cfg2 60x60, cfg5 32x32).
+template <int... Rs> struct Plan {
+  static constexpr int L = PlanLen<Rs...>::value;
+  template <typename TI, typename TC, typename TO, int NT, int TIL>
+  __device__ static void run(const PassArgs& a, const C<TI>* gin, C<TO>* gout, C<TC>* b0, C<TC>* b1,
+                             const C<TC>* tw, int ncol, TC scale) {
+    plan_stage<TI, TC, TO, NT, TIL, L, 1, Rs...>(a, gin, gout, b0, b1, tw, ncol, scale);
+  }
+};
+
+struct Fft2dArgs {
+  const void* in;
+  void* out;
+  int n2, n1;
+  int64_t inner;
+  int sign;
+  const double* in_scale;
+  const int* stop;
+};
+
+constexpr int k2dThreads = 512;
+
+template <typename TC, int TILX, int TILY, typename PX, typename PY>
+struct Fft2dSmem {
+  static constexpr int kBuf = (PX::L * TILX > PY::L * TILY) ? PX::L * TILX : PY::L * TILY;
+  static size_t bytes(int n2) { return sizeof(C<TC>) * (PX::L + PY::L + 2 * kBuf + static_cast<size_t>(n2) * PX::L); }
+};
+
+template <typename TI, typename TC, typename TO, int TILX, int TILY, typename PX, typename PY, bool INV>
+__global__ void __launch_bounds__(k2dThreads, 1) fft2d_kernel(Fft2dArgs f) {
+  using Z = C<TC>;
+  using S = Fft2dSmem<TC, TILX, TILY, PX, PY>;
+  constexpr int L1 = PX::L, L2 = PY::L;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Z* twx = reinterpret_cast<Z*>(smem_raw);
+  Z* twy = twx + L1;
+  Z* b0 = twy + L2;
+  Z* b1 = b0 + S::kBuf;
+  Z* G = b1 + S::kBuf;  // [n2][L1]
+  pdl_trigger();
+  for (int t = threadIdx.x; t < L1 + L2; t += k2dThreads) {
+    const int L = t < L1 ? L1 : L2;
+    const int tt = t < L1 ? t : t - L1;
+    TC s, c;
+    sincospi_t<TC>(static_cast<TC>(2.0 * tt / L), &s, &c);
+    (t < L1 ? twx[tt] : twy[tt]) = mk<TC>(c, f.sign * s);
+  }
+  pdl_wait();
+  if (f.stop != nullptr && *f.stop != 0) return;
+  __syncthreads();
+  const int64_t b = blockIdx.x;
+  const int64_t inner = f.inner;
+  const int n2 = f.n2, n1 = f.n1;
+  if constexpr (!INV) {
+    PassArgs ax;  // level 1: slots x (pad fused), columns y -> G[y][kx]
+    ax.L = L1; ax.n_lo = n1; ax.n_hi = 0; ax.n_out = L1; ax.in_sa = inner; ax.in_cs = n1 * inner;
+    ax.out_sa = 1; ax.out_cs = L1; ax.sign = f.sign;
+    const TC sc = static_cast<TC>(f.in_scale != nullptr ? *f.in_scale : 1.0);
+    PX::template run<TI, TC, TC, k2dThreads, TILX>(ax, static_cast<const C<TI>*>(f.in) + b, G, b0, b1, twx, n2, sc);
+    __syncthreads();
+    PassArgs ay;  // level 2: slots y (n2 non-zero rows), columns kx -> u_hat[ky][kx][b]
+    ay.L = L2; ay.n_lo = n2; ay.n_hi = 0; ay.n_out = L2; ay.in_sa = L1; ay.in_cs = 1;
+    ay.out_sa = static_cast<int64_t>(L1) * inner; ay.out_cs = inner; ay.sign = f.sign;
+    PY::template run<TC, TC, TO, k2dThreads, TILY>(ay, G, static_cast<C<TO>*>(f.out) + b, b0, b1, twy, L1,
+                                                   static_cast<TC>(1));
+  } else {
+    PassArgs ay;  // inverse level 2 over all ky, keep y < n2 -> G[y][kx]
+    ay.L = L2; ay.n_lo = L2; ay.n_hi = 0; ay.n_out = n2; ay.in_sa = static_cast<int64_t>(L1) * inner; ay.in_cs = inner;
+    ay.out_sa = L1; ay.out_cs = 1; ay.sign = f.sign;
+    PY::template run<TI, TC, TC, k2dThreads, TILY>(ay, static_cast<const C<TI>*>(f.in) + b, G, b0, b1, twy, L1,
+                                                   static_cast<TC>(1));
+    __syncthreads();
+    PassArgs ax;  // inverse level 1, keep x < n1, 1/(l1 l2) -> v[y][x][b]
+    ax.L = L1; ax.n_lo = L1; ax.n_hi = 0; ax.n_out = n1; ax.in_sa = 1; ax.in_cs = L1; ax.out_sa = inner;
+    ax.out_cs = n1 * inner; ax.sign = f.sign;
+    PX::template run<TC, TC, TO, k2dThreads, TILX>(ax, G, static_cast<C<TO>*>(f.out) + b, b0, b1, twx, n2,
+                                                   static_cast<TC>(1.0 / (static_cast<double>(L1) * L2)));
+  }
+}
+
+template <typename TI, typename TC, typename TO, int TILX, int TILY, typename PX, typename PY>
+int launch2d(bool inverse, const Fft2dArgs& f, cudaStream_t s) {
+  using S = Fft2dSmem<TC, TILX, TILY, PX, PY>;
+  const size_t smem = S::bytes(f.n2);
+  TOEP_REQUIRE(smem <= 227 * 1024, TOEP_ERR_ARG, "fft2d shared memory too large");
+  auto kf = fft2d_kernel<TI, TC, TO, TILX, TILY, PX, PY, false>;
+  auto ki = fft2d_kernel<TI, TC, TO, TILX, TILY, PX, PY, true>;
+  auto k = inverse ? ki : kf;
+  static size_t attr_f = 0, attr_i = 0;
+  size_t& attr = inverse ? attr_i : attr_f;
+  if (attr < smem) {
+    TOEP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  return launch_k(k, dim3(static_cast<unsigned>(f.inner)), dim3(k2dThreads), smem, s, f);
+}
+
+template <typename TI, typename TC, typename TO>
+int fft2d_t(bool inverse, const Fft2dArgs& f, int l2, int l1, cudaStream_t s) {
+  if (l2 == 60 && l1 == 60 && f.n2 <= 32) return launch2d<TI, TC, TO, 32, 64, Plan<4, 3, 5>, Plan<4, 3, 5>>(inverse, f, s);
+  if (l2 == 32 && l1 == 32 && f.n2 <= 16) return launch2d<TI, TC, TO, 16, 32, Plan<4, 4, 2>, Plan<4, 4, 2>>(inverse, f, s);
   return -1;
 }
 
@@ -415,6 +523,24 @@ int factorize(int L, int* rad, int* nrad) {
     return TOEP_ERR_ARG;
   }
   return TOEP_OK;
+}
+
+int fft2d(bool inverse, const void* in, void* out, int n2, int n1, int l2, int l1, int64_t inner, int sign, int tin,
+          int tc, int tout, const double* in_scale, const int* stop, cudaStream_t s) {
+  static const bool off = [] {
+    const char* e = std::getenv("TOEP_FFT2D");
+    return e != nullptr && e[0] == '0';
+  }();
+  if (off || inner > 65535 || inner < 1) return -1;
+  Fft2dArgs f{in, out, n2, n1, inner, sign, in_scale, stop};
+  const int code = tin * 4 + tc * 2 + tout;
+  switch (code) {
+    case 0: return fft2d_t<double, double, double>(inverse, f, l2, l1, s);
+    case 7: return fft2d_t<float, float, float>(inverse, f, l2, l1, s);
+    case 6: return fft2d_t<float, float, double>(inverse, f, l2, l1, s);
+    case 3: return fft2d_t<double, float, float>(inverse, f, l2, l1, s);
+    default: return -1;
+  }
 }
 
 int fft_pass(const PassArgs& a, int tin, int tcomp, int tout, cudaStream_t s) {

@@ -35,7 +35,16 @@ struct PassArgs {
   // (the per-CTA inverse level-2 partials of the fused spectral kernel)
   const int* part_count = nullptr;
   int64_t part_stride = 0;
+  // stride of the batch ("column") index; 1 = contiguous batch (all standalone passes)
+  int64_t in_cs = 1, out_cs = 1;
 };
+
+// Whole 2-D transforms of the single-RHS matvec in one kernel each (one CTA per batch column,
+// intermediate in shared memory): forward = pad + level-1 DFT + level-2 DFT -> u_hat (bin-major);
+// inverse = inverse level-2 DFT (kept rows) + inverse level-1 DFT + crop + 1/(l1 l2).
+// Returns -1 when no compiled 2-D plan covers (l2, l1, n2).
+int fft2d(bool inverse, const void* in, void* out, int n2, int n1, int l2, int l1, int64_t inner, int sign,
+          int tin, int tc, int tout, const double* in_scale, const int* stop, cudaStream_t s);
 
 // type codes: 0 = complex128, 1 = complex64
 int fft_pass(const PassArgs& a, int tin, int tcomp, int tout, cudaStream_t s);

@@ -117,6 +117,19 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
     return fft_pass(d, tc, tc, tio, s);
   }
 
+  // one-CTA-per-column 2-D transforms when a compiled 2-D plan covers the grid
+  if (w == 1) {
+    const int rf = fft2d(false, u, ws->hat, op->n2, op->n1, op->l2, op->l1, inner, s1, tio, tc, tc, in_scale, stop, s);
+    if (rf == TOEP_OK) {
+      TOEP_TRY(bin_product(op->dtype, op->DT, ws->hat, ws->hat2, op->K, op->n0, w, transpose, stop, s));
+      // the overall 1/(l1 l2) is applied by the second kernel (linear, so also right for transpose())
+      const int ri = fft2d(true, ws->hat2, v, op->n2, op->n1, op->l2, op->l1, inner, -s1, tc, tc, tio, nullptr, stop, s);
+      return ri == -1 ? TOEP_ERR_ARG : ri;
+    } else if (rf != -1) {
+      return rf;
+    }
+  }
+
   PassArgs a;  // level-1 (x) pass: u [n2][n1][inner] -> x1 [n2][l1][inner]  (pad fused)
   a.in = u; a.out = ws->x1; a.L = op->l1; a.n_lo = op->n1; a.n_hi = 0; a.n_out = op->l1;
   a.inner = inner; a.outer = op->n2; a.in_sa = inner; a.in_so = op->n1 * inner; a.out_sa = inner;
