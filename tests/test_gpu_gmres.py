@@ -161,6 +161,24 @@ class TestBaselineCfg1:
         assert rel_err(x, np.linalg.solve(scipy.linalg.block_diag(*[r0] * 4), b)) <= 1e-12
 
 
+class TestSpectrum:
+    def test_top_singular_values_vs_dense(self):
+        from paper_2506_20350_b200.solvers import spectrum_estimate
+
+        gen = generator_from_stacked(seeded_stacked4(3, 3, 4, seed=11))
+        sys_ = system_from_generator(gen)
+        op = BorderedOperator.from_system(sys_)
+        pk = build_pk(sys_)
+        dense = assemble_dense(gen)
+        blk = scipy.linalg.block_diag(*([gen.block(0, 0)] * 9))
+        want = np.linalg.svd(np.linalg.solve(blk, dense), compute_uv=False)[:8]
+        got = spectrum_estimate(op, pk, count=8, oversample=28, power_iters=3)
+        assert np.allclose(got, want, rtol=1e-6)
+        want0 = np.linalg.svd(dense, compute_uv=False)[:8]
+        got0 = spectrum_estimate(op, None, count=8, oversample=28, power_iters=3)
+        assert np.allclose(got0, want0, rtol=1e-6)
+
+
 @pytest.mark.slow
 class TestBaselineCfg2:
     @pytest.mark.parametrize("tag", ["none", "pk"])
