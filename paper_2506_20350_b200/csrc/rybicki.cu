@@ -15,7 +15,8 @@
 namespace toep {
 namespace {
 
-constexpr int kNB = 32;         // LU / TRSM block size
+constexpr int kOB = 32;           // outer LU block (trailing-update GEMM depth), TRSM block
+constexpr int kPB = 8;            // sub-panel factored in shared memory
 constexpr int kPanelThreads = 1024;
 constexpr double kPivotTiny = 1e-300;
 
@@ -25,21 +26,28 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
   return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
 }
 
-// Factor panel columns [j0, j0+nb) of the n x n row-major matrix A (rows j0..n-1) with partial
-// pivoting; rows are swapped across all n columns immediately.  One CTA.
-__global__ void __launch_bounds__(kPanelThreads) lu_panel(double2* A, int n, int lda, int j0, int nb, int* ipiv,
-                                                          int* info) {
+// Factor the kPB columns [j0, j0+kPB) over rows [j0, n) with partial pivoting, the sub-panel
+// resident in shared memory (row-major (n-j0) x kPB).  Interchanges are applied inside the
+// sub-panel only (laswp_cols applies them to the other columns); ipiv[j] = absolute pivot row.
+__global__ void __launch_bounds__(kPanelThreads) lu_subpanel(double2* A, int n, int lda, int j0, int* ipiv, int* info) {
+  extern __shared__ double2 P[];
   __shared__ double sval[kPanelThreads / 32];
   __shared__ int sidx[kPanelThreads / 32];
   __shared__ int piv_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int j = j0; j < j0 + nb; ++j) {
-    // argmax_i |A[i][j]| (first max on ties, like LAPACK's izamax)
+  const int rows = n - j0;
+  const int pb = min(kPB, n - j0);
+  for (int e = tid; e < rows * kPB; e += kPanelThreads) {
+    const int r = e / kPB, c = e - r * kPB;
+    P[e] = (c < pb) ? A[static_cast<int64_t>(j0 + r) * lda + j0 + c] : make_double2(0, 0);
+  }
+  __syncthreads();
+  for (int jj = 0; jj < pb; ++jj) {
     double best = -1.0;
-    int bi = n;
-    for (int i = j + tid; i < n; i += kPanelThreads) {
-      const double v = cabs2(A[static_cast<int64_t>(i) * lda + j]);
-      if (v > best) { best = v; bi = i; }
+    int bi = rows;
+    for (int r = jj + tid; r < rows; r += kPanelThreads) {
+      const double v = cabs2(P[r * kPB + jj]);
+      if (v > best) { best = v; bi = r; }
     }
     for (int off = 16; off > 0; off >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, best, off);
@@ -49,88 +57,157 @@ __global__ void __launch_bounds__(kPanelThreads) lu_panel(double2* A, int n, int
     if (lane == 0) { sval[warp] = best; sidx[warp] = bi; }
     __syncthreads();
     if (tid == 0) {
-      double b = sval[0];
+      double bb = sval[0];
       int id = sidx[0];
       for (int w2 = 1; w2 < kPanelThreads / 32; ++w2)
-        if (sval[w2] > b || (sval[w2] == b && sidx[w2] < id)) { b = sval[w2]; id = sidx[w2]; }
+        if (sval[w2] > bb || (sval[w2] == bb && sidx[w2] < id)) { bb = sval[w2]; id = sidx[w2]; }
       piv_s = id;
-      ipiv[j] = id;
-      if (!(sqrt(b) >= kPivotTiny) && *info == 0) *info = j + 1;
+      ipiv[j0 + jj] = j0 + id;
+      if (!(sqrt(bb) >= kPivotTiny) && *info == 0) *info = j0 + jj + 1;
     }
     __syncthreads();
     const int p = piv_s;
-    if (p != j) {
-      for (int c = tid; c < n; c += kPanelThreads) {
-        const double2 t = A[static_cast<int64_t>(j) * lda + c];
-        A[static_cast<int64_t>(j) * lda + c] = A[static_cast<int64_t>(p) * lda + c];
-        A[static_cast<int64_t>(p) * lda + c] = t;
-      }
+    if (p != jj && tid < kPB) {
+      const double2 t = P[jj * kPB + tid];
+      P[jj * kPB + tid] = P[p * kPB + tid];
+      P[p * kPB + tid] = t;
     }
     __syncthreads();
-    const double2 d = A[static_cast<int64_t>(j) * lda + j];
+    const double2 d = P[jj * kPB + jj];
     const bool ok = cabs2(d) > 0.0;
-    // scale the column below the pivot and update the rest of the panel (rank 1)
-    const int rows = n - j - 1, cols = j0 + nb - j - 1;
-    for (int i = tid; i < rows; i += kPanelThreads) {
-      double2* a = A + static_cast<int64_t>(j + 1 + i) * lda;
-      const double2 l = ok ? cdiv(a[j], d) : a[j];
-      a[j] = l;
-      for (int c = 0; c < cols; ++c) cfma(a[j + 1 + c], make_double2(-l.x, -l.y), A[static_cast<int64_t>(j) * lda + j + 1 + c]);
+    for (int r = jj + 1 + tid; r < rows; r += kPanelThreads) {
+      const double2 l = ok ? cdiv(P[r * kPB + jj], d) : P[r * kPB + jj];
+      P[r * kPB + jj] = l;
+#pragma unroll
+      for (int c = 0; c < kPB; ++c)
+        if (c > jj) cfma(P[r * kPB + c], make_double2(-l.x, -l.y), P[jj * kPB + c]);
     }
     __syncthreads();
   }
-}
-
-// U12 = L11^-1 A12: unit-lower forward substitution on rows [j0, j0+nb), columns [c0, n)
-__global__ void trsm_lower_unit_rows(double2* A, int lda, int j0, int nb, int c0, int ncols) {
-  const int c = c0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= c0 + ncols) return;
-  for (int i = 1; i < nb; ++i) {
-    double2 acc = A[static_cast<int64_t>(j0 + i) * lda + c];
-    for (int k = 0; k < i; ++k)
-      cfma(acc, make_double2(-A[static_cast<int64_t>(j0 + i) * lda + j0 + k].x, -A[static_cast<int64_t>(j0 + i) * lda + j0 + k].y),
-           A[static_cast<int64_t>(j0 + k) * lda + c]);
-    A[static_cast<int64_t>(j0 + i) * lda + c] = acc;
+  for (int e = tid; e < rows * kPB; e += kPanelThreads) {
+    const int r = e / kPB, c = e - r * kPB;
+    if (c < pb) A[static_cast<int64_t>(j0 + r) * lda + j0 + c] = P[e];
   }
 }
 
-// B[j] <-> B[ipiv[j]] for j = 0..n-1 (sequential in j, parallel over the nrhs columns)
-__global__ void laswp_rows(double2* B, int ldb, int nrhs, const int* ipiv, int n) {
+// apply the interchanges ipiv[j0 .. j0+cnt) to every column outside [j0, j0+cnt)
+__global__ void laswp_cols(double2* A, int n, int lda, int j0, int cnt, const int* ipiv) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nrhs) return;
-  for (int j = 0; j < n; ++j) {
-    const int p = ipiv[j];
-    if (p != j) {
-      const double2 t = B[static_cast<int64_t>(j) * ldb + c];
-      B[static_cast<int64_t>(j) * ldb + c] = B[static_cast<int64_t>(p) * ldb + c];
-      B[static_cast<int64_t>(p) * ldb + c] = t;
+  if (c >= n || (c >= j0 && c < j0 + cnt)) return;
+  for (int jj = 0; jj < cnt; ++jj) {
+    const int r = j0 + jj, p = ipiv[r];
+    if (p != r) {
+      const double2 t = A[static_cast<int64_t>(r) * lda + c];
+      A[static_cast<int64_t>(r) * lda + c] = A[static_cast<int64_t>(p) * lda + c];
+      A[static_cast<int64_t>(p) * lda + c] = t;
     }
   }
 }
 
-// diagonal-block triangular solve on rows [r0, r0+nb) of B (nrhs columns):
-// lower (unit): forward;  upper: backward with the diagonal of LU
-__global__ void trsm_diag_block(const double2* LU, int lda, double2* B, int ldb, int nrhs, int r0, int nb, int upper) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nrhs) return;
+constexpr int kTrsmWarps = 8;
+
+// X = T^-1 X on the nb (<= NB) rows [r0, r0+nb) of X (row stride ldx), T = the diagonal block
+// LU[r0.., r0..] (unit lower, or upper), staged in shared memory.  One warp per column of X
+// (columns [c0, c0+ncols)): lane l holds rows l, l+32, ...; the substitution broadcasts the
+// solved entry with a shuffle and updates the remaining rows in parallel.
+template <int NB>
+__global__ void __launch_bounds__(kTrsmWarps * 32) trsm_block(const double2* LU, int lda, double2* X, int64_t ldx,
+                                                               int r0, int nb, int c0, int ncols, int upper) {
+  extern __shared__ double2 trsm_smem[];
+  double2 (*T)[NB + 1] = reinterpret_cast<double2 (*)[NB + 1]>(trsm_smem);
+  for (int e = threadIdx.x; e < nb * nb; e += kTrsmWarps * 32) {
+    const int i = e / nb, k = e - i * nb;
+    T[i][k] = LU[static_cast<int64_t>(r0 + i) * lda + r0 + k];
+  }
+  __syncthreads();
+  constexpr int R = NB / 32;
+  const int lane = threadIdx.x & 31;
+  const int c = c0 + blockIdx.x * kTrsmWarps + (threadIdx.x >> 5);
+  if (c >= c0 + ncols) return;
+  double2 x[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int i = lane + 32 * q;
+    x[q] = (i < nb) ? X[static_cast<int64_t>(r0 + i) * ldx + c] : make_double2(0, 0);
+  }
   if (!upper) {
-    for (int i = 1; i < nb; ++i) {
-      double2 acc = B[static_cast<int64_t>(r0 + i) * ldb + c];
-      for (int k = 0; k < i; ++k) {
-        const double2 l = LU[static_cast<int64_t>(r0 + i) * lda + r0 + k];
-        cfma(acc, make_double2(-l.x, -l.y), B[static_cast<int64_t>(r0 + k) * ldb + c]);
+    for (int k = 0; k < nb - 1; ++k) {
+      const int qk = k >> 5;
+      double2 xk;
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (q == qk) {
+          xk.x = __shfl_sync(0xffffffffu, x[q].x, k & 31);
+          xk.y = __shfl_sync(0xffffffffu, x[q].y, k & 31);
+        }
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = lane + 32 * q;
+        if (i > k && i < nb) cfma(x[q], make_double2(-T[i][k].x, -T[i][k].y), xk);
       }
-      B[static_cast<int64_t>(r0 + i) * ldb + c] = acc;
     }
   } else {
-    for (int i = nb - 1; i >= 0; --i) {
-      double2 acc = B[static_cast<int64_t>(r0 + i) * ldb + c];
-      for (int k = i + 1; k < nb; ++k) {
-        const double2 u = LU[static_cast<int64_t>(r0 + i) * lda + r0 + k];
-        cfma(acc, make_double2(-u.x, -u.y), B[static_cast<int64_t>(r0 + k) * ldb + c]);
+    for (int k = nb - 1; k >= 0; --k) {
+      const int qk = k >> 5;
+      double2 xk;
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (q == qk) {
+          if (lane == (k & 31)) x[q] = cdiv(x[q], T[k][k]);
+          xk.x = __shfl_sync(0xffffffffu, x[q].x, k & 31);
+          xk.y = __shfl_sync(0xffffffffu, x[q].y, k & 31);
+        }
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = lane + 32 * q;
+        if (i < k) cfma(x[q], make_double2(-T[i][k].x, -T[i][k].y), xk);
       }
-      B[static_cast<int64_t>(r0 + i) * ldb + c] = cdiv(acc, LU[static_cast<int64_t>(r0 + i) * lda + r0 + i]);
     }
+  }
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int i = lane + 32 * q;
+    if (i < nb) X[static_cast<int64_t>(r0 + i) * ldx + c] = x[q];
+  }
+}
+
+template <int NB>
+void trsm(const double2* LU, int lda, double2* X, int64_t ldx, int r0, int nb, int c0, int ncols, int upper,
+          cudaStream_t s) {
+  constexpr int smem = NB * (NB + 1) * static_cast<int>(sizeof(double2));
+  static bool configured = false;  // opt-in above 48 KB, once per process
+  if (!configured) {
+    cudaFuncSetAttribute(trsm_block<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  trsm_block<NB><<<(ncols + kTrsmWarps - 1) / kTrsmWarps, kTrsmWarps * 32, smem, s>>>(LU, lda, X, ldx, r0, nb, c0, ncols,
+                                                                                  upper);
+}
+
+// perm[i] = source row of position i after the interchanges ipiv[0..n) (one thread; n <= 8192)
+__global__ void build_perm(const int* ipiv, int n, int* perm) {
+  extern __shared__ int pm[];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) pm[i] = i;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < n; ++j) {
+      const int p = ipiv[j];
+      const int t = pm[j];
+      pm[j] = pm[p];
+      pm[p] = t;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = pm[i];
+}
+
+__global__ void gather_rows(const double2* __restrict__ B, double2* __restrict__ out, const int* __restrict__ perm,
+                            int n, int nrhs, int64_t ldb) {
+  const int64_t total = static_cast<int64_t>(n) * nrhs;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = t / nrhs, c = t - i * nrhs;
+    out[i * ldb + c] = B[static_cast<int64_t>(perm[i]) * ldb + c];
   }
 }
 
@@ -153,20 +230,45 @@ int gemm_rm(int64_t m, int64_t nn, int64_t k, double2 alpha, const double2* A, i
   return gemm(TOEP_C128, m, nn, k, alpha, A, lda, 1, 0, B, ldb, 1, 0, beta, C, ldc, 1, 0, 1, s);
 }
 
-// in-place LU with partial pivoting of the n x n row-major A; info (device) > 0: singular
+// in-place LU with partial pivoting of the n x n row-major A; info (device) > 0: singular.
+// Blocked right-looking: outer blocks of kOB columns; inside, kPB-column sub-panels factored in
+// shared memory (lu_subpanel), their interchanges applied to all other columns, the sub-panel's
+// U rows solved and the rest of the outer block updated; then the outer block's U12 = L11^-1 A12
+// (trsm_block) and the trailing update A22 -= L21 U12 on the tensor cores (K = kOB).
 int getrf(double2* A, int n, int* ipiv, int* info, cudaStream_t s) {
-  for (int j0 = 0; j0 < n; j0 += kNB) {
-    const int nb = std::min(kNB, n - j0);
-    lu_panel<<<1, kPanelThreads, 0, s>>>(A, n, n, j0, nb, ipiv, info);
-    TOEP_LAUNCHED();
-    const int c0 = j0 + nb, rest = n - c0;
-    if (rest > 0) {
-      trsm_lower_unit_rows<<<(rest + 127) / 128, 128, 0, s>>>(A, n, j0, nb, c0, rest);
+  const size_t psmem = sizeof(double2) * static_cast<size_t>(n) * kPB;
+  TOEP_REQUIRE(psmem <= 227 * 1024, TOEP_ERR_ARG, "lu_factor: n = %d exceeds the shared-memory sub-panel (<= 1816)", n);
+  static size_t attr = 0;
+  if (psmem > 48 * 1024 && attr < psmem) {
+    TOEP_CUDA(cudaFuncSetAttribute(lu_subpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+    attr = psmem;
+  }
+  for (int j0 = 0; j0 < n; j0 += kOB) {
+    const int ob = std::min(kOB, n - j0);
+    for (int jj = j0; jj < j0 + ob; jj += kPB) {
+      const int pb = std::min(kPB, j0 + ob - jj);
+      lu_subpanel<<<1, kPanelThreads, sizeof(double2) * static_cast<size_t>(n - jj) * kPB, s>>>(A, n, n, jj, ipiv, info);
       TOEP_LAUNCHED();
-      // A22 -= L21 U12
-      TOEP_TRY(gemm_rm(rest, rest, nb, make_double2(-1, 0), A + static_cast<int64_t>(c0) * n + j0, n,
-                       A + static_cast<int64_t>(j0) * n + c0, n, make_double2(1, 0), A + static_cast<int64_t>(c0) * n + c0,
-                       n, s));
+      laswp_cols<<<(n + 255) / 256, 256, 0, s>>>(A, n, n, jj, pb, ipiv);
+      TOEP_LAUNCHED();
+      const int c0 = jj + pb, ncol = j0 + ob - c0;  // rest of the outer block
+      if (ncol > 0) {
+        trsm<32>(A, n, A, n, jj, pb, c0, ncol, 0, s);
+        TOEP_LAUNCHED();
+        const int rows = n - c0;
+        if (rows > 0)
+          TOEP_TRY(gemm_rm(rows, ncol, pb, make_double2(-1, 0), A + static_cast<int64_t>(c0) * n + jj, n,
+                           A + static_cast<int64_t>(jj) * n + c0, n, make_double2(1, 0),
+                           A + static_cast<int64_t>(c0) * n + c0, n, s));
+      }
+    }
+    const int c0 = j0 + ob, rest = n - c0;
+    if (rest > 0) {
+      trsm<32>(A, n, A, n, j0, ob, c0, rest, 0, s);
+      TOEP_LAUNCHED();
+      TOEP_TRY(gemm_rm(rest, rest, ob, make_double2(-1, 0), A + static_cast<int64_t>(c0) * n + j0, n,
+                       A + static_cast<int64_t>(j0) * n + c0, n, make_double2(1, 0),
+                       A + static_cast<int64_t>(c0) * n + c0, n, s));
     }
   }
   return TOEP_OK;
@@ -174,12 +276,25 @@ int getrf(double2* A, int n, int* ipiv, int* info, cudaStream_t s) {
 
 // B <- A^-1 B with A = P L U from getrf; B: n x nrhs row-major (ldb)
 int getrs(const double2* LU, int n, const int* ipiv, double2* B, int ldb, int nrhs, cudaStream_t s) {
-  const int gr = (nrhs + 127) / 128;
-  laswp_rows<<<gr, 128, 0, s>>>(B, ldb, nrhs, ipiv, n);
+  int* perm = nullptr;
+  double2* tmp = nullptr;
+  TOEP_REQUIRE(cudaMallocAsync(reinterpret_cast<void**>(&perm), sizeof(int) * n, s) == cudaSuccess &&
+                   cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(double2) * static_cast<size_t>(n) * ldb, s) ==
+                       cudaSuccess,
+               TOEP_ERR_OOM, "out of device memory in lu_solve");
+  build_perm<<<1, 256, sizeof(int) * n, s>>>(ipiv, n, perm);
   TOEP_LAUNCHED();
-  for (int r0 = 0; r0 < n; r0 += kNB) {  // L y = P b (unit lower)
-    const int nb = std::min(kNB, n - r0);
-    trsm_diag_block<<<gr, 128, 0, s>>>(LU, n, B, ldb, nrhs, r0, nb, 0);
+  const int64_t total = static_cast<int64_t>(n) * nrhs;
+  const int gg = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  gather_rows<<<gg, 256, 0, s>>>(B, tmp, perm, n, nrhs, ldb);
+  TOEP_LAUNCHED();
+  TOEP_CUDA(cudaMemcpyAsync(B, tmp, sizeof(double2) * static_cast<size_t>(n) * ldb, cudaMemcpyDeviceToDevice, s));
+  cudaFreeAsync(tmp, s);
+  cudaFreeAsync(perm, s);
+  constexpr int kSB = 64;  // solve block: halves the GEMM count of the 32-row LU block
+  for (int r0 = 0; r0 < n; r0 += kSB) {  // L y = P b (unit lower)
+    const int nb = std::min(kSB, n - r0);
+    trsm<kSB>(LU, n, B, ldb, r0, nb, 0, nrhs, 0, s);
     TOEP_LAUNCHED();
     const int rest = n - r0 - nb;
     if (rest > 0)
@@ -187,10 +302,10 @@ int getrs(const double2* LU, int n, const int* ipiv, double2* B, int ldb, int nr
                        B + static_cast<int64_t>(r0) * ldb, ldb, make_double2(1, 0), B + static_cast<int64_t>(r0 + nb) * ldb,
                        ldb, s));
   }
-  for (int r1 = n; r1 > 0; r1 -= kNB) {  // U x = y
-    const int r0 = std::max(0, r1 - kNB);
+  for (int r1 = n; r1 > 0; r1 -= kSB) {  // U x = y
+    const int r0 = std::max(0, r1 - kSB);
     const int nb = r1 - r0;
-    trsm_diag_block<<<gr, 128, 0, s>>>(LU, n, B, ldb, nrhs, r0, nb, 1);
+    trsm<kSB>(LU, n, B, ldb, r0, nb, 0, nrhs, 1, s);
     TOEP_LAUNCHED();
     if (r0 > 0)
       TOEP_TRY(gemm_rm(r0, nrhs, nb, make_double2(-1, 0), LU + r0, n, B + static_cast<int64_t>(r0) * ldb, ldb,
