@@ -1,107 +1,33 @@
 // Block Rybicki (bordering) direct solver on the device: rybicki.py:63-144 + numerics.lu_factor /
 // lu_solve (numerics.py:67-96).
 //
-// Every block product of the recursion (the block sums d1, d2, the numerators, the generator
-// cross-updates) is a dense complex GEMM on the FP64 tensor cores (zgemm_tc); the two
-// denominators per step are LU-factored on the device with partial pivoting (right-looking
-// blocked LU: single-CTA panel + TRSM + tensor-core GEMM trailing update) and applied through
+// Every block sum of the recursion (d1, d2, the numerators) is ONE complex GEMM of depth m*s on
+// the FP64 tensor cores (zgemm_tc) against "wide" copies of the generator blocks, and the
+// generator cross-updates are single batched GEMMs (negative batch stride walks the reversed
+// block order).  The two denominators per step are LU-factored together on the device with
+// partial pivoting (LAPACK zgetrf semantics, |re|+|im| pivots): kPW-column panels factored by an
+// 8-CTA cluster with the panel resident in distributed shared memory, the row permutation and
+// U12 solve in one warp-per-column kernel, the trailing update on the tensor cores.  Solves are
 // blocked triangular solves whose off-diagonal work is again GEMM.  All matrices are row-major
-// complex128; row swaps are contiguous.  Singular pivots (|p| < 1e-300, numerics.py:27) raise
-// SingularBlock for R_0 and SingularDenominator(step) for D1 / D2, as the reference.
+// complex128.  Singular pivots (|p| < 1e-300, numerics.py:27) raise SingularBlock for R_0 and
+// SingularDenominator(step) for D1 / D2, as the reference.
+#include <climits>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "op.h"
 
 namespace toep {
 namespace {
 
-constexpr int kOB = 32;           // outer LU block (trailing-update GEMM depth), TRSM block
-constexpr int kPB = 8;            // sub-panel factored in shared memory
-constexpr int kPanelThreads = 1024;
+namespace cg = cooperative_groups;
+
 constexpr double kPivotTiny = 1e-300;
 
-__device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
 __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
   const double den = b.x * b.x + b.y * b.y;
   return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
-}
-
-// Factor the kPB columns [j0, j0+kPB) over rows [j0, n) with partial pivoting, the sub-panel
-// resident in shared memory (row-major (n-j0) x kPB).  Interchanges are applied inside the
-// sub-panel only (laswp_cols applies them to the other columns); ipiv[j] = absolute pivot row.
-__global__ void __launch_bounds__(kPanelThreads) lu_subpanel(double2* A, int n, int lda, int j0, int* ipiv, int* info) {
-  extern __shared__ double2 P[];
-  __shared__ double sval[kPanelThreads / 32];
-  __shared__ int sidx[kPanelThreads / 32];
-  __shared__ int piv_s;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rows = n - j0;
-  const int pb = min(kPB, n - j0);
-  for (int e = tid; e < rows * kPB; e += kPanelThreads) {
-    const int r = e / kPB, c = e - r * kPB;
-    P[e] = (c < pb) ? A[static_cast<int64_t>(j0 + r) * lda + j0 + c] : make_double2(0, 0);
-  }
-  __syncthreads();
-  for (int jj = 0; jj < pb; ++jj) {
-    double best = -1.0;
-    int bi = rows;
-    for (int r = jj + tid; r < rows; r += kPanelThreads) {
-      const double v = cabs2(P[r * kPB + jj]);
-      if (v > best) { best = v; bi = r; }
-    }
-    for (int off = 16; off > 0; off >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, best, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-    }
-    if (lane == 0) { sval[warp] = best; sidx[warp] = bi; }
-    __syncthreads();
-    if (tid == 0) {
-      double bb = sval[0];
-      int id = sidx[0];
-      for (int w2 = 1; w2 < kPanelThreads / 32; ++w2)
-        if (sval[w2] > bb || (sval[w2] == bb && sidx[w2] < id)) { bb = sval[w2]; id = sidx[w2]; }
-      piv_s = id;
-      ipiv[j0 + jj] = j0 + id;
-      if (!(sqrt(bb) >= kPivotTiny) && *info == 0) *info = j0 + jj + 1;
-    }
-    __syncthreads();
-    const int p = piv_s;
-    if (p != jj && tid < kPB) {
-      const double2 t = P[jj * kPB + tid];
-      P[jj * kPB + tid] = P[p * kPB + tid];
-      P[p * kPB + tid] = t;
-    }
-    __syncthreads();
-    const double2 d = P[jj * kPB + jj];
-    const bool ok = cabs2(d) > 0.0;
-    for (int r = jj + 1 + tid; r < rows; r += kPanelThreads) {
-      const double2 l = ok ? cdiv(P[r * kPB + jj], d) : P[r * kPB + jj];
-      P[r * kPB + jj] = l;
-#pragma unroll
-      for (int c = 0; c < kPB; ++c)
-        if (c > jj) cfma(P[r * kPB + c], make_double2(-l.x, -l.y), P[jj * kPB + c]);
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < rows * kPB; e += kPanelThreads) {
-    const int r = e / kPB, c = e - r * kPB;
-    if (c < pb) A[static_cast<int64_t>(j0 + r) * lda + j0 + c] = P[e];
-  }
-}
-
-// apply the interchanges ipiv[j0 .. j0+cnt) to every column outside [j0, j0+cnt)
-__global__ void laswp_cols(double2* A, int n, int lda, int j0, int cnt, const int* ipiv) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n || (c >= j0 && c < j0 + cnt)) return;
-  for (int jj = 0; jj < cnt; ++jj) {
-    const int r = j0 + jj, p = ipiv[r];
-    if (p != r) {
-      const double2 t = A[static_cast<int64_t>(r) * lda + c];
-      A[static_cast<int64_t>(r) * lda + c] = A[static_cast<int64_t>(p) * lda + c];
-      A[static_cast<int64_t>(p) * lda + c] = t;
-    }
-  }
 }
 
 constexpr int kTrsmWarps = 8;
@@ -184,6 +110,202 @@ void trsm(const double2* LU, int lda, double2* X, int64_t ldx, int r0, int nb, i
                                                                                   upper);
 }
 
+// ----------------------------------------------------------------------------- cluster panel LU
+// The kPW-column panel [j0, j0+kPW) over all rows [j0, n) is factored by one 8-CTA thread-block
+// cluster, the panel resident in the cluster's distributed shared memory (CTA r owns physical rows
+// [r*rpc, (r+1)*rpc)).  Rows never move during the panel: per column, every CTA proposes its
+// local pivot candidate (max |re|+|im|, LAPACK izamax's measure), one cluster barrier publishes
+// the candidates, every warp reads the winner and the pivot row straight from the owner's shared
+// memory (DSMEM) and each thread eliminates the rows it owns.  The row interchanges are tracked as
+// a permutation (LAPACK ipiv semantics) and applied once, at write-back; `moves` receives the
+// (destination, source) row pairs so the other columns can be permuted by swap_trsm.
+constexpr int kCL = 8;
+constexpr int kPW = 32;
+constexpr int kPanelThr = 256;
+constexpr int kMovesStride = 1 + 4 * kPW;  // count + up to 2*kPW (dst, src) pairs
+
+__device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y); }
+
+__device__ __forceinline__ void argmax_merge(double& v, int& i, double ov, int oi) {
+  if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
+}
+
+__device__ __forceinline__ void warp_argmax(double& v, int& i) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, i, off);
+    argmax_merge(v, i, ov, oi);
+  }
+}
+
+size_t panel_smem(int n, int j0) {
+  const int R = n - j0, rpc = (R + kCL - 1) / kCL;
+  return sizeof(double2) * static_cast<size_t>(rpc) * (kPW + 1) + 2 * sizeof(int) * static_cast<size_t>(R);
+}
+
+__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kPanelThr)
+    lu_panel_cluster(double2* A0, int64_t mstride, int n, int j0, int* ipiv0, int* info0, int* moves0) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  double2* A = A0 + blockIdx.y * mstride;
+  int* ipiv = ipiv0 + static_cast<int64_t>(blockIdx.y) * n;
+  int* info = info0 + blockIdx.y;
+  int* moves = moves0 + blockIdx.y * kMovesStride;
+  const int R = n - j0, pw = min(kPW, R);
+  const int rpc = (R + kCL - 1) / kCL;
+  const int row0 = rank * rpc, nrow = max(0, min(R, row0 + rpc) - row0);
+  extern __shared__ double2 panel_sm[];
+  double2* P = panel_sm;                                        // [rpc][kPW+1]
+  int* pos_of = reinterpret_cast<int*>(P + static_cast<int64_t>(rpc) * (kPW + 1));  // [R]
+  int* phys_at = pos_of + R;                                    // [R]
+  __shared__ double wv[2][kPanelThr / 32];
+  __shared__ int wi[2][kPanelThr / 32];
+  __shared__ double cv[2];
+  __shared__ int ci[2];
+  __shared__ int nmoves;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  for (int e = tid; e < nrow * kPW; e += kPanelThr) {
+    const int i = e / kPW, c = e - i * kPW;
+    P[i * (kPW + 1) + c] = c < pw ? A[static_cast<int64_t>(j0 + row0 + i) * n + j0 + c] : make_double2(0, 0);
+  }
+  for (int i = tid; i < R; i += kPanelThr) {
+    pos_of[i] = i;
+    phys_at[i] = i;
+  }
+  if (tid == 0) nmoves = 0;
+  constexpr int kRowsPerThread = 2;  // rpc <= 2 * kPanelThr (checked on the host)
+  bool used[kRowsPerThread] = {false, false};
+  __syncthreads();
+
+  for (int jj = 0; jj < pw; ++jj) {
+    const int par = jj & 1;
+    double best = -1.0;
+    int bi = INT_MAX;
+#pragma unroll
+    for (int q = 0; q < kRowsPerThread; ++q) {
+      const int i = tid + q * kPanelThr;
+      if (i < nrow && !used[q]) argmax_merge(best, bi, cabs1(P[i * (kPW + 1) + jj]), row0 + i);
+    }
+    warp_argmax(best, bi);
+    if (lane == 0) {
+      wv[par][warp] = best;
+      wi[par][warp] = bi;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double b = lane < kPanelThr / 32 ? wv[par][lane] : -1.0;
+      int i = lane < kPanelThr / 32 ? wi[par][lane] : INT_MAX;
+      warp_argmax(b, i);
+      if (lane == 0) {
+        cv[par] = b;
+        ci[par] = i;
+      }
+    }
+    cluster.sync();
+    double gb = -1.0;
+    int p = INT_MAX;
+    if (lane < kCL) {
+      gb = *cluster.map_shared_rank(&cv[par], lane);
+      p = *cluster.map_shared_rank(&ci[par], lane);
+    }
+    warp_argmax(gb, p);
+    const int owner = p / rpc, li = p - owner * rpc;
+    const double2* rP = cluster.map_shared_rank(P, owner);
+    const double2 u = (lane >= jj && lane < pw) ? rP[li * (kPW + 1) + lane] : make_double2(0, 0);
+    double2 piv;
+    piv.x = __shfl_sync(0xffffffffu, u.x, jj);
+    piv.y = __shfl_sync(0xffffffffu, u.y, jj);
+    const bool zero = !(gb >= kPivotTiny);
+    if (tid == 0) {  // interchange bookkeeping (redundantly in every CTA)
+      const int ppos = pos_of[p], phj = phys_at[jj];
+      phys_at[jj] = p;
+      phys_at[ppos] = phj;
+      pos_of[p] = jj;
+      pos_of[phj] = ppos;
+      if (rank == 0) {
+        ipiv[j0 + jj] = j0 + ppos;
+        if (zero && *info == 0) *info = j0 + jj + 1;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kRowsPerThread; ++q) {
+      const int i = tid + q * kPanelThr;
+      bool act = i < nrow && !used[q];
+      if (act && row0 + i == p) {
+        used[q] = true;
+        act = false;
+      }
+      double2 l = make_double2(0, 0);
+      if (act) {
+        l = P[i * (kPW + 1) + jj];
+        if (!zero) l = cdiv(l, piv);
+        P[i * (kPW + 1) + jj] = l;
+      }
+      const double2 nl = make_double2(-l.x, -l.y);
+      for (int c = jj + 1; c < pw; ++c) {
+        double2 uc;
+        uc.x = __shfl_sync(0xffffffffu, u.x, c);
+        uc.y = __shfl_sync(0xffffffffu, u.y, c);
+        if (act) cfma(P[i * (kPW + 1) + c], nl, uc);
+      }
+    }
+  }
+  cluster.sync();  // no CTA may leave while its shared memory can still be read remotely
+  for (int e = tid; e < nrow * kPW; e += kPanelThr) {
+    const int i = e / kPW, c = e - i * kPW;
+    if (c < pw) A[static_cast<int64_t>(j0 + pos_of[row0 + i]) * n + j0 + c] = P[i * (kPW + 1) + c];
+  }
+  if (rank == 0) {
+    for (int q = tid; q < R; q += kPanelThr)
+      if (phys_at[q] != q) {
+        const int k = atomicAdd(&nmoves, 1);
+        moves[1 + 2 * k] = q;
+        moves[2 + 2 * k] = phys_at[q];
+      }
+    __syncthreads();
+    if (tid == 0) moves[0] = nmoves;
+  }
+}
+
+// Columns outside the panel: apply the panel's row permutation (moves), then, right of the
+// panel, U12 = L11^-1 A12 (unit lower, L11 in shared memory).  One warp per column; lane = row.
+__global__ void __launch_bounds__(256) swap_trsm(double2* A0, int64_t mstride, int n, int j0, int pw,
+                                                 const int* moves0) {
+  double2* A = A0 + blockIdx.y * mstride;
+  const int* moves = moves0 + blockIdx.y * kMovesStride;
+  __shared__ double2 L[kPW][kPW + 1];
+  __shared__ int mv[kMovesStride];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int cnt = moves[0];
+  for (int e = tid; e < 2 * cnt; e += 256) mv[e] = moves[1 + e];
+  for (int e = tid; e < pw * pw; e += 256) {
+    const int i = e / pw, k = e - i * pw;
+    L[i][k] = A[static_cast<int64_t>(j0 + i) * n + j0 + k];
+  }
+  __syncthreads();
+  const int t = blockIdx.x * 8 + (tid >> 5);
+  if (t >= n - pw) return;
+  const int c = t < j0 ? t : t + pw;
+  double2 v0 = make_double2(0, 0), v1 = make_double2(0, 0);
+  if (lane < cnt) v0 = A[static_cast<int64_t>(j0 + mv[2 * lane + 1]) * n + c];
+  if (lane + 32 < cnt) v1 = A[static_cast<int64_t>(j0 + mv[2 * lane + 65]) * n + c];
+  __syncwarp();
+  if (lane < cnt) A[static_cast<int64_t>(j0 + mv[2 * lane]) * n + c] = v0;
+  if (lane + 32 < cnt) A[static_cast<int64_t>(j0 + mv[2 * lane + 64]) * n + c] = v1;
+  __syncwarp();
+  if (c < j0 + pw) return;
+  double2 x = lane < pw ? A[static_cast<int64_t>(j0 + lane) * n + c] : make_double2(0, 0);
+  for (int k = 0; k < pw - 1; ++k) {
+    double2 xk;
+    xk.x = __shfl_sync(0xffffffffu, x.x, k);
+    xk.y = __shfl_sync(0xffffffffu, x.y, k);
+    if (lane > k && lane < pw) cfma(x, make_double2(-L[lane][k].x, -L[lane][k].y), xk);
+  }
+  if (lane < pw) A[static_cast<int64_t>(j0 + lane) * n + c] = x;
+}
+
 // perm[i] = source row of position i after the interchanges ipiv[0..n) (one thread; n <= 8192)
 __global__ void build_perm(const int* ipiv, int n, int* perm) {
   extern __shared__ int pm[];
@@ -230,49 +352,53 @@ int gemm_rm(int64_t m, int64_t nn, int64_t k, double2 alpha, const double2* A, i
   return gemm(TOEP_C128, m, nn, k, alpha, A, lda, 1, 0, B, ldb, 1, 0, beta, C, ldc, 1, 0, 1, s);
 }
 
-// in-place LU with partial pivoting of the n x n row-major A; info (device) > 0: singular.
-// Blocked right-looking: outer blocks of kOB columns; inside, kPB-column sub-panels factored in
-// shared memory (lu_subpanel), their interchanges applied to all other columns, the sub-panel's
-// U rows solved and the rest of the outer block updated; then the outer block's U12 = L11^-1 A12
-// (trsm_block) and the trailing update A22 -= L21 U12 on the tensor cores (K = kOB).
-int getrf(double2* A, int n, int* ipiv, int* info, cudaStream_t s) {
-  const size_t psmem = sizeof(double2) * static_cast<size_t>(n) * kPB;
-  TOEP_REQUIRE(psmem <= 227 * 1024, TOEP_ERR_ARG, "lu_factor: n = %d exceeds the shared-memory sub-panel (<= 1816)", n);
+// In-place LU with partial pivoting of `batch` n x n row-major matrices spaced mstride apart
+// (LAPACK getrf semantics: ipiv 0-based absolute rows, info > 0 = first zero pivot, 1-based).
+// Right-looking, kPW-column panels: cluster panel factorisation (lu_panel_cluster), the row
+// permutation + U12 solve for the other columns (swap_trsm), then the trailing update
+// A22 -= L21 U12 on the tensor cores (K = kPW), batched over the matrices.
+int getrf_batched(double2* A, int64_t mstride, int batch, int n, int* ipiv, int* info, cudaStream_t s) {
+  const size_t psmem = panel_smem(n, 0);
+  const int rpc = (n + kCL - 1) / kCL;
+  TOEP_REQUIRE(psmem <= 220 * 1024 && rpc <= 2 * kPanelThr, TOEP_ERR_ARG,
+               "lu_factor: n = %d exceeds the cluster-resident panel (n <= 3000)", n);
   static size_t attr = 0;
   if (psmem > 48 * 1024 && attr < psmem) {
-    TOEP_CUDA(cudaFuncSetAttribute(lu_subpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+    TOEP_CUDA(cudaFuncSetAttribute(lu_panel_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
     attr = psmem;
   }
-  for (int j0 = 0; j0 < n; j0 += kOB) {
-    const int ob = std::min(kOB, n - j0);
-    for (int jj = j0; jj < j0 + ob; jj += kPB) {
-      const int pb = std::min(kPB, j0 + ob - jj);
-      lu_subpanel<<<1, kPanelThreads, sizeof(double2) * static_cast<size_t>(n - jj) * kPB, s>>>(A, n, n, jj, ipiv, info);
-      TOEP_LAUNCHED();
-      laswp_cols<<<(n + 255) / 256, 256, 0, s>>>(A, n, n, jj, pb, ipiv);
-      TOEP_LAUNCHED();
-      const int c0 = jj + pb, ncol = j0 + ob - c0;  // rest of the outer block
-      if (ncol > 0) {
-        trsm<32>(A, n, A, n, jj, pb, c0, ncol, 0, s);
-        TOEP_LAUNCHED();
-        const int rows = n - c0;
-        if (rows > 0)
-          TOEP_TRY(gemm_rm(rows, ncol, pb, make_double2(-1, 0), A + static_cast<int64_t>(c0) * n + jj, n,
-                           A + static_cast<int64_t>(jj) * n + c0, n, make_double2(1, 0),
-                           A + static_cast<int64_t>(c0) * n + c0, n, s));
+  int* moves = nullptr;
+  TOEP_REQUIRE(cudaMallocAsync(reinterpret_cast<void**>(&moves), sizeof(int) * kMovesStride * batch, s) == cudaSuccess,
+               TOEP_ERR_OOM, "out of device memory in lu_factor");
+  TOEP_CUDA(cudaMemsetAsync(info, 0, sizeof(int) * batch, s));
+  int rc = TOEP_OK;
+  for (int j0 = 0; j0 < n && rc == TOEP_OK; j0 += kPW) {
+    const int pw = std::min(kPW, n - j0);
+    lu_panel_cluster<<<dim3(kCL, batch), kPanelThr, panel_smem(n, j0), s>>>(A, mstride, n, j0, ipiv, info, moves);
+    if (cudaGetLastError() != cudaSuccess) {
+      set_error("lu_panel_cluster launch failed");
+      rc = TOEP_ERR_CUDA;
+      break;
+    }
+    if (n - pw > 0) {
+      swap_trsm<<<dim3((n - pw + 7) / 8, batch), 256, 0, s>>>(A, mstride, n, j0, pw, moves);
+      if (cudaGetLastError() != cudaSuccess) {
+        set_error("swap_trsm launch failed");
+        rc = TOEP_ERR_CUDA;
+        break;
       }
     }
-    const int c0 = j0 + ob, rest = n - c0;
-    if (rest > 0) {
-      trsm<32>(A, n, A, n, j0, ob, c0, rest, 0, s);
-      TOEP_LAUNCHED();
-      TOEP_TRY(gemm_rm(rest, rest, ob, make_double2(-1, 0), A + static_cast<int64_t>(c0) * n + j0, n,
-                       A + static_cast<int64_t>(j0) * n + c0, n, make_double2(1, 0),
-                       A + static_cast<int64_t>(c0) * n + c0, n, s));
-    }
+    const int c0 = j0 + pw, rest = n - c0;
+    if (rest > 0)
+      rc = gemm(TOEP_C128, rest, rest, pw, make_double2(-1, 0), A + static_cast<int64_t>(c0) * n + j0, n, 1, mstride,
+                A + static_cast<int64_t>(j0) * n + c0, n, 1, mstride, make_double2(1, 0),
+                A + static_cast<int64_t>(c0) * n + c0, n, 1, mstride, batch, s);
   }
-  return TOEP_OK;
+  cudaFreeAsync(moves, s);
+  return rc;
 }
+
+int getrf(double2* A, int n, int* ipiv, int* info, cudaStream_t s) { return getrf_batched(A, 0, 1, n, ipiv, info, s); }
 
 // B <- A^-1 B with A = P L U from getrf; B: n x nrhs row-major (ldb)
 int getrs(const double2* LU, int n, const int* ipiv, double2* B, int ldb, int nrhs, cudaStream_t s) {
@@ -322,7 +448,6 @@ using namespace toep;
 extern "C" int toep_lu_factor(void* a, int n, int* ipiv, int* info, void* stream) {
   TOEP_REQUIRE(a != nullptr && ipiv != nullptr && info != nullptr && n >= 1, TOEP_ERR_ARG, "bad lu_factor args");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  TOEP_CUDA(cudaMemsetAsync(info, 0, sizeof(int), s));
   return getrf(static_cast<double2*>(a), n, ipiv, info, s);
 }
 
@@ -346,12 +471,11 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   auto rb = [&](int o) { return blocks + static_cast<int64_t>(((o % nb2) + nb2) % nb2) * ss; };
   if (fail_step) *fail_step = -1;
 
-  double2 *g = nullptr, *h = nullptr, *gtmp = nullptr, *lu0 = nullptr, *lu1 = nullptr, *lu2 = nullptr;
-  double2 *gnew = nullptr, *hnew = nullptr, *num = nullptr;
-  int *piv0 = nullptr, *piv1 = nullptr, *piv2 = nullptr, *info = nullptr;
+  double2 *g = nullptr, *h = nullptr, *gtmp = nullptr, *lu0 = nullptr, *lu12 = nullptr, *wide = nullptr;
+  int *piv0 = nullptr, *piv12 = nullptr, *info = nullptr;
   auto cleanup = [&]() {
-    for (void* q : {(void*)g, (void*)h, (void*)gtmp, (void*)lu0, (void*)lu1, (void*)lu2, (void*)gnew, (void*)hnew,
-                    (void*)num, (void*)piv0, (void*)piv1, (void*)piv2, (void*)info})
+    for (void* q : {(void*)g, (void*)h, (void*)gtmp, (void*)lu0, (void*)lu12, (void*)wide, (void*)piv0, (void*)piv12,
+                    (void*)info})
       if (q) cudaFreeAsync(q, st);
     cudaStreamSynchronize(st);
   };
@@ -374,25 +498,36 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     }                    \
   } while (0)
   const int nm1 = std::max(N - 1, 1);
-  R_ALLOC(g, nm1 * ss);
-  R_ALLOC(h, nm1 * ss);
-  R_ALLOC(gtmp, nm1 * ss);
+  R_ALLOC(g, N * ss);  // G_1..G_m stacked (+1 slot for G_new)
+  R_ALLOC(h, N * ss);
+  R_ALLOC(gtmp, N * ss);
   R_ALLOC(lu0, ss);
-  R_ALLOC(lu1, ss);
-  R_ALLOC(lu2, ss);
-  R_ALLOC(gnew, ss);
-  R_ALLOC(hnew, ss);
-  R_ALLOC(num, std::max<int64_t>(sw, 1));
+  R_ALLOC(lu12, 2 * ss);  // D1, D2 factored together
   R_ALLOC(piv0, s);
-  R_ALLOC(piv1, s);
-  R_ALLOC(piv2, s);
-  R_ALLOC(info, 1);
+  R_ALLOC(piv12, 2 * s);
+  R_ALLOC(info, 2);
+  // Block sums over k become single GEMMs of depth m*s against "wide" copies of the generator
+  // blocks, s x (N-1)s row-major each:  Wp = [R_1 .. R_{N-1}],  Wpr = [R_{N-1} .. R_1],
+  // Wn = [R_-1 .. R_-(N-1)],  Wnr = [R_-(N-1) .. R_-1].
+  const int64_t wld = static_cast<int64_t>(nm1) * s, wsz = static_cast<int64_t>(s) * wld;
+  if (N > 1) {
+    R_ALLOC(wide, 4 * wsz);
+    for (int t = 0; t < N - 1; ++t) {
+      const double2* src[4] = {rb(t + 1), rb(N - 1 - t), rb(-(t + 1)), rb(-(N - 1 - t))};
+      for (int q = 0; q < 4; ++q)
+        TOEP_CUDA(cudaMemcpy2DAsync(wide + q * wsz + static_cast<int64_t>(t) * s, wld * sizeof(double2), src[q],
+                                    s * sizeof(double2), s * sizeof(double2), s, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  double2 *Wp = wide, *Wpr = wide + wsz, *Wn = wide + 2 * wsz, *Wnr = wide + 3 * wsz;
+  double2 *lu1 = lu12, *lu2 = lu12 + ss;
+  int *piv1 = piv12, *piv2 = piv12 + s;
   const double2 one = make_double2(1, 0), mone = make_double2(-1, 0);
-  auto check_info = [&](int code, int step) -> int {
-    int hinfo = 0;
-    TOEP_CUDA(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  auto check_info = [&](int code, int step, int count) -> int {
+    int hinfo[2] = {0, 0};
+    TOEP_CUDA(cudaMemcpyAsync(hinfo, info, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
     TOEP_CUDA(cudaStreamSynchronize(st));
-    if (hinfo != 0) {
+    if (hinfo[0] != 0 || (count > 1 && hinfo[1] != 0)) {
       if (fail_step) *fail_step = step;
       set_error(code == TOEP_ERR_SINGULAR_BLOCK ? "self block R_0 is singular"
                                                 : "singular denominator at bordering step %d", step);
@@ -405,65 +540,67 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     TOEP_REQUIRE(hook(hook_ctx, stage, x, g, h, stream) == 0, TOEP_ERR_ARG, "rybicki step hook failed");
     return TOEP_OK;
   };
+  // C (+)= alpha * W[:, t0*s : (t0+m)*s] @ stack(m blocks of s x ncol), one GEMM of depth m*s
+  auto wide_gemm = [&](const double2* W, int t0, int m, const double2* B, int64_t ncol, double2* C) {
+    return gemm_rm(s, ncol, static_cast<int64_t>(m) * s, one, W + static_cast<int64_t>(t0) * s, wld, B, ncol, one, C,
+                   ncol, st);
+  };
+  // C_b (+)= alpha * A_{m-1-b} @ B for b = 0..m-1 (A blocks s x s stacked, reversed), one batched GEMM
+  auto rev_batched = [&](const double2* Astack, int m, const double2* B, int64_t ncol, double2* C, int64_t c_bs) {
+    return gemm(TOEP_C128, s, ncol, s, mone, Astack + static_cast<int64_t>(m - 1) * ss, s, 1, -ss, B, ncol, 1, 0, one,
+                C, ncol, 1, c_bs, m, st);
+  };
 
   // base stage (rybicki.py:94-108)
   TOEP_CUDA(cudaMemcpyAsync(lu0, rb(0), ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
-  R_TRY(toep_lu_factor(lu0, s, piv0, info, stream));
-  R_TRY(check_info(TOEP_ERR_SINGULAR_BLOCK, 0));
+  R_TRY(getrf(lu0, s, piv0, info, st));
+  R_TRY(check_info(TOEP_ERR_SINGULAR_BLOCK, 0, 1));
   TOEP_CUDA(cudaMemcpyAsync(x, y, sw * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   R_TRY(getrs(lu0, s, piv0, x, static_cast<int>(w), static_cast<int>(w), st));
   if (N > 1) {
     TOEP_CUDA(cudaMemcpyAsync(g, rb(-1), ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
-    R_TRY(getrs(lu0, s, piv0, g, s, s, st));
     TOEP_CUDA(cudaMemcpyAsync(h, rb(1), ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+    // G_1 and H_1 share the factor: one solve with 2s right-hand sides would need them side by
+    // side; two solves keep the stacked layout.
+    R_TRY(getrs(lu0, s, piv0, g, s, s, st));
     R_TRY(getrs(lu0, s, piv0, h, s, s, st));
   }
   R_TRY(stage_hook(1));
 
   for (int m = 1; m < N; ++m) {
-    // d1 = sum_{k=1..m} R_k G_k - R_0  (G_k = g[k-1])
+    const bool more = m < N - 1;
+    // d1 = sum_{k=1..m} R_k G_k - R_0 ;  d2 = sum_{k=1..m} R_{-k} H_k - R_0   (factored together)
     R_TRY(copy_neg(rb(0), lu1, ss, -1.0, st));
-    for (int k = 1; k <= m; ++k)
-      R_TRY(gemm_rm(s, s, s, one, rb(k), s, g + (k - 1) * ss, s, one, lu1, s, st));
-    R_TRY(toep_lu_factor(lu1, s, piv1, info, stream));
-    R_TRY(check_info(TOEP_ERR_SINGULAR_DENOM, m));
-    // x_{m+1} = D1^-1 (sum_j R_{m+1-j} x_j - y_{m+1})
-    R_TRY(copy_neg(y + m * sw, num, sw, -1.0, st));
-    for (int jj = 1; jj <= m; ++jj)
-      R_TRY(gemm_rm(s, w, s, one, rb(m + 1 - jj), s, x + (jj - 1) * sw, w, one, num, w, st));
-    R_TRY(getrs(lu1, s, piv1, num, static_cast<int>(w), static_cast<int>(w), st));
-    TOEP_CUDA(cudaMemcpyAsync(x + m * sw, num, sw * sizeof(double2), cudaMemcpyDeviceToDevice, st));
-    // x_j -= G_{m+1-j} x_{m+1}
-    for (int jj = 1; jj <= m; ++jj)
-      R_TRY(gemm_rm(s, w, s, mone, g + (m - jj) * ss, s, x + m * sw, w, one, x + (jj - 1) * sw, w, st));
-    if (m < N - 1) {
-      // d2 = sum_{k=1..m} R_{-k} H_k - R_0
+    R_TRY(wide_gemm(Wp, 0, m, g, s, lu1));
+    if (more) {
       R_TRY(copy_neg(rb(0), lu2, ss, -1.0, st));
-      for (int k = 1; k <= m; ++k)
-        R_TRY(gemm_rm(s, s, s, one, rb(-k), s, h + (k - 1) * ss, s, one, lu2, s, st));
-      R_TRY(toep_lu_factor(lu2, s, piv2, info, stream));
-      R_TRY(check_info(TOEP_ERR_SINGULAR_DENOM, m));
-      // G_new = D2^-1 (sum_j R_{j-m-1} G_j - R_{-(m+1)})
+      R_TRY(wide_gemm(Wn, 0, m, h, s, lu2));
+    }
+    R_TRY(getrf_batched(lu12, ss, more ? 2 : 1, s, piv12, info, st));
+    R_TRY(check_info(TOEP_ERR_SINGULAR_DENOM, m, more ? 2 : 1));
+    // x_{m+1} = D1^-1 (sum_j R_{m+1-j} x_j - y_{m+1})
+    double2* xn = x + m * sw;
+    R_TRY(copy_neg(y + m * sw, xn, sw, -1.0, st));
+    R_TRY(wide_gemm(Wpr, N - 1 - m, m, x, w, xn));
+    R_TRY(getrs(lu1, s, piv1, xn, static_cast<int>(w), static_cast<int>(w), st));
+    // x_j -= G_{m+1-j} x_{m+1}
+    R_TRY(rev_batched(g, m, xn, w, x, sw));
+    if (more) {
+      // G_new = D2^-1 (sum_j R_{j-m-1} G_j - R_{-(m+1)})   -> slot m of the next G stack
+      double2* gnew = gtmp + m * ss;
       R_TRY(copy_neg(rb(-(m + 1)), gnew, ss, -1.0, st));
-      for (int jj = 1; jj <= m; ++jj)
-        R_TRY(gemm_rm(s, s, s, one, rb(jj - m - 1), s, g + (jj - 1) * ss, s, one, gnew, s, st));
+      R_TRY(wide_gemm(Wnr, N - 1 - m, m, g, s, gnew));
       R_TRY(getrs(lu2, s, piv2, gnew, s, s, st));
-      // H_new = D1^-1 (sum_j R_{m+1-j} H_j - R_{m+1})
+      // H_new = D1^-1 (sum_j R_{m+1-j} H_j - R_{m+1})       -> slot m of H
+      double2* hnew = h + m * ss;
       R_TRY(copy_neg(rb(m + 1), hnew, ss, -1.0, st));
-      for (int jj = 1; jj <= m; ++jj)
-        R_TRY(gemm_rm(s, s, s, one, rb(m + 1 - jj), s, h + (jj - 1) * ss, s, one, hnew, s, st));
+      R_TRY(wide_gemm(Wpr, N - 1 - m, m, h, s, hnew));
       R_TRY(getrs(lu1, s, piv1, hnew, s, s, st));
-      // G_j -= H_{m+1-j} G_new (into gtmp, old H);  H_j -= G_{m+1-j} H_new (old G)
-      for (int jj = 1; jj <= m; ++jj) {
-        TOEP_CUDA(cudaMemcpyAsync(gtmp + (jj - 1) * ss, g + (jj - 1) * ss, ss * sizeof(double2),
-                                  cudaMemcpyDeviceToDevice, st));
-        R_TRY(gemm_rm(s, s, s, mone, h + (m - jj) * ss, s, gnew, s, one, gtmp + (jj - 1) * ss, s, st));
-      }
-      for (int jj = 1; jj <= m; ++jj)
-        R_TRY(gemm_rm(s, s, s, mone, g + (m - jj) * ss, s, hnew, s, one, h + (jj - 1) * ss, s, st));
-      TOEP_CUDA(cudaMemcpyAsync(g, gtmp, m * ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
-      TOEP_CUDA(cudaMemcpyAsync(g + m * ss, gnew, ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
-      TOEP_CUDA(cudaMemcpyAsync(h + m * ss, hnew, ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+      // G_j' = G_j - H_{m+1-j} G_new (old H, into the next stack);  H_j -= G_{m+1-j} H_new (old G)
+      TOEP_CUDA(cudaMemcpyAsync(gtmp, g, m * ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+      R_TRY(rev_batched(h, m, gnew, s, gtmp, ss));
+      R_TRY(rev_batched(g, m, hnew, s, h, ss));
+      std::swap(g, gtmp);
     }
     R_TRY(stage_hook(m + 1));
   }
