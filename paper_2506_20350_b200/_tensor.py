@@ -34,7 +34,7 @@ def to_columns(data, dtype: torch.dtype = torch.complex128, keep_c64: bool = Fal
         kind = "cuda" if t.is_cuda else "cpu"
         pinned = (not t.is_cuda) and t.is_pinned()
         want = torch.complex64 if (keep_c64 and t.dtype == torch.complex64) else dtype
-        t = t.to(device=dev, dtype=want, non_blocking=pinned)
+        t = t.to(device=dev, dtype=want, non_blocking=pinned).resolve_conj().resolve_neg()  # lazy views -> memory
     else:
         arr = np.asarray(data, dtype=np.complex128)
         kind, pinned = "numpy", False

@@ -494,6 +494,76 @@ int bin_product(int dtype, const void* DT, const void* U, void* V, int64_t K, in
   return bin_product_t<float>(DT, U, V, K, n0, w, transpose, stop, s);
 }
 
+// Skinny complex128 GEMM, all operands row-major, n <= NC columns: C = alpha A B + beta C.
+// One CTA per RB rows of A (x batch); its 256 threads stride over K (coalesced 512-byte rows of
+// A per warp, B rows from L2), then a fixed-order warp-shuffle + shared-memory reduction (no
+// atomics: deterministic).  Used where the tile GEMM would launch only m/64 CTAs (n <= 8
+// right-hand sides against a long K) and run at a fraction of HBM bandwidth.
+template <int NC, int RB>
+__global__ void __launch_bounds__(256) skinny_gemm_kernel(int64_t m, int n, int64_t k, double2 alpha,
+                                                          const double2* __restrict__ A, int64_t lda, int64_t a_bs,
+                                                          const double2* __restrict__ B, int64_t ldb, int64_t b_bs,
+                                                          double2 beta, double2* C, int64_t ldc, int64_t c_bs) {
+  __shared__ double2 red[8][RB][NC];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * RB;
+  A += blockIdx.y * a_bs + r0 * lda;
+  B += blockIdx.y * b_bs;
+  C += blockIdx.y * c_bs;
+  const int rows = static_cast<int>(std::min<int64_t>(RB, m - r0));
+  double2 acc[RB][NC];
+#pragma unroll
+  for (int r = 0; r < RB; ++r)
+#pragma unroll
+    for (int j = 0; j < NC; ++j) acc[r][j] = make_double2(0, 0);
+  for (int64_t kk = tid; kk < k; kk += 256) {
+    double2 b[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) b[j] = j < n ? B[kk * ldb + j] : make_double2(0, 0);
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const double2 av = r < rows ? A[r * lda + kk] : make_double2(0, 0);
+#pragma unroll
+      for (int j = 0; j < NC; ++j) cfma(acc[r][j], av, b[j]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RB; ++r)
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        acc[r][j].x += __shfl_xor_sync(0xffffffffu, acc[r][j].x, off);
+        acc[r][j].y += __shfl_xor_sync(0xffffffffu, acc[r][j].y, off);
+      }
+      if (lane == 0) red[warp][r][j] = acc[r][j];
+    }
+  __syncthreads();
+  if (tid < RB * NC) {
+    const int r = tid / NC, j = tid % NC;
+    if (r < rows && j < n) {
+      double2 sum = red[0][r][j];
+      for (int w = 1; w < 8; ++w) sum = cadd(sum, red[w][r][j]);
+      double2* cp = C + (r0 + r) * ldc + j;
+      double2 out = cmul(alpha, sum);
+      if (beta.x != 0.0 || beta.y != 0.0) cfma(out, beta, *cp);
+      *cp = out;
+    }
+  }
+}
+
+template <int NC, int RB>
+int skinny_launch(int64_t m, int64_t n, int64_t k, double2 alpha, const void* a, int64_t lda, int64_t a_bs,
+                  const void* b, int64_t ldb, int64_t b_bs, double2 beta, void* c, int64_t ldc, int64_t c_bs,
+                  int64_t batch, cudaStream_t s) {
+  const dim3 grid(static_cast<unsigned>((m + RB - 1) / RB), static_cast<unsigned>(batch));
+  skinny_gemm_kernel<NC, RB><<<grid, 256, 0, s>>>(m, static_cast<int>(n), k, alpha, static_cast<const double2*>(a), lda,
+                                                  a_bs, static_cast<const double2*>(b), ldb, b_bs, beta,
+                                                  static_cast<double2*>(c), ldc, c_bs);
+  TOEP_LAUNCHED();
+  return TOEP_OK;
+}
+
 int gemm(int dtype, int64_t m, int64_t n, int64_t k, double2 alpha, const void* a, int64_t a_rs, int64_t a_cs,
          int64_t a_bs, const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, double2 beta, void* c, int64_t c_rs,
          int64_t c_cs, int64_t c_bs, int64_t batch, cudaStream_t s, const int* stop) {
@@ -502,6 +572,11 @@ int gemm(int dtype, int64_t m, int64_t n, int64_t k, double2 alpha, const void* 
     const char* e = std::getenv("TOEP_ZGEMM");
     return e != nullptr && std::strcmp(e, "simt") == 0;
   }();
+  if (dtype == TOEP_C128 && stop == nullptr && !simt_only && n <= 8 && k >= 256 && a_cs == 1 && b_cs == 1 &&
+      c_cs == 1 && batch <= 65535 && (m + 3) / 4 <= 0x7fffffff) {
+    if (n <= 4) return skinny_launch<4, 4>(m, n, k, alpha, a, a_rs, a_bs, b, b_rs, b_bs, beta, c, c_rs, c_bs, batch, s);
+    return skinny_launch<8, 2>(m, n, k, alpha, a, a_rs, a_bs, b, b_rs, b_bs, beta, c, c_rs, c_bs, batch, s);
+  }
   if (dtype == TOEP_C128 && stop == nullptr && !simt_only && m * n * k >= 32 * 32 * 32) {
     const int rc = zgemm_tc(m, n, k, alpha, a, a_rs, a_cs, a_bs, b, b_rs, b_cs, b_bs, beta, c, c_rs, c_cs, c_bs,
                             batch, s);

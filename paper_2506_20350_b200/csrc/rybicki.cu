@@ -121,7 +121,6 @@ void trsm(const double2* LU, int lda, double2* X, int64_t ldx, int r0, int nb, i
 // (destination, source) row pairs so the other columns can be permuted by swap_trsm.
 constexpr int kCL = 8;
 constexpr int kPW = 32;
-constexpr int kPanelThr = 256;
 constexpr int kMovesStride = 1 + 4 * kPW;  // count + up to 2*kPW (dst, src) pairs
 
 __device__ __forceinline__ double cabs1(double2 a) { return fabs(a.x) + fabs(a.y); }
@@ -139,12 +138,48 @@ __device__ __forceinline__ void warp_argmax(double& v, int& i) {
   }
 }
 
-size_t panel_smem(int n, int j0) {
-  const int R = n - j0, rpc = (R + kCL - 1) / kCL;
-  return sizeof(double2) * static_cast<size_t>(rpc) * (kPW + 1) + 2 * sizeof(int) * static_cast<size_t>(R);
+// explicit distributed-shared-memory stores (st.shared::cluster on a mapa'd address)
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dsmem_st_c128(uint32_t a, double2 v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void dsmem_st_f64(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_st_s32(uint32_t a, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+size_t panel_smem(int n, int j0) { return 2 * sizeof(int) * static_cast<size_t>(n - j0); }
+
+// Panel rows live in registers, each row split over kTPR adjacent lanes (kCPT columns each):
+// thread t of CTA r owns columns (t % kTPR)*kCPT .. +kCPT of physical rows
+// r*rpc + t / kTPR + q*kRowsPass, q < RPT.
+constexpr int kPanelThr2 = 512;
+constexpr int kTPR = 4;
+constexpr int kCPT = kPW / kTPR;                 // 8 columns per thread
+constexpr int kRowsPass = kPanelThr2 / kTPR;     // 128 rows per pass
+
+template <int RPT>
+__device__ __forceinline__ double2 pick(const double2 (&a)[RPT][kCPT], int q, int k) {
+  double2 v = make_double2(0, 0);
+#pragma unroll
+  for (int qq = 0; qq < RPT; ++qq)
+#pragma unroll
+    for (int kk = 0; kk < kCPT; ++kk)
+      if (qq == q && kk == k) v = a[qq][kk];
+  return v;
 }
 
-__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kPanelThr)
+#ifdef TOEP_PANEL_PROBE
+__device__ long long g_probe[kCL][8];
+#endif
+
+template <int RPT>
+__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kPanelThr2, 1)
     lu_panel_cluster(double2* A0, int64_t mstride, int n, int j0, int* ipiv0, int* info0, int* moves0) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
@@ -155,110 +190,154 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kPanelThr)
   const int R = n - j0, pw = min(kPW, R);
   const int rpc = (R + kCL - 1) / kCL;
   const int row0 = rank * rpc, nrow = max(0, min(R, row0 + rpc) - row0);
-  extern __shared__ double2 panel_sm[];
-  double2* P = panel_sm;                                        // [rpc][kPW+1]
-  int* pos_of = reinterpret_cast<int*>(P + static_cast<int64_t>(rpc) * (kPW + 1));  // [R]
-  int* phys_at = pos_of + R;                                    // [R]
-  __shared__ double wv[2][kPanelThr / 32];
-  __shared__ int wi[2][kPanelThr / 32];
-  __shared__ double cv[2];
-  __shared__ int ci[2];
+  extern __shared__ int panel_sm[];
+  int* pos_of = panel_sm;     // [R]
+  int* phys_at = pos_of + R;  // [R]
+  // inbox: every CTA pushes its candidate (|pivot|, row index, row) into every CTA's inbox slot
+  // [column parity][source rank] with remote stores before the cluster barrier, so that after
+  // the barrier all pivot decisions read local shared memory only
+  __shared__ double2 ib_row[2][kCL][kPW];
+  __shared__ double ib_v[2][kCL];
+  __shared__ int ib_i[2][kCL];
+  __shared__ double wv[2][kPanelThr2 / 32];
+  __shared__ int wi[2][kPanelThr2 / 32];
   __shared__ int nmoves;
+  __shared__ int spiv[kPW];  // ipiv of the panel, written to global memory once at the end
+  __shared__ int sinfo;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = tid % kTPR, rl = tid / kTPR, cbase = sub * kCPT;
 
-  for (int e = tid; e < nrow * kPW; e += kPanelThr) {
-    const int i = e / kPW, c = e - i * kPW;
-    P[i * (kPW + 1) + c] = c < pw ? A[static_cast<int64_t>(j0 + row0 + i) * n + j0 + c] : make_double2(0, 0);
+  double2 a[RPT][kCPT];
+  bool used[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = rl + q * kRowsPass;
+    used[q] = !(i < nrow);
+    const double2* src = A + static_cast<int64_t>(j0 + row0 + (used[q] ? 0 : i)) * n + j0 + cbase;
+#pragma unroll
+    for (int k = 0; k < kCPT; ++k) a[q][k] = (!used[q] && cbase + k < pw) ? src[k] : make_double2(0, 0);
   }
-  for (int i = tid; i < R; i += kPanelThr) {
+  for (int i = tid; i < R; i += kPanelThr2) {
     pos_of[i] = i;
     phys_at[i] = i;
   }
-  if (tid == 0) nmoves = 0;
-  constexpr int kRowsPerThread = 2;  // rpc <= 2 * kPanelThr (checked on the host)
-  bool used[kRowsPerThread] = {false, false};
+  if (tid == 0) {
+    nmoves = 0;
+    sinfo = 0;
+  }
   __syncthreads();
 
+#ifdef TOEP_PANEL_PROBE
+#define PROBE(k)                        \
+  do {                                  \
+    const long long t1 = clock64();     \
+    acc[k] += t1 - tp;                  \
+    tp = t1;                            \
+  } while (0)
+  long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tp = clock64();
+#else
+#define PROBE(k)
+#endif
   for (int jj = 0; jj < pw; ++jj) {
-    const int par = jj & 1;
+    const int par = jj & 1, jc = jj / kCPT, jk = jj % kCPT;
+    const bool mine = (sub == jc);  // this thread holds column jj of its rows
     double best = -1.0;
     int bi = INT_MAX;
 #pragma unroll
-    for (int q = 0; q < kRowsPerThread; ++q) {
-      const int i = tid + q * kPanelThr;
-      if (i < nrow && !used[q]) argmax_merge(best, bi, cabs1(P[i * (kPW + 1) + jj]), row0 + i);
-    }
+    for (int q = 0; q < RPT; ++q)
+      if (mine && !used[q]) argmax_merge(best, bi, cabs1(pick<RPT>(a, q, jk)), row0 + rl + q * kRowsPass);
     warp_argmax(best, bi);
+    PROBE(0);
     if (lane == 0) {
       wv[par][warp] = best;
       wi[par][warp] = bi;
     }
     __syncthreads();
-    if (warp == 0) {
-      double b = lane < kPanelThr / 32 ? wv[par][lane] : -1.0;
-      int i = lane < kPanelThr / 32 ? wi[par][lane] : INT_MAX;
-      warp_argmax(b, i);
-      if (lane == 0) {
-        cv[par] = b;
-        ci[par] = i;
+    PROBE(1);
+    double cb = lane < kPanelThr2 / 32 ? wv[par][lane] : -1.0;
+    int cix = lane < kPanelThr2 / 32 ? wi[par][lane] : INT_MAX;
+    warp_argmax(cb, cix);
+#pragma unroll
+    for (int q = 0; q < RPT; ++q)  // the CTA's candidate row is pushed by its kTPR owners
+      if (!used[q] && row0 + rl + q * kRowsPass == cix) {
+#pragma unroll
+        for (int d = 0; d < kCL; ++d) {
+          const uint32_t dst = dsmem_addr(&ib_row[par][rank][cbase], d);
+#pragma unroll
+          for (int k = 0; k < kCPT; ++k) dsmem_st_c128(dst + k * 16, a[q][k]);
+        }
       }
+    if (tid < kCL) {
+      dsmem_st_f64(dsmem_addr(&ib_v[par][rank], tid), cb);
+      dsmem_st_s32(dsmem_addr(&ib_i[par][rank], tid), cix);
     }
+    PROBE(2);
     cluster.sync();
-    double gb = -1.0;
-    int p = INT_MAX;
-    if (lane < kCL) {
-      gb = *cluster.map_shared_rank(&cv[par], lane);
-      p = *cluster.map_shared_rank(&ci[par], lane);
-    }
-    warp_argmax(gb, p);
-    const int owner = p / rpc, li = p - owner * rpc;
-    const double2* rP = cluster.map_shared_rank(P, owner);
-    const double2 u = (lane >= jj && lane < pw) ? rP[li * (kPW + 1) + lane] : make_double2(0, 0);
-    double2 piv;
-    piv.x = __shfl_sync(0xffffffffu, u.x, jj);
-    piv.y = __shfl_sync(0xffffffffu, u.y, jj);
-    const bool zero = !(gb >= kPivotTiny);
+    PROBE(3);
+    double gpv = lane < kCL ? ib_v[par][lane] : -1.0;
+    int p = lane < kCL ? ib_i[par][lane] : INT_MAX;
+    warp_argmax(gpv, p);
+    const int owner = p / rpc;
     if (tid == 0) {  // interchange bookkeeping (redundantly in every CTA)
       const int ppos = pos_of[p], phj = phys_at[jj];
       phys_at[jj] = p;
       phys_at[ppos] = phj;
       pos_of[p] = jj;
       pos_of[phj] = ppos;
-      if (rank == 0) {
-        ipiv[j0 + jj] = j0 + ppos;
-        if (zero && *info == 0) *info = j0 + jj + 1;
-      }
+      spiv[jj] = j0 + ppos;
+      if (!(gpv >= kPivotTiny) && sinfo == 0) sinfo = j0 + jj + 1;
     }
+    PROBE(4);
+    const bool zero = !(gpv >= kPivotTiny);
+    const double2 piv = ib_row[par][owner][jj];
+    // multiplier = a / piv as a * (1 / piv): one reciprocal per column, as LAPACK's zgetf2 scales
+    const double rden = zero ? 0.0 : 1.0 / (piv.x * piv.x + piv.y * piv.y);
+    const double2 rpiv = make_double2(piv.x * rden, -piv.y * rden);
+    double2 u[kCPT];
 #pragma unroll
-    for (int q = 0; q < kRowsPerThread; ++q) {
-      const int i = tid + q * kPanelThr;
-      bool act = i < nrow && !used[q];
-      if (act && row0 + i == p) {
+    for (int k = 0; k < kCPT; ++k) u[k] = ib_row[par][owner][cbase + k];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      bool act = !used[q];
+      if (act && row0 + rl + q * kRowsPass == p) {
         used[q] = true;
         act = false;
       }
-      double2 l = make_double2(0, 0);
-      if (act) {
-        l = P[i * (kPW + 1) + jj];
-        if (!zero) l = cdiv(l, piv);
-        P[i * (kPW + 1) + jj] = l;
-      }
+      double2 l = pick<RPT>(a, q, jk);
+      if (!zero) l = cmul(l, rpiv);
+      // the multiplier lives with the column-jj owner of the row; share it across the row's lanes
+      const int src = (lane & ~(kTPR - 1)) | jc;
+      l.x = __shfl_sync(0xffffffffu, l.x, src);
+      l.y = __shfl_sync(0xffffffffu, l.y, src);
       const double2 nl = make_double2(-l.x, -l.y);
-      for (int c = jj + 1; c < pw; ++c) {
-        double2 uc;
-        uc.x = __shfl_sync(0xffffffffu, u.x, c);
-        uc.y = __shfl_sync(0xffffffffu, u.y, c);
-        if (act) cfma(P[i * (kPW + 1) + c], nl, uc);
+#pragma unroll
+      for (int k = 0; k < kCPT; ++k) {
+        const int c = cbase + k;
+        if (act && c > jj) cfma(a[q][k], nl, u[k]);
+        if (act && c == jj) a[q][k] = l;
       }
     }
   }
-  cluster.sync();  // no CTA may leave while its shared memory can still be read remotely
-  for (int e = tid; e < nrow * kPW; e += kPanelThr) {
-    const int i = e / kPW, c = e - i * kPW;
-    if (c < pw) A[static_cast<int64_t>(j0 + pos_of[row0 + i]) * n + j0 + c] = P[i * (kPW + 1) + c];
+#ifdef TOEP_PANEL_PROBE
+  if (tid == 0)
+    for (int k = 0; k < 8; ++k) g_probe[rank][k] = acc[k];
+#endif
+  cluster.sync();  // remote reads done; pos_of final
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = rl + q * kRowsPass;
+    if (i < nrow) {
+      double2* dst = A + static_cast<int64_t>(j0 + pos_of[row0 + i]) * n + j0 + cbase;
+#pragma unroll
+      for (int k = 0; k < kCPT; ++k)
+        if (cbase + k < pw) dst[k] = a[q][k];
+    }
   }
   if (rank == 0) {
-    for (int q = tid; q < R; q += kPanelThr)
+    if (tid < pw) ipiv[j0 + tid] = spiv[tid];
+    if (tid == 0 && sinfo != 0 && *info == 0) *info = sinfo;
+    for (int q = tid; q < R; q += kPanelThr2)
       if (phys_at[q] != q) {
         const int k = atomicAdd(&nmoves, 1);
         moves[1 + 2 * k] = q;
@@ -360,11 +439,13 @@ int gemm_rm(int64_t m, int64_t nn, int64_t k, double2 alpha, const double2* A, i
 int getrf_batched(double2* A, int64_t mstride, int batch, int n, int* ipiv, int* info, cudaStream_t s) {
   const size_t psmem = panel_smem(n, 0);
   const int rpc = (n + kCL - 1) / kCL;
-  TOEP_REQUIRE(psmem <= 220 * 1024 && rpc <= 2 * kPanelThr, TOEP_ERR_ARG,
-               "lu_factor: n = %d exceeds the cluster-resident panel (n <= 3000)", n);
+  TOEP_REQUIRE(rpc <= 4 * kRowsPass, TOEP_ERR_ARG, "lu_factor: n = %d exceeds the cluster-resident panel (n <= 4096)",
+               n);
   static size_t attr = 0;
-  if (psmem > 48 * 1024 && attr < psmem) {
-    TOEP_CUDA(cudaFuncSetAttribute(lu_panel_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+  if (psmem > 40 * 1024 && attr < psmem) {
+    TOEP_CUDA(cudaFuncSetAttribute(lu_panel_cluster<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+    TOEP_CUDA(cudaFuncSetAttribute(lu_panel_cluster<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+    TOEP_CUDA(cudaFuncSetAttribute(lu_panel_cluster<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
     attr = psmem;
   }
   int* moves = nullptr;
@@ -374,7 +455,15 @@ int getrf_batched(double2* A, int64_t mstride, int batch, int n, int* ipiv, int*
   int rc = TOEP_OK;
   for (int j0 = 0; j0 < n && rc == TOEP_OK; j0 += kPW) {
     const int pw = std::min(kPW, n - j0);
-    lu_panel_cluster<<<dim3(kCL, batch), kPanelThr, panel_smem(n, j0), s>>>(A, mstride, n, j0, ipiv, info, moves);
+    const int rows_cta = (n - j0 + kCL - 1) / kCL;
+    const dim3 pg(kCL, batch);
+    const size_t ps = panel_smem(n, j0);
+    if (rows_cta <= kRowsPass)
+      lu_panel_cluster<1><<<pg, kPanelThr2, ps, s>>>(A, mstride, n, j0, ipiv, info, moves);
+    else if (rows_cta <= 2 * kRowsPass)
+      lu_panel_cluster<2><<<pg, kPanelThr2, ps, s>>>(A, mstride, n, j0, ipiv, info, moves);
+    else
+      lu_panel_cluster<4><<<pg, kPanelThr2, ps, s>>>(A, mstride, n, j0, ipiv, info, moves);
     if (cudaGetLastError() != cudaSuccess) {
       set_error("lu_panel_cluster launch failed");
       rc = TOEP_ERR_CUDA;

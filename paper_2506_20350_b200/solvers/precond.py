@@ -72,11 +72,11 @@ class Preconditioner:
             inv = numerics.block_inverse(lu)
             self._dev["pinv"] = torch.from_numpy(np.ascontiguousarray(inv)).to(dev)
             self._dev["pmat"] = torch.from_numpy(_reassemble(lu)).to(dev)
-            self._dev["pinv_h"] = self._dev["pinv"].conj().T.contiguous()
+            self._dev["pinv_h"] = torch.conj_physical(self._dev["pinv"]).T.contiguous()
             if self.border_lu is not None:
                 binv = numerics.block_inverse(self.border_lu)
                 self._dev["binv"] = torch.from_numpy(binv).to(dev)
-                self._dev["binv_h"] = self._dev["binv"].conj().T.contiguous()
+                self._dev["binv_h"] = torch.conj_physical(self._dev["binv"]).T.contiguous()
         return self._dev
 
     def _apply(self, v, adjoint: bool):

@@ -162,6 +162,25 @@ class TestBaselineCfg1:
 
 
 class TestSpectrum:
+    def test_adjoint_and_precond_adjoint_vs_dense(self):
+        # complex inputs, including a lazily conjugated torch view (its conj bit must be resolved
+        # before the storage reaches the C ABI)
+        from paper_2506_20350_b200.solvers.bordered import bordered_matvec_adjoint
+
+        gen = generator_from_stacked(seeded_stacked4(3, 3, 4, seed=11))
+        sys_ = system_from_generator(gen)
+        op = BorderedOperator.from_system(sys_)
+        pk = build_pk(sys_)
+        dense = assemble_dense(gen)
+        pinv = np.linalg.inv(scipy.linalg.block_diag(*([gen.block(0, 0)] * 9)))
+        rng = np.random.default_rng(5)
+        x = rng.standard_normal((dense.shape[0], 3)) + 1j * rng.standard_normal((dense.shape[0], 3))
+        xt = torch.from_numpy(x).cuda()
+        assert rel_err(bordered_matvec_adjoint(op, x), dense.conj().T @ x) <= 1e-12
+        assert rel_err(bordered_matvec_adjoint(op, xt.conj()).cpu().numpy(), dense.conj().T @ x.conj()) <= 1e-12
+        assert rel_err(pk.apply_adjoint(xt).cpu().numpy(), pinv.conj().T @ x) <= 1e-12
+        assert rel_err(pk.apply(xt.conj()).cpu().numpy(), pinv @ x.conj()) <= 1e-12
+
     def test_top_singular_values_vs_dense(self):
         from paper_2506_20350_b200.solvers import spectrum_estimate
 

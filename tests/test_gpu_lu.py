@@ -43,7 +43,7 @@ def _rand(rng, *shape):
     return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
 
 
-@pytest.mark.parametrize("n", [1, 2, 5, 31, 32, 33, 63, 64, 65, 100, 257, 512, 1024, 1500])
+@pytest.mark.parametrize("n", [1, 2, 5, 31, 32, 33, 63, 64, 65, 100, 257, 512, 1024, 1500, 2100, 3000])
 def test_factor_matches_lapack(n):
     rng = np.random.default_rng(n)
     a = _rand(rng, n, n)
@@ -97,7 +97,7 @@ def test_too_large_is_an_argument_error():
     from paper_2506_20350_b200 import _lib
     from paper_2506_20350_b200.errors import ToepsolveError
 
-    n = 4096
+    n = 5000  # > kCL * 2 * 256 rows: beyond the cluster-resident panel (checked before any access)
     lu = torch.empty((1, 1), dtype=torch.complex128, device="cuda")
     piv = torch.empty(1, dtype=torch.int32, device="cuda")
     info = torch.zeros(1, dtype=torch.int32, device="cuda")
