@@ -25,10 +25,6 @@ namespace cg = cooperative_groups;
 
 constexpr double kPivotTiny = 1e-300;
 
-__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
-  const double den = b.x * b.x + b.y * b.y;
-  return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
-}
 
 constexpr int kTrsmWarps = 8;
 
@@ -41,13 +37,31 @@ __global__ void __launch_bounds__(kTrsmWarps * 32) trsm_block(const double2* LU,
                                                                int r0, int nb, int c0, int ncols, int upper) {
   extern __shared__ double2 trsm_smem[];
   double2 (*T)[NB + 1] = reinterpret_cast<double2 (*)[NB + 1]>(trsm_smem);
-  for (int e = threadIdx.x; e < nb * nb; e += kTrsmWarps * 32) {
-    const int i = e / nb, k = e - i * nb;
-    T[i][k] = LU[static_cast<int64_t>(r0 + i) * lda + r0 + k];
+  __shared__ double2 rdiag[NB];
+  constexpr int R = NB / 32;
+  constexpr int kRowsPerWarp = NB / kTrsmWarps;
+  const int lane = threadIdx.x & 31, wrp = threadIdx.x >> 5;
+  {  // stage the diagonal block: all loads issued before any store (one latency, not NB*NB/256)
+    double2 v[kRowsPerWarp][R];
+#pragma unroll
+    for (int t = 0; t < kRowsPerWarp; ++t)
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = wrp + t * kTrsmWarps, k = lane + 32 * q;
+        v[t][q] = (i < nb && k < nb) ? LU[static_cast<int64_t>(r0 + i) * lda + r0 + k] : make_double2(0, 0);
+      }
+#pragma unroll
+    for (int t = 0; t < kRowsPerWarp; ++t)
+#pragma unroll
+      for (int q = 0; q < R; ++q) T[wrp + t * kTrsmWarps][lane + 32 * q] = v[t][q];
   }
   __syncthreads();
-  constexpr int R = NB / 32;
-  const int lane = threadIdx.x & 31;
+  if (upper && threadIdx.x < nb) {  // reciprocal pivots: the substitution chain multiplies
+    const double2 d = T[threadIdx.x][threadIdx.x];
+    const double r = 1.0 / (d.x * d.x + d.y * d.y);
+    rdiag[threadIdx.x] = make_double2(d.x * r, -d.y * r);
+  }
+  __syncthreads();
   const int c = c0 + blockIdx.x * kTrsmWarps + (threadIdx.x >> 5);
   if (c >= c0 + ncols) return;
   double2 x[R];
@@ -79,7 +93,7 @@ __global__ void __launch_bounds__(kTrsmWarps * 32) trsm_block(const double2* LU,
 #pragma unroll
       for (int q = 0; q < R; ++q)
         if (q == qk) {
-          if (lane == (k & 31)) x[q] = cdiv(x[q], T[k][k]);
+          if (lane == (k & 31)) x[q] = cmul(x[q], rdiag[k]);
           xk.x = __shfl_sync(0xffffffffu, x[q].x, k & 31);
           xk.y = __shfl_sync(0xffffffffu, x[q].y, k & 31);
         }
@@ -100,6 +114,7 @@ __global__ void __launch_bounds__(kTrsmWarps * 32) trsm_block(const double2* LU,
 template <int NB>
 void trsm(const double2* LU, int lda, double2* X, int64_t ldx, int r0, int nb, int c0, int ncols, int upper,
           cudaStream_t s) {
+  static_assert(NB % kTrsmWarps == 0 && NB % 32 == 0, "trsm block");
   constexpr int smem = NB * (NB + 1) * static_cast<int>(sizeof(double2));
   static bool configured = false;  // opt-in above 48 KB, once per process
   if (!configured) {
@@ -359,9 +374,15 @@ __global__ void __launch_bounds__(256) swap_trsm(double2* A0, int64_t mstride, i
   const int tid = threadIdx.x, lane = tid & 31;
   const int cnt = moves[0];
   for (int e = tid; e < 2 * cnt; e += 256) mv[e] = moves[1 + e];
-  for (int e = tid; e < pw * pw; e += 256) {
-    const int i = e / pw, k = e - i * pw;
-    L[i][k] = A[static_cast<int64_t>(j0 + i) * n + j0 + k];
+  {
+    double2 v[kPW / 8];
+#pragma unroll
+    for (int t = 0; t < kPW / 8; ++t) {
+      const int i = (tid >> 5) + 8 * t;
+      v[t] = (i < pw && lane < pw) ? A[static_cast<int64_t>(j0 + i) * n + j0 + lane] : make_double2(0, 0);
+    }
+#pragma unroll
+    for (int t = 0; t < kPW / 8; ++t) L[(tid >> 5) + 8 * t][lane] = v[t];
   }
   __syncthreads();
   const int t = blockIdx.x * 8 + (tid >> 5);
