@@ -487,6 +487,30 @@ int bin_product_t(const void* DT, const void* U, void* V, int64_t K, int n0, int
 
 }  // namespace
 
+L2Prefetch binprod_prefetch_plan(int dtype, const void* DT, int64_t K, int n0, bool inverse_side) {
+  L2Prefetch pf;
+  if (n0 != 128 || binprod_variant() != 3) return pf;  // only the whole-row TMA stream has this bin order
+  static const int64_t budget_fwd = [] {
+    const char* e = std::getenv("TOEP_PREFETCH_MB");
+    return static_cast<int64_t>(e != nullptr ? std::atoll(e) : 48) << 20;
+  }();
+  static const int64_t budget_inv = [] {
+    const char* e = std::getenv("TOEP_PREFETCH_INV_MB");
+    return static_cast<int64_t>(e != nullptr ? std::atoll(e) : 0) << 20;
+  }();
+  const int64_t budget = inverse_side ? budget_inv : budget_fwd;
+  const int64_t bin_bytes = static_cast<int64_t>(n0) * n0 * (dtype == TOEP_C64 ? 8 : 16);
+  pf.ranges = static_cast<int>(std::min<int64_t>(K, sm_count()));
+  // bytes prefetched at the head of every range (whole 32 KB stages, at most the range's first bin)
+  const int64_t head = std::min<int64_t>(budget / pf.ranges, bin_bytes * (K / pf.ranges)) / 32768 * 32768;
+  if (head <= 0) return L2Prefetch{};
+  pf.base = DT;
+  pf.bin_bytes = bin_bytes;
+  pf.bytes = head;
+  pf.K = K;
+  return pf;
+}
+
 int bin_product(int dtype, const void* DT, const void* U, void* V, int64_t K, int n0, int64_t w, bool transpose,
                 const int* stop, cudaStream_t s) {
   if (K == 0 || w == 0) return TOEP_OK;

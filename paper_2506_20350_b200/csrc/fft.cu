@@ -12,6 +12,7 @@
 // straight to global memory with the crop and the 1/L scale fused.
 #include "kernels.cuh"
 #include "launch.cuh"
+#include "tma.cuh"
 
 namespace toep {
 
@@ -267,6 +268,7 @@ struct Fft2dArgs {
   int sign;
   const double* in_scale;
   const int* stop;
+  L2Prefetch pf;
 };
 
 constexpr int k2dThreads = 512;
@@ -274,7 +276,9 @@ constexpr int k2dThreads = 512;
 template <typename TC, int TILX, int TILY, typename PX, typename PY>
 struct Fft2dSmem {
   static constexpr int kBuf = (PX::L * TILX > PY::L * TILY) ? PX::L * TILX : PY::L * TILY;
-  static size_t bytes(int n2) { return sizeof(C<TC>) * (PX::L + PY::L + 2 * kBuf + static_cast<size_t>(n2) * PX::L); }
+  // G rows padded to an odd stride: the level-1 pass walks G down a column (one row per lane)
+  static constexpr int kGs = PX::L | 1;
+  static size_t bytes(int n2) { return sizeof(C<TC>) * (PX::L + PY::L + 2 * kBuf + static_cast<size_t>(n2) * kGs); }
 };
 
 template <typename TI, typename TC, typename TO, int TILX, int TILY, typename PX, typename PY, bool INV>
@@ -287,8 +291,19 @@ __global__ void __launch_bounds__(k2dThreads, 1) fft2d_kernel(Fft2dArgs f) {
   Z* twy = twx + L1;
   Z* b0 = twy + L2;
   Z* b1 = b0 + S::kBuf;
-  Z* G = b1 + S::kBuf;  // [n2][L1]
+  Z* G = b1 + S::kBuf;  // [n2][kGs]
+  constexpr int Gs = S::kGs;
   pdl_trigger();
+  if (f.pf.bytes > 0 && threadIdx.x < 32) {  // constant operator data: no dependency to wait for
+    const int64_t per = f.pf.K / f.pf.ranges, rem = f.pf.K % f.pf.ranges;
+    for (int c = blockIdx.x; c < f.pf.ranges; c += gridDim.x) {
+      const int64_t b0 = c * per + (c < rem ? c : rem);
+      const char* p0 = static_cast<const char*>(f.pf.base) + b0 * f.pf.bin_bytes;
+      constexpr int64_t kChunk = 32768;
+      for (int64_t o = static_cast<int64_t>(threadIdx.x) * kChunk; o < f.pf.bytes; o += 32 * kChunk)
+        bulk_prefetch_l2(p0 + o, static_cast<uint32_t>(f.pf.bytes - o < kChunk ? f.pf.bytes - o : kChunk));
+    }
+  }
   for (int t = threadIdx.x; t < L1 + L2; t += k2dThreads) {
     const int L = t < L1 ? L1 : L2;
     const int tt = t < L1 ? t : t - L1;
@@ -305,24 +320,24 @@ __global__ void __launch_bounds__(k2dThreads, 1) fft2d_kernel(Fft2dArgs f) {
   if constexpr (!INV) {
     PassArgs ax;  // level 1: slots x (pad fused), columns y -> G[y][kx]
     ax.L = L1; ax.n_lo = n1; ax.n_hi = 0; ax.n_out = L1; ax.in_sa = inner; ax.in_cs = n1 * inner;
-    ax.out_sa = 1; ax.out_cs = L1; ax.sign = f.sign;
+    ax.out_sa = 1; ax.out_cs = Gs; ax.sign = f.sign;
     const TC sc = static_cast<TC>(f.in_scale != nullptr ? *f.in_scale : 1.0);
     PX::template run<TI, TC, TC, k2dThreads, TILX>(ax, static_cast<const C<TI>*>(f.in) + b, G, b0, b1, twx, n2, sc);
     __syncthreads();
     PassArgs ay;  // level 2: slots y (n2 non-zero rows), columns kx -> u_hat[ky][kx][b]
-    ay.L = L2; ay.n_lo = n2; ay.n_hi = 0; ay.n_out = L2; ay.in_sa = L1; ay.in_cs = 1;
+    ay.L = L2; ay.n_lo = n2; ay.n_hi = 0; ay.n_out = L2; ay.in_sa = Gs; ay.in_cs = 1;
     ay.out_sa = static_cast<int64_t>(L1) * inner; ay.out_cs = inner; ay.sign = f.sign;
     PY::template run<TC, TC, TO, k2dThreads, TILY>(ay, G, static_cast<C<TO>*>(f.out) + b, b0, b1, twy, L1,
                                                    static_cast<TC>(1));
   } else {
     PassArgs ay;  // inverse level 2 over all ky, keep y < n2 -> G[y][kx]
     ay.L = L2; ay.n_lo = L2; ay.n_hi = 0; ay.n_out = n2; ay.in_sa = static_cast<int64_t>(L1) * inner; ay.in_cs = inner;
-    ay.out_sa = L1; ay.out_cs = 1; ay.sign = f.sign;
+    ay.out_sa = Gs; ay.out_cs = 1; ay.sign = f.sign;
     PY::template run<TI, TC, TC, k2dThreads, TILY>(ay, static_cast<const C<TI>*>(f.in) + b, G, b0, b1, twy, L1,
                                                    static_cast<TC>(1));
     __syncthreads();
     PassArgs ax;  // inverse level 1, keep x < n1, 1/(l1 l2) -> v[y][x][b]
-    ax.L = L1; ax.n_lo = L1; ax.n_hi = 0; ax.n_out = n1; ax.in_sa = 1; ax.in_cs = L1; ax.out_sa = inner;
+    ax.L = L1; ax.n_lo = L1; ax.n_hi = 0; ax.n_out = n1; ax.in_sa = 1; ax.in_cs = Gs; ax.out_sa = inner;
     ax.out_cs = n1 * inner; ax.sign = f.sign;
     PX::template run<TC, TC, TO, k2dThreads, TILX>(ax, G, static_cast<C<TO>*>(f.out) + b, b0, b1, twx, n2,
                                                    static_cast<TC>(1.0 / (static_cast<double>(L1) * L2)));
@@ -526,13 +541,13 @@ int factorize(int L, int* rad, int* nrad) {
 }
 
 int fft2d(bool inverse, const void* in, void* out, int n2, int n1, int l2, int l1, int64_t inner, int sign, int tin,
-          int tc, int tout, const double* in_scale, const int* stop, cudaStream_t s) {
+          int tc, int tout, const double* in_scale, const int* stop, cudaStream_t s, const L2Prefetch* pf) {
   static const bool off = [] {
     const char* e = std::getenv("TOEP_FFT2D");
     return e != nullptr && e[0] == '0';
   }();
   if (off || inner > 65535 || inner < 1) return -1;
-  Fft2dArgs f{in, out, n2, n1, inner, sign, in_scale, stop};
+  Fft2dArgs f{in, out, n2, n1, inner, sign, in_scale, stop, pf != nullptr ? *pf : L2Prefetch{}};
   const int code = tin * 4 + tc * 2 + tout;
   switch (code) {
     case 0: return fft2d_t<double, double, double>(inverse, f, l2, l1, s);

@@ -43,8 +43,22 @@ struct PassArgs {
 // intermediate in shared memory): forward = pad + level-1 DFT + level-2 DFT -> u_hat (bin-major);
 // inverse = inverse level-2 DFT (kept rows) + inverse level-1 DFT + crop + 1/(l1 l2).
 // Returns -1 when no compiled 2-D plan covers (l2, l1, n2).
+//
+// `pf` (optional): while the transform runs, its CTAs prefetch into L2 the first `bytes` of each
+// of the `ranges` contiguous bin ranges the streaming product kernel assigns to its CTAs, so the
+// product's HBM stream effectively starts during the DFT.  The operator is constant, so the
+// inverse transform of one matvec may prefetch for the next one.
+struct L2Prefetch {
+  const void* base = nullptr;
+  int64_t bin_bytes = 0, K = 0, bytes = 0;
+  int ranges = 0;
+};
 int fft2d(bool inverse, const void* in, void* out, int n2, int n1, int l2, int l1, int64_t inner, int sign,
-          int tin, int tc, int tout, const double* in_scale, const int* stop, cudaStream_t s);
+          int tin, int tc, int tout, const double* in_scale, const int* stop, cudaStream_t s,
+          const L2Prefetch* pf = nullptr);
+
+// L2 prefetch plan for the streaming bin product that follows a forward transform (w == 1)
+L2Prefetch binprod_prefetch_plan(int dtype, const void* DT, int64_t K, int n0, bool inverse_side = false);
 
 // type codes: 0 = complex128, 1 = complex64
 int fft_pass(const PassArgs& a, int tin, int tcomp, int tout, cudaStream_t s);

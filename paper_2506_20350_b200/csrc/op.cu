@@ -119,11 +119,16 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
 
   // one-CTA-per-column 2-D transforms when a compiled 2-D plan covers the grid
   if (w == 1) {
-    const int rf = fft2d(false, u, ws->hat, op->n2, op->n1, op->l2, op->l1, inner, s1, tio, tc, tc, in_scale, stop, s);
+    const L2Prefetch pf = transpose ? L2Prefetch{} : binprod_prefetch_plan(op->dtype, op->DT, op->K, op->n0);
+    const int rf =
+        fft2d(false, u, ws->hat, op->n2, op->n1, op->l2, op->l1, inner, s1, tio, tc, tc, in_scale, stop, s, &pf);
     if (rf == TOEP_OK) {
       TOEP_TRY(bin_product(op->dtype, op->DT, ws->hat, ws->hat2, op->K, op->n0, w, transpose, stop, s));
       // the overall 1/(l1 l2) is applied by the second kernel (linear, so also right for transpose())
-      const int ri = fft2d(true, ws->hat2, v, op->n2, op->n1, op->l2, op->l1, inner, -s1, tc, tc, tio, nullptr, stop, s);
+      const L2Prefetch pfi =
+          transpose ? L2Prefetch{} : binprod_prefetch_plan(op->dtype, op->DT, op->K, op->n0, /*inverse_side=*/true);
+      const int ri =
+          fft2d(true, ws->hat2, v, op->n2, op->n1, op->l2, op->l1, inner, -s1, tc, tc, tio, nullptr, stop, s, &pfi);
       return ri == -1 ? TOEP_ERR_ARG : ri;
     } else if (rf != -1) {
       return rf;

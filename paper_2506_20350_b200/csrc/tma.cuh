@@ -46,6 +46,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 // named barrier over the 8 consumer warps (the producer warp does not participate)
+// fire-and-forget bulk prefetch of [src, src+bytes) into L2 (bytes: multiple of 16)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 constexpr int kTmaConsumerWarps = 8;
