@@ -52,6 +52,12 @@ struct GState {
   double beta0, beta, hnext;
 };
 
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct HostFlags {
   volatile int stop;
   volatile int total;
@@ -297,11 +303,12 @@ __global__ void k_init(GState* st, const double* partial, int nblk, double* hist
 
 // cycle start (gmres.py:130-144): beta = ||z||, convergence test, g[0] = beta, vs[0] = 1/beta
 __global__ void k_cycle_start(GState* st, const double* partial, int nblk, double tol, double2* g, double* vs,
-                              HostFlags* hf) {
+                              HostFlags* hf, long long* ts) {
   pdl_wait();
   pdl_trigger();
   const double s = sum_partials_warp(partial, nblk);
   if (threadIdx.x == 0) {
+    if (ts != nullptr) ts[2 * st->total + 1] = global_ns();  // "previous step end" of the cycle's first step
     const double beta = sqrt(s);
     st->beta = beta;
     st->m = 0;
@@ -436,6 +443,7 @@ struct OrthArgs {
   int max_total, cycle_len;
   HostFlags* hf;
   unsigned* bar;    // [2] grid barrier: arrival count, generation
+  long long* ts;    // optional phase stamps: [2k+2] = step k orth start, [2k+3] = step k end
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
@@ -528,6 +536,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
   pdl_wait();
   pdl_trigger();
   if (*stop) return;  // uniform across the grid (written by the previous step, read-only here)
+  if (a.ts != nullptr && blockIdx.x == 0 && threadIdx.x == 0) a.ts[2 * a.st->total + 2] = global_ns();
   extern __shared__ double2 osm[];  // coef [ldr] | dot partials [32][ldr]; Givens scratch reuses it
   __shared__ double red[kCoopThreads / 32];
   double2* coef = osm;
@@ -559,7 +568,9 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
     double s = 0.0;
     for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32) s += __ldcg(a.npart + b);
     s = warp_sum(s);
+    const int k = a.st->total;  // this step's global index (Givens advances it)
     givens_warp(a.st, s, a.rcols, a.ldr, a.cs, a.sn, a.g, a.hist, a.vsw, a.tol, a.max_total, a.cycle_len, a.hf, osm);
+    if (a.ts != nullptr && threadIdx.x == 0) a.ts[2 * k + 3] = global_ns();
   }
 }
 
@@ -771,6 +782,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   double *cs = nullptr, *hist = nullptr, *vs = nullptr;
   GState* st = nullptr;
   unsigned* bar = nullptr;  // grid barrier of k_orth_coop
+  long long* ts = nullptr;  // device phase stamps (replace per-step events on the cooperative path)
   HostRes& res = host_res();
   res.used = 0;
   HostFlags* hf = res.hf;
@@ -779,7 +791,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   auto cleanup = [&]() {
     for (void* q : {(void*)V, (void*)tmp, (void*)tmp2, (void*)pb, (void*)h1, (void*)rcols, (void*)sn, (void*)g,
                     (void*)y, (void*)part1, (void*)part2, (void*)cs, (void*)hist, (void*)vs, (void*)st,
-                    (void*)e.norm_partial, (void*)e.nred, (void*)e.hred, (void*)bar})
+                    (void*)e.norm_partial, (void*)e.nred, (void*)e.hred, (void*)bar, (void*)ts})
       if (q) cudaFreeAsync(q, s);
     cudaStreamSynchronize(s);
     res.used = 0;
@@ -825,6 +837,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   }
   // single-kernel cooperative orthogonalisation when all CTAs fit co-resident
   G_ALLOC(bar, 2);
+  G_ALLOC(ts, 2 * max_total + 4);
   TOEP_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s));
   const size_t coop_smem = std::max(sizeof(double2) * ldr * (1 + kCoopThreads / 32),
                                     (2 * sizeof(double2) + sizeof(double)) * ldr);
@@ -849,6 +862,10 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   tr.mark("allocations");
 
   const bool timed = cfg->timings != 0;
+  // per-step matvec / orthogonalisation split from device timestamps: events between the
+  // kernels of a step would break their programmatic-dependent-launch overlap
+  bool stamped = timed && use_coop && !e.precond_per_step();
+  long long* ts_dev = stamped ? ts : nullptr;
   struct Phase { cudaEvent_t a, b; int kind; };
   std::vector<Phase> phases;
   auto mark = [&](int kind, cudaEvent_t a) {
@@ -940,7 +957,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     first = false;
     G_TRY(e.norm2_partials(v0));
     G_TRY(e.finish_norm(&nptr, &ncnt));
-    G_TRY(launch_k(k_cycle_start, dim3(1), dim3(32), 0, s, st, nptr, ncnt, cfg->tol, g, vs, hf_dev));
+    G_TRY(launch_k(k_cycle_start, dim3(1), dim3(32), 0, s, st, nptr, ncnt, cfg->tol, g, vs, hf_dev, ts_dev));
 
     // ---- Arnoldi steps (gmres.py:146-190)
     int j = 0;
@@ -949,24 +966,29 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       const auto t_launch0 = clk::now();
       const double2* vj = V + static_cast<int64_t>(j) * N;
       double2* w = V + static_cast<int64_t>(j + 1) * N;  // unnormalised v_{j+1} is built in place
-      cudaEvent_t t0 = timed ? start_mark() : nullptr;
+      const bool ev_timed = timed && !(stamped && use_coop);
+      cudaEvent_t t0 = ev_timed ? start_mark() : nullptr;
       if (e.precond_per_step()) {
         G_TRY(e.apply_a(vj, vs + j, tmp, stop_dev));
-        if (timed) t0 = mark(0, t0);
+        if (ev_timed) t0 = mark(0, t0);
         G_TRY(e.apply_p(tmp, w, stop_dev));
-        if (timed) t0 = mark(1, t0);
+        if (ev_timed) t0 = mark(1, t0);
       } else {
         G_TRY(e.apply_a(vj, vs + j, w, stop_dev));
-        if (timed) t0 = mark(0, t0);
+        if (ev_timed) t0 = mark(0, t0);
       }
       const int m = j + 1;
       if (use_coop) {
         OrthArgs oa{V, N, m, vs, w, part1, e.norm_partial, h1, st, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
-                    static_cast<int>(max_total), cycle_len, hf_dev, bar};
+                    static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev};
         rc = launch_coop(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa, (const int*)stop_dev);
         if (rc != TOEP_OK) {  // cooperative launch unavailable: permanent fallback to the 4-kernel chain
           use_coop = false;
           rc = TOEP_OK;
+          if (stamped) {  // this step's matvec went unmeasured; events from here on
+            stamped = false;
+            ts_dev = nullptr;
+          }
         }
       }
       if (use_coop) {
@@ -987,7 +1009,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       G_TRY(launch_k(k_givens, dim3(1), dim3(32), givens_smem, s, st, nptr, ncnt, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
                      static_cast<int>(max_total), cycle_len, hf_dev));
       }
-      if (timed) mark(2, t0);
+      if (ev_timed) mark(2, t0);
       cudaEvent_t ev = res.event();
       cudaEventRecord(ev, s);
       step_ev.push_back(ev);
@@ -1049,6 +1071,16 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     set_error("gmres exit failed: %s", cudaGetErrorString(cudaGetLastError()));
     cleanup();
     return TOEP_ERR_CUDA;
+  }
+  if (timed && stamped) {
+    std::vector<long long> hts(2 * static_cast<size_t>(hst.total) + 2);
+    if (cudaMemcpy(hts.data(), ts, hts.size() * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess) {
+      for (int k = 0; k < hst.total; ++k) {
+        rep->t_matvec += 1e-9 * static_cast<double>(hts[2 * k + 2] - hts[2 * k + 1]);
+        rep->t_orth += 1e-9 * static_cast<double>(hts[2 * k + 3] - hts[2 * k + 2]);
+      }
+    }
+    cudaGetLastError();
   }
   if (timed) {
     for (auto& ph : phases) {
