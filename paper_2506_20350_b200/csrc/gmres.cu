@@ -446,27 +446,29 @@ struct OrthArgs {
   long long* ts;    // optional phase stamps: [2k+2] = step k orth start, [2k+3] = step k end
 };
 
+// Grid barrier on a monotonic arrival counter (zeroed once per solve): every CTA adds 1 and
+// waits until the counter reaches the next multiple of gridDim.x (one atomic per CTA, no reset).
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    const unsigned gen = *vgen;
     __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == gen) {
-      }
+    const unsigned old = atomicAdd(bar, 1u);
+    const unsigned target = (old / gridDim.x + 1) * gridDim.x;
+    while (static_cast<int>(ld_acquire_gpu(bar) - target) < 0) {
     }
-    __threadfence();
   }
   __syncthreads();
 }
 
 // coef[l] = vs_l * (vs_l * sum_b part[l][b]); CTA 0 stores h (mode 1) or hprev + h (mode 2)
-__device__ __forceinline__ void orth_coefs(const OrthArgs& a, double2* coef, int mode, double2* hout) {
+__device__ __forceinline__ void orth_coefs(const OrthArgs& a, double2* coef, int mode, double2* hout,
+                                           double2* hsm = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nblk = gridDim.x;
   for (int l = warp; l < a.m; l += kCoopThreads / 32) {
@@ -476,7 +478,11 @@ __device__ __forceinline__ void orth_coefs(const OrthArgs& a, double2* coef, int
     if (lane == 0) {
       const double2 h = cscale(s, a.vs[l]);
       coef[l] = cscale(h, a.vs[l]);
-      if (blockIdx.x == 0) hout[l] = (mode == 1) ? h : cadd(a.h1[l], h);
+      if (blockIdx.x == 0) {
+        const double2 hv = (mode == 1) ? h : cadd(a.h1[l], h);
+        hout[l] = hv;
+        if (hsm != nullptr) hsm[l] = hv;
+      }
     }
   }
   __syncthreads();
@@ -502,34 +508,88 @@ __device__ __forceinline__ double orth_update(const OrthArgs& a, const double2* 
   return nrm;
 }
 
-// all 1024 threads sweep the chunk (element-parallel, every basis vector), per-warp partials
-// meet in shared memory: red [32][m]
-__device__ __forceinline__ void orth_dots(const OrthArgs& a, int64_t c0, int64_t c1, double2* red) {
-  constexpr int G = 8;
+// one warp per basis vector: warp l sweeps the CTA's chunk of V_l and w with 8 independent
+// loads in flight per lane and ends with a single warp reduction; lane 0 stores the CTA partial
+__device__ __forceinline__ void orth_dots(const OrthArgs& a, int64_t c0, int64_t c1) {
+  constexpr int NW = kCoopThreads / 32, U = 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nblk = gridDim.x;
-  for (int l0 = 0; l0 < a.m; l0 += G) {
-    double2 acc[G];
+  for (int l = warp; l < a.m; l += NW) {
+    const double2* v = a.V + static_cast<int64_t>(l) * a.N;
+    double2 acc[U];
 #pragma unroll
-    for (int gg = 0; gg < G; ++gg) acc[gg] = make_double2(0, 0);
-    for (int64_t i = c0 + threadIdx.x; i < c1; i += kCoopThreads) {
-      const double2 wi = a.w[i];
+    for (int u = 0; u < U; ++u) acc[u] = make_double2(0, 0);
+    int64_t i = c0 + lane;
+    for (; i + 32 * (U - 1) < c1; i += 32 * U) {
+      double2 vv[U], ww[U];
 #pragma unroll
-      for (int gg = 0; gg < G; ++gg)
-        if (l0 + gg < a.m) cfmac(acc[gg], a.V[(l0 + gg) * a.N + i], wi);
+      for (int u = 0; u < U; ++u) {
+        vv[u] = v[i + 32 * u];
+        ww[u] = a.w[i + 32 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) cfmac(acc[u], vv[u], ww[u]);
     }
+    for (; i < c1; i += 32) cfmac(acc[0], v[i], a.w[i]);
 #pragma unroll
-    for (int gg = 0; gg < G; ++gg) {
-      const double2 s = warp_sum(acc[gg]);
-      if (lane == 0 && l0 + gg < a.m) red[warp * a.ldr + l0 + gg] = s;
-    }
+    for (int u = 1; u < U; ++u) acc[0] = cadd(acc[0], acc[u]);
+    const double2 s = warp_sum(acc[0]);
+    if (lane == 0) a.part[static_cast<int64_t>(l) * nblk + blockIdx.x] = s;
   }
-  __syncthreads();
-  for (int l = threadIdx.x; l < a.m; l += kCoopThreads) {
-    double2 s = red[l];
-    for (int ww = 1; ww < kCoopThreads / 32; ++ww) s = cadd(s, red[ww * a.ldr + l]);
-    a.part[static_cast<int64_t>(l) * nblk + blockIdx.x] = s;
+}
+
+// the new rotation from the rotated column's diagonal entry and h_{j+1,j} = ||w|| (gmres.py:
+// 87-95, 171-190); same arithmetic as givens_warp's tail, with the scalars prefetched
+__device__ void givens_finish(const OrthArgs& a, int j, double2 hj, double hn2, double2 gj, double beta0, int nhist) {
+  GState* st = a.st;
+  double2* hcol_g = a.rcols + static_cast<int64_t>(j) * a.ldr;
+  const double hnext = sqrt(hn2);
+  const double absa = hypot(hj.x, hj.y);
+  const double t = hypot(absa, hnext);
+  double c;
+  double2 s, r;
+  if (t == 0.0) {
+    c = 1.0; s = make_double2(0, 0); r = make_double2(0, 0);
+  } else if (hj.x == 0.0 && hj.y == 0.0) {
+    c = 0.0; s = make_double2(1, 0); r = make_double2(hnext, 0);
+  } else {
+    const double2 alpha = make_double2(hj.x / absa, hj.y / absa);
+    c = absa / t;
+    s = cscale(alpha, hnext / t);
+    r = cscale(alpha, t);
   }
+  hcol_g[j] = r;
+  a.cs[j] = c;
+  a.sn[j] = s;
+  const double2 gn = cscale(cmulc(s, gj), -1.0);
+  a.g[j + 1] = gn;
+  a.g[j] = cscale(gj, c);
+  const int m = j + 1, total = st->total + 1;
+  st->m = m;
+  st->total = total;
+  const double est = hypot(gn.x, gn.y) / beta0;
+  a.hist[nhist] = est;
+  st->nhist = nhist + 1;
+  st->hnext = hnext;
+  int stop = 0, conv = st->converged, brk = st->breakdown;
+  if (est <= a.tol) {
+    conv = 1;
+    stop = 1;
+  } else if (hnext == 0.0) {
+    conv = 1;
+    brk = 1;
+    stop = 1;
+  } else {
+    a.vsw[j + 1] = 1.0 / hnext;  // v_{j+1} = w / h_{j+1,j}, applied lazily
+    if (m >= a.cycle_len || total >= a.max_total) stop = 2;
+  }
+  st->converged = conv;
+  st->breakdown = brk;
+  st->stop = stop;
+  a.hf->stop = stop;
+  a.hf->total = total;
+  a.hf->converged = conv;
+  a.hf->breakdown = brk;
 }
 
 __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const int* stop) {
@@ -537,23 +597,72 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
   pdl_trigger();
   if (*stop) return;  // uniform across the grid (written by the previous step, read-only here)
   if (a.ts != nullptr && blockIdx.x == 0 && threadIdx.x == 0) a.ts[2 * a.st->total + 2] = global_ns();
+#ifdef TOEP_ORTH_PROBE
+  long long pt[8];
+  int np = 0;
+#define OPROBE() \
+  if (blockIdx.x == 0 && threadIdx.x == 0) pt[np++] = global_ns()
+#else
+#define OPROBE()
+#endif
+  OPROBE();
   extern __shared__ double2 osm[];  // coef [ldr] | dot partials [32][ldr]; Givens scratch reuses it
   __shared__ double red[kCoopThreads / 32];
   double2* coef = osm;
-  double2* dred = osm + a.ldr;
-  int64_t c0, c1;
-  chunk_of(a.N, &c0, &c1);
+  double2* hsm = osm + a.ldr;        // CTA 0: the new Hessenberg column
+  double2* snl = hsm + a.ldr;        // CTA 0: previous rotations
+  double* csl = reinterpret_cast<double*>(snl + a.ldr);
+  // CTA 0 owns no elements (unless it is alone): it prepares the Givens step while the others
+  // sweep the basis
+  int64_t c0 = 0, c1 = gridDim.x == 1 ? a.N : 0;
+  if (blockIdx.x > 0) {
+    const int64_t nb = gridDim.x - 1, b = blockIdx.x - 1;
+    c0 = ((a.N * b / nb) / 32) * 32;
+    c1 = (b + 1 == nb) ? a.N : ((a.N * (b + 1) / nb) / 32) * 32;
+  }
+  const int jcol = a.m - 1;  // this step's column index in the cycle (st->m)
+  double2 g_j = make_double2(0, 0);
+  double beta0 = 1.0;
+  int k_step = 0, nhist = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // scalars for the final rotation, fetched early
+    g_j = a.g[jcol];
+    beta0 = a.st->beta0;
+    k_step = a.st->total;
+    nhist = a.st->nhist;
+  }
   // pass 1: h1 = V^H w
-  orth_dots(a, c0, c1, dred);
+  orth_dots(a, c0, c1);
+  OPROBE();
   grid_barrier(a.bar);
+  OPROBE();
   orth_coefs(a, coef, 1, a.h1);
+  OPROBE();
   orth_update(a, coef, c0, c1);
   __syncthreads();
+  OPROBE();
   // pass 2 (re-orthogonalisation): h2 = V^H w', H[:, j] = h1 + h2
-  orth_dots(a, c0, c1, dred);
+  orth_dots(a, c0, c1);
   grid_barrier(a.bar);
-  double2* hcol = a.rcols + static_cast<int64_t>(a.st->m) * a.ldr;
-  orth_coefs(a, coef, 2, hcol);
+  OPROBE();
+  double2* hcol = a.rcols + static_cast<int64_t>(jcol) * a.ldr;
+  orth_coefs(a, coef, 2, hcol, blockIdx.x == 0 ? hsm : nullptr);
+  if (blockIdx.x == 0) {  // apply the cycle's previous rotations to the new column (gmres.py:165-170)
+    for (int i = threadIdx.x; i < jcol; i += kCoopThreads) {
+      snl[i] = a.sn[i];
+      csl[i] = a.cs[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < jcol; ++i) {
+        const double2 a0 = hsm[i], a1 = hsm[i + 1];
+        const double c = csl[i];
+        const double2 sv = snl[i];
+        hsm[i] = cadd(cscale(a0, c), cmul(sv, a1));
+        hsm[i + 1] = cadd(cscale(cmulc(sv, a0), -1.0), cscale(a1, c));
+        hcol[i] = hsm[i];
+      }
+    }
+  }
   double nrm = orth_update(a, coef, c0, c1);
   nrm = warp_sum(nrm);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
@@ -565,12 +674,21 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
   }
   grid_barrier(a.bar);
   if (blockIdx.x == 0 && threadIdx.x < 32) {
-    double s = 0.0;
-    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32) s += __ldcg(a.npart + b);
-    s = warp_sum(s);
-    const int k = a.st->total;  // this step's global index (Givens advances it)
-    givens_warp(a.st, s, a.rcols, a.ldr, a.cs, a.sn, a.g, a.hist, a.vsw, a.tol, a.max_total, a.cycle_len, a.hf, osm);
-    if (a.ts != nullptr && threadIdx.x == 0) a.ts[2 * k + 3] = global_ns();
+    double hn2 = 0.0;
+    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32) hn2 += __ldcg(a.npart + b);
+    hn2 = warp_sum(hn2);
+    OPROBE();
+    if (threadIdx.x == 0) {
+      givens_finish(a, jcol, hsm[jcol], hn2, g_j, beta0, nhist);
+      if (a.ts != nullptr) a.ts[2 * k_step + 3] = global_ns();
+    }
+#ifdef TOEP_ORTH_PROBE
+    OPROBE();
+    if (threadIdx.x == 0 && (k_step == 8 || k_step == 16 || k_step == 24))
+      printf("orth k=%d m=%d: dots1 %lld bar %lld coef %lld upd %lld dots2+bar %lld upd2+norm+bar %lld givens %lld ns\n",
+             k_step, a.m, pt[1] - pt[0], pt[2] - pt[1], pt[3] - pt[2], pt[4] - pt[3], pt[5] - pt[4], pt[6] - pt[5],
+             pt[7] - pt[6]);
+#endif
   }
 }
 
