@@ -487,22 +487,29 @@ int bin_product_t(const void* DT, const void* U, void* V, int64_t K, int n0, int
 
 }  // namespace
 
-L2Prefetch binprod_prefetch_plan(int dtype, const void* DT, int64_t K, int n0, bool inverse_side) {
+L2Prefetch binprod_prefetch_plan(int dtype, const void* DT, int64_t K, int n0, int side) {
   L2Prefetch pf;
   if (n0 != 128 || binprod_variant() != 3) return pf;  // only the whole-row TMA stream has this bin order
-  static const int64_t budget_fwd = [] {
-    const char* e = std::getenv("TOEP_PREFETCH_MB");
-    return static_cast<int64_t>(e != nullptr ? std::atoll(e) : 48) << 20;
-  }();
-  static const int64_t budget_inv = [] {
-    const char* e = std::getenv("TOEP_PREFETCH_INV_MB");
-    return static_cast<int64_t>(e != nullptr ? std::atoll(e) : 0) << 20;
-  }();
-  const int64_t budget = inverse_side ? budget_inv : budget_fwd;
+  auto env_mb = [](const char* name, int64_t dflt) {
+    const char* e = std::getenv(name);
+    return static_cast<int64_t>(e != nullptr ? std::atoll(e) : dflt) << 20;
+  };
+  static const int64_t budget[3] = {env_mb("TOEP_PREFETCH_MB", 48), env_mb("TOEP_PREFETCH_INV_MB", 0),
+                                    env_mb("TOEP_PREFETCH_ORTH_MB", 0)};
   const int64_t bin_bytes = static_cast<int64_t>(n0) * n0 * (dtype == TOEP_C64 ? 8 : 16);
   pf.ranges = static_cast<int>(std::min<int64_t>(K, sm_count()));
-  // bytes prefetched at the head of every range (whole 32 KB stages, at most the range's first bin)
-  const int64_t head = std::min<int64_t>(budget / pf.ranges, bin_bytes * (K / pf.ranges)) / 32768 * 32768;
+  const int64_t range_min = bin_bytes * (K / pf.ranges);
+  auto share = [&](int64_t b) { return std::min<int64_t>(b / pf.ranges, range_min) / 32768 * 32768; };
+  const int64_t fwd = share(budget[0]);
+  int64_t head = 0;
+  if (side == 0) {
+    head = fwd;
+  } else if (side == 1) {
+    head = share(budget[1]);
+  } else {
+    pf.skip = fwd;
+    head = std::min<int64_t>(share(budget[2]), range_min - fwd);
+  }
   if (head <= 0) return L2Prefetch{};
   pf.base = DT;
   pf.bin_bytes = bin_bytes;

@@ -60,6 +60,46 @@ __device__ __forceinline__ void butterfly(Z* v, const Z* wr, int sign) {
     v[2] = csub(t0, t2);
     v[1] = cadd(t1, t3);
     v[3] = csub(t1, t3);
+  } else if constexpr (R == 3) {
+    // y0 = v0 + s, y1,2 = (v0 - s/2) +- sign*i*(sqrt(3)/2)(v1 - v2), s = v1 + v2
+    using T = decltype(v[0].x);
+    constexpr T kS3 = static_cast<T>(0.86602540378443864676);
+    const Z sm = cadd(v[1], v[2]), d = csub(v[1], v[2]);
+    Z m;
+    m.x = v[0].x - static_cast<T>(0.5) * sm.x;
+    m.y = v[0].y - static_cast<T>(0.5) * sm.y;
+    Z rot;
+    rot.x = -sign * kS3 * d.y;
+    rot.y = sign * kS3 * d.x;
+    v[0] = cadd(v[0], sm);
+    v[1] = cadd(m, rot);
+    v[2] = csub(m, rot);
+  } else if constexpr (R == 5) {
+    // a_k = v_k + v_{5-k}, b_k = v_k - v_{5-k}; y_k / y_{5-k} = p_k +- sign*i*q_k
+    using T = decltype(v[0].x);
+    constexpr T c1 = static_cast<T>(0.30901699437494742410), c2 = static_cast<T>(-0.80901699437494742410);
+    constexpr T s1 = static_cast<T>(0.95105651629515357212), s2 = static_cast<T>(0.58778525229247312917);
+    const Z a1 = cadd(v[1], v[4]), b1 = csub(v[1], v[4]);
+    const Z a2 = cadd(v[2], v[3]), b2 = csub(v[2], v[3]);
+    Z p1, p2, q1, q2;
+    p1.x = v[0].x + c1 * a1.x + c2 * a2.x;
+    p1.y = v[0].y + c1 * a1.y + c2 * a2.y;
+    p2.x = v[0].x + c2 * a1.x + c1 * a2.x;
+    p2.y = v[0].y + c2 * a1.y + c1 * a2.y;
+    q1.x = s1 * b1.x + s2 * b2.x;
+    q1.y = s1 * b1.y + s2 * b2.y;
+    q2.x = s2 * b1.x - s1 * b2.x;
+    q2.y = s2 * b1.y - s1 * b2.y;
+    Z r1, r2;  // sign*i*q
+    r1.x = -sign * q1.y;
+    r1.y = sign * q1.x;
+    r2.x = -sign * q2.y;
+    r2.y = sign * q2.x;
+    v[0] = cadd(v[0], cadd(a1, a2));
+    v[1] = cadd(p1, r1);
+    v[4] = csub(p1, r1);
+    v[2] = cadd(p2, r2);
+    v[3] = csub(p2, r2);
   } else {
     Z o[R];
 #pragma unroll
@@ -83,8 +123,10 @@ __device__ __forceinline__ void run_stage(const C<TC>* __restrict__ src, C<TC>* 
   const int nb = L / R;
   const int tstep = L / (Ns * R);
   Z wr[R];
+  if constexpr (R == 7) {
 #pragma unroll
-  for (int m = 0; m < R; ++m) wr[m] = tw[m * nb];
+    for (int m = 0; m < R; ++m) wr[m] = tw[m * nb];
+  }
   for (int e = threadIdx.x; e < nb * TIL; e += kThreads) {
     const int j = e / TIL;
     const int col = e - j * TIL;
@@ -144,8 +186,8 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
   constexpr bool kLast = sizeof...(Rest) == 0;
   constexpr int nb = L / R;
   constexpr int tstep = L / (Ns * R);
-  Z wr[R];
-  if constexpr (R != 2 && R != 4) {
+  Z wr[R];  // roots of unity, only for the generic (radix-7) butterfly
+  if constexpr (R == 7) {
 #pragma unroll
     for (int m = 0; m < R; ++m) wr[m] = tw[m * nb];
   }
@@ -294,16 +336,8 @@ __global__ void __launch_bounds__(k2dThreads, 1) fft2d_kernel(Fft2dArgs f) {
   Z* G = b1 + S::kBuf;  // [n2][kGs]
   constexpr int Gs = S::kGs;
   pdl_trigger();
-  if (f.pf.bytes > 0 && threadIdx.x < 32) {  // constant operator data: no dependency to wait for
-    const int64_t per = f.pf.K / f.pf.ranges, rem = f.pf.K % f.pf.ranges;
-    for (int c = blockIdx.x; c < f.pf.ranges; c += gridDim.x) {
-      const int64_t b0 = c * per + (c < rem ? c : rem);
-      const char* p0 = static_cast<const char*>(f.pf.base) + b0 * f.pf.bin_bytes;
-      constexpr int64_t kChunk = 32768;
-      for (int64_t o = static_cast<int64_t>(threadIdx.x) * kChunk; o < f.pf.bytes; o += 32 * kChunk)
-        bulk_prefetch_l2(p0 + o, static_cast<uint32_t>(f.pf.bytes - o < kChunk ? f.pf.bytes - o : kChunk));
-    }
-  }
+  if (threadIdx.x < 32)  // constant operator data: no dependency to wait for
+    l2_prefetch_heads(f.pf, blockIdx.x, gridDim.x, threadIdx.x);
   for (int t = threadIdx.x; t < L1 + L2; t += k2dThreads) {
     const int L = t < L1 ? L1 : L2;
     const int tt = t < L1 ? t : t - L1;

@@ -212,7 +212,15 @@ k_axpy_basis(const double2* __restrict__ V, int64_t ld, int m_max, const int* m_
   for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < N;
        i += static_cast<int64_t>(gridDim.x) * kThreads) {
     double2 acc = x[i];
-    for (int l = 0; l < m; ++l) cfma(acc, V[l * ld + i], coef[l]);
+    int l = 0;
+    for (; l + 7 < m; l += 8) {  // 8 independent basis loads in flight
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = V[(l + u) * ld + i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cfma(acc, v[u], coef[l + u]);
+    }
+    for (; l < m; ++l) cfma(acc, V[l * ld + i], coef[l]);
     x[i] = acc;
   }
 }
@@ -444,6 +452,7 @@ struct OrthArgs {
   HostFlags* hf;
   unsigned* bar;    // [2] grid barrier: arrival count, generation
   long long* ts;    // optional phase stamps: [2k+2] = step k orth start, [2k+3] = step k end
+  L2Prefetch pf;    // operator stream prefetched into L2 for the next matvec (HBM is idle here)
 };
 
 // Grid barrier on a monotonic arrival counter (zeroed once per solve): every CTA adds 1 and
@@ -597,6 +606,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
   pdl_trigger();
   if (*stop) return;  // uniform across the grid (written by the previous step, read-only here)
   if (a.ts != nullptr && blockIdx.x == 0 && threadIdx.x == 0) a.ts[2 * a.st->total + 2] = global_ns();
+  if (threadIdx.x >= kCoopThreads - 32) l2_prefetch_heads(a.pf, blockIdx.x, gridDim.x, threadIdx.x & 31);
 #ifdef TOEP_ORTH_PROBE
   long long pt[8];
   int np = 0;
@@ -692,8 +702,58 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
   }
 }
 
-// y = R^-1 g (gmres.py:193-204), R upper triangular from the rotated columns
-__global__ void k_backsub(const GState* st, const double2* rcols, int ldr, const double2* g, double2* y) {
+// y = R^-1 g (gmres.py:193-204), R upper triangular from the rotated columns (rcols[j][0..j]).
+// One warp: R is staged in shared memory by all lanes at once (one load latency), then a
+// column-oriented substitution: lane l owns rows l, l+32, ...; each solved y_i is broadcast with a
+// shuffle and subtracted from the remaining rows.  A zero pivot gives y_i = 0, as before.
+constexpr int kBsRows = 8;  // rows per lane: cycles up to 256 steps
+__global__ void k_backsub(const GState* st, const double2* rcols, int ldr, const double2* g, double2* y, int staged) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ double2 rsm[];  // staged: [m][m] column-major upper triangle
+  const int lane = threadIdx.x;
+  const int m = st->m;
+  const double2* rs = rcols;
+  int rld = ldr;
+  if (staged) {
+    for (int i = 0; i < m; ++i)
+      for (int r = lane; r <= i; r += 32) rsm[i * m + r] = rcols[static_cast<int64_t>(i) * ldr + r];
+    rs = rsm;
+    rld = m;
+  }
+  double2 acc[kBsRows];
+#pragma unroll
+  for (int q = 0; q < kBsRows; ++q) {
+    const int r = lane + 32 * q;
+    acc[q] = r < m ? g[r] : make_double2(0, 0);
+  }
+  __syncwarp();
+  for (int i = m - 1; i >= 0; --i) {
+    const int qi = i >> 5;
+    double2 yi = make_double2(0, 0);
+#pragma unroll
+    for (int q = 0; q < kBsRows; ++q)
+      if (q == qi && lane == (i & 31)) {
+        const double2 d = rs[static_cast<int64_t>(i) * rld + i];
+        if (!(d.x == 0.0 && d.y == 0.0)) {
+          const double den = d.x * d.x + d.y * d.y;
+          yi = make_double2((acc[q].x * d.x + acc[q].y * d.y) / den, (acc[q].y * d.x - acc[q].x * d.y) / den);
+        }
+        y[i] = yi;
+      }
+    yi.x = __shfl_sync(0xffffffffu, yi.x, i & 31);
+    yi.y = __shfl_sync(0xffffffffu, yi.y, i & 31);
+    const double2 ny = make_double2(-yi.x, -yi.y);
+#pragma unroll
+    for (int q = 0; q < kBsRows; ++q) {
+      const int r = lane + 32 * q;
+      if (r < i) cfma(acc[q], rs[static_cast<int64_t>(i) * rld + r], ny);
+    }
+  }
+}
+
+// long cycles (> 256 steps): the same substitution on one thread, row-oriented
+__global__ void k_backsub_serial(const GState* st, const double2* rcols, int ldr, const double2* g, double2* y) {
   pdl_wait();
   pdl_trigger();
   if (threadIdx.x != 0) return;
@@ -980,6 +1040,9 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   tr.mark("allocations");
 
   const bool timed = cfg->timings != 0;
+  const L2Prefetch orth_pf = (p->op != nullptr && p->w == 1) ? binprod_prefetch_plan(p->op->dtype, p->op->DT,
+                                                                                    p->op->K, p->op->n0, 2)
+                                                            : L2Prefetch{};
   // per-step matvec / orthogonalisation split from device timestamps: events between the
   // kernels of a step would break their programmatic-dependent-launch overlap
   bool stamped = timed && use_coop && !e.precond_per_step();
@@ -998,6 +1061,11 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     return a;
   };
   const size_t coef_smem = sizeof(double2) * ldr;
+  const bool backsub_warp = cycle_len <= 32 * kBsRows;  // else the serial kernel
+  const int backsub_staged = sizeof(double2) * static_cast<size_t>(cycle_len) * cycle_len <= 200 * 1024 ? 1 : 0;
+  const size_t backsub_smem = backsub_staged ? sizeof(double2) * static_cast<size_t>(cycle_len) * cycle_len : 0;
+  if (backsub_smem > 48 * 1024)
+    cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)backsub_smem);
   const size_t givens_smem = (2 * sizeof(double2) + sizeof(double)) * ldr;
   if (givens_smem > 48 * 1024)
     cudaFuncSetAttribute(k_givens, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)givens_smem);
@@ -1098,7 +1166,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       const int m = j + 1;
       if (use_coop) {
         OrthArgs oa{V, N, m, vs, w, part1, e.norm_partial, h1, st, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
-                    static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev};
+                    static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev, orth_pf};
         rc = launch_coop(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa, (const int*)stop_dev);
         if (rc != TOEP_OK) {  // cooperative launch unavailable: permanent fallback to the 4-kernel chain
           use_coop = false;
@@ -1147,8 +1215,12 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     }
     tr.mark("arnoldi steps launched");
     // ---- assemble x += V y (gmres.py:192-204)
-    G_TRY(launch_k(k_backsub, dim3(1), dim3(32), 0, s, (const GState*)st, (const double2*)rcols, ldr,
-                   (const double2*)g, y));
+    if (backsub_warp)
+      G_TRY(launch_k(k_backsub, dim3(1), dim3(32), backsub_smem, s, (const GState*)st, (const double2*)rcols, ldr,
+                     (const double2*)g, y, backsub_staged));
+    else
+      G_TRY(launch_k(k_backsub_serial, dim3(1), dim3(32), 0, s, (const GState*)st, (const double2*)rcols, ldr,
+                     (const double2*)g, y));
     G_TRY(launch_k(k_axpy_basis, dim3(grid1), dim3(kThreads), coef_smem, s, (const double2*)V, N, cycle_len,
                    (const int*)m_dev, (const double*)vs, (const double2*)y, x, N));
     if (cudaMemcpyAsync(&hst, st, sizeof(GState), cudaMemcpyDeviceToHost, s) != cudaSuccess ||

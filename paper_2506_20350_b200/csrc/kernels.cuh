@@ -51,14 +51,32 @@ struct PassArgs {
 struct L2Prefetch {
   const void* base = nullptr;
   int64_t bin_bytes = 0, K = 0, bytes = 0;
+  int64_t skip = 0;  // start this many bytes into every range
   int ranges = 0;
 };
+
+// one warp of each of `ncta` CTAs issues the bulk L2 prefetches of its share of the ranges
+__device__ __forceinline__ void l2_prefetch_heads(const L2Prefetch& pf, int cta, int ncta, int lane) {
+  if (pf.bytes <= 0) return;
+  const int64_t per = pf.K / pf.ranges, rem = pf.K % pf.ranges;
+  constexpr int64_t kChunk = 32768;
+  for (int c = cta; c < pf.ranges; c += ncta) {
+    const int64_t b0 = c * per + (c < rem ? c : rem);
+    const char* p0 = static_cast<const char*>(pf.base) + b0 * pf.bin_bytes + pf.skip;
+    for (int64_t o = static_cast<int64_t>(lane) * kChunk; o < pf.bytes; o += 32 * kChunk) {
+      const uint32_t n = static_cast<uint32_t>(pf.bytes - o < kChunk ? pf.bytes - o : kChunk);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0 + o), "r"(n) : "memory");
+    }
+  }
+}
 int fft2d(bool inverse, const void* in, void* out, int n2, int n1, int l2, int l1, int64_t inner, int sign,
           int tin, int tc, int tout, const double* in_scale, const int* stop, cudaStream_t s,
           const L2Prefetch* pf = nullptr);
 
 // L2 prefetch plan for the streaming bin product that follows a forward transform (w == 1)
-L2Prefetch binprod_prefetch_plan(int dtype, const void* DT, int64_t K, int n0, bool inverse_side = false);
+// side: 0 = forward DFT (range heads), 1 = inverse DFT, 2 = GMRES orthogonalisation (the bytes
+// after the forward DFT's share)
+L2Prefetch binprod_prefetch_plan(int dtype, const void* DT, int64_t K, int n0, int side = 0);
 
 // type codes: 0 = complex128, 1 = complex64
 int fft_pass(const PassArgs& a, int tin, int tcomp, int tout, cudaStream_t s);

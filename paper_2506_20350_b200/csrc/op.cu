@@ -126,7 +126,7 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
       TOEP_TRY(bin_product(op->dtype, op->DT, ws->hat, ws->hat2, op->K, op->n0, w, transpose, stop, s));
       // the overall 1/(l1 l2) is applied by the second kernel (linear, so also right for transpose())
       const L2Prefetch pfi =
-          transpose ? L2Prefetch{} : binprod_prefetch_plan(op->dtype, op->DT, op->K, op->n0, /*inverse_side=*/true);
+          transpose ? L2Prefetch{} : binprod_prefetch_plan(op->dtype, op->DT, op->K, op->n0, 1);
       const int ri =
           fft2d(true, ws->hat2, v, op->n2, op->n1, op->l2, op->l1, inner, -s1, tc, tc, tio, nullptr, stop, s, &pfi);
       return ri == -1 ? TOEP_ERR_ARG : ri;
