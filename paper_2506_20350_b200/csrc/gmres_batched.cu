@@ -359,7 +359,14 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int ctiles = (W + kCols - 1) / kCols;
-  const int nchunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n / 16, (4 * sms + ctiles - 1) / ctiles)));
+  // row chunks: enough CTAs of kCols threads for ~32 resident warps per SM (the sweeps are
+  // latency-bound per thread; occupancy is what keeps HBM busy)
+  static const int chunk_mult = [] {
+    const char* e = std::getenv("TOEP_BATCH_CHUNKS");
+    return e != nullptr ? std::max(1, std::atoi(e)) : 32;
+  }();
+  const int nchunks = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(n / 16, (chunk_mult * sms + ctiles - 1) / ctiles)));
   const int g1 = static_cast<int>(std::min<int64_t>((N + 255) / 256, 8 * sms));
   const int gc = (W + 127) / 128;
   const bool per_step_pc = p->precond == TOEP_PC_BLOCK;
