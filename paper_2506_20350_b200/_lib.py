@@ -124,16 +124,34 @@ def lib():
     return _lib if _lib is not None else load()
 
 
+_CUDA_OK = False
+_DEVICES: dict = {}
+
+
 def require_cuda() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2506_20350_b200 needs a CUDA device (B200 / sm_100a); no CPU fallback exists")
-    lib()
-    return torch.device("cuda", torch.cuda.current_device())
+    global _CUDA_OK
+    if not _CUDA_OK:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2506_20350_b200 needs a CUDA device (B200 / sm_100a); no CPU fallback exists")
+        lib()
+        _CUDA_OK = True
+    idx = torch.cuda.current_device()
+    dev = _DEVICES.get(idx)
+    if dev is None:
+        dev = _DEVICES[idx] = torch.device("cuda", idx)
+    return dev
+
+
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 
 
 def stream_handle(stream=None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    """cudaStream_t of ``stream`` (default: torch's current stream on the current device)."""
+    if stream is not None:
+        return int(stream.cuda_stream)
+    if _raw_stream is not None:  # skips building a torch.cuda.Stream object per call
+        return int(_raw_stream(torch.cuda.current_device()))
+    return int(torch.cuda.current_stream().cuda_stream)
 
 
 def last_error() -> str:

@@ -45,3 +45,45 @@ def manual():
 
 
 print("manual h2d+mv+d2h+sync us: %.1f %.1f" % ev(manual))
+
+
+def manual_spin():
+    ud.copy_(uh, non_blocking=True)
+    v = matvec(spec, ud)
+    oh.copy_(v, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    while not ev.query():
+        pass
+
+
+print("manual + event spin us: %.1f %.1f" % ev(manual_spin))
+
+g = torch.cuda.CUDAGraph()
+vg = None
+s2 = torch.cuda.Stream()
+s2.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(s2):
+    for _ in range(3):
+        ud.copy_(uh, non_blocking=True)
+        vg = matvec(spec, ud)
+        oh.copy_(vg, non_blocking=True)
+torch.cuda.current_stream().wait_stream(s2)
+torch.cuda.synchronize()
+try:
+    with torch.cuda.graph(g):
+        ud.copy_(uh, non_blocking=True)
+        vg = matvec(spec, ud)
+        oh.copy_(vg, non_blocking=True)
+
+    def graph_spin():
+        g.replay()
+        e = torch.cuda.Event()
+        e.record()
+        while not e.query():
+            pass
+
+    print("graph + event spin us: %.1f %.1f" % ev(graph_spin))
+    print("graph result ok:", bool(torch.allclose(oh, matvec(spec, uh))))
+except Exception as exc:  # capture of the library's launches may be refused
+    print("graph capture failed:", repr(exc)[:200])
