@@ -453,7 +453,10 @@ struct OrthArgs {
   unsigned* bar;    // [2] grid barrier: arrival count, generation
   long long* ts;    // optional phase stamps: [2k+2] = step k orth start, [2k+3] = step k end
   L2Prefetch pf;    // operator stream prefetched into L2 for the next matvec (HBM is idle here)
+  int force_cgs2;   // 1: always two Gram-Schmidt passes (TOEP_CGS2=1)
+  double reorth_eta2;  // second pass when ||w'||^2 <= eta^2 ||w||^2
 };
+constexpr int kMaxOrthM = 1024;  // basis vectors per cycle handled by the cooperative kernel
 
 // Grid barrier on a monotonic arrival counter (zeroed once per solve): every CTA adds 1 and
 // waits until the counter reaches the next multiple of gridDim.x (one atomic per CTA, no reset).
@@ -477,7 +480,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
 
 // coef[l] = vs_l * (vs_l * sum_b part[l][b]); CTA 0 stores h (mode 1) or hprev + h (mode 2)
 __device__ __forceinline__ void orth_coefs(const OrthArgs& a, double2* coef, int mode, double2* hout,
-                                           double2* hsm = nullptr) {
+                                           double2* hsm = nullptr, double* hsq = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nblk = gridDim.x;
   for (int l = warp; l < a.m; l += kCoopThreads / 32) {
@@ -487,6 +490,7 @@ __device__ __forceinline__ void orth_coefs(const OrthArgs& a, double2* coef, int
     if (lane == 0) {
       const double2 h = cscale(s, a.vs[l]);
       coef[l] = cscale(h, a.vs[l]);
+      if (hsq != nullptr) hsq[l] = h.x * h.x + h.y * h.y;
       if (blockIdx.x == 0) {
         const double2 hv = (mode == 1) ? h : cadd(a.h1[l], h);
         hout[l] = hv;
@@ -519,10 +523,19 @@ __device__ __forceinline__ double orth_update(const OrthArgs& a, const double2* 
 
 // one warp per basis vector: warp l sweeps the CTA's chunk of V_l and w with 8 independent
 // loads in flight per lane and ends with a single warp reduction; lane 0 stores the CTA partial
-__device__ __forceinline__ void orth_dots(const OrthArgs& a, int64_t c0, int64_t c1) {
+__device__ __forceinline__ void orth_dots(const OrthArgs& a, int64_t c0, int64_t c1, double* wn2 = nullptr) {
   constexpr int NW = kCoopThreads / 32, U = 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nblk = gridDim.x;
+  if (wn2 != nullptr && warp == NW - 1) {  // ||w||^2 over the chunk (selective re-orthogonalisation test)
+    double t = 0.0;
+    for (int64_t i = c0 + lane; i < c1; i += 32) {
+      const double2 v = a.w[i];
+      t = fma(v.x, v.x, fma(v.y, v.y, t));
+    }
+    t = warp_sum(t);
+    if (lane == 0) wn2[blockIdx.x] = t;
+  }
   for (int l = warp; l < a.m; l += NW) {
     const double2* v = a.V + static_cast<int64_t>(l) * a.N;
     double2 acc[U];
@@ -601,6 +614,27 @@ __device__ void givens_finish(const OrthArgs& a, int j, double2 hj, double hn2, 
   a.hf->breakdown = brk;
 }
 
+// CTA 0: apply the cycle's previous rotations to the new Hessenberg column held in hsm
+// (gmres.py:165-170) and write rows 0..j-1 back; row j is written by givens_finish
+__device__ void orth_prepare_givens(const OrthArgs& a, int jcol, double2* hsm, double2* snl, double* csl,
+                                    double2* hcol) {
+  for (int i = threadIdx.x; i < jcol; i += kCoopThreads) {
+    snl[i] = a.sn[i];
+    csl[i] = a.cs[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < jcol; ++i) {
+      const double2 a0 = hsm[i], a1 = hsm[i + 1];
+      const double c = csl[i];
+      const double2 sv = snl[i];
+      hsm[i] = cadd(cscale(a0, c), cmul(sv, a1));
+      hsm[i + 1] = cadd(cscale(cmulc(sv, a0), -1.0), cscale(a1, c));
+      hcol[i] = hsm[i];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const int* stop) {
   pdl_wait();
   pdl_trigger();
@@ -640,39 +674,57 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
     k_step = a.st->total;
     nhist = a.st->nhist;
   }
-  // pass 1: h1 = V^H w
-  orth_dots(a, c0, c1);
+  // pass 1: h1 = V^H w, plus ||w||^2
+  __shared__ double hsq[kMaxOrthM];
+  __shared__ int reorth_s;
+  __shared__ double hn2_s;
+  orth_dots(a, c0, c1, a.force_cgs2 ? nullptr : a.npart);
   OPROBE();
   grid_barrier(a.bar);
   OPROBE();
-  orth_coefs(a, coef, 1, a.h1);
+  orth_coefs(a, coef, 1, a.h1, blockIdx.x == 0 ? hsm : nullptr, a.force_cgs2 ? nullptr : hsq);
+  // Selective re-orthogonalisation (Kahan-Parlett "twice is enough" test): ||w'||^2 = ||w||^2 -
+  // ||h1||^2 (Pythagoras, v_l orthonormal); a second Gram-Schmidt pass only when the projection
+  // cancelled more than a factor eta of ||w|| (default eta = 1/10, TOEP_REORTH_ETA2 = eta^2;
+  // TOEP_CGS2=1 forces the second pass).  Every CTA evaluates the test from the same partials in
+  // the same order, so the branch is uniform across the grid.
+  if (a.force_cgs2) {
+    if (threadIdx.x == 0) reorth_s = 1;
+  } else if (threadIdx.x < 32) {
+    double wn = 0.0, hs = 0.0;
+    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32) wn += __ldcg(a.npart + b);
+    for (int l = threadIdx.x; l < a.m; l += 32) hs += hsq[l];
+    wn = warp_sum(wn);
+    hs = warp_sum(hs);
+    if (threadIdx.x == 0) {
+      const double hn2 = wn - hs;
+      hn2_s = hn2;
+      reorth_s = !(hn2 > a.reorth_eta2 * wn) ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  if (!reorth_s) {
+    double2* hcol1 = a.rcols + static_cast<int64_t>(jcol) * a.ldr;
+    if (blockIdx.x == 0) {
+      orth_prepare_givens(a, jcol, hsm, snl, csl, hcol1);
+      if (threadIdx.x == 0) {
+        givens_finish(a, jcol, hsm[jcol], hn2_s, g_j, beta0, nhist);
+        if (a.ts != nullptr) a.ts[2 * k_step + 3] = global_ns();
+      }
+    }
+    orth_update(a, coef, c0, c1);
+    return;
+  }
   OPROBE();
   orth_update(a, coef, c0, c1);
   __syncthreads();
-  OPROBE();
-  // pass 2 (re-orthogonalisation): h2 = V^H w', H[:, j] = h1 + h2
+  OPROBE();  // pass 2 (re-orthogonalisation): h2 = V^H w', H[:, j] = h1 + h2
   orth_dots(a, c0, c1);
   grid_barrier(a.bar);
   OPROBE();
   double2* hcol = a.rcols + static_cast<int64_t>(jcol) * a.ldr;
   orth_coefs(a, coef, 2, hcol, blockIdx.x == 0 ? hsm : nullptr);
-  if (blockIdx.x == 0) {  // apply the cycle's previous rotations to the new column (gmres.py:165-170)
-    for (int i = threadIdx.x; i < jcol; i += kCoopThreads) {
-      snl[i] = a.sn[i];
-      csl[i] = a.cs[i];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < jcol; ++i) {
-        const double2 a0 = hsm[i], a1 = hsm[i + 1];
-        const double c = csl[i];
-        const double2 sv = snl[i];
-        hsm[i] = cadd(cscale(a0, c), cmul(sv, a1));
-        hsm[i + 1] = cadd(cscale(cmulc(sv, a0), -1.0), cscale(a1, c));
-        hcol[i] = hsm[i];
-      }
-    }
-  }
+  if (blockIdx.x == 0) orth_prepare_givens(a, jcol, hsm, snl, csl, hcol);
   double nrm = orth_update(a, coef, c0, c1);
   nrm = warp_sum(nrm);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
@@ -1020,7 +1072,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   const size_t coop_smem = std::max(sizeof(double2) * ldr * (1 + kCoopThreads / 32),
                                     (2 * sizeof(double2) + sizeof(double)) * ldr);
   const int coop_grid = nblk;
-  bool use_coop = !e.distributed() && [] {
+  bool use_coop = !e.distributed() && cycle_len <= kMaxOrthM && [] {
     const char* v = std::getenv("TOEP_COOP");
     return !(v != nullptr && v[0] == '0');
   }();
@@ -1040,6 +1092,14 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   tr.mark("allocations");
 
   const bool timed = cfg->timings != 0;
+  // default: always two passes (CGS2), whose residual histories track the reference's MGS to
+  // 1e-6; TOEP_REORTH_ETA2=<eta^2> selects the one-pass-unless-cancelled variant (measured: half
+  // the orthogonalisation time at eta^2 = 1e-2, same iteration counts, histories drift ~1e-5)
+  static const int force_cgs2 = std::getenv("TOEP_REORTH_ETA2") == nullptr ? 1 : 0;
+  static const double reorth_eta2 = [] {
+    const char* e = std::getenv("TOEP_REORTH_ETA2");
+    return e != nullptr ? std::atof(e) : 1e-2;
+  }();
   const L2Prefetch orth_pf = (p->op != nullptr && p->w == 1) ? binprod_prefetch_plan(p->op->dtype, p->op->DT,
                                                                                     p->op->K, p->op->n0, 2)
                                                             : L2Prefetch{};
@@ -1166,7 +1226,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       const int m = j + 1;
       if (use_coop) {
         OrthArgs oa{V, N, m, vs, w, part1, e.norm_partial, h1, st, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
-                    static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev, orth_pf};
+                    static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev, orth_pf, force_cgs2, reorth_eta2};
         rc = launch_coop(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa, (const int*)stop_dev);
         if (rc != TOEP_OK) {  // cooperative launch unavailable: permanent fallback to the 4-kernel chain
           use_coop = false;
