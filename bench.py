@@ -36,6 +36,7 @@ NB = 128
 DIM = NY * NX * NB
 METRIC = "MLFFT Toeplitz matvec/s & GMRES solve time, 30x30, N_b=128; % HBM roofline"
 UNIT = "matvec/s"
+WORKLOAD = "cfg2: 30x30 array, N_b=128, complex128, single dense RHS (BASELINE configs[1])"
 
 
 def algorithmic_bytes(bins: int, nb: int = NB, dim: int = DIM, s: int = 16) -> dict:
@@ -162,7 +163,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (BASELINE seeded generator)",
-            "config": {"workload": "cfg2: 30x30 array, N_b=128, single RHS, (2N-1)^2 embedding (reference)",
+            "config": {"workload": WORKLOAD, "embedding": "59x59 circulant (3481 bins, the reference's 2N-1)",
                        "n_bins": (2 * NY - 1) * (2 * NX - 1), "dim": DIM},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
@@ -313,7 +314,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128", "data": "synthetic (BASELINE seeded generator, seed 0; dense default_rng(1) vector)",
-        "config": {"workload": "cfg2: 30x30 array, N_b=128, single RHS, 60x60 circulant (3600 bins)",
+        "config": {"workload": WORKLOAD, "embedding": "60x60 circulant (3600 bins, smallest 7-smooth >= 2N-1)",
                    "parallelism": f"replicas x{world}", "l2_policy": "inputs larger than L2 (944 MB spectral blocks)",
                    "matvec_hbm_frac": achieved_mv / peak, "matvec_GBps": achieved_mv,
                    "algorithmic_bytes_per_matvec": by["matvec"],
