@@ -873,9 +873,10 @@ struct Trace {
   }
   // spin on the event: cudaEventSynchronize may yield the thread and wake it up
   // hundreds of microseconds late, which starves the launch queue
-  void sync_event(cudaEvent_t ev) {
+  // spin until the device has completed `target` steps overall (or stopped)
+  void wait_total(const HostFlags* hf, int target) {
     const auto a = clk::now();
-    while (cudaEventQuery(ev) == cudaErrorNotReady) {
+    while (hf->total < target && !hf->stop) {
     }
     if (on) wait += std::chrono::duration<double, std::milli>(clk::now() - a).count();
   }
@@ -1072,6 +1073,12 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   const size_t coop_smem = std::max(sizeof(double2) * ldr * (1 + kCoopThreads / 32),
                                     (2 * sizeof(double2) + sizeof(double)) * ldr);
   const int coop_grid = nblk;
+  // TOEP_COOP_LAUNCH=0: plain PDL launch of the grid-barrier kernel (co-residency from the
+  // resource budget: one CTA per SM, fits next to either 2-D DFT kernel)
+  static const bool coop_attr = [] {
+    const char* v = std::getenv("TOEP_COOP_LAUNCH");
+    return !(v != nullptr && v[0] == '0');
+  }();
   bool use_coop = !e.distributed() && cycle_len <= kMaxOrthM && [] {
     const char* v = std::getenv("TOEP_COOP");
     return !(v != nullptr && v[0] == '0');
@@ -1079,6 +1086,9 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   if (use_coop) {
     if (coop_smem > 48 * 1024)
       cudaFuncSetAttribute(k_orth_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem);
+    // same (maximal) shared-memory carveout as the 2-D DFT kernels, so the next forward DFT can
+    // become resident next to this kernel without an SM reconfiguration
+    cudaFuncSetAttribute(k_orth_coop, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_orth_coop, kCoopThreads, coop_smem) != cudaSuccess ||
         per_sm * sms < coop_grid)
@@ -1180,7 +1190,6 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   int* m_dev = &st->m;
   int total = 0;
   bool first = true;
-  std::vector<cudaEvent_t> step_ev;
   while (true) {
     // ---- cycle start (gmres.py:123-144): V[0] = P^-1 (b - A x), vs[0] = 1 / ||.||
     double2* v0 = V;
@@ -1207,7 +1216,6 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
 
     // ---- Arnoldi steps (gmres.py:146-190)
     int j = 0;
-    step_ev.clear();
     while (j < cycle_len && total + j < max_total) {
       const auto t_launch0 = clk::now();
       const double2* vj = V + static_cast<int64_t>(j) * N;
@@ -1227,7 +1235,10 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       if (use_coop) {
         OrthArgs oa{V, N, m, vs, w, part1, e.norm_partial, h1, st, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
                     static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev, orth_pf, force_cgs2, reorth_eta2};
-        rc = launch_coop(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa, (const int*)stop_dev);
+        rc = coop_attr ? launch_coop(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa,
+                                     (const int*)stop_dev)
+                       : launch_k(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa,
+                                  (const int*)stop_dev);
         if (rc != TOEP_OK) {  // cooperative launch unavailable: permanent fallback to the 4-kernel chain
           use_coop = false;
           rc = TOEP_OK;
@@ -1256,9 +1267,6 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
                      static_cast<int>(max_total), cycle_len, hf_dev));
       }
       if (ev_timed) mark(2, t0);
-      cudaEvent_t ev = res.event();
-      cudaEventRecord(ev, s);
-      step_ev.push_back(ev);
       if (tr.on) {
         const double us = std::chrono::duration<double, std::micro>(clk::now() - t_launch0).count();
         tr.launch_us_sum += us;
@@ -1266,10 +1274,12 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
         tr.steps++;
       }
       ++j;
-      // keep up to kLag steps queued ahead of the one the host last saw finish
+      // keep up to kLag steps queued ahead of the one the host last saw finish.  Progress is read
+      // from the mapped flag word the Givens step writes (no events between the kernels: an event
+      // record would break their programmatic-dependent-launch chain)
       constexpr int kLag = 2;
       if (j > kLag) {
-        tr.sync_event(step_ev[j - 1 - kLag]);
+        tr.wait_total(hf, total + (j - kLag));
         if (hf->stop) break;
       }
     }
