@@ -455,6 +455,7 @@ struct OrthArgs {
   L2Prefetch pf;    // operator stream prefetched into L2 for the next matvec (HBM is idle here)
   int force_cgs2;   // 1: always two Gram-Schmidt passes (TOEP_CGS2=1)
   double reorth_eta2;  // second pass when ||w'||^2 <= eta^2 ||w||^2
+  int direct_norm;  // 1: h_{j+1,j} = ||w''|| from a third sweep + barrier (TOEP_DIRECT_NORM=1)
 };
 constexpr int kMaxOrthM = 1024;  // basis vectors per cycle handled by the cooperative kernel
 
@@ -469,8 +470,8 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned old = atomicAdd(bar, 1u);
+    unsigned old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
     const unsigned target = (old / gridDim.x + 1) * gridDim.x;
     while (static_cast<int>(ld_acquire_gpu(bar) - target) < 0) {
     }
@@ -718,12 +719,33 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
   OPROBE();
   orth_update(a, coef, c0, c1);
   __syncthreads();
-  OPROBE();  // pass 2 (re-orthogonalisation): h2 = V^H w', H[:, j] = h1 + h2
-  orth_dots(a, c0, c1);
+  OPROBE();  // pass 2 (re-orthogonalisation): h2 = V^H w', H[:, j] = h1 + h2, plus ||w'||^2
+  orth_dots(a, c0, c1, a.direct_norm ? nullptr : a.npart);
   grid_barrier(a.bar);
   OPROBE();
   double2* hcol = a.rcols + static_cast<int64_t>(jcol) * a.ldr;
-  orth_coefs(a, coef, 2, hcol, blockIdx.x == 0 ? hsm : nullptr);
+  orth_coefs(a, coef, 2, hcol, blockIdx.x == 0 ? hsm : nullptr, a.direct_norm ? nullptr : hsq);
+  if (!a.direct_norm) {
+    // h_{j+1,j}^2 = ||w''||^2 = ||w'||^2 - ||h2||^2 (Pythagoras; h2 is the small second-pass
+    // correction, so there is no cancellation): no third grid barrier, CTA 0 finishes the Givens
+    // step while the other CTAs apply the second update
+    if (blockIdx.x == 0) {
+      orth_prepare_givens(a, jcol, hsm, snl, csl, hcol);
+      if (threadIdx.x < 32) {
+        double wn = 0.0, hs = 0.0;
+        for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32) wn += __ldcg(a.npart + b);
+        for (int l = threadIdx.x; l < a.m; l += 32) hs += hsq[l];
+        wn = warp_sum(wn);
+        hs = warp_sum(hs);
+        if (threadIdx.x == 0) {
+          givens_finish(a, jcol, hsm[jcol], fmax(wn - hs, 0.0), g_j, beta0, nhist);
+          if (a.ts != nullptr) a.ts[2 * k_step + 3] = global_ns();
+        }
+      }
+    }
+    orth_update(a, coef, c0, c1);
+    return;
+  }
   if (blockIdx.x == 0) orth_prepare_givens(a, jcol, hsm, snl, csl, hcol);
   double nrm = orth_update(a, coef, c0, c1);
   nrm = warp_sum(nrm);
@@ -1105,6 +1127,10 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   // default: always two passes (CGS2), whose residual histories track the reference's MGS to
   // 1e-6; TOEP_REORTH_ETA2=<eta^2> selects the one-pass-unless-cancelled variant (measured: half
   // the orthogonalisation time at eta^2 = 1e-2, same iteration counts, histories drift ~1e-5)
+  static const int direct_norm = [] {
+    const char* e = std::getenv("TOEP_DIRECT_NORM");
+    return e != nullptr && e[0] == '1' ? 1 : 0;
+  }();
   static const int force_cgs2 = std::getenv("TOEP_REORTH_ETA2") == nullptr ? 1 : 0;
   static const double reorth_eta2 = [] {
     const char* e = std::getenv("TOEP_REORTH_ETA2");
@@ -1234,7 +1260,8 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       const int m = j + 1;
       if (use_coop) {
         OrthArgs oa{V, N, m, vs, w, part1, e.norm_partial, h1, st, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
-                    static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev, orth_pf, force_cgs2, reorth_eta2};
+                    static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev, orth_pf, force_cgs2, reorth_eta2,
+                    direct_norm};
         rc = coop_attr ? launch_coop(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa,
                                      (const int*)stop_dev)
                        : launch_k(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa,
