@@ -67,6 +67,10 @@ typedef struct {
 TOEP_API const char* toep_last_error(void);
 TOEP_API int toep_version(void);
 
+/* problems.py:219-226 fnv1a64: 64-bit FNV-1a of `bytes` host bytes (the TBZ1 payload checksum,
+ * problems.py:236-322).  Host-only; the Python host code parses the container. */
+TOEP_API int toep_fnv1a64(const void* data, uint64_t bytes, uint64_t* out);
+
 /* toeplitz.py:248-253 precompute_spectral (+ SpectralOperator, :135-155).
  * stacked4: the generator, (2n2-1, 2n1-1, n0, n0) complex128 row-major in
  * circulant order (BlockGenerator2L.stacked4(), toeplitz.py:129-131), on the

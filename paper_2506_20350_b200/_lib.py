@@ -75,6 +75,7 @@ class GmresReport(ctypes.Structure):
 SIGNATURES = {
     "toep_last_error": (ctypes.c_char_p, []),
     "toep_version": (c_int, []),
+    "toep_fnv1a64": (c_int, [c_vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]),
     "toep_op_create": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, ctypes.POINTER(c_vp)]),
     "toep_op_destroy": (c_int, [c_vp]),
     "toep_op_info": (c_int, [c_vp, ctypes.POINTER(OpInfo)]),

@@ -18,11 +18,20 @@ so one ``(2Nx-1, 2, Nb, Nb)`` draw equals the per-block re/im draws of the loop.
 
 from __future__ import annotations
 
+import ctypes
+import json
+import struct
 from dataclasses import dataclass
 
 import numpy as np
 
+from .errors import ChecksumMismatch, FormatVersionMismatch, InvalidSpec
+
 __all__ = [
+    "ArrayProblemSpec",
+    "fnv1a64",
+    "save",
+    "load",
     "ConfigSpec",
     "CONFIGS",
     "seeded_stacked4",
@@ -137,3 +146,129 @@ def seeded_system(ny: int, nx: int, nb: int, seed: int = 0) -> BorderedSystem:
     from .toeplitz import generator_from_stacked
 
     return system_from_generator(generator_from_stacked(seeded_stacked4(ny, nx, nb, seed)))
+
+
+# ------------------------------------------------------------------ TBZ1 problem files
+# Container of the reference's problems.save / load (problems.py:219-322): magic, little-endian
+# u32 header length, sorted-key JSON header, the c128 payload (generator blocks in circulant
+# order, then Z_B and Z_C, row-major, little-endian interleaved), FNV-1a-64 of the payload.
+_MAGIC = b"TBZ1\n"
+_VERSION = 1
+
+
+@dataclass
+class ArrayProblemSpec:
+    """Parameters of a bordered array problem (problems.py:56-87): ``nb`` defaults to 8*(nx+ny),
+    ``regularization`` to pitch/10."""
+
+    ny: int
+    nx: int
+    ne: int
+    nb: int | None = None
+    wavenumber: float = 3.0
+    pitch: float = 1.0
+    regularization: float | None = None
+    diagonal_shift: float = 1.0
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.nb is None:
+            self.nb = 8 * (self.nx + self.ny)
+        if self.regularization is None:
+            self.regularization = self.pitch / 10.0
+        if min(self.ny, self.nx, self.ne) < 1:
+            raise InvalidSpec(f"ny, nx, ne must be >= 1, got {(self.ny, self.nx, self.ne)}")
+        if self.nb < 0:
+            raise InvalidSpec(f"nb must be >= 0, got {self.nb}")
+        if not self.pitch > 0:
+            raise InvalidSpec(f"pitch must be > 0, got {self.pitch}")
+        if not self.regularization > 0:
+            raise InvalidSpec(f"regularization must be > 0, got {self.regularization}")
+
+    @property
+    def elements(self) -> int:
+        return self.ny * self.nx
+
+    @property
+    def array_dim(self) -> int:
+        return self.elements * self.ne
+
+    @property
+    def dim(self) -> int:
+        return self.array_dim + self.nb
+
+
+def fnv1a64(data) -> int:
+    """64-bit FNV-1a (problems.py:219-224), computed by libtoepcuda (host code)."""
+    from . import _lib
+
+    buf = np.frombuffer(memoryview(data).cast("B"), dtype=np.uint8) if not isinstance(data, np.ndarray) \
+        else np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+    out = ctypes.c_uint64()
+    _lib.check(_lib.lib().toep_fnv1a64(buf.ctypes.data if buf.size else None, buf.size, ctypes.byref(out)),
+               "fnv1a64")
+    return int(out.value)
+
+
+def _payload(sys) -> list:
+    return [np.ascontiguousarray(sys.gen.stacked4(), dtype="<c16"), np.ascontiguousarray(sys.zb, dtype="<c16"),
+            np.ascontiguousarray(sys.zc, dtype="<c16")]
+
+
+def save(sys, path) -> None:
+    """Write a TBZ1 file (problems.py:236-266); ``sys.spec`` supplies the header fields."""
+    s = sys.spec
+    if s is None:
+        raise InvalidSpec("saving a problem file needs the system's ArrayProblemSpec (sys.spec)")
+    header = {"version": _VERSION, "ny": s.ny, "nx": s.nx, "ne": s.ne, "nb": s.nb, "seed": s.seed,
+              "k": s.wavenumber, "pitch": s.pitch, "a": s.regularization, "shift": s.diagonal_shift,
+              "dtype": "c128", "order": "row-major", "endian": "little"}
+    hb = json.dumps(header, sort_keys=True).encode("utf-8")
+    parts = _payload(sys)
+    payload = b"".join(p.tobytes() for p in parts)
+    with open(path, "wb") as fh:
+        fh.write(_MAGIC)
+        fh.write(struct.pack("<I", len(hb)))
+        fh.write(hb)
+        fh.write(payload)
+        fh.write(struct.pack("<Q", fnv1a64(payload)))
+
+
+def load(path) -> BorderedSystem:
+    """Read a TBZ1 file (problems.py:269-322): FormatVersionMismatch for a foreign magic or
+    version, ChecksumMismatch for truncated or corrupted payloads."""
+    from .toeplitz import generator_from_stacked
+
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if blob[: len(_MAGIC)] != _MAGIC:
+        raise FormatVersionMismatch(f"bad magic {blob[:5]!r}")
+    off = len(_MAGIC)
+    if len(blob) < off + 4:
+        raise ChecksumMismatch("file truncated inside header length")
+    (hlen,) = struct.unpack_from("<I", blob, off)
+    off += 4
+    if len(blob) < off + hlen:
+        raise ChecksumMismatch("file truncated inside header")
+    header = json.loads(blob[off: off + hlen].decode("utf-8"))
+    off += hlen
+    if header.get("version") != _VERSION:
+        raise FormatVersionMismatch(f"unsupported version {header.get('version')!r}")
+    ny, nx, ne, nb = header["ny"], header["nx"], header["ne"], header["nb"]
+    n_gen = (2 * ny - 1) * (2 * nx - 1) * ne * ne
+    n_zb = nb * ny * nx * ne
+    n_zc = nb * nb
+    expect = (n_gen + n_zb + n_zc) * 16
+    if len(blob) != off + expect + 8:
+        raise ChecksumMismatch(f"payload size mismatch: have {len(blob) - off - 8} bytes, expected {expect}")
+    payload = memoryview(blob)[off: off + expect]
+    (stored,) = struct.unpack_from("<Q", blob, off + expect)
+    if fnv1a64(payload) != stored:
+        raise ChecksumMismatch("payload checksum mismatch")
+    scalars = np.frombuffer(payload, dtype="<c16")
+    stacked4 = scalars[:n_gen].reshape(2 * ny - 1, 2 * nx - 1, ne, ne).astype(np.complex128)
+    zb = scalars[n_gen: n_gen + n_zb].reshape(nb, ny * nx * ne).astype(np.complex128)
+    zc = scalars[n_gen + n_zb:].reshape(nb, nb).astype(np.complex128)
+    spec = ArrayProblemSpec(ny=ny, nx=nx, ne=ne, nb=nb, wavenumber=header["k"], pitch=header["pitch"],
+                            regularization=header["a"], diagonal_shift=header["shift"], seed=header["seed"])
+    return BorderedSystem(generator_from_stacked(stacked4), zb, zc, spec)

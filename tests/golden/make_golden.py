@@ -4,7 +4,7 @@ Run in the build container (where ``/root/reference`` exists):
 
     python tests/golden/make_golden.py [parts...]
 
-parts: small sweep cfg1 cfg2 cfg3 cfg4 cfg5 (default: small sweep cfg1 cfg2).
+parts: small sweep cfg1 cfg2 cfg3 cfg4 cfg5 tbz (default: small sweep cfg1 cfg2).
 It imports ``toepsolve`` read-only from ``/root/reference/pkg/src`` and calls
 only the reference's public API (``embed_2l``, ``precompute_spectral``,
 ``matvec``, ``matvec_transpose``, ``gmres``, ``build_pk``, ``rybicki_solve``,
@@ -192,6 +192,26 @@ def part_cfg5(out):
     out["x_proj"] = probes(x.size, 1) @ x.reshape(-1)
 
 
+def part_tbz(out):
+    """A small bordered problem written by the reference's own TBZ1 writer (problems.py:236-266),
+    plus what the reference's loader (problems.py:269-322) reads back from it."""
+    from toepsolve import problems as ref_problems
+
+    spec = ref_problems.ArrayProblemSpec(ny=2, nx=3, ne=4, nb=5, wavenumber=2.5, pitch=1.0, seed=7)
+    sys_ = ref_problems.generate(spec)
+    path = os.path.join(HERE, "small.tbz")
+    ref_problems.save(sys_, path)
+    back = ref_problems.load(path)
+    out["stacked4"] = back.gen.stacked4()
+    out["zb"] = back.zb
+    out["zc"] = back.zc
+    out["spec"] = np.array([back.spec.ny, back.spec.nx, back.spec.ne, back.spec.nb, back.spec.seed])
+    out["spec_f"] = np.array([back.spec.wavenumber, back.spec.pitch, back.spec.regularization,
+                              back.spec.diagonal_shift])
+    with open(path, "rb") as fh:
+        out["fnv"] = np.array([ref_problems.fnv1a64(fh.read()[:64])], dtype=np.uint64)
+
+
 def main(parts):
     for part in parts:
         out = {}
@@ -210,6 +230,8 @@ def main(parts):
             part_cfg("cfg3", 30, 30, 256, 1e-6, None, out, percol=[0, 1, 449, 899])
         elif part == "cfg5":
             part_cfg5(out)
+        elif part == "tbz":
+            part_tbz(out)
         else:
             raise SystemExit(f"unknown part {part}")
         path = os.path.join(HERE, f"{part}.npz")

@@ -104,3 +104,20 @@ def test_schur_solve_with_border_vs_dense(inner):
     x, rep = schur_solve(sys_, v, inner)
     assert rep.method == f"schur-{inner}"
     assert rel_err(x, np.linalg.solve(dense, v)) <= 1e-11
+
+
+def test_tbz1_problem_file_to_device():
+    # a bordered problem written by the reference (tests/golden/small.tbz) -> device operator
+    import os
+
+    from paper_2506_20350_b200 import problems
+
+    sys_ = problems.load(os.path.join(os.path.dirname(__file__), "golden", "small.tbz"))
+    op = BorderedOperator.from_system(sys_)
+    dense = np.block([[assemble_dense(sys_.gen), sys_.zb.T], [sys_.zb, sys_.zc]])
+    rng = np.random.default_rng(9)
+    x = _rand(rng, sys_.dim, 2)
+    assert rel_err(bordered_matvec(op, x), dense @ x) <= 1e-12
+    v = _rand(rng, sys_.dim, 1)
+    sol, _ = schur_solve(sys_, v, "rybicki")
+    assert rel_err(sol, np.linalg.solve(dense, v)) <= 1e-10

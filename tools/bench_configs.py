@@ -9,6 +9,17 @@ from paper_2506_20350_b200.solvers import (BorderedOperator, GmresConfig, build_
 from paper_2506_20350_b200.toeplitz import generator_from_stacked, matvec, precompute_spectral  # noqa
 
 
+def med_time(fn, warm=2, reps=5):
+    """median of `reps` CUDA-event-timed calls after `warm` untimed ones (transient slow windows)."""
+    for _ in range(warm):
+        fn()
+    ts, out = [], None
+    for _ in range(reps):
+        t, out = ev_time(fn)
+        ts.append(t)
+    return float(np.median(ts)), out
+
+
 def ev_time(fn, reps=1):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
@@ -32,7 +43,7 @@ if "cfg1" in which:
     g = {}
     for tag, p in (("none", None), ("pk", build_pk(sys_))):
         solve_multi_rhs_vectorized(op, p, b, GmresConfig(tol=1e-8, restart=30))
-        t, (x, rep) = ev_time(lambda: solve_multi_rhs_vectorized(op, p, b, GmresConfig(tol=1e-8, restart=30)))
+        t, (x, rep) = med_time(lambda: solve_multi_rhs_vectorized(op, p, b, GmresConfig(tol=1e-8, restart=30)))
         g[tag] = {"iterations": rep.iterations, "ms": t}
     res["cfg1"] = {"matvec_us": ms * 1e3, "gmres": g}
     print(json.dumps(res["cfg1"]), flush=True)
@@ -48,7 +59,7 @@ if "cfg4" in which:
         g = {}
         for tag, p in (("none", None), ("pk", build_pk(sys_))):
             solve_multi_rhs_vectorized(op, p, b, GmresConfig(tol=1e-6, restart=50))
-            t, (x, rep) = ev_time(lambda: solve_multi_rhs_vectorized(op, p, b, GmresConfig(tol=1e-6, restart=50)))
+            t, (x, rep) = med_time(lambda: solve_multi_rhs_vectorized(op, p, b, GmresConfig(tol=1e-6, restart=50)))
             g[tag] = {"iterations": rep.iterations, "ms": t, "final_residual": rep.final_residual}
         es = 16 if dt == torch.complex128 else 8
         byt = op.spectral.bins * 128 * 128 * es + 2 * sys_.dim * 16
