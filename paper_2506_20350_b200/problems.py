@@ -29,6 +29,9 @@ from .errors import ChecksumMismatch, FormatVersionMismatch, InvalidSpec
 
 __all__ = [
     "ArrayProblemSpec",
+    "generate",
+    "ExcitationSet",
+    "build_excitations",
     "fnv1a64",
     "save",
     "load",
@@ -146,6 +149,88 @@ def seeded_system(ny: int, nx: int, nb: int, seed: int = 0) -> BorderedSystem:
     from .toeplitz import generator_from_stacked
 
     return system_from_generator(generator_from_stacked(seeded_stacked4(ny, nx, nb, seed)))
+
+
+# ------------------------------------------------------------------ synthetic bordered problems
+def _helmholtz(dist2: np.ndarray, k: float, a: float) -> np.ndarray:
+    """Regularised free-space kernel e^{-ikr} / (4 pi r), r = sqrt(d^2 + a^2) (problems.py:135-137)."""
+    r = np.sqrt(dist2 + a * a)
+    return np.exp(-1j * k * r) / (4.0 * np.pi * r)
+
+
+def _border_points(rng: np.random.Generator, nb: int, wx: float, wy: float) -> np.ndarray:
+    """nb sorted arc-length positions on the rectangle [0,wx]x[0,wy], walked counter-clockwise from
+    the origin: bottom, right, top (right to left), left (top to bottom) (problems.py:140-154)."""
+    t = np.sort(rng.uniform(0.0, 2.0 * (wx + wy), size=nb))
+    pts = np.empty((nb, 2))
+    edges = np.cumsum([wx, wy, wx])
+    for i, ti in enumerate(t):
+        if ti < edges[0]:
+            pts[i] = (ti, 0.0)
+        elif ti < edges[1]:
+            pts[i] = (wx, ti - wx)
+        elif ti < edges[2]:
+            pts[i] = (2 * wx + wy - ti, wy)
+        else:
+            pts[i] = (0.0, 2.0 * (wx + wy) - ti)
+    return pts
+
+
+def generate(spec: ArrayProblemSpec) -> BorderedSystem:
+    """Deterministic bordered array problem of a spec (problems.py:157-197): per-element DOF
+    offsets drawn first, border positions second; block (dr, dc) entry (m, n) is the kernel at the
+    element displacement plus the DOF offset difference; Z_B couples border points to every DOF,
+    Z_C border to border (+ shift I).  Raises SingularMatrix if Z_C is singular."""
+    from . import numerics
+    from .toeplitz import generator_from_stacked
+
+    rng = np.random.default_rng(spec.seed)
+    d, k, a = spec.pitch, spec.wavenumber, spec.regularization
+    dof = rng.uniform(0.0, d, size=(spec.ne, 2))
+    border = _border_points(rng, spec.nb, spec.nx * d, spec.ny * d)
+    # circulant offset order 0..N-1, -(N-1)..-1 at both levels (toeplitz.py:59-61)
+    off_y = np.concatenate([np.arange(spec.ny), np.arange(-(spec.ny - 1), 0)]).astype(float) * d
+    off_x = np.concatenate([np.arange(spec.nx), np.arange(-(spec.nx - 1), 0)]).astype(float) * d
+    ddx = dof[None, :, 0] - dof[:, None, 0]
+    ddy = dof[None, :, 1] - dof[:, None, 1]
+    dist2 = (off_x[None, :, None, None] + ddx[None, None]) ** 2 + (off_y[:, None, None, None] + ddy[None, None]) ** 2
+    stacked4 = _helmholtz(dist2, k, a)
+    stacked4[0, 0] += spec.diagonal_shift * np.eye(spec.ne)
+    pos = np.empty((spec.ny, spec.nx, spec.ne, 2))
+    pos[..., 0] = np.arange(spec.nx)[None, :, None] * d + dof[:, 0]
+    pos[..., 1] = np.arange(spec.ny)[:, None, None] * d + dof[:, 1]
+    pos = pos.reshape(spec.array_dim, 2)
+    zb = _helmholtz(((border[:, None, :] - pos[None, :, :]) ** 2).sum(-1), k, a)
+    zc = _helmholtz(((border[:, None, :] - border[None, :, :]) ** 2).sum(-1), k, a) + \
+        spec.diagonal_shift * np.eye(spec.nb)
+    if spec.nb:
+        numerics.lu_factor(zc)  # invertibility check (raises SingularMatrix)
+    return BorderedSystem(generator_from_stacked(stacked4), zb, zc, spec)
+
+
+@dataclass
+class ExcitationSet:
+    """One unit-feed column per array element, border rows zero (problems.py:123-132)."""
+
+    matrix: np.ndarray
+    feed_index: int
+
+    @property
+    def columns(self) -> int:
+        return self.matrix.shape[1]
+
+
+def build_excitations(sys: BorderedSystem, feed_index: int = 0) -> ExcitationSet:
+    """Unit excitation of DOF ``feed_index`` of every element (problems.py:208-216)."""
+    from .errors import IndexOutOfRange
+
+    ne = sys.spec.ne
+    if not 0 <= feed_index < ne:
+        raise IndexOutOfRange(f"feed index {feed_index} outside 0..{ne - 1}")
+    m = sys.spec.elements
+    v = np.zeros((sys.dim, m), dtype=np.complex128)
+    v[np.arange(m) * ne + feed_index, np.arange(m)] = 1.0
+    return ExcitationSet(v, feed_index)
 
 
 # ------------------------------------------------------------------ TBZ1 problem files

@@ -84,3 +84,23 @@ def test_spec_validation():
         problems.ArrayProblemSpec(ny=1, nx=1, ne=1, nb=-1)
     s = problems.ArrayProblemSpec(ny=2, nx=3, ne=4)
     assert s.nb == 8 * (2 + 3) and s.regularization == pytest.approx(0.1)
+
+
+def test_generate_matches_reference(ref):
+    # the golden file was written from the reference's generate() of this spec
+    spec = problems.ArrayProblemSpec(ny=2, nx=3, ne=4, nb=5, wavenumber=2.5, pitch=1.0, seed=7)
+    sys_ = problems.generate(spec)
+    np.testing.assert_allclose(sys_.gen.stacked4(), ref["stacked4"], rtol=1e-14, atol=0)
+    np.testing.assert_allclose(sys_.zb, ref["zb"], rtol=1e-14, atol=0)
+    np.testing.assert_allclose(sys_.zc, ref["zc"], rtol=1e-14, atol=0)
+
+
+def test_build_excitations():
+    from paper_2506_20350_b200.errors import IndexOutOfRange
+
+    sys_ = problems.load(TBZ)
+    ex = problems.build_excitations(sys_, feed_index=2)
+    assert ex.matrix.shape == (sys_.dim, 6) and ex.columns == 6
+    assert ex.matrix.sum() == 6 and ex.matrix[2, 0] == 1 and ex.matrix[4 + 2, 1] == 1
+    with pytest.raises(IndexOutOfRange):
+        problems.build_excitations(sys_, feed_index=4)
