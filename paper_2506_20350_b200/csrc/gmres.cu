@@ -40,7 +40,6 @@ namespace toep {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kLG = 8;  // basis vectors per accumulation group
 
 struct GState {
   int stop;       // 0 running, 1 converged / breakdown, 2 cycle exhausted
@@ -91,7 +90,6 @@ __device__ __forceinline__ Z block_sum(Z v, Z* red /* [kThreads/32] */) {
   __syncthreads();
   return t;
 }
-__device__ __forceinline__ double2 operator+(double2 a, double2 b) { return cadd(a, b); }
 
 // CTA b of nblk owns the contiguous element range [c0, c1) (32-aligned starts, coalesced)
 __device__ __forceinline__ void chunk_of(int64_t N, int64_t* c0, int64_t* c1) {
