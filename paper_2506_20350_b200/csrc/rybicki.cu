@@ -583,7 +583,21 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
 
   double2 *g = nullptr, *h = nullptr, *gtmp = nullptr, *lu0 = nullptr, *lu12 = nullptr, *wide = nullptr;
   int *piv0 = nullptr, *piv12 = nullptr, *info = nullptr;
+  // side stream: the block sums that do not depend on the step's LU factors run on it while the
+  // (latency-bound, few-SM) cluster LU of D1/D2 runs on `st`
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_step = nullptr, ev_sums = nullptr;
+  static const bool overlap = [] {
+    const char* e = std::getenv("TOEP_RYB_OVERLAP");
+    return !(e != nullptr && e[0] == '0');
+  }();
   auto cleanup = [&]() {
+    if (s2 != nullptr) {
+      cudaStreamSynchronize(s2);
+      cudaStreamDestroy(s2);
+    }
+    if (ev_step != nullptr) cudaEventDestroy(ev_step);
+    if (ev_sums != nullptr) cudaEventDestroy(ev_sums);
     for (void* q : {(void*)g, (void*)h, (void*)gtmp, (void*)lu0, (void*)lu12, (void*)wide, (void*)piv0, (void*)piv12,
                     (void*)info})
       if (q) cudaFreeAsync(q, st);
@@ -651,10 +665,17 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     return TOEP_OK;
   };
   // C (+)= alpha * W[:, t0*s : (t0+m)*s] @ stack(m blocks of s x ncol), one GEMM of depth m*s
-  auto wide_gemm = [&](const double2* W, int t0, int m, const double2* B, int64_t ncol, double2* C) {
+  auto wide_gemm = [&](const double2* W, int t0, int m, const double2* B, int64_t ncol, double2* C,
+                       cudaStream_t sx) {
     return gemm_rm(s, ncol, static_cast<int64_t>(m) * s, one, W + static_cast<int64_t>(t0) * s, wld, B, ncol, one, C,
-                   ncol, st);
+                   ncol, sx);
   };
+  if (overlap && N > 1) {
+    TOEP_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    TOEP_CUDA(cudaEventCreateWithFlags(&ev_step, cudaEventDisableTiming));
+    TOEP_CUDA(cudaEventCreateWithFlags(&ev_sums, cudaEventDisableTiming));
+  }
+  cudaStream_t ss2 = s2 != nullptr ? s2 : st;
   // C_b (+)= alpha * A_{m-1-b} @ B for b = 0..m-1 (A blocks s x s stacked, reversed), one batched GEMM
   auto rev_batched = [&](const double2* Astack, int m, const double2* B, int64_t ncol, double2* C, int64_t c_bs) {
     return gemm(TOEP_C128, s, ncol, s, mone, Astack + static_cast<int64_t>(m - 1) * ss, s, 1, -ss, B, ncol, 1, 0, one,
@@ -679,32 +700,43 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
 
   for (int m = 1; m < N; ++m) {
     const bool more = m < N - 1;
+    double2* xn = x + m * sw;
+    double2* gnew = gtmp + m * ss;  // slot m of the next G stack
+    double2* hnew = h + m * ss;     // slot m of H
+    // Right-hand sides of this step's three solves (independent of the D1/D2 factors), on the
+    // side stream once the previous step's updates are done:
+    //   x_{m+1} <- sum_j R_{m+1-j} x_j - y_{m+1},  G_new <- sum_j R_{j-m-1} G_j - R_{-(m+1)},
+    //   H_new <- sum_j R_{m+1-j} H_j - R_{m+1}
+    if (s2 != nullptr) {
+      TOEP_CUDA(cudaEventRecord(ev_step, st));
+      TOEP_CUDA(cudaStreamWaitEvent(s2, ev_step, 0));
+    }
+    R_TRY(copy_neg(y + m * sw, xn, sw, -1.0, ss2));
+    R_TRY(wide_gemm(Wpr, N - 1 - m, m, x, w, xn, ss2));
+    if (more) {
+      R_TRY(copy_neg(rb(-(m + 1)), gnew, ss, -1.0, ss2));
+      R_TRY(wide_gemm(Wnr, N - 1 - m, m, g, s, gnew, ss2));
+      R_TRY(copy_neg(rb(m + 1), hnew, ss, -1.0, ss2));
+      R_TRY(wide_gemm(Wpr, N - 1 - m, m, h, s, hnew, ss2));
+    }
+    if (s2 != nullptr) TOEP_CUDA(cudaEventRecord(ev_sums, s2));
     // d1 = sum_{k=1..m} R_k G_k - R_0 ;  d2 = sum_{k=1..m} R_{-k} H_k - R_0   (factored together)
     R_TRY(copy_neg(rb(0), lu1, ss, -1.0, st));
-    R_TRY(wide_gemm(Wp, 0, m, g, s, lu1));
+    R_TRY(wide_gemm(Wp, 0, m, g, s, lu1, st));
     if (more) {
       R_TRY(copy_neg(rb(0), lu2, ss, -1.0, st));
-      R_TRY(wide_gemm(Wn, 0, m, h, s, lu2));
+      R_TRY(wide_gemm(Wn, 0, m, h, s, lu2, st));
     }
     R_TRY(getrf_batched(lu12, ss, more ? 2 : 1, s, piv12, info, st));
+    if (s2 != nullptr) TOEP_CUDA(cudaStreamWaitEvent(st, ev_sums, 0));
     R_TRY(check_info(TOEP_ERR_SINGULAR_DENOM, m, more ? 2 : 1));
-    // x_{m+1} = D1^-1 (sum_j R_{m+1-j} x_j - y_{m+1})
-    double2* xn = x + m * sw;
-    R_TRY(copy_neg(y + m * sw, xn, sw, -1.0, st));
-    R_TRY(wide_gemm(Wpr, N - 1 - m, m, x, w, xn));
+    // x_{m+1} = D1^-1 (...)
     R_TRY(getrs(lu1, s, piv1, xn, static_cast<int>(w), static_cast<int>(w), st));
     // x_j -= G_{m+1-j} x_{m+1}
     R_TRY(rev_batched(g, m, xn, w, x, sw));
     if (more) {
-      // G_new = D2^-1 (sum_j R_{j-m-1} G_j - R_{-(m+1)})   -> slot m of the next G stack
-      double2* gnew = gtmp + m * ss;
-      R_TRY(copy_neg(rb(-(m + 1)), gnew, ss, -1.0, st));
-      R_TRY(wide_gemm(Wnr, N - 1 - m, m, g, s, gnew));
+      // G_new = D2^-1 (...), H_new = D1^-1 (...)
       R_TRY(getrs(lu2, s, piv2, gnew, s, s, st));
-      // H_new = D1^-1 (sum_j R_{m+1-j} H_j - R_{m+1})       -> slot m of H
-      double2* hnew = h + m * ss;
-      R_TRY(copy_neg(rb(m + 1), hnew, ss, -1.0, st));
-      R_TRY(wide_gemm(Wpr, N - 1 - m, m, h, s, hnew));
       R_TRY(getrs(lu1, s, piv1, hnew, s, s, st));
       // G_j' = G_j - H_{m+1-j} G_new (old H, into the next stack);  H_j -= G_{m+1-j} H_new (old G)
       TOEP_CUDA(cudaMemcpyAsync(gtmp, g, m * ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
