@@ -730,14 +730,21 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     R_TRY(getrf_batched(lu12, ss, more ? 2 : 1, s, piv12, info, st));
     if (s2 != nullptr) TOEP_CUDA(cudaStreamWaitEvent(st, ev_sums, 0));
     R_TRY(check_info(TOEP_ERR_SINGULAR_DENOM, m, more ? 2 : 1));
-    // x_{m+1} = D1^-1 (...)
+    // G_new = D2^-1 (...) on the side stream (latency-bound blocked TRSM chain), concurrently with
+    // x_{m+1} = D1^-1 (...), the x update and H_new = D1^-1 (...) here
+    if (more && s2 != nullptr) {
+      TOEP_CUDA(cudaEventRecord(ev_step, st));
+      TOEP_CUDA(cudaStreamWaitEvent(s2, ev_step, 0));
+      R_TRY(getrs(lu2, s, piv2, gnew, s, s, s2));
+      TOEP_CUDA(cudaEventRecord(ev_sums, s2));
+    }
     R_TRY(getrs(lu1, s, piv1, xn, static_cast<int>(w), static_cast<int>(w), st));
     // x_j -= G_{m+1-j} x_{m+1}
     R_TRY(rev_batched(g, m, xn, w, x, sw));
     if (more) {
-      // G_new = D2^-1 (...), H_new = D1^-1 (...)
-      R_TRY(getrs(lu2, s, piv2, gnew, s, s, st));
+      if (s2 == nullptr) R_TRY(getrs(lu2, s, piv2, gnew, s, s, st));
       R_TRY(getrs(lu1, s, piv1, hnew, s, s, st));
+      if (s2 != nullptr) TOEP_CUDA(cudaStreamWaitEvent(st, ev_sums, 0));
       // G_j' = G_j - H_{m+1-j} G_new (old H, into the next stack);  H_j -= G_{m+1-j} H_new (old G)
       TOEP_CUDA(cudaMemcpyAsync(gtmp, g, m * ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
       R_TRY(rev_batched(h, m, gnew, s, gtmp, ss));
