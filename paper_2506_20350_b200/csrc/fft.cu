@@ -351,30 +351,46 @@ __global__ void __launch_bounds__(k2dThreads, 1) fft2d_kernel(Fft2dArgs f) {
   const int64_t b = blockIdx.x;
   const int64_t inner = f.inner;
   const int n2 = f.n2, n1 = f.n1;
+  // each level runs over its columns in tiles of TILX (level 1: array rows y) / TILY (level 2:
+  // frequencies kx); the ping-pong buffers are reused, hence the barrier between tiles
   if constexpr (!INV) {
     PassArgs ax;  // level 1: slots x (pad fused), columns y -> G[y][kx]
     ax.L = L1; ax.n_lo = n1; ax.n_hi = 0; ax.n_out = L1; ax.in_sa = inner; ax.in_cs = n1 * inner;
     ax.out_sa = 1; ax.out_cs = Gs; ax.sign = f.sign;
     const TC sc = static_cast<TC>(f.in_scale != nullptr ? *f.in_scale : 1.0);
-    PX::template run<TI, TC, TC, k2dThreads, TILX>(ax, static_cast<const C<TI>*>(f.in) + b, G, b0, b1, twx, n2, sc);
+    for (int y0 = 0; y0 < n2; y0 += TILX) {
+      if (y0) __syncthreads();
+      PX::template run<TI, TC, TC, k2dThreads, TILX>(ax, static_cast<const C<TI>*>(f.in) + y0 * n1 * inner + b,
+                                                     G + y0 * Gs, b0, b1, twx, min(TILX, n2 - y0), sc);
+    }
     __syncthreads();
     PassArgs ay;  // level 2: slots y (n2 non-zero rows), columns kx -> u_hat[ky][kx][b]
     ay.L = L2; ay.n_lo = n2; ay.n_hi = 0; ay.n_out = L2; ay.in_sa = Gs; ay.in_cs = 1;
     ay.out_sa = static_cast<int64_t>(L1) * inner; ay.out_cs = inner; ay.sign = f.sign;
-    PY::template run<TC, TC, TO, k2dThreads, TILY>(ay, G, static_cast<C<TO>*>(f.out) + b, b0, b1, twy, L1,
-                                                   static_cast<TC>(1));
+    for (int k0 = 0; k0 < L1; k0 += TILY) {
+      if (k0) __syncthreads();
+      PY::template run<TC, TC, TO, k2dThreads, TILY>(ay, G + k0, static_cast<C<TO>*>(f.out) + k0 * inner + b, b0,
+                                                     b1, twy, min(TILY, L1 - k0), static_cast<TC>(1));
+    }
   } else {
     PassArgs ay;  // inverse level 2 over all ky, keep y < n2 -> G[y][kx]
     ay.L = L2; ay.n_lo = L2; ay.n_hi = 0; ay.n_out = n2; ay.in_sa = static_cast<int64_t>(L1) * inner; ay.in_cs = inner;
     ay.out_sa = Gs; ay.out_cs = 1; ay.sign = f.sign;
-    PY::template run<TI, TC, TC, k2dThreads, TILY>(ay, static_cast<const C<TI>*>(f.in) + b, G, b0, b1, twy, L1,
-                                                   static_cast<TC>(1));
+    for (int k0 = 0; k0 < L1; k0 += TILY) {
+      if (k0) __syncthreads();
+      PY::template run<TI, TC, TC, k2dThreads, TILY>(ay, static_cast<const C<TI>*>(f.in) + k0 * inner + b, G + k0,
+                                                     b0, b1, twy, min(TILY, L1 - k0), static_cast<TC>(1));
+    }
     __syncthreads();
     PassArgs ax;  // inverse level 1, keep x < n1, 1/(l1 l2) -> v[y][x][b]
     ax.L = L1; ax.n_lo = L1; ax.n_hi = 0; ax.n_out = n1; ax.in_sa = 1; ax.in_cs = Gs; ax.out_sa = inner;
     ax.out_cs = n1 * inner; ax.sign = f.sign;
-    PX::template run<TC, TC, TO, k2dThreads, TILX>(ax, G, static_cast<C<TO>*>(f.out) + b, b0, b1, twx, n2,
-                                                   static_cast<TC>(1.0 / (static_cast<double>(L1) * L2)));
+    for (int y0 = 0; y0 < n2; y0 += TILX) {
+      if (y0) __syncthreads();
+      PX::template run<TC, TC, TO, k2dThreads, TILX>(ax, G + y0 * Gs, static_cast<C<TO>*>(f.out) + y0 * n1 * inner + b,
+                                                     b0, b1, twx, min(TILX, n2 - y0),
+                                                     static_cast<TC>(1.0 / (static_cast<double>(L1) * L2)));
+    }
   }
 }
 
@@ -399,6 +415,8 @@ template <typename TI, typename TC, typename TO>
 int fft2d_t(bool inverse, const Fft2dArgs& f, int l2, int l1, cudaStream_t s) {
   if (l2 == 60 && l1 == 60 && f.n2 <= 32) return launch2d<TI, TC, TO, 32, 64, Plan<4, 3, 5>, Plan<4, 3, 5>>(inverse, f, s);
   if (l2 == 32 && l1 == 32 && f.n2 <= 16) return launch2d<TI, TC, TO, 16, 32, Plan<4, 4, 2>, Plan<4, 4, 2>>(inverse, f, s);
+  // (a 128 x 128 variant with column tiles fits in shared memory but measured slower than the
+  // four-pass path at cfg4: 728 vs 693 us per matvec — one CTA per column serialises 12 tiles)
   return -1;
 }
 
