@@ -99,6 +99,11 @@ int zgemm_tc(int64_t m, int64_t n, int64_t k, double2 alpha, const void* a, int6
              const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, double2 beta, void* c, int64_t c_rs,
              int64_t c_cs, int64_t c_bs, int64_t batch, cudaStream_t s);
 
+// real FP64 tensor-core GEMM, all row-major, batched (zgemm_tc.cu)
+int dgemm_tc_rm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t lda, int64_t a_bs,
+                const double* b, int64_t ldb, int64_t b_bs, double beta, double* c, int64_t ldc, int64_t c_bs,
+                int64_t batch, cudaStream_t s);
+
 // batched transpose of complex matrices: out[b][c][r] = in[b][r][c]  (rows x cols)
 int transpose_batched(int dtype, const void* in, void* out, int64_t batch, int rows, int cols, cudaStream_t s);
 

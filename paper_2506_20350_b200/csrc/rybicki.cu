@@ -433,6 +433,67 @@ __global__ void gather_rows(const double2* __restrict__ B, double2* __restrict__
   }
 }
 
+// 3M complex products (Gauss): A B = (Ar Br - Ai Bi) + i ((Ar + Ai)(Br + Bi) - Ar Br - Ai Bi), three
+// real FP64 tensor-core GEMMs instead of the four real products of a complex GEMM.  Operands are
+// split into planes (re, im, re + im) with a common leading dimension.
+struct Planes {
+  double* re = nullptr;
+  double* im = nullptr;
+  double* sm = nullptr;
+  int64_t ld = 0;
+  Planes at(int64_t off) const { return Planes{re + off, im + off, sm + off, ld}; }
+};
+
+__global__ void k_split3(const double2* __restrict__ src, int64_t rows, int64_t cols, int64_t lds, Planes d) {
+  const int64_t total = rows * cols;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / cols, c = t - r * cols;
+    const double2 v = src[r * lds + c];
+    const int64_t o = r * d.ld + c;
+    d.re[o] = v.x;
+    d.im[o] = v.y;
+    d.sm[o] = v.x + v.y;
+  }
+}
+
+// C += sign * ((T1 - T2) + i (T3 - T1 - T2)),  C and T: rows x cols with leading dims ldc / ldt
+__global__ void k_combine3(Planes t, int64_t rows, int64_t cols, double2* __restrict__ c, int64_t ldc, double sign) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, q = i - r * cols;
+    const int64_t o = r * t.ld + q;
+    const double t1 = t.re[o], t2 = t.im[o], t3 = t.sm[o];
+    double2 v = c[r * ldc + q];
+    v.x += sign * (t1 - t2);
+    v.y += sign * (t3 - t1 - t2);
+    c[r * ldc + q] = v;
+  }
+}
+
+int split3(const double2* src, int64_t rows, int64_t cols, int64_t lds, const Planes& d, cudaStream_t st) {
+  const int grid = static_cast<int>(std::min<int64_t>((rows * cols + 255) / 256, 148 * 16));
+  k_split3<<<grid, 256, 0, st>>>(src, rows, cols, lds, d);
+  TOEP_LAUNCHED();
+  return TOEP_OK;
+}
+
+int combine3(const Planes& t, int64_t rows, int64_t cols, double2* c, int64_t ldc, double sign, cudaStream_t st) {
+  const int grid = static_cast<int>(std::min<int64_t>((rows * cols + 255) / 256, 148 * 16));
+  k_combine3<<<grid, 256, 0, st>>>(t, rows, cols, c, ldc, sign);
+  TOEP_LAUNCHED();
+  return TOEP_OK;
+}
+
+// T_p = A_p B_p for p in (re, im, sm), batched (row-major planes, batch strides in doubles)
+int gemm3(int64_t m, int64_t n, int64_t k, const Planes& a, int64_t a_bs, const Planes& b, int64_t b_bs,
+          const Planes& t, int64_t t_bs, int64_t batch, cudaStream_t st) {
+  TOEP_TRY(dgemm_tc_rm(m, n, k, 1.0, a.re, a.ld, a_bs, b.re, b.ld, b_bs, 0.0, t.re, t.ld, t_bs, batch, st));
+  TOEP_TRY(dgemm_tc_rm(m, n, k, 1.0, a.im, a.ld, a_bs, b.im, b.ld, b_bs, 0.0, t.im, t.ld, t_bs, batch, st));
+  return dgemm_tc_rm(m, n, k, 1.0, a.sm, a.ld, a_bs, b.sm, b.ld, b_bs, 0.0, t.sm, t.ld, t_bs, batch, st);
+}
+
 __global__ void copy_scaled(const double2* __restrict__ src, double2* __restrict__ dst, int64_t count, double s) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -583,6 +644,7 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
 
   double2 *g = nullptr, *h = nullptr, *gtmp = nullptr, *lu0 = nullptr, *lu12 = nullptr, *wide = nullptr;
   int *piv0 = nullptr, *piv12 = nullptr, *info = nullptr;
+  double *wplanes = nullptr, *scr = nullptr;  // 3M: planes of the wide blocks; per-stream B / T scratch
   // side stream: the block sums that do not depend on the step's LU factors run on it while the
   // (latency-bound, few-SM) cluster LU of D1/D2 runs on `st`
   cudaStream_t s2 = nullptr;
@@ -599,7 +661,7 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     if (ev_step != nullptr) cudaEventDestroy(ev_step);
     if (ev_sums != nullptr) cudaEventDestroy(ev_sums);
     for (void* q : {(void*)g, (void*)h, (void*)gtmp, (void*)lu0, (void*)lu12, (void*)wide, (void*)piv0, (void*)piv12,
-                    (void*)info})
+                    (void*)info, (void*)wplanes, (void*)scr})
       if (q) cudaFreeAsync(q, st);
     cudaStreamSynchronize(st);
   };
@@ -644,6 +706,27 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     }
   }
   double2 *Wp = wide, *Wpr = wide + wsz, *Wn = wide + 2 * wsz, *Wnr = wide + 3 * wsz;
+  // 3M products for the s x s block products (TOEP_RYB_3M=0: complex GEMMs)
+  static const bool use3m = [] {
+    const char* e = std::getenv("TOEP_RYB_3M");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  Planes wp[4];
+  Planes bsc[2], tsc[2];  // per stream (st, s2): B planes (N s x s) and T planes (N s x s)
+  if (use3m && N > 1) {
+    R_ALLOC(wplanes, 12 * wsz);
+    for (int q = 0; q < 4; ++q) {
+      wp[q] = Planes{wplanes + (3 * q) * wsz, wplanes + (3 * q + 1) * wsz, wplanes + (3 * q + 2) * wsz, wld};
+      R_TRY(split3(wide + q * wsz, s, wld, wld, wp[q], st));
+    }
+    const int64_t pl = static_cast<int64_t>(N) * ss;  // one plane
+    R_ALLOC(scr, 2 * 2 * 3 * pl);
+    for (int k = 0; k < 2; ++k) {
+      double* base = scr + static_cast<int64_t>(k) * 6 * pl;
+      bsc[k] = Planes{base, base + pl, base + 2 * pl, s};
+      tsc[k] = Planes{base + 3 * pl, base + 4 * pl, base + 5 * pl, s};
+    }
+  }
   double2 *lu1 = lu12, *lu2 = lu12 + ss;
   int *piv1 = piv12, *piv2 = piv12 + s;
   const double2 one = make_double2(1, 0), mone = make_double2(-1, 0);
@@ -667,6 +750,14 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   // C (+)= alpha * W[:, t0*s : (t0+m)*s] @ stack(m blocks of s x ncol), one GEMM of depth m*s
   auto wide_gemm = [&](const double2* W, int t0, int m, const double2* B, int64_t ncol, double2* C,
                        cudaStream_t sx) {
+    if (use3m && ncol == s) {  // G / H stacks: 3 real tensor-core GEMMs of depth m*s
+      const int k = sx == st ? 0 : 1;
+      const Planes& a = wp[(W - wide) / wsz];
+      TOEP_TRY(split3(B, static_cast<int64_t>(m) * s, s, s, bsc[k], sx));
+      TOEP_TRY(gemm3(s, s, static_cast<int64_t>(m) * s, a.at(static_cast<int64_t>(t0) * s), 0, bsc[k], 0, tsc[k], 0, 1,
+                     sx));
+      return combine3(tsc[k], s, s, C, s, 1.0, sx);
+    }
     return gemm_rm(s, ncol, static_cast<int64_t>(m) * s, one, W + static_cast<int64_t>(t0) * s, wld, B, ncol, one, C,
                    ncol, sx);
   };
@@ -678,6 +769,13 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   cudaStream_t ss2 = s2 != nullptr ? s2 : st;
   // C_b (+)= alpha * A_{m-1-b} @ B for b = 0..m-1 (A blocks s x s stacked, reversed), one batched GEMM
   auto rev_batched = [&](const double2* Astack, int m, const double2* B, int64_t ncol, double2* C, int64_t c_bs) {
+    if (use3m && ncol == s && c_bs == ss) {  // C stack -= reversed A stack x B, as 3 batched real GEMMs
+      TOEP_TRY(split3(Astack, static_cast<int64_t>(m) * s, s, s, bsc[0], st));       // A stack planes
+      const Planes bb = tsc[0].at(static_cast<int64_t>(m) * ss);                       // B planes after T
+      TOEP_TRY(split3(B, s, s, s, bb, st));
+      TOEP_TRY(gemm3(s, s, s, bsc[0].at(static_cast<int64_t>(m - 1) * ss), -ss, bb, 0, tsc[0], ss, m, st));
+      return combine3(tsc[0], static_cast<int64_t>(m) * s, s, C, s, -1.0, st);
+    }
     return gemm(TOEP_C128, s, ncol, s, mone, Astack + static_cast<int64_t>(m - 1) * ss, s, 1, -ss, B, ncol, 1, 0, one,
                 C, ncol, 1, c_bs, m, st);
   };
