@@ -19,7 +19,7 @@ namespace toep {
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kMinBlocks = 4;  // 128 regs/thread cap: several CTAs per SM, one wave for the matvec passes
+constexpr int kMinBlocks = 8;  // 64 regs/thread cap: 8 CTAs x 31 KB per SM keep enough loads in flight for the big passes
 constexpr int kMaxStages = 16;
 
 struct Radices {
