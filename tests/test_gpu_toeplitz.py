@@ -218,3 +218,19 @@ class TestBaselineConfigs:
         del op
         op32 = precompute_spectral(gen, dtype=torch.complex64)
         assert rel_err(matvec(op32, u)[::97], g["mv_sub"]) <= 1e-5
+
+
+@pytest.mark.parametrize("wcols", [1, 2, 4, 8, 16])
+def test_nb128_kernel_variants_vs_dense(wcols):
+    # N_b = 128 selects the streaming TMA product (W = 1), the SIMT column kernels (W <= 8) and the
+    # DMMA GEMM (W >= 16); transpose runs the row-dot kernel.  Small grid, dense reference.
+    rng = np.random.default_rng(40 + wcols)
+    gen = generator_from_stacked(seeded_stacked4(3, 2, 128, seed=wcols))
+    op = precompute_spectral(gen)
+    dense = assemble_dense(gen)
+    u = random_complex(rng, gen.dim, wcols)
+    assert rel_err(matvec(op, u), dense @ u) <= 1e-12
+    assert rel_err(matvec_transpose(op, u), dense.T @ u) <= 1e-12
+    op32 = precompute_spectral(gen, dtype=torch.complex64)
+    got = matvec(op32, u.astype(np.complex64))
+    assert rel_err(np.asarray(got, dtype=np.complex128), dense @ u.astype(np.complex64)) <= 1e-5
