@@ -454,6 +454,8 @@ struct OrthArgs {
   int force_cgs2;   // 1: always two Gram-Schmidt passes (TOEP_CGS2=1)
   double reorth_eta2;  // second pass when ||w'||^2 <= eta^2 ||w||^2
   int direct_norm;  // 1: h_{j+1,j} = ||w''|| from a third sweep + barrier (TOEP_DIRECT_NORM=1)
+  double2* gram;    // one-sweep CGS2: Gram matrix of the cycle's basis [ldr][ldr] (col-major), or null
+  double2* part2;   // [ldr][nblk] partials of V^H v_{m-1}
 };
 constexpr int kMaxOrthM = 1024;  // basis vectors per cycle handled by the cooperative kernel
 
@@ -518,6 +520,60 @@ __device__ __forceinline__ double orth_update(const OrthArgs& a, const double2* 
     nrm = fma(acc.x, acc.x, fma(acc.y, acc.y, nrm));
   }
   return nrm;
+}
+
+// One-sweep CGS2 dots: warp l computes both V_l^H w and V_l^H V_{m-1} over the chunk (the last
+// basis vector's Gram column), reading V_l once; warp NW-1 also accumulates ||w||^2
+__device__ __forceinline__ void orth_dots_gram(const OrthArgs& a, int64_t c0, int64_t c1) {
+  constexpr int NW = kCoopThreads / 32, U = 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nblk = gridDim.x;
+  const double2* vl = a.V + static_cast<int64_t>(a.m - 1) * a.N;
+  if (warp == NW - 1) {
+    double t = 0.0;
+    for (int64_t i = c0 + lane; i < c1; i += 32) {
+      const double2 v = a.w[i];
+      t = fma(v.x, v.x, fma(v.y, v.y, t));
+    }
+    t = warp_sum(t);
+    if (lane == 0) a.npart[blockIdx.x] = t;
+  }
+  for (int l = warp; l < a.m; l += NW) {
+    const double2* v = a.V + static_cast<int64_t>(l) * a.N;
+    double2 acc[U], acg[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = acg[u] = make_double2(0, 0);
+    int64_t i = c0 + lane;
+    for (; i + 32 * (U - 1) < c1; i += 32 * U) {
+      double2 vv[U], ww[U], ll[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        vv[u] = v[i + 32 * u];
+        ww[u] = a.w[i + 32 * u];
+        ll[u] = vl[i + 32 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        cfmac(acc[u], vv[u], ww[u]);
+        cfmac(acg[u], vv[u], ll[u]);
+      }
+    }
+    for (; i < c1; i += 32) {
+      cfmac(acc[0], v[i], a.w[i]);
+      cfmac(acg[0], v[i], vl[i]);
+    }
+#pragma unroll
+    for (int u = 1; u < U; ++u) {
+      acc[0] = cadd(acc[0], acc[u]);
+      acg[0] = cadd(acg[0], acg[u]);
+    }
+    const double2 s1 = warp_sum(acc[0]);
+    const double2 s2 = warp_sum(acg[0]);
+    if (lane == 0) {
+      a.part[static_cast<int64_t>(l) * nblk + blockIdx.x] = s1;
+      a.part2[static_cast<int64_t>(l) * nblk + blockIdx.x] = s2;
+    }
+  }
 }
 
 // one warp per basis vector: warp l sweeps the CTA's chunk of V_l and w with 8 independent
@@ -672,6 +728,114 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
     beta0 = a.st->beta0;
     k_step = a.st->total;
     nhist = a.st->nhist;
+  }
+  if (a.gram != nullptr) {
+    // ---- one-sweep CGS2 (Gram-matrix form): the second pass coefficients V^H w' = h1 - G h1 with
+    // G = V^H V, the basis Gram matrix, whose new column comes out of the same sweep as h1; then
+    // one update w'' = w - V (h1 + h2) and ||w''||^2 = ||w||^2 - 2 Re(h^H h1) + h^H G h.
+    // One grid barrier and two basis sweeps per step instead of three barriers and four sweeps.
+    orth_dots_gram(a, c0, c1);
+    grid_barrier(a.bar);
+    const int m = a.m, nblk = gridDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double2* h1s = osm + 4 * a.ldr;
+    double2* gcol = osm + 5 * a.ldr;
+    double2* gh = osm + 6 * a.ldr;
+    const double vlast = a.vs[m - 1];
+    for (int l = warp; l < m; l += kCoopThreads / 32) {
+      double2 s1 = make_double2(0, 0), s2 = make_double2(0, 0);
+      for (int b = lane; b < nblk; b += 32) {
+        s1 = cadd(s1, __ldcg(a.part + static_cast<int64_t>(l) * nblk + b));
+        s2 = cadd(s2, __ldcg(a.part2 + static_cast<int64_t>(l) * nblk + b));
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        h1s[l] = cscale(s1, a.vs[l]);
+        gcol[l] = cscale(s2, a.vs[l] * vlast);  // G[l][m-1]
+      }
+    }
+    __syncthreads();
+    auto G = [&](int l, int k) -> double2 {  // G[l][k], Hermitian; column m-1 from this step
+      if (k == m - 1) return gcol[l];
+      if (l == m - 1) return make_double2(gcol[k].x, -gcol[k].y);
+      return a.gram[static_cast<int64_t>(k) * a.ldr + l];
+    };
+    // h2 = h1 - G h1, h = h1 + h2; gh = G h (for the norm)
+    for (int l = warp; l < m; l += kCoopThreads / 32) {
+      double2 t = make_double2(0, 0);
+      for (int k = lane; k < m; k += 32) t = cadd(t, cmul(G(l, k), h1s[k]));
+      t = warp_sum(t);
+      if (lane == 0) {
+        const double2 h = csub(cscale(h1s[l], 2.0), t);
+        coef[l] = cscale(h, a.vs[l]);
+        hsm[l] = h;
+      }
+    }
+    __syncthreads();
+    // (G h)_l, then ||w''||^2 = ||w||^2 - 2 Re(h^H h1) + h^H G h -- every CTA evaluates it (same
+    // data, same order), so the precision test below is uniform across the grid
+    for (int l = warp; l < m; l += kCoopThreads / 32) {
+      double2 t = make_double2(0, 0);
+      for (int k = lane; k < m; k += 32) t = cadd(t, cmul(G(l, k), hsm[k]));
+      t = warp_sum(t);
+      if (lane == 0) gh[l] = t;
+    }
+    __shared__ double wn_s, hn2_g;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double wn = 0.0;
+      for (int b = threadIdx.x; b < nblk; b += 32) wn += __ldcg(a.npart + b);
+      double t = 0.0;
+      for (int l = threadIdx.x; l < m; l += 32)
+        t += -2.0 * (hsm[l].x * h1s[l].x + hsm[l].y * h1s[l].y) + (hsm[l].x * gh[l].x + hsm[l].y * gh[l].y);
+      wn = warp_sum(wn);
+      t = warp_sum(t);
+      if (threadIdx.x == 0) {
+        wn_s = wn;
+        hn2_g = wn + t;
+      }
+    }
+    __syncthreads();
+    // below ~1e-13 of ||w||^2 the formula is cancellation noise (e.g. a lucky breakdown): measure
+    // ||w''|| directly instead (third sweep + barrier)
+    const bool direct = !(hn2_g > 1e-13 * wn_s);
+    double2* hcol = a.rcols + static_cast<int64_t>(jcol) * a.ldr;
+    if (blockIdx.x == 0) {
+      for (int l = threadIdx.x; l < m; l += kCoopThreads) {  // keep the Gram matrix for later steps
+        a.gram[static_cast<int64_t>(m - 1) * a.ldr + l] = gcol[l];
+        a.gram[static_cast<int64_t>(l) * a.ldr + (m - 1)] = make_double2(gcol[l].x, -gcol[l].y);
+      }
+      orth_prepare_givens(a, jcol, hsm, snl, csl, hcol);
+      if (!direct && threadIdx.x == 0) {
+        givens_finish(a, jcol, hsm[jcol], hn2_g, g_j, beta0, nhist);
+        if (a.ts != nullptr) a.ts[2 * k_step + 3] = global_ns();
+      }
+    }
+    if (!direct) {
+      orth_update(a, coef, c0, c1);
+      return;
+    }
+    double nrm = orth_update(a, coef, c0, c1);
+    nrm = warp_sum(nrm);
+    if (lane == 0) red[warp] = nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = red[0];
+      for (int ww = 1; ww < kCoopThreads / 32; ++ww) t += red[ww];
+      a.npart[blockIdx.x] = t;
+    }
+    grid_barrier(a.bar);
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+      double hn2 = 0.0;
+      for (int b = threadIdx.x; b < nblk; b += 32) hn2 += __ldcg(a.npart + b);
+      hn2 = warp_sum(hn2);
+      if (threadIdx.x == 0) {
+        givens_finish(a, jcol, hsm[jcol], hn2, g_j, beta0, nhist);
+        if (a.ts != nullptr) a.ts[2 * k_step + 3] = global_ns();
+      }
+    }
+    return;
   }
   // pass 1: h1 = V^H w, plus ||w||^2
   __shared__ double hsq[kMaxOrthM];
@@ -1034,6 +1198,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   GState* st = nullptr;
   unsigned* bar = nullptr;  // grid barrier of k_orth_coop
   long long* ts = nullptr;  // device phase stamps (replace per-step events on the cooperative path)
+  double2* gram = nullptr;  // Gram matrix of the cycle's basis (one-sweep CGS2)
   HostRes& res = host_res();
   res.used = 0;
   HostFlags* hf = res.hf;
@@ -1042,7 +1207,8 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   auto cleanup = [&]() {
     for (void* q : {(void*)V, (void*)tmp, (void*)tmp2, (void*)pb, (void*)h1, (void*)rcols, (void*)sn, (void*)g,
                     (void*)y, (void*)part1, (void*)part2, (void*)cs, (void*)hist, (void*)vs, (void*)st,
-                    (void*)e.norm_partial, (void*)e.nred, (void*)e.hred, (void*)bar, (void*)ts})
+                    (void*)e.norm_partial, (void*)e.nred, (void*)e.hred, (void*)bar, (void*)ts,
+                    (void*)gram})
       if (q) cudaFreeAsync(q, s);
     cudaStreamSynchronize(s);
     res.used = 0;
@@ -1089,6 +1255,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   // single-kernel cooperative orthogonalisation when all CTAs fit co-resident
   G_ALLOC(bar, 2);
   G_ALLOC(ts, 2 * max_total + 4);
+  G_ALLOC(gram, (int64_t)ldr * ldr);
   TOEP_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s));
   const size_t coop_smem = std::max(sizeof(double2) * ldr * (1 + kCoopThreads / 32),
                                     (2 * sizeof(double2) + sizeof(double)) * ldr);
@@ -1125,6 +1292,11 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   // default: always two passes (CGS2), whose residual histories track the reference's MGS to
   // 1e-6; TOEP_REORTH_ETA2=<eta^2> selects the one-pass-unless-cancelled variant (measured: half
   // the orthogonalisation time at eta^2 = 1e-2, same iteration counts, histories drift ~1e-5)
+  // TOEP_ORTH=cgs2: the two-sweep-pair CGS2 kernel path (three barriers); default: one-sweep CGS2
+  static const bool gram_form = [] {
+    const char* e = std::getenv("TOEP_ORTH");
+    return !(e != nullptr && std::strcmp(e, "cgs2") == 0);
+  }();
   static const int direct_norm = [] {
     const char* e = std::getenv("TOEP_DIRECT_NORM");
     return e != nullptr && e[0] == '1' ? 1 : 0;
@@ -1259,7 +1431,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       if (use_coop) {
         OrthArgs oa{V, N, m, vs, w, part1, e.norm_partial, h1, st, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
                     static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev, orth_pf, force_cgs2, reorth_eta2,
-                    direct_norm};
+                    direct_norm, gram_form ? gram : nullptr, part2};
         rc = coop_attr ? launch_coop(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa,
                                      (const int*)stop_dev)
                        : launch_k(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa,
