@@ -14,6 +14,7 @@
 // contiguous columns of a row), partials [l][chunk][column] are reduced in fixed order.
 #include <chrono>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "launch.cuh"
@@ -62,6 +63,81 @@ __global__ void __launch_bounds__(kCols) kb_dots(const double2* const* __restric
 #pragma unroll
     for (int g = 0; g < kLG; ++g)
       if (l0 + g < m) partial[(static_cast<int64_t>(l0 + g) * nchunks + chunk) * W + c] = acc[g];
+  }
+}
+
+// One-sweep CGS2 (Gram-matrix form), per column: partial[l] = V_l^H w and partial2[l] =
+// V_l^H V_{m-1} (the newest basis vector's Gram column) in the same basis sweep
+constexpr int kLGG = 4;
+__global__ void __launch_bounds__(kCols) kb_dots_gram(const double2* const* __restrict__ Vp, int m,
+                                                      const double2* __restrict__ w, int64_t n, int W, int nchunks,
+                                                      double2* __restrict__ partial, double2* __restrict__ partial2) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.y * kCols + threadIdx.x;
+  if (c >= W) return;
+  const int chunk = blockIdx.x;
+  const int64_t r0 = rows_begin(chunk, nchunks, n), r1 = rows_begin(chunk + 1, nchunks, n);
+  const double2* vl = Vp[m - 1];
+  for (int l0 = 0; l0 < m; l0 += kLGG) {
+    double2 acc[kLGG], acg[kLGG];
+#pragma unroll
+    for (int g = 0; g < kLGG; ++g) acc[g] = acg[g] = make_double2(0, 0);
+    for (int64_t i = r0; i < r1; ++i) {
+      const double2 wi = w[i * W + c], li = vl[i * W + c];
+#pragma unroll
+      for (int g = 0; g < kLGG; ++g)
+        if (l0 + g < m) {
+          const double2 v = Vp[l0 + g][i * W + c];
+          cfmac(acc[g], v, wi);
+          cfmac(acg[g], v, li);
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < kLGG; ++g)
+      if (l0 + g < m) {
+        partial[(static_cast<int64_t>(l0 + g) * nchunks + chunk) * W + c] = acc[g];
+        partial2[(static_cast<int64_t>(l0 + g) * nchunks + chunk) * W + c] = acg[g];
+      }
+  }
+}
+
+// h1[l][c] = sum_chunk partial; Gram column G[l][m-1] = sum_chunk partial2 (stored with its conjugate
+// row; gram[(k*ldr + l)*W + c] = G[l][k])
+__global__ void kb_reduce_gram(const double2* __restrict__ partial, const double2* __restrict__ partial2, int m,
+                               int nchunks, int W, double2* __restrict__ h1, double2* __restrict__ gram, int ldr,
+                               const int* __restrict__ stop) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= static_cast<int64_t>(m) * W) return;
+  const int l = static_cast<int>(t / W), c = static_cast<int>(t - static_cast<int64_t>(l) * W);
+  if (stop[c]) return;
+  double2 s1 = make_double2(0, 0), s2 = make_double2(0, 0);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    s1 = cadd(s1, partial[(static_cast<int64_t>(l) * nchunks + ch) * W + c]);
+    s2 = cadd(s2, partial2[(static_cast<int64_t>(l) * nchunks + ch) * W + c]);
+  }
+  h1[static_cast<int64_t>(l) * W + c] = s1;
+  gram[(static_cast<int64_t>(m - 1) * ldr + l) * W + c] = s2;
+  gram[(static_cast<int64_t>(l) * ldr + (m - 1)) * W + c] = make_double2(s2.x, -s2.y);
+}
+
+// per column: h = h1 + (h1 - G h1) (the second CGS pass from the Gram matrix) -> h, Hessenberg column
+__global__ void kb_coef_gram(const double2* __restrict__ h1, const double2* __restrict__ gram, int m, int ldr, int W,
+                             double2* __restrict__ h, double2* __restrict__ hcol, const int* __restrict__ stop) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= W || stop[c]) return;
+  for (int l = 0; l < m; ++l) {
+    double2 t = make_double2(0, 0);
+    for (int k = 0; k < m; ++k)
+      cfma(t, gram[(static_cast<int64_t>(k) * ldr + l) * W + c], h1[static_cast<int64_t>(k) * W + c]);
+    const double2 a = h1[static_cast<int64_t>(l) * W + c];
+    const double2 hv = make_double2(2.0 * a.x - t.x, 2.0 * a.y - t.y);
+    h[static_cast<int64_t>(l) * W + c] = hv;
+    hcol[static_cast<int64_t>(l) * W + c] = hv;
   }
 }
 
@@ -375,6 +451,7 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
   std::vector<double2*> Vh;  // basis vectors, allocated as the cycle grows
   double2 *w = nullptr, *tmp = nullptr, *pb = nullptr, *h1 = nullptr, *h2 = nullptr, *rcols = nullptr;
   double2 *sn = nullptr, *g = nullptr, *y = nullptr, *part = nullptr;
+  double2 *part2 = nullptr, *gram = nullptr;  // one-sweep CGS2: Gram-column partials, per-column Gram matrices
   double *cs = nullptr, *hist = nullptr, *inv = nullptr, *npart = nullptr;
   double2** Vp = nullptr;
   int *ran = nullptr, *active = nullptr;
@@ -385,7 +462,7 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
     for (auto v : Vh) cudaFreeAsync(v, s);
     for (void* q : {(void*)w, (void*)tmp, (void*)pb, (void*)h1, (void*)h2, (void*)rcols, (void*)sn, (void*)g, (void*)y,
                     (void*)part, (void*)cs, (void*)hist, (void*)inv, (void*)npart, (void*)Vp, (void*)ran,
-                    (void*)active, (void*)st.beta0, (void*)st.stop, (void*)st.conv, (void*)st.brk, (void*)st.m,
+                    (void*)part2, (void*)gram, (void*)active, (void*)st.beta0, (void*)st.stop, (void*)st.conv, (void*)st.brk, (void*)st.m,
                     (void*)st.total, (void*)st.nhist})
       if (q) cudaFreeAsync(q, s);
     cudaStreamSynchronize(s);
@@ -412,6 +489,15 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
   B_ALLOC(pb, N);
   B_ALLOC(h1, static_cast<int64_t>(ldr) * W);
   B_ALLOC(h2, static_cast<int64_t>(ldr) * W);
+  // one-sweep CGS2 (Gram form) unless TOEP_BATCH_ORTH=cgs2
+  static const bool gram_form = [] {
+    const char* e = std::getenv("TOEP_BATCH_ORTH");
+    return !(e != nullptr && std::strcmp(e, "cgs2") == 0);
+  }();
+  if (gram_form) {
+    B_ALLOC(part2, static_cast<int64_t>(ldr) * nchunks * W);
+    B_ALLOC(gram, static_cast<int64_t>(ldr) * ldr * W);
+  }
   B_ALLOC(rcols, static_cast<int64_t>(cycle_len) * ldr * W);
   B_ALLOC(sn, static_cast<int64_t>(ldr) * W);
   B_ALLOC(cs, static_cast<int64_t>(ldr) * W);
@@ -504,15 +590,24 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
       } else {
         B_TRY(matvec_impl(p->op, Vh[j], w, W, false, io64, nullptr, s));
       }
+      const int rg = static_cast<int>((static_cast<int64_t>(m) * W + 255) / 256);
+      if (gram_form) {
+        B_TRY(launch_k(kb_dots_gram, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)w, n, W,
+                       nchunks, part, part2));
+        B_TRY(launch_k(kb_reduce_gram, dim3(rg), dim3(256), 0, s, (const double2*)part, (const double2*)part2, m,
+                       nchunks, W, h1, gram, ldr, (const int*)st.stop));
+        B_TRY(launch_k(kb_coef_gram, dim3(gc), dim3(128), 0, s, (const double2*)h1, (const double2*)gram, m, ldr, W,
+                       h2, rcols + static_cast<int64_t>(j) * ldr * W, (const int*)st.stop));
+      } else {
       B_TRY(launch_k(kb_dots, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)w, n, W,
                      nchunks, part));
-      const int rg = static_cast<int>((static_cast<int64_t>(m) * W + 255) / 256);
       B_TRY(launch_k(kb_reduce, dim3(rg), dim3(256), 0, s, (const double2*)part, m, nchunks, W, h1,
                      (const double2*)nullptr, (double2*)nullptr, 0, (const int*)st.stop));
       B_TRY(launch_k(kb_upd, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)h1, w, n,
                      W, nchunks, 1, part, (double*)nullptr, (const int*)st.stop));
       B_TRY(launch_k(kb_reduce, dim3(rg), dim3(256), 0, s, (const double2*)part, m, nchunks, W, h2,
                      (const double2*)h1, rcols + static_cast<int64_t>(j) * ldr * W, W, (const int*)st.stop));
+      }
       B_TRY(launch_k(kb_upd, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)h2, w, n,
                      W, nchunks, 2, (double2*)nullptr, npart, (const int*)st.stop));
       B_TRY(launch_k(kb_givens, dim3(gc), dim3(128), 0, s, st, (const double*)npart, nchunks, W, rcols, ldr, cs, sn, g,
