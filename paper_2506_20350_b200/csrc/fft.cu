@@ -207,7 +207,11 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
         else if (slot >= hi_start) row = a.n_lo + slot - hi_start;
         v[r] = mk<TC>(0, 0);
         if (row >= 0 && col < ncol) {
-          if (a.part_count == nullptr) {
+          if (a.in_planes != nullptr) {
+            const int64_t e = (gin - static_cast<const C<TI>*>(a.in)) + row * a.in_sa + col * a.in_cs;
+            const double t1 = a.in_planes[e], t2 = a.in_planes[a.plane + e], t3 = a.in_planes[2 * a.plane + e];
+            v[r] = mk<TC>(static_cast<TC>(t1 - t2), static_cast<TC>(t3 - t1 - t2));
+          } else if (a.part_count == nullptr) {
             v[r] = cvt<Z>(gin[row * a.in_sa + col * a.in_cs]);
           } else {
             const int np = a.part_count[row];
@@ -232,7 +236,17 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
 #pragma unroll
         for (int q = 0; q < R; ++q) {
           const int idx = base + q * Ns;
-          if (idx < a.n_out) gout[idx * a.out_sa + col * a.out_cs] = cvt<C<TO>>(cscale(v[q], scale));
+          if (idx < a.n_out) {
+            if (a.out_planes != nullptr) {
+              const int64_t e = (gout - static_cast<C<TO>*>(a.out)) + idx * a.out_sa + col * a.out_cs;
+              const Z val = cscale(v[q], scale);
+              a.out_planes[e] = static_cast<double>(val.x);
+              a.out_planes[a.plane + e] = static_cast<double>(val.y);
+              a.out_planes[2 * a.plane + e] = static_cast<double>(val.x) + static_cast<double>(val.y);
+            } else {
+              gout[idx * a.out_sa + col * a.out_cs] = cvt<C<TO>>(cscale(v[q], scale));
+            }
+          }
         }
       }
     }
@@ -537,6 +551,8 @@ int launch(const PassArgs& a, const Radices& rad, bool direct, cudaStream_t s) {
     const int rc = try_plan<TI, TC, TO>(a, s);
     if (rc >= 0) return rc;
   }
+  TOEP_REQUIRE(a.in_planes == nullptr && a.out_planes == nullptr, TOEP_ERR_ARG,
+               "split-plane I/O needs a compiled pass plan (L=%d)", a.L);
   const size_t es = sizeof(C<TC>);
   const int nbuf = direct ? 1 : 2;
   int til = 32;
@@ -608,6 +624,10 @@ int fft2d(bool inverse, const void* in, void* out, int n2, int n1, int l2, int l
     case 3: return fft2d_t<double, float, float>(inverse, f, l2, l1, s);
     default: return -1;
   }
+}
+
+bool fft_plan_has_planes(int L, int64_t inner) {
+  return (L == 60 && inner >= 16) || (L == 128 && inner >= 8) || (L == 32 && inner >= 32) || (L == 64 && inner >= 16);
 }
 
 int fft_pass(const PassArgs& a, int tin, int tcomp, int tout, cudaStream_t s) {

@@ -37,6 +37,13 @@ struct PassArgs {
   int64_t part_stride = 0;
   // stride of the batch ("column") index; 1 = contiguous batch (all standalone passes)
   int64_t in_cs = 1, out_cs = 1;
+  // optional split-plane I/O (3M products of the multi-RHS path): out_planes receives (re, im,
+  // re+im) planes `plane` doubles apart instead of the complex output; in_planes supplies
+  // (T1, T2, T3) planes combined into (T1 - T2) + i (T3 - T1 - T2).  Element indexing as for the
+  // complex arrays (`in` / `out` must still be set: they anchor the element offsets).
+  double* out_planes = nullptr;
+  const double* in_planes = nullptr;
+  int64_t plane = 0;
 };
 
 // Whole 2-D transforms of the single-RHS matvec in one kernel each (one CTA per batch column,
@@ -98,6 +105,12 @@ int gemm(int dtype, int64_t m, int64_t n, int64_t k, double2 alpha, const void* 
 int zgemm_tc(int64_t m, int64_t n, int64_t k, double2 alpha, const void* a, int64_t a_rs, int64_t a_cs, int64_t a_bs,
              const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, double2 beta, void* c, int64_t c_rs,
              int64_t c_cs, int64_t c_bs, int64_t batch, cudaStream_t s);
+
+// real FP64 tensor-core GEMM, A column-major, B / C row-major, batched (zgemm_tc.cu)
+int dgemm_tc_crr(int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, int64_t a_bs, const double* b,
+                 int64_t ldb, int64_t b_bs, double* c, int64_t ldc, int64_t c_bs, int64_t batch, cudaStream_t s);
+// true when the compiled pass plan for length L supports split-plane I/O
+bool fft_plan_has_planes(int L, int64_t inner);
 
 // real FP64 tensor-core GEMM, all row-major, batched (zgemm_tc.cu)
 int dgemm_tc_rm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t lda, int64_t a_bs,

@@ -48,28 +48,106 @@ void keep_pool() {
   done_dev = dev;
 }
 
-int op_workspace(toep_op_s* op, int64_t w, cudaStream_t s, toep_op_s::Workspace** out) {
+int op_workspace(toep_op_s* op, int64_t w, cudaStream_t s, toep_op_s::Workspace** out, bool need_hat) {
   keep_pool();
   std::lock_guard<std::mutex> lock(op->mu);
   auto& ws = op->ws[s];
+  const size_t es = elt_size(op->dtype);
   if (ws.w_cap < w) {
-    const size_t es = elt_size(op->dtype);
     if (ws.x1) TOEP_CUDA(cudaFreeAsync(ws.x1, s));
-    if (ws.hat) TOEP_CUDA(cudaFreeAsync(ws.hat, s));
-    if (ws.hat2) TOEP_CUDA(cudaFreeAsync(ws.hat2, s));
-    ws.x1 = ws.hat = ws.hat2 = nullptr;
+    ws.x1 = nullptr;
     ws.w_cap = 0;
     const size_t nx1 = static_cast<size_t>(op->n2) * op->l1 * op->n0 * w * es;
-    const size_t nhat = static_cast<size_t>(op->K) * op->n0 * w * es;
-    if (cudaMallocAsync(&ws.x1, nx1, s) != cudaSuccess || cudaMallocAsync(&ws.hat, nhat, s) != cudaSuccess ||
-        cudaMallocAsync(&ws.hat2, nhat, s) != cudaSuccess) {
+    if (cudaMallocAsync(&ws.x1, nx1, s) != cudaSuccess) {
       cudaGetLastError();
       set_error("out of device memory for matvec workspace (w=%lld)", static_cast<long long>(w));
       return TOEP_ERR_OOM;
     }
     ws.w_cap = w;
   }
+  if (need_hat && ws.hat_cap < w) {  // complex spectral buffers (not used by the 3M multi-RHS path)
+    if (ws.hat) TOEP_CUDA(cudaFreeAsync(ws.hat, s));
+    if (ws.hat2) TOEP_CUDA(cudaFreeAsync(ws.hat2, s));
+    ws.hat = ws.hat2 = nullptr;
+    ws.hat_cap = 0;
+    const size_t nhat = static_cast<size_t>(op->K) * op->n0 * w * es;
+    if (cudaMallocAsync(&ws.hat, nhat, s) != cudaSuccess || cudaMallocAsync(&ws.hat2, nhat, s) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("out of device memory for matvec workspace (w=%lld)", static_cast<long long>(w));
+      return TOEP_ERR_OOM;
+    }
+    ws.hat_cap = w;
+  }
   *out = &ws;
+  return TOEP_OK;
+}
+
+// DT (bins ky-major, k = ky*l1 + kx) -> three planes with bins kx-major (kx*l2 + ky), so the bins
+// of a kx-chunk are contiguous
+__global__ void k_split_planes(const double2* __restrict__ src, int64_t count, int l2, int l1, int64_t bsz,
+                               double* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t k = i / bsz, e = i - k * bsz;
+    const int64_t ky = k / l1, kx = k - ky * l1;
+    const int64_t o = (kx * l2 + ky) * bsz + e;
+    const double2 v = src[i];
+    dst[o] = v.x;
+    dst[count + o] = v.y;
+    dst[2 * count + o] = v.x + v.y;
+  }
+}
+
+// kx columns per chunk of the 3M multi-RHS path: planes of one chunk stay under ~4 GB per buffer
+int mrhs_chunk(const toep_op_s* op, int64_t w) {
+  const int64_t per_kx = static_cast<int64_t>(op->l2) * op->n0 * w * 3 * static_cast<int64_t>(sizeof(double));
+  const int64_t budget = int64_t{4} << 30;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(op->l1, budget / std::max<int64_t>(per_kx, 1))));
+}
+
+// Multi-RHS per-bin products as 3M (Gauss): V = D U with three real FP64 tensor-core GEMMs on split
+// planes, T1 = Dr Ur, T2 = Di Ui, T3 = (Dr + Di)(Ur + Ui); the level-2 DFT passes write / read the
+// planes directly, so the split and the recombination cost no extra pass.  Enabled for c128,
+// W >= 16 and a compiled level-2 plan (TOEP_MRHS_3M=0: complex GEMMs).
+bool mrhs_3m(const toep_op_s* op, int64_t w, bool transpose) {
+  static const bool on = [] {
+    const char* e = std::getenv("TOEP_MRHS_3M");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on && !transpose && w >= 16 && op->dtype == TOEP_C128 && op->slab_kxs == 0 &&
+         fft_plan_has_planes(op->l2, static_cast<int64_t>(op->n0) * w);
+}
+
+int ensure_planes(toep_op_s* op, toep_op_s::Workspace* ws, int64_t w, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(op->mu);
+  const int64_t kn = op->K * op->n0;
+  if (op->DTp == nullptr) {
+    const int64_t cnt = kn * op->n0;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&op->DTp), 3 * cnt * sizeof(double), s) != cudaSuccess) {
+      cudaGetLastError();
+      op->DTp = nullptr;
+      set_error("out of device memory for the 3M operator planes");
+      return TOEP_ERR_OOM;
+    }
+    const int grid = static_cast<int>(std::min<int64_t>((cnt + 255) / 256, 148 * 16));
+    k_split_planes<<<grid, 256, 0, s>>>(static_cast<const double2*>(op->DT), cnt, op->l2, op->l1,
+                                        static_cast<int64_t>(op->n0) * op->n0, op->DTp);
+    TOEP_LAUNCHED();
+  }
+  if (ws->p_cap < w) {
+    if (ws->hatp) TOEP_CUDA(cudaFreeAsync(ws->hatp, s));
+    if (ws->hat2p) TOEP_CUDA(cudaFreeAsync(ws->hat2p, s));
+    ws->hatp = ws->hat2p = nullptr;
+    ws->p_cap = 0;
+    const size_t bytes = 3 * static_cast<size_t>(op->l2) * mrhs_chunk(op, w) * op->n0 * w * sizeof(double);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&ws->hatp), bytes, s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&ws->hat2p), bytes, s) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("out of device memory for the 3M workspace (w=%lld)", static_cast<long long>(w));
+      return TOEP_ERR_OOM;
+    }
+    ws->p_cap = w;
+  }
   return TOEP_OK;
 }
 
@@ -77,7 +155,8 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
                 cudaStream_t s, const double* in_scale) {
   if (w == 0) return TOEP_OK;
   toep_op_s::Workspace* ws = nullptr;
-  TOEP_TRY(op_workspace(op, w, s, &ws));
+  const bool planar = mrhs_3m(op, w, transpose);
+  TOEP_TRY(op_workspace(op, w, s, &ws, !planar));
   const int tc = op->dtype == TOEP_C64 ? 1 : 0;
   const int tio = io_c128 ? 0 : tc;
   const int64_t inner = static_cast<int64_t>(op->n0) * w;
@@ -141,19 +220,51 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
   a.out_so = op->l1 * inner; a.sign = s1; a.scale = sc1x; a.stop = stop; a.in_scale = in_scale;
   TOEP_TRY(fft_pass(a, tio, tc, tc, s));
 
-  PassArgs b;  // level-2 (y) pass over the n2 non-zero rows: x1 -> hat [l2][l1][inner]
-  b.in = ws->x1; b.out = ws->hat; b.L = op->l2; b.n_lo = op->n2; b.n_hi = 0; b.n_out = op->l2;
-  b.inner = inner; b.outer = op->l1; b.in_sa = op->l1 * inner; b.in_so = inner; b.out_sa = op->l1 * inner;
-  b.out_so = inner; b.sign = s1; b.scale = sc1y; b.stop = stop;
-  TOEP_TRY(fft_pass(b, tc, tc, tc, s));
+  if (planar) {
+    // 3M in kx-chunks: level-2 DFT of the chunk's columns into split planes (bins kx-major within
+    // the chunk), three real batched GEMMs against the operator planes, inverse level-2 DFT
+    // recombining (T1 - T2) + i (T3 - T1 - T2) into x1
+    TOEP_TRY(ensure_planes(op, ws, w, s));
+    const int kc = mrhs_chunk(op, w);
+    const int64_t n0 = op->n0, nw = n0 * w, dn = op->K * n0 * n0;
+    const int64_t plane = static_cast<int64_t>(op->l2) * kc * nw;  // doubles per plane (one chunk)
+    for (int kx0 = 0; kx0 < op->l1; kx0 += kc) {
+      const int cnt = std::min(kc, op->l1 - kx0);
+      PassArgs b;  // level 2 over rows y < n2 of columns [kx0, kx0+cnt): out (kx_local, ky, inner)
+      b.in = static_cast<const char*>(ws->x1) + kx0 * inner * elt_size(op->dtype);
+      b.out = ws->hatp; b.L = op->l2; b.n_lo = op->n2; b.n_hi = 0; b.n_out = op->l2;
+      b.inner = inner; b.outer = cnt; b.in_sa = op->l1 * inner; b.in_so = inner; b.out_sa = inner;
+      b.out_so = op->l2 * inner; b.sign = s1; b.scale = sc1y; b.stop = stop;
+      b.out_planes = ws->hatp; b.plane = plane;
+      TOEP_TRY(fft_pass(b, tc, tc, tc, s));
+      const int64_t bins = static_cast<int64_t>(cnt) * op->l2;
+      const int64_t dofs = static_cast<int64_t>(kx0) * op->l2 * n0 * n0;
+      for (int q = 0; q < 3; ++q)
+        TOEP_TRY(dgemm_tc_crr(n0, w, n0, op->DTp + q * dn + dofs, n0, n0 * n0, ws->hatp + q * plane, w, nw,
+                              ws->hat2p + q * plane, w, nw, bins, s));
+      PassArgs c;  // inverse level 2, keep rows y < n2 -> x1 columns [kx0, kx0+cnt)
+      c.in = ws->hat2p; c.out = static_cast<char*>(ws->x1) + kx0 * inner * elt_size(op->dtype);
+      c.L = op->l2; c.n_lo = op->l2; c.n_hi = 0; c.n_out = op->n2;
+      c.inner = inner; c.outer = cnt; c.in_sa = inner; c.in_so = op->l2 * inner; c.out_sa = op->l1 * inner;
+      c.out_so = inner; c.sign = -s1; c.scale = sc2y; c.stop = stop;
+      c.in_planes = ws->hat2p; c.plane = plane;
+      TOEP_TRY(fft_pass(c, tc, tc, tc, s));
+    }
+  } else {
+    PassArgs b;  // level-2 (y) pass over the n2 non-zero rows: x1 -> hat [l2][l1][inner]
+    b.in = ws->x1; b.out = ws->hat; b.L = op->l2; b.n_lo = op->n2; b.n_hi = 0; b.n_out = op->l2;
+    b.inner = inner; b.outer = op->l1; b.in_sa = op->l1 * inner; b.in_so = inner; b.out_sa = op->l1 * inner;
+    b.out_so = inner; b.sign = s1; b.scale = sc1y; b.stop = stop;
+    TOEP_TRY(fft_pass(b, tc, tc, tc, s));
 
-  TOEP_TRY(bin_product(op->dtype, op->DT, ws->hat, ws->hat2, op->K, op->n0, w, transpose, stop, s));
+    TOEP_TRY(bin_product(op->dtype, op->DT, ws->hat, ws->hat2, op->K, op->n0, w, transpose, stop, s));
 
-  PassArgs c;  // inverse level-2 pass, keep the n2 payload rows: hat2 -> x1 [n2][l1][inner]
-  c.in = ws->hat2; c.out = ws->x1; c.L = op->l2; c.n_lo = op->l2; c.n_hi = 0; c.n_out = op->n2;
-  c.inner = inner; c.outer = op->l1; c.in_sa = op->l1 * inner; c.in_so = inner; c.out_sa = op->l1 * inner;
-  c.out_so = inner; c.sign = -s1; c.scale = sc2y; c.stop = stop;
-  TOEP_TRY(fft_pass(c, tc, tc, tc, s));
+    PassArgs c;  // inverse level-2 pass, keep the n2 payload rows: hat2 -> x1 [n2][l1][inner]
+    c.in = ws->hat2; c.out = ws->x1; c.L = op->l2; c.n_lo = op->l2; c.n_hi = 0; c.n_out = op->n2;
+    c.inner = inner; c.outer = op->l1; c.in_sa = op->l1 * inner; c.in_so = inner; c.out_sa = op->l1 * inner;
+    c.out_so = inner; c.sign = -s1; c.scale = sc2y; c.stop = stop;
+    TOEP_TRY(fft_pass(c, tc, tc, tc, s));
+  }
 
   PassArgs d;  // inverse level-1 pass + extract_result crop: x1 -> v [n2][n1][inner]
   d.in = ws->x1; d.out = v; d.L = op->l1; d.n_lo = op->l1; d.n_hi = 0; d.n_out = op->n1;
@@ -298,8 +409,11 @@ int toep_op_destroy(toep_op_t op) {
     cudaFree(kv.second.hat2);
     cudaFree(kv.second.parts);
     cudaFree(kv.second.cnt);
+    cudaFree(kv.second.hatp);
+    cudaFree(kv.second.hat2p);
   }
   cudaFree(op->DT);
+  cudaFree(op->DTp);
   cudaFree(op->part_count);
   delete op;
   TOEP_LAUNCHED();

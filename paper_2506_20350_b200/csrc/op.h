@@ -10,14 +10,19 @@ struct toep_op_s {
   int n2 = 0, n1 = 0, n0 = 0, l2 = 0, l1 = 0, dtype = TOEP_C128;
   int64_t K = 0;
   void* DT = nullptr;  // [K][n0][n0], DT[k][j][m] = D_k[m][j]
+  double* DTp = nullptr;  // multi-RHS 3M: (re, im, re+im) planes of DT, K*n0*n0 doubles apart
   int device = 0;
   struct Workspace {
-    int64_t w_cap = 0;
+    int64_t w_cap = 0;    // x1
+    int64_t hat_cap = 0;  // hat / hat2
     void* x1 = nullptr;    // [n2][l1][n0*w]
     void* hat = nullptr;   // [K][n0][w]
     void* hat2 = nullptr;  // [K][n0][w]
     void* parts = nullptr; // fused path: [l1][maxp][n2][n0] inverse level-2 partial slabs
     int* cnt = nullptr;    // fused path: [l1] slab arrival counters
+    double* hatp = nullptr;   // multi-RHS 3M: planes of u_hat (3 x K*n0*w)
+    double* hat2p = nullptr;  // multi-RHS 3M: product planes T1, T2, T3
+    int64_t p_cap = 0;
   };
   // kx-slab operator of the multi-GPU row/slab decomposition (toep_op_slab): bins
   // k' = ky*slab_kxs + (kx - slab_k0); 0 = full operator
@@ -34,7 +39,7 @@ namespace toep {
 
 size_t elt_size(int dtype);
 int64_t op_dim(const toep_op_s* op);
-int op_workspace(toep_op_s* op, int64_t w, cudaStream_t s, toep_op_s::Workspace** out);
+int op_workspace(toep_op_s* op, int64_t w, cudaStream_t s, toep_op_s::Workspace** out, bool need_hat = true);
 
 // matvec with optional device-side stop flag (GMRES speculative steps).
 // io_c128: u / v are complex128 while the operator computes in its own dtype.

@@ -36,6 +36,13 @@ using DGemmRM = cutlass::gemm::device::GemmUniversal<
     cutlass::epilogue::thread::LinearCombination<double, 1, double, double>,
     cutlass::gemm::threadblock::GemmIdentityThreadblockSwizzle<>, 3>;
 
+using DGemmCRR = cutlass::gemm::device::GemmUniversal<
+    double, cutlass::layout::ColumnMajor, double, cutlass::layout::RowMajor, double, cutlass::layout::RowMajor,
+    double, cutlass::arch::OpClassTensorOp, cutlass::arch::Sm80, cutlass::gemm::GemmShape<64, 64, 16>,
+    cutlass::gemm::GemmShape<32, 32, 16>, cutlass::gemm::GemmShape<8, 8, 4>,
+    cutlass::epilogue::thread::LinearCombination<double, 1, double, double>,
+    cutlass::gemm::threadblock::GemmIdentityThreadblockSwizzle<>, 3>;
+
 template <typename G>
 int run(int64_t m, int64_t n, int64_t k, double2 alpha, const void* a, int64_t lda, int64_t a_bs, const void* b,
         int64_t ldb, int64_t b_bs, double2 beta, void* c, int64_t ldc, int64_t c_bs, int64_t batch, cudaStream_t s) {
@@ -72,6 +79,31 @@ int dgemm_tc_rm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, 
                                    static_cast<int>(batch), {alpha, beta}, a, b, c, c, a_bs, b_bs, c_bs, c_bs, lda, ldb,
                                    ldc, ldc);
   DGemmRM op;
+  cutlass::Status st = op.can_implement(args);
+  if (st != cutlass::Status::kSuccess) {
+    set_error("dgemm_tc: cannot implement (%s)", cutlassGetStatusString(st));
+    return TOEP_ERR_ARG;
+  }
+  st = op.initialize(args, nullptr, s);
+  if (st == cutlass::Status::kSuccess) st = op.run(s);
+  if (st != cutlass::Status::kSuccess) {
+    set_error("dgemm_tc: %s", cutlassGetStatusString(st));
+    return TOEP_ERR_CUDA;
+  }
+  TOEP_LAUNCHED();
+  return TOEP_OK;
+}
+
+int dgemm_tc_crr(int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, int64_t a_bs, const double* b,
+                 int64_t ldb, int64_t b_bs, double* c, int64_t ldc, int64_t c_bs, int64_t batch, cudaStream_t s) {
+  if (m == 0 || n == 0 || batch == 0) return TOEP_OK;
+  TOEP_REQUIRE(m <= INT32_MAX && n <= INT32_MAX && k <= INT32_MAX && batch <= INT32_MAX, TOEP_ERR_ARG,
+               "dgemm_tc: size too large");
+  typename DGemmCRR::Arguments args(cutlass::gemm::GemmUniversalMode::kBatched,
+                                    {static_cast<int>(m), static_cast<int>(n), static_cast<int>(k)},
+                                    static_cast<int>(batch), {1.0, 0.0}, a, b, c, c, a_bs, b_bs, c_bs, c_bs, lda, ldb,
+                                    ldc, ldc);
+  DGemmCRR op;
   cutlass::Status st = op.can_implement(args);
   if (st != cutlass::Status::kSuccess) {
     set_error("dgemm_tc: cannot implement (%s)", cutlassGetStatusString(st));
