@@ -173,8 +173,11 @@ size_t panel_smem(int n, int j0) { return 2 * sizeof(int) * static_cast<size_t>(
 // Panel rows live in registers, each row split over kTPR adjacent lanes (kCPT columns each):
 // thread t of CTA r owns columns (t % kTPR)*kCPT .. +kCPT of physical rows
 // r*rpc + t / kTPR + q*kRowsPass, q < RPT.
-constexpr int kPanelThr2 = 512;
-constexpr int kTPR = 4;
+#ifndef TOEP_PANEL_TPR
+#define TOEP_PANEL_TPR 2  // lanes per panel row (measured: 2 -> 105 us, 4 -> 121 us, 8 -> 134 us per 1024-row panel)
+#endif
+constexpr int kTPR = TOEP_PANEL_TPR;
+constexpr int kPanelThr2 = 128 * kTPR;
 constexpr int kCPT = kPW / kTPR;                 // 8 columns per thread
 constexpr int kRowsPass = kPanelThr2 / kTPR;     // 128 rows per pass
 
