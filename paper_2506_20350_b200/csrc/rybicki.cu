@@ -134,7 +134,10 @@ void trsm(const double2* LU, int lda, double2* X, int64_t ldx, int r0, int nb, i
 // memory (DSMEM) and each thread eliminates the rows it owns.  The row interchanges are tracked as
 // a permutation (LAPACK ipiv semantics) and applied once, at write-back; `moves` receives the
 // (destination, source) row pairs so the other columns can be permuted by swap_trsm.
-constexpr int kCL = 8;
+#ifndef TOEP_PANEL_CL
+#define TOEP_PANEL_CL 8
+#endif
+constexpr int kCL = TOEP_PANEL_CL;
 constexpr int kPW = 32;
 constexpr int kMovesStride = 1 + 4 * kPW;  // count + up to 2*kPW (dst, src) pairs
 
