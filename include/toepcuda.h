@@ -106,6 +106,36 @@ TOEP_API int toep_op_slab(toep_op_t op, int kx0, int kx1, void* stream, toep_op_
 TOEP_API int toep_matvec_stage(toep_op_t op, int stage, const void* in, void* out, int64_t w, int count,
                                void* stream);
 
+/* Peer-memory exchange (NVLink P2P through CUDA IPC): stages 0 and 1 of toep_matvec_stage with
+ * their output stored straight into the destination ranks' receive buffers, so the all-to-all
+ * that follows each of them is fused into the DFT's final store.  Output index a of the pass
+ * (stage 0: level-1 frequency kx; stage 1: array row y) in [lo[q], lo[q+1]) is written to
+ *   base[q] + es * (off[q] + a*sa[q] + o*so[q] + i)     (o: the pass's outer index, i: n0*w index)
+ * and after its last store every launch adds 1 to each destination's arrival counter
+ * (release, system scope).  `scatter` is a DEVICE copy of the table; `done` must start at 0 and
+ * is owned by the kernel.  toep_peer_wait blocks the stream until *counter >= target (acquire,
+ * system scope; traps after 30 s so a missing peer fails loudly instead of hanging). */
+#define TOEP_MAX_PEERS 8
+typedef struct toep_peer_scatter {
+  int64_t parts;                     /* destinations, 1..TOEP_MAX_PEERS */
+  int64_t lo[TOEP_MAX_PEERS + 1];
+  uint64_t base[TOEP_MAX_PEERS];     /* device (peer-mapped) address of destination q's buffer */
+  int64_t off[TOEP_MAX_PEERS];
+  int64_t sa[TOEP_MAX_PEERS];
+  int64_t so[TOEP_MAX_PEERS];
+  uint64_t signal[TOEP_MAX_PEERS];   /* device address of destination q's u64 arrival counter */
+  uint64_t done;                     /* CTA completion count of the running launch */
+} toep_peer_scatter;
+TOEP_API int toep_matvec_stage_peer(toep_op_t op, int stage, const void* in, const toep_peer_scatter* scatter,
+                                    int64_t w, int count, void* stream);
+TOEP_API int toep_peer_wait(const uint64_t* counter, uint64_t target, void* stream);
+/* cudaMalloc'd (not pool) memory for exchange buffers, and its IPC handle (64 bytes) / mapping */
+TOEP_API int toep_peer_alloc(uint64_t bytes, void** out);
+TOEP_API int toep_peer_free(void* ptr);
+TOEP_API int toep_ipc_handle(const void* ptr, void* handle64);
+TOEP_API int toep_ipc_open(const void* handle64, void** out);
+TOEP_API int toep_ipc_close(void* ptr);
+
 /* toeplitz.py:300 (flags & TOEP_MV_TRANSPOSE: :320): the per-bin product alone,
  * hat_out[k] = D_k @ hat_in[k] for every bin k, hat_* (bins, n0, w) in the
  * operator dtype.  This is the streaming kernel that carries >98% of the

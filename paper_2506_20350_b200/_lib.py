@@ -55,6 +55,16 @@ class OpInfo(ctypes.Structure):
                 ("bins", c_i64), ("dim", c_i64), ("resident_bytes", c_i64)]
 
 
+MAX_PEERS = 8
+
+
+class PeerScatter(ctypes.Structure):
+    """toep_peer_scatter (include/toepcuda.h): output-row routing table of a peer-scatter pass."""
+    _fields_ = [("parts", c_i64), ("lo", c_i64 * (MAX_PEERS + 1)), ("base", ctypes.c_uint64 * MAX_PEERS),
+                ("off", c_i64 * MAX_PEERS), ("sa", c_i64 * MAX_PEERS), ("so", c_i64 * MAX_PEERS),
+                ("signal", ctypes.c_uint64 * MAX_PEERS), ("done", ctypes.c_uint64)]
+
+
 class GmresProblem(ctypes.Structure):
     _fields_ = [("op", c_vp), ("apply", APPLY_FN), ("apply_ctx", c_vp), ("precond", c_i32), ("pside", c_i32),
                 ("pinv", c_vp), ("pmat", c_vp), ("papply", APPLY_FN), ("papply_ctx", c_vp),
@@ -84,6 +94,13 @@ SIGNATURES = {
     "toep_matvec": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
     "toep_op_slab": (c_int, [c_vp, c_int, c_int, c_vp, ctypes.POINTER(c_vp)]),
     "toep_matvec_stage": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_int, c_vp]),
+    "toep_matvec_stage_peer": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_int, c_vp]),
+    "toep_peer_wait": (c_int, [c_vp, ctypes.c_uint64, c_vp]),
+    "toep_peer_alloc": (c_int, [ctypes.c_uint64, ctypes.POINTER(c_vp)]),
+    "toep_peer_free": (c_int, [c_vp]),
+    "toep_ipc_handle": (c_int, [c_vp, c_vp]),
+    "toep_ipc_open": (c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "toep_ipc_close": (c_int, [c_vp]),
     "toep_op_spectral_apply": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
     "toep_block_dft": (c_int, [c_vp, c_vp, c_int, c_int, c_i64, c_int, c_int, c_vp]),
     "toep_block_apply": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_i64, c_int, c_vp]),

@@ -20,6 +20,7 @@ namespace {
 
 constexpr int kThreads = 128;
 constexpr int kMinBlocks = 8;  // 64 regs/thread cap: 8 CTAs x 31 KB per SM keep enough loads in flight for the big passes
+constexpr int kMinBlocksGeneric = 4;  // runtime-radix pass: the generic butterflies need >64 regs (spilled ~700 B at 8)
 constexpr int kMaxStages = 16;
 
 struct Radices {
@@ -434,8 +435,24 @@ int fft2d_t(bool inverse, const Fft2dArgs& f, int l2, int l1, cudaStream_t s) {
   return -1;
 }
 
+// Completion signal of a peer-scatter launch: every CTA counts itself in (acq_rel, system
+// scope: its threads' peer stores are ordered before by the barrier); the last one adds 1 to each
+// destination's arrival counter with a system-scope release and re-arms the count.
+__device__ __forceinline__ void peer_signal(const toep_peer_scatter* sc) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  unsigned long long* done = const_cast<unsigned long long*>(reinterpret_cast<const unsigned long long*>(&sc->done));
+  const unsigned long long total = static_cast<unsigned long long>(gridDim.x) * gridDim.y * gridDim.z;
+  unsigned long long old;
+  asm volatile("atom.acq_rel.sys.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(done) : "memory");
+  if (old + 1 != total) return;
+  asm volatile("st.relaxed.sys.global.u64 [%0], 0;" ::"l"(done) : "memory");
+  for (int q = 0; q < sc->parts; ++q)
+    asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(sc->signal[q]) : "memory");
+}
+
 template <typename TI, typename TC, typename TO, int TIL>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) fft_pass_kernel(PassArgs a, Radices rad, double two_over_L) {
+__global__ void __launch_bounds__(kThreads, kMinBlocksGeneric) fft_pass_kernel(PassArgs a, Radices rad, double two_over_L) {
   pdl_wait();
   if (a.stop != nullptr && *a.stop != 0) return;
   using Z = C<TC>;
@@ -480,9 +497,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fft_pass_kernel(PassArgs
   Z* src = buf0;
   Z* dst = buf1;
   int Ns = 1;
+  const bool scat = a.scatter != nullptr;
   for (int s = 0; s < rad.n; ++s) {
     const int R = rad.r[s];
-    if (s + 1 < rad.n) {
+    if (s + 1 < rad.n || scat) {
       dispatch_stage<TC, TO, TIL, false>(R, src, dst, tw, L, Ns, a.sign, out, a.out_sa, a.n_out, ncol, scale);
       __syncthreads();
       Z* t = src;
@@ -492,6 +510,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fft_pass_kernel(PassArgs
     } else {
       dispatch_stage<TC, TO, TIL, true>(R, src, dst, tw, L, Ns, a.sign, out, a.out_sa, a.n_out, ncol, scale);
     }
+  }
+  if (scat) {  // spectrum in natural order in `src`: store each row to the rank that owns it, then signal
+    const toep_peer_scatter* sc = a.scatter;
+    for (int e = threadIdx.x; e < a.n_out * TIL; e += kThreads) {
+      const int idx = e / TIL;
+      const int col = e - idx * TIL;
+      if (col >= ncol) continue;
+      int q = 0;
+      while (q + 1 < sc->parts && idx >= sc->lo[q + 1]) ++q;
+      C<TO>* dstp = reinterpret_cast<C<TO>*>(sc->base[q]) + sc->off[q] + idx * sc->sa[q] + o * sc->so[q] + i0 + col;
+      *dstp = cvt<C<TO>>(cscale(src[idx * TIL + col], scale));
+    }
+    peer_signal(sc);
   }
 }
 
@@ -547,10 +578,12 @@ __global__ void __launch_bounds__(kThreads) dft_direct_kernel(PassArgs a, double
 
 template <typename TI, typename TC, typename TO>
 int launch(const PassArgs& a, const Radices& rad, bool direct, cudaStream_t s) {
-  if (!direct) {
+  if (!direct && a.scatter == nullptr) {
     const int rc = try_plan<TI, TC, TO>(a, s);
     if (rc >= 0) return rc;
   }
+  TOEP_REQUIRE(a.scatter == nullptr || (!direct && a.L > 1), TOEP_ERR_ARG,
+               "peer scatter needs a 7-smooth pass length > 1 (L=%d)", a.L);
   TOEP_REQUIRE(a.in_planes == nullptr && a.out_planes == nullptr, TOEP_ERR_ARG,
                "split-plane I/O needs a compiled pass plan (L=%d)", a.L);
   const size_t es = sizeof(C<TC>);

@@ -44,6 +44,9 @@ struct PassArgs {
   double* out_planes = nullptr;
   const double* in_planes = nullptr;
   int64_t plane = 0;
+  // optional peer scatter (toep_matvec_stage_peer): device table routing output index a to the
+  // destination rank's receive buffer, plus the arrival signal after the launch's last store
+  const toep_peer_scatter* scatter = nullptr;
 };
 
 // Whole 2-D transforms of the single-RHS matvec in one kernel each (one CTA per batch column,

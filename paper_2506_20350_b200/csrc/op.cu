@@ -508,13 +508,31 @@ int toep_op_slab(toep_op_t op, int kx0, int kx1, void* stream, toep_op_t* out) {
 int toep_matvec_stage(toep_op_t op, int stage, const void* in, void* out, int64_t w, int count, void* stream) {
   TOEP_REQUIRE(op != nullptr && in != nullptr && out != nullptr && in != out && w >= 1 && count >= 0, TOEP_ERR_ARG,
                "bad matvec_stage arguments");
+  return toep::matvec_stage_impl(op, stage, in, out, w, count, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int toep_matvec_stage_peer(toep_op_t op, int stage, const void* in, const toep_peer_scatter* scatter, int64_t w,
+                           int count, void* stream) {
+  TOEP_REQUIRE(op != nullptr && in != nullptr && scatter != nullptr && w >= 1 && count >= 0, TOEP_ERR_ARG,
+               "bad matvec_stage_peer arguments");
+  TOEP_REQUIRE(stage == 0 || stage == 1, TOEP_ERR_ARG, "peer scatter is defined for stages 0 and 1, not %d", stage);
+  return toep::matvec_stage_impl(op, stage, in, nullptr, w, count, scatter, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+namespace toep {
+
+// stage 0 / 2: level-1 pass over `count` rows; stage 1: slab spectral step.  With `scatter` (device
+// table, stages 0 and 1) the last pass stores into the destination ranks' buffers instead of `out`.
+int matvec_stage_impl(toep_op_s* op, int stage, const void* in, void* out, int64_t w, int count,
+                      const toep_peer_scatter* scatter, cudaStream_t s) {
   if (count == 0) return TOEP_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int tc = op->dtype == TOEP_C64 ? 1 : 0;
   const int64_t inner = static_cast<int64_t>(op->n0) * w;
   if (stage == 0 || stage == 2) {  // level-1 forward / inverse pass over `count` array rows
     PassArgs a;
-    a.in = in; a.out = out; a.L = op->l1; a.inner = inner; a.outer = count;
+    a.in = in; a.out = out; a.L = op->l1; a.inner = inner; a.outer = count; a.scatter = scatter;
     if (stage == 0) {
       a.n_lo = op->n1; a.n_out = op->l1; a.in_sa = inner; a.in_so = op->n1 * inner; a.out_sa = inner;
       a.out_so = op->l1 * inner; a.sign = -1; a.scale = 1.0;
@@ -538,8 +556,13 @@ int toep_matvec_stage(toep_op_t op, int stage, const void* in, void* out, int64_
   c.in = ws->hat2; c.out = out; c.L = op->l2; c.n_lo = op->l2; c.n_out = op->n2; c.inner = inner; c.outer = kxs;
   c.in_sa = kxs * inner; c.in_so = inner; c.out_sa = kxs * inner; c.out_so = inner; c.sign = +1;
   c.scale = 1.0 / op->l2;
+  c.scatter = scatter;
   return fft_pass(c, tc, tc, tc, s);
 }
+
+}  // namespace toep
+
+extern "C" {
 
 int toep_matvec(toep_op_t op, const void* u, void* v, int64_t w, int flags, void* stream) {
   TOEP_REQUIRE(op != nullptr && (w == 0 || (u != nullptr && v != nullptr)), TOEP_ERR_ARG, "null argument");

@@ -49,6 +49,10 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
 
 void keep_pool();
 
+// the local stages of the slab-decomposed matvec (toep_matvec_stage / toep_matvec_stage_peer)
+int matvec_stage_impl(toep_op_s* op, int stage, const void* in, void* out, int64_t w, int count,
+                      const toep_peer_scatter* scatter, cudaStream_t s);
+
 // fused.cu
 bool fused_eligible(const toep_op_s* op, int64_t w, bool transpose);
 int fused_prepare(toep_op_s* op, cudaStream_t s);

@@ -14,6 +14,12 @@ shards:
   Only the Ny kept rows are exchanged (16.8 MB per transpose).
 * single-RHS cfg2 does not shard usefully: ``bench.py --gpus N`` runs replicas.
 
+Exchange modes of ``SlabOperator``: ``"collective"`` (``all_to_all_single`` through the process
+group: NCCL on GPUs, gloo in the CPU tests) and ``"peer"`` (B200 / NVSwitch): the DFT pass that
+produces each exchange stores its output rows straight into the owning rank's receive buffer
+(CUDA IPC mapping over NVLink) and bumps that rank's arrival counter; the consumer's stream waits
+on its counter.  The all-to-all disappears into the DFT's final store (``PeerExchange``).
+
 The local stages go through libtoepcuda (``toep_matvec_stage``); tests inject CPU stage
 doubles to exercise the decomposition / exchange logic on gloo with world size 2.
 """
@@ -29,7 +35,8 @@ import torch.distributed as dist
 from . import _lib
 from .errors import NoConvergence, ShapeError
 
-__all__ = ["column_range", "row_range", "solve_columns_sharded", "SlabOperator", "slab_ranges"]
+__all__ = ["column_range", "row_range", "solve_columns_sharded", "SlabOperator", "slab_ranges", "PeerExchange",
+           "scatter_plan"]
 
 
 def column_range(w: int, world: int, rank: int) -> tuple[int, int]:
@@ -113,7 +120,10 @@ class SlabOperator:
     * ``inv_x(x2_rows (ny_r, L1, inner)) -> (ny_r, n1, inner)`` with the 1/(L1 L2) scale
     """
 
-    def __init__(self, n2: int, n1: int, n0: int, l2: int, l1: int, stages, group=None):
+    def __init__(self, n2: int, n1: int, n0: int, l2: int, l1: int, stages, group=None,
+                 exchange: str = "collective"):
+        if exchange not in ("collective", "peer"):
+            raise ValueError(f"exchange must be 'collective' or 'peer', got {exchange!r}")
         self.n2, self.n1, self.n0, self.l2, self.l1 = n2, n1, n0, l2, l1
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -121,14 +131,16 @@ class SlabOperator:
         self.rows = row_range(n2, self.world, self.rank)
         self.slab = slab_ranges(l1, self.world, self.rank)
         self.stages = stages
+        self.exchange = exchange
+        self._peer = {}  # w -> PeerExchange
 
     @classmethod
-    def from_generator(cls, gen, group=None, dtype=torch.complex128):
+    def from_generator(cls, gen, group=None, dtype=torch.complex128, exchange: str = "collective"):
         """Device slab operator: each rank keeps only its kx slab of the spectral blocks."""
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         st = DeviceSlabStages(gen, world, rank, dtype)
-        return cls(gen.n2, gen.n1, gen.n0, st.l2, st.l1, st, group)
+        return cls(gen.n2, gen.n1, gen.n0, st.l2, st.l1, st, group, exchange)
 
     @property
     def local_dim(self) -> int:
@@ -164,6 +176,11 @@ class SlabOperator:
         ny = y1 - y0
         if u_local.shape[0] != ny * self.n1 * self.n0:
             raise ShapeError(f"local rows {u_local.shape[0]} != {ny * self.n1 * self.n0}")
+        if self.exchange == "peer" and self.world > 1:
+            ex = self._peer.get(w)
+            if ex is None:
+                ex = self._peer[w] = PeerExchange.over_group(self, w)
+            return ex.matvec(self.stages, u_local.reshape(ny, self.n1, inner)).reshape(ny * self.n1 * self.n0, w)
         x1 = self.stages.fwd_x(u_local.reshape(ny, self.n1, inner))            # (ny, L1, inner)
         slabs = [slab_ranges(self.l1, self.world, q) for q in range(self.world)]
         rows = [row_range(self.n2, self.world, q) for q in range(self.world)]
@@ -266,3 +283,179 @@ class DeviceSlabStages:
     def inv_x(self, x2_rows):
         ny, _, inner = x2_rows.shape
         return self._stage(2, x2_rows, (ny, self.n1, inner), ny)
+
+    # peer mode: stages 0 / 1 store into the destination ranks' receive buffers (table: device
+    # toep_peer_scatter built by PeerExchange) and signal their arrival counters
+    def _stage_peer(self, stage: int, x: torch.Tensor, table: torch.Tensor, count: int):
+        x = x.contiguous()
+        w = x.shape[-1] // self.n0
+        _lib.check(_lib.lib().toep_matvec_stage_peer(self.op.handle, stage, x.data_ptr(), table.data_ptr(), w, count,
+                                                     _lib.stream_handle()), f"matvec_stage_peer {stage}")
+
+    def fwd_x_peer(self, u_rows, table):
+        self._stage_peer(0, u_rows, table, u_rows.shape[0])
+
+    def spectral_peer(self, x1_slab, table):
+        self._stage_peer(1, x1_slab, table, x1_slab.shape[1])
+
+
+def scatter_plan(stage: int, rank: int, world: int, n2: int, l1: int, inner: int):
+    """Routing of one peer-scatter pass of ``rank`` (elements of each destination's buffer).
+
+    stage 0 — level-1 DFT of this rank's rows; output index = kx, outer index o = local row.
+        Destination q's receive buffer 1 is (n2, kxs_q, inner): element (y0_r + o, kx - k0_q, i).
+    stage 1 — inverse level-2 DFT of this rank's kx slab; output index = y, outer o = local kx.
+        Destination q's receive buffer 2 is (ny_q, l1, inner): element (y - y0_q, k0_r + o, i).
+    Returns ``(lo, parts)``: output index range [lo[q], lo[q+1]) goes to q at
+    ``off + a*sa + o*so + i`` with ``parts[q] = (off, sa, so)`` — the C table's fields.
+    """
+    if not 1 <= world <= _lib.MAX_PEERS:
+        raise ValueError(f"peer exchange supports 1..{_lib.MAX_PEERS} ranks, got {world}")
+    if world > n2 or world > l1:  # every rank must own rows and a slab: each pass signals every peer
+        raise ShapeError(f"peer exchange needs world ({world}) <= rows ({n2}) and <= level-1 length ({l1})")
+    rows = [row_range(n2, world, q) for q in range(world)]
+    slabs = [slab_ranges(l1, world, q) for q in range(world)]
+    y0, _ = rows[rank]
+    k0, _ = slabs[rank]
+    if stage == 0:
+        lo = [a for a, _ in slabs] + [l1]
+        parts = [((y0 * (b - a) - a) * inner, inner, (b - a) * inner) for a, b in slabs]
+    elif stage == 1:
+        lo = [a for a, _ in rows] + [n2]
+        parts = [((-a * l1 + k0) * inner, l1 * inner, inner) for a, _ in rows]
+    else:
+        raise ValueError(f"peer scatter is defined for stages 0 and 1, not {stage}")
+    return lo, parts
+
+
+class PeerExchange:
+    """Receive buffers + arrival counters of one rank, mapped into every peer (CUDA IPC).
+
+    One ``cudaMalloc`` region per rank and column count w: two u64 arrival counters, receive
+    buffer 1 (n2, kxs_r, n0*w) and receive buffer 2 (ny_r, l1, n0*w).  ``tables`` are the device
+    routing tables of this rank's two scatter passes (``scatter_plan`` resolved to the peers'
+    mapped addresses).  A matvec: stage 0 scatters to the slab owners, wait for ``world`` arrivals
+    on counter 1, stage 1 on receive buffer 1 scatters to the row owners, wait on counter 2,
+    stage 2 on receive buffer 2.  Buffer reuse across matvecs is safe by construction: a rank
+    writes a peer's buffer for matvec m+1 only after that peer has signalled the exchange that
+    follows its last read of it in matvec m.
+    """
+
+    _HDR = 256
+
+    def __init__(self, sizes, es: int, device):
+        self.es = es
+        self.device = device
+        self.seq = 0
+        self.world = None
+        n1b, n2b = sizes
+        self.off1 = self._HDR
+        self.off2 = self._HDR + -(-n1b * es // 256) * 256
+        self.bytes = self.off2 + n2b * es
+        ptr = ctypes.c_void_p()
+        _lib.check(_lib.lib().toep_peer_alloc(self.bytes, ctypes.byref(ptr)), "peer_alloc")
+        self.base = ptr.value
+        self.sizes = sizes
+        self._opened = []
+        self.tables = None
+
+    @staticmethod
+    def _sizes(op: "SlabOperator", rank: int, w: int):
+        inner = op.n0 * w
+        y0, y1 = row_range(op.n2, op.world, rank)
+        k0, k1 = slab_ranges(op.l1, op.world, rank)
+        return op.n2 * (k1 - k0) * inner, (y1 - y0) * op.l1 * inner
+
+    @classmethod
+    def over_group(cls, op: "SlabOperator", w: int) -> "PeerExchange":
+        """Collective setup over op.group: allocate, exchange IPC handles, open the peers."""
+        es = 8 if op.stages.op.dtype == torch.complex64 else 16
+        ex = cls(cls._sizes(op, op.rank, w), es, torch.device("cuda", torch.cuda.current_device()))
+        h = (ctypes.c_char * 64)()
+        _lib.check(_lib.lib().toep_ipc_handle(ctypes.c_void_p(ex.base), h), "ipc_handle")
+        mine = (bytes(h), ex.off1, ex.off2)
+        got = [None] * op.world
+        dist.all_gather_object(got, mine, group=op.group)
+        bases = []
+        for q, (hq, _, _) in enumerate(got):
+            if q == op.rank:
+                bases.append(ex.base)
+                continue
+            p = ctypes.c_void_p()
+            _lib.check(_lib.lib().toep_ipc_open(ctypes.create_string_buffer(hq, 64), ctypes.byref(p)), "ipc_open")
+            ex._opened.append(p.value)
+            bases.append(p.value)
+        ex.bind(op.rank, op.world, op.n2, op.l1, op.n0 * w,
+                [(b, g[1], g[2]) for b, g in zip(bases, got)])
+        return ex
+
+    def bind(self, rank: int, world: int, n2: int, l1: int, inner: int, peers):
+        """Build this rank's two device routing tables; peers[q] = (base address, off1, off2)."""
+        self.world, self.rank = world, rank
+        tables = []
+        for stage, (sig_off, buf) in ((0, (0, 1)), (1, (8, 2))):
+            lo, parts = scatter_plan(stage, rank, world, n2, l1, inner)
+            t = _lib.PeerScatter()
+            t.parts = world
+            for q in range(world + 1):
+                t.lo[q] = lo[q]
+            for q, (off, sa, so) in enumerate(parts):
+                base_q, o1, o2 = peers[q]
+                t.base[q] = base_q + (o1 if buf == 1 else o2)
+                t.off[q], t.sa[q], t.so[q] = off, sa, so
+                t.signal[q] = base_q + sig_off
+            t.done = 0
+            raw = torch.frombuffer(bytearray(bytes(t)), dtype=torch.uint8)
+            tables.append(raw.to(self.device))
+        self.tables = tables
+
+    def recv(self, which: int, shape, dtype):
+        """Device tensor view of receive buffer 1 or 2 (owned by this object)."""
+        off, n = (self.off1, self.sizes[0]) if which == 1 else (self.off2, self.sizes[1])
+        return _device_view(self.base + off, n, dtype, self.device).reshape(shape)
+
+    def counter(self, which: int) -> int:
+        return self.base + (0 if which == 1 else 8)
+
+    def wait(self, which: int, stream=None):
+        _lib.check(_lib.lib().toep_peer_wait(ctypes.c_void_p(self.counter(which)), self.seq * self.world,
+                                             stream if stream is not None else _lib.stream_handle()), "peer_wait")
+
+    def matvec(self, stages: "DeviceSlabStages", u_rows: torch.Tensor) -> torch.Tensor:
+        """One distributed matvec of this rank's rows (ny_r, n1, n0*w) -> (ny_r, n1, n0*w)."""
+        ny, _, inner = u_rows.shape
+        dtype = stages.op.dtype
+        kxs = stages.k1 - stages.k0
+        self.seq += 1
+        stages.fwd_x_peer(u_rows, self.tables[0])
+        self.wait(1)
+        stages.spectral_peer(self.recv(1, (stages.n2, kxs, inner), dtype), self.tables[1])
+        self.wait(2)
+        return stages.inv_x(self.recv(2, (ny, stages.l1, inner), dtype))
+
+    def close(self):
+        lib = _lib.lib()
+        for p in self._opened:
+            lib.toep_ipc_close(ctypes.c_void_p(p))
+        self._opened = []
+        if self.base:
+            lib.toep_peer_free(ctypes.c_void_p(self.base))
+            self.base = 0
+
+    def __del__(self):
+        try:
+            if torch.cuda.is_available():
+                torch.cuda.synchronize(self.device)
+            self.close()
+        except Exception:
+            pass
+
+
+def _device_view(addr: int, numel: int, dtype, device) -> torch.Tensor:
+    """Non-owning torch view of device memory allocated by libtoepcuda."""
+    es = torch.empty((), dtype=dtype).element_size()
+
+    class _Mem:
+        __cuda_array_interface__ = {"shape": (numel * es,), "typestr": "|u1", "data": (addr, False), "version": 3}
+
+    return torch.as_tensor(_Mem(), device=device).view(dtype)

@@ -171,3 +171,56 @@ def test_slab_matvec_gloo():
         assert np.linalg.norm(v - want[lo:hi]) <= 1e-12 * np.linalg.norm(want)
         assert abs(dot - np.vdot(u, u)) <= 1e-10 * abs(np.vdot(u, u))
         assert abs(nrm - np.linalg.norm(u)) <= 1e-10 * np.linalg.norm(u)
+
+
+def _emulate_scatter(plan, outputs, recv, shape_of):
+    """Apply scatter_plan routing with numpy: outputs[r] indexed [a][o][i] (pass order)."""
+    for r, (lo, parts) in plan.items():
+        out = outputs[r]
+        n_out, outer, inner = out.shape
+        for a in range(n_out):
+            q = max(j for j in range(len(parts)) if lo[j] <= a and (j + 1 == len(parts) or a < lo[j + 1]))
+            off, sa, so = parts[q]
+            for o in range(outer):
+                start = off + a * sa + o * so
+                recv[q][start:start + inner] = out[a, o]
+    return [recv[q].reshape(shape_of(q)) for q in range(len(recv))]
+
+
+@pytest.mark.parametrize("world,n2,l1", [(2, 6, 12), (3, 7, 16), (4, 5, 12), (8, 9, 20)])
+def test_peer_scatter_plan_matches_all_to_all(world, n2, l1):
+    """The peer-exchange routing tables reproduce the collective exchanges' layouts."""
+    from paper_2506_20350_b200.distributed import scatter_plan, slab_ranges
+
+    inner = 3
+    rng = np.random.default_rng(world)
+    rows = [row_range(n2, world, q) for q in range(world)]
+    slabs = [slab_ranges(l1, world, q) for q in range(world)]
+    # exchange 1: rank r's level-1 output (ny_r, l1, inner) -> slab owners (n2, kxs_q, inner)
+    x1 = [rng.standard_normal(((b - a), l1, inner)) for a, b in rows]
+    want1 = [np.concatenate([x1[r][:, k0:k1] for r in range(world)], axis=0) for k0, k1 in slabs]
+    plan0 = {r: scatter_plan(0, r, world, n2, l1, inner) for r in range(world)}
+    recv1 = [np.full(n2 * (k1 - k0) * inner, np.nan) for k0, k1 in slabs]
+    got1 = _emulate_scatter(plan0, {r: x1[r].transpose(1, 0, 2) for r in range(world)}, recv1,
+                            lambda q: (n2, slabs[q][1] - slabs[q][0], inner))
+    for q in range(world):
+        np.testing.assert_array_equal(got1[q], want1[q])
+    # exchange 2: rank r's slab output (n2, kxs_r, inner) -> row owners (ny_q, l1, inner)
+    x2 = [rng.standard_normal((n2, (b - a), inner)) for a, b in slabs]
+    want2 = [np.concatenate([x2[r][y0:y1] for r in range(world)], axis=1) for y0, y1 in rows]
+    plan1 = {r: scatter_plan(1, r, world, n2, l1, inner) for r in range(world)}
+    recv2 = [np.full((y1 - y0) * l1 * inner, np.nan) for y0, y1 in rows]
+    got2 = _emulate_scatter(plan1, {r: x2[r] for r in range(world)}, recv2,
+                            lambda q: (rows[q][1] - rows[q][0], l1, inner))
+    for q in range(world):
+        np.testing.assert_array_equal(got2[q], want2[q])
+
+
+def test_peer_scatter_plan_rejects_empty_ranks():
+    from paper_2506_20350_b200.distributed import scatter_plan
+    from paper_2506_20350_b200.errors import ShapeError
+
+    with pytest.raises(ShapeError):
+        scatter_plan(0, 0, 8, 5, 12, 4)
+    with pytest.raises(ValueError):
+        scatter_plan(0, 0, 9, 30, 60, 4)

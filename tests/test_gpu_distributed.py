@@ -57,3 +57,102 @@ def test_world1_slab_operator():
     want = matvec(precompute_spectral(gen), u)
     assert rel_err(op.matvec_local(u).cpu().numpy(), want.cpu().numpy()) <= 1e-12
     assert abs(op.norm(u) - torch.linalg.norm(u).item()) <= 1e-10 * op.norm(u)
+
+
+@pytest.mark.parametrize("dims,world,w", [((6, 5, 8), 2, 2), ((16, 16, 64), 4, 1), ((9, 7, 16), 3, 3)])
+def test_peer_exchange_matvec_emulated(dims, world, w):
+    """Peer-scatter stages (fused all-to-all stores + arrival counters) for `world` simulated ranks
+    on one GPU: every rank's pass of an exchange runs before any rank waits on it, so no kernel
+    waits on another; three matvecs in a row exercise the counter epochs and the re-armed counts."""
+    from paper_2506_20350_b200.distributed import PeerExchange
+
+    ny, nx, nb = dims
+    gen = generator_from_stacked(seeded_stacked4(ny, nx, nb, seed=4))
+    op_full = precompute_spectral(gen)
+    st = [DeviceSlabStages(gen, world, r, torch.complex128) for r in range(world)]
+    l1 = st[0].l1
+    inner = nb * w
+    rows = [row_range(ny, world, r) for r in range(world)]
+    slabs = [slab_ranges(l1, world, r) for r in range(world)]
+    dev = torch.device("cuda", 0)
+    ex = [PeerExchange((ny * (k1 - k0) * inner, (y1 - y0) * l1 * inner), 16, dev)
+          for (k0, k1), (y0, y1) in zip(slabs, rows)]
+    peers = [(e.base, e.off1, e.off2) for e in ex]
+    for r in range(world):
+        ex[r].bind(r, world, ny, l1, inner, peers)
+    for it in range(3):
+        u = torch.from_numpy(dense_rhs(gen.dim, w, seed=10 + it)).cuda()
+        want = matvec(op_full, u)
+        ur = u.reshape(ny, nx, inner)
+        for r in range(world):
+            ex[r].seq += 1
+            st[r].fwd_x_peer(ur[rows[r][0]:rows[r][1]], ex[r].tables[0])
+        for r in range(world):
+            ex[r].wait(1)
+            kxs = slabs[r][1] - slabs[r][0]
+            st[r].spectral_peer(ex[r].recv(1, (ny, kxs, inner), torch.complex128), ex[r].tables[1])
+        outs = []
+        for r in range(world):
+            ex[r].wait(2)
+            ny_r = rows[r][1] - rows[r][0]
+            outs.append(st[r].inv_x(ex[r].recv(2, (ny_r, l1, inner), torch.complex128)))
+        got = torch.cat(outs, dim=0).reshape(gen.dim, w)
+        assert rel_err(got.cpu().numpy(), want.cpu().numpy()) <= 1e-12
+        for r in range(world):  # each counter saw exactly `world` arrivals per matvec
+            c = torch.empty(2, dtype=torch.int64, device=dev)
+            c.copy_(_counter_view(ex[r]))
+            assert c.tolist() == [world * (it + 1)] * 2
+    for e in ex:
+        e.close()
+
+
+def _counter_view(ex):
+    from paper_2506_20350_b200.distributed import _device_view
+
+    return _device_view(ex.base, 2, torch.int64, ex.device)
+
+
+def _ipc_child(handle, q):
+    import ctypes
+
+    from paper_2506_20350_b200 import _lib
+    from paper_2506_20350_b200.distributed import _device_view
+
+    torch.cuda.set_device(0)
+    _lib.require_cuda()
+    p = ctypes.c_void_p()
+    _lib.check(_lib.lib().toep_ipc_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(p)), "ipc_open")
+    v = _device_view(p.value, 1024, torch.float64, torch.device("cuda", 0))
+    q.put(float(v.sum().item()))
+    torch.cuda.synchronize()
+    _lib.check(_lib.lib().toep_ipc_close(p), "ipc_close")
+
+
+def test_ipc_handle_maps_exchange_memory_in_another_process():
+    import ctypes
+
+    import torch.multiprocessing as mp
+
+    from paper_2506_20350_b200 import _lib
+    from paper_2506_20350_b200.distributed import _device_view
+
+    _lib.require_cuda()
+    p = ctypes.c_void_p()
+    _lib.check(_lib.lib().toep_peer_alloc(1024 * 8, ctypes.byref(p)), "peer_alloc")
+    try:
+        v = _device_view(p.value, 1024, torch.float64, torch.device("cuda", 0))
+        assert float(v.abs().sum().item()) == 0.0  # zero-initialised (arrival counters start at 0)
+        v.copy_(torch.arange(1024, dtype=torch.float64, device="cuda"))
+        torch.cuda.synchronize()
+        h = (ctypes.c_char * 64)()
+        _lib.check(_lib.lib().toep_ipc_handle(p, h), "ipc_handle")
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        child = ctx.Process(target=_ipc_child, args=(bytes(h), q))
+        child.start()
+        got = q.get(timeout=180)
+        child.join(timeout=60)
+        assert child.exitcode == 0
+        assert got == float(1023 * 1024 // 2)
+    finally:
+        _lib.lib().toep_peer_free(p)
