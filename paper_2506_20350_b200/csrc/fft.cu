@@ -168,6 +168,41 @@ __device__ __forceinline__ void dispatch_stage(int R, const C<TC>* src, C<TC>* d
   }
 }
 
+// Completion signal of a peer-scatter launch: every CTA counts itself in (acq_rel, system
+// scope: its threads' peer stores are ordered before by the barrier); the last one adds 1 to each
+// destination's arrival counter with a system-scope release and re-arms the count.
+__device__ __forceinline__ void peer_signal(const toep_peer_scatter* sc) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  unsigned long long* done = const_cast<unsigned long long*>(reinterpret_cast<const unsigned long long*>(&sc->done));
+  const unsigned long long total = static_cast<unsigned long long>(gridDim.x) * gridDim.y * gridDim.z;
+  unsigned long long old;
+  asm volatile("atom.acq_rel.sys.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(done) : "memory");
+  if (old + 1 != total) return;
+  asm volatile("st.relaxed.sys.global.u64 [%0], 0;" ::"l"(done) : "memory");
+  for (int q = 0; q < sc->parts; ++q)
+    asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(sc->signal[q]) : "memory");
+}
+
+// Peer-scatter epilogue: the pass result (natural order, unscaled) sits in shared memory `res`
+// [L][TIL]; output row idx goes to the rank whose range holds it (table lo/base/off/sa/so).
+template <typename TC, typename TO, int TIL>
+__device__ __forceinline__ void scatter_tile(const PassArgs& a, const C<TC>* res, int ncol, TC scale) {
+  const toep_peer_scatter* sc = a.scatter;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * TIL;
+  const int64_t o = blockIdx.y;
+  for (int e = threadIdx.x; e < a.n_out * TIL; e += kThreads) {
+    const int idx = e / TIL;
+    const int col = e - idx * TIL;
+    if (col >= ncol) continue;
+    int q = 0;
+    while (q + 1 < sc->parts && idx >= sc->lo[q + 1]) ++q;
+    C<TO>* dstp = reinterpret_cast<C<TO>*>(sc->base[q]) + sc->off[q] + idx * sc->sa[q] + o * sc->so[q] + i0 + col;
+    *dstp = cvt<C<TO>>(cscale(res[idx * TIL + col], scale));
+  }
+  peer_signal(sc);
+}
+
 // ------------------------------------------------------------------------------------------
 // Compile-time plans for the embedding lengths the BASELINE grids use (7, 32, 60, 128): every
 // index, stride and trip count is a constant.  The first stage reads its radix inputs straight
@@ -232,6 +267,9 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
     if constexpr (!kLast) {
 #pragma unroll
       for (int q = 0; q < R; ++q) dst[(base + q * Ns) * TIL + col] = v[q];
+    } else if (a.scatter != nullptr) {  // peer scatter: the epilogue stores from shared memory
+#pragma unroll
+      for (int q = 0; q < R; ++q) dst[(base + q * Ns) * TIL + col] = v[q];
     } else {
       if (col < ncol) {
 #pragma unroll
@@ -281,6 +319,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fft_plan_kernel(PassArgs
   if (a.out_idx != nullptr) out += static_cast<int64_t>(*a.out_idx) * a.out_idx_stride;
   __syncthreads();  // twiddle table
   plan_stage<TI, TC, TO, kThreads, TIL, L, 1, Rs...>(a, in, out, buf[0], buf[1], tw, ncol, pass_scale<TC>(a));
+  if (a.scatter != nullptr) {  // stage s writes buf[(s + 1) % 2]
+    __syncthreads();
+    scatter_tile<TC, TO, TIL>(a, buf[sizeof...(Rs) % 2], ncol, pass_scale<TC>(a));
+  }
 }
 
 template <typename TI, typename TC, typename TO, int TIL, int... Rs>
@@ -435,22 +477,6 @@ int fft2d_t(bool inverse, const Fft2dArgs& f, int l2, int l1, cudaStream_t s) {
   return -1;
 }
 
-// Completion signal of a peer-scatter launch: every CTA counts itself in (acq_rel, system
-// scope: its threads' peer stores are ordered before by the barrier); the last one adds 1 to each
-// destination's arrival counter with a system-scope release and re-arms the count.
-__device__ __forceinline__ void peer_signal(const toep_peer_scatter* sc) {
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  unsigned long long* done = const_cast<unsigned long long*>(reinterpret_cast<const unsigned long long*>(&sc->done));
-  const unsigned long long total = static_cast<unsigned long long>(gridDim.x) * gridDim.y * gridDim.z;
-  unsigned long long old;
-  asm volatile("atom.acq_rel.sys.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(done) : "memory");
-  if (old + 1 != total) return;
-  asm volatile("st.relaxed.sys.global.u64 [%0], 0;" ::"l"(done) : "memory");
-  for (int q = 0; q < sc->parts; ++q)
-    asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(sc->signal[q]) : "memory");
-}
-
 template <typename TI, typename TC, typename TO, int TIL>
 __global__ void __launch_bounds__(kThreads, kMinBlocksGeneric) fft_pass_kernel(PassArgs a, Radices rad, double two_over_L) {
   pdl_wait();
@@ -511,19 +537,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocksGeneric) fft_pass_kernel(P
       dispatch_stage<TC, TO, TIL, true>(R, src, dst, tw, L, Ns, a.sign, out, a.out_sa, a.n_out, ncol, scale);
     }
   }
-  if (scat) {  // spectrum in natural order in `src`: store each row to the rank that owns it, then signal
-    const toep_peer_scatter* sc = a.scatter;
-    for (int e = threadIdx.x; e < a.n_out * TIL; e += kThreads) {
-      const int idx = e / TIL;
-      const int col = e - idx * TIL;
-      if (col >= ncol) continue;
-      int q = 0;
-      while (q + 1 < sc->parts && idx >= sc->lo[q + 1]) ++q;
-      C<TO>* dstp = reinterpret_cast<C<TO>*>(sc->base[q]) + sc->off[q] + idx * sc->sa[q] + o * sc->so[q] + i0 + col;
-      *dstp = cvt<C<TO>>(cscale(src[idx * TIL + col], scale));
-    }
-    peer_signal(sc);
-  }
+  if (scat) scatter_tile<TC, TO, TIL>(a, src, ncol, scale);  // result in `src` after the last swap
 }
 
 // Direct O(L^2) DFT for lengths that are not 7-smooth (API block_fft_* on prime
@@ -578,7 +592,7 @@ __global__ void __launch_bounds__(kThreads) dft_direct_kernel(PassArgs a, double
 
 template <typename TI, typename TC, typename TO>
 int launch(const PassArgs& a, const Radices& rad, bool direct, cudaStream_t s) {
-  if (!direct && a.scatter == nullptr) {
+  if (!direct) {
     const int rc = try_plan<TI, TC, TO>(a, s);
     if (rc >= 0) return rc;
   }
