@@ -10,6 +10,10 @@
 // TIL batch columns into shared memory (zero-padding fused), runs the radix
 // stages ping-ponging between two shared buffers, and the last stage writes
 // straight to global memory with the crop and the 1/L scale fused.
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+
 #include "kernels.cuh"
 #include "launch.cuh"
 #include "tma.cuh"
@@ -213,11 +217,13 @@ template <int... Rs> struct PlanLen;
 template <> struct PlanLen<> { static constexpr int value = 1; };
 template <int R, int... Rest> struct PlanLen<R, Rest...> { static constexpr int value = R * PlanLen<Rest...>::value; };
 
-template <typename TI, typename TC, typename TO, int NT, int TIL, int L, int Ns, int R, int... Rest>
+template <typename TI, typename TC, typename TO, int NT, int TIL, int L, int Ns, int kIn, int R, int... Rest>
 __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __restrict__ gin, C<TO>* __restrict__ gout,
                                            C<TC>* __restrict__ src, C<TC>* __restrict__ dst,
                                            const C<TC>* __restrict__ tw, int ncol, TC scale) {
   using Z = C<TC>;
+  static_assert(kIn >= 0 && kIn <= 2, "plan_stage input mode");
+  static_assert(Ns * R * PlanLen<Rest...>::value == L, "plan radices must multiply to L");
   constexpr bool kFirst = (Ns == 1);
   constexpr bool kLast = sizeof...(Rest) == 0;
   constexpr int nb = L / R;
@@ -242,7 +248,16 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
         if (slot < a.n_lo) row = slot;
         else if (slot >= hi_start) row = a.n_lo + slot - hi_start;
         v[r] = mk<TC>(0, 0);
-        if (row >= 0 && col < ncol) {
+        if constexpr (kIn == 1) {  // staged by the streaming kernel: rows [n_lo + n_hi][TIL] in `src`
+          if (row >= 0 && col < ncol) v[r] = src[row * TIL + col];
+        } else if constexpr (kIn == 2) {  // staged (T1, T2, T3) planes [3][n_lo + n_hi][TIL] doubles
+          if (row >= 0 && col < ncol) {
+            const double* sp = reinterpret_cast<const double*>(src);
+            const int nr = a.n_lo + a.n_hi;
+            const double t1 = sp[row * TIL + col], t2 = sp[(nr + row) * TIL + col], t3 = sp[(2 * nr + row) * TIL + col];
+            v[r] = mk<TC>(static_cast<TC>(t1 - t2), static_cast<TC>(t3 - t1 - t2));
+          }
+        } else if (row >= 0 && col < ncol) {
           if (a.in_planes != nullptr) {
             const int64_t e = (gin - static_cast<const C<TI>*>(a.in)) + row * a.in_sa + col * a.in_cs;
             const double t1 = a.in_planes[e], t2 = a.in_planes[a.plane + e], t3 = a.in_planes[2 * a.plane + e];
@@ -292,7 +307,7 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
   }
   if constexpr (!kLast) {
     __syncthreads();
-    plan_stage<TI, TC, TO, NT, TIL, L, Ns * R, Rest...>(a, gin, gout, dst, src, tw, ncol, scale);
+    plan_stage<TI, TC, TO, NT, TIL, L, Ns * R, kIn, Rest...>(a, gin, gout, dst, src, tw, ncol, scale);
   }
 }
 
@@ -318,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fft_plan_kernel(PassArgs
   C<TO>* out = static_cast<C<TO>*>(a.out) + o * a.out_so + i0;
   if (a.out_idx != nullptr) out += static_cast<int64_t>(*a.out_idx) * a.out_idx_stride;
   __syncthreads();  // twiddle table
-  plan_stage<TI, TC, TO, kThreads, TIL, L, 1, Rs...>(a, in, out, buf[0], buf[1], tw, ncol, pass_scale<TC>(a));
+  plan_stage<TI, TC, TO, kThreads, TIL, L, 1, 0, Rs...>(a, in, out, buf[0], buf[1], tw, ncol, pass_scale<TC>(a));
   if (a.scatter != nullptr) {  // stage s writes buf[(s + 1) % 2]
     __syncthreads();
     scatter_tile<TC, TO, TIL>(a, buf[sizeof...(Rs) % 2], ncol, pass_scale<TC>(a));
@@ -332,11 +347,148 @@ int launch_plan(const PassArgs& a, cudaStream_t s) {
                   2.0 / PlanLen<Rs...>::value);
 }
 
+// Persistent, software-pipelined variant of fft_plan_kernel for the very large passes of the
+// multi-RHS matvec (hundreds of thousands of tiles streamed through HBM): each CTA walks tiles
+// t = blockIdx.x + k * gridDim.x and stages tile t + gridDim.x with cp.async (LDGSTS) while it
+// transforms tile t, so every SM keeps input bytes in flight across its whole lifetime instead of
+// paying load latency + launch ramp per short-lived CTA.  Shared memory: two staging buffers
+// (also used as the ping-pong partner of `work`) and `work`.  kIn = 1: complex rows; kIn = 2: the
+// (T1, T2, T3) planes of the 3M product, recombined when the first stage reads them.
+constexpr int kStreamBlocks = 4;
+
+template <typename TC, int TIL, int kIn, int L>
+struct StreamSmem {
+  static constexpr int kStageZ = kIn == 2 ? (3 * L * TIL + 1) / 2 : L * TIL;  // complex slots per staging buffer
+  static constexpr size_t bytes = sizeof(C<TC>) * (L + 2 * static_cast<size_t>(kStageZ) + L * TIL);
+};
+
+__device__ __forceinline__ void cp_async(void* smem, const void* g, int nbytes) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  if (nbytes == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(g) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(g) : "memory");
+}
+
+template <typename TC, typename TO, int TIL, int kIn, int... Rs>
+__global__ void __launch_bounds__(kThreads, kStreamBlocks) fft_plan_stream_kernel(PassArgs a, double two_over_L,
+                                                                                 int64_t ntiles, int64_t tiles_x) {
+  using Z = C<TC>;
+  constexpr int L = PlanLen<Rs...>::value;
+  using SM = StreamSmem<TC, TIL, kIn, L>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Z* tw = reinterpret_cast<Z*>(smem_raw);
+  Z* stage[2] = {tw + L, tw + L + SM::kStageZ};
+  Z* work = tw + L + 2 * SM::kStageZ;
+  pdl_trigger();
+  for (int t = threadIdx.x; t < L; t += kThreads) {
+    TC s, c;
+    sincospi_t<TC>(static_cast<TC>(t * two_over_L), &s, &c);
+    tw[t] = mk<TC>(c, a.sign * s);
+  }
+  pdl_wait();
+  if (a.stop != nullptr && *a.stop != 0) return;
+  const int nrows = a.n_lo + a.n_hi;
+  auto issue = [&](int64_t tile, Z* buf) {
+    const int64_t o = tile / tiles_x;
+    const int64_t i0 = (tile - o * tiles_x) * TIL;
+    const int ncol = static_cast<int>(std::min<int64_t>(TIL, a.inner - i0));
+    const int64_t g0 = o * a.in_so + i0;  // complex-element offset of the tile's (row 0, col 0)
+    for (int e = threadIdx.x; e < nrows * TIL; e += kThreads) {
+      const int row = e / TIL;
+      const int col = e - row * TIL;
+      if (col >= ncol) continue;
+      const int64_t ge = g0 + row * a.in_sa + col * a.in_cs;
+      if constexpr (kIn == 1) {
+        cp_async(buf + e, static_cast<const Z*>(a.in) + ge, static_cast<int>(sizeof(Z)));
+      } else {
+        double* bd = reinterpret_cast<double*>(buf);
+#pragma unroll
+        for (int p = 0; p < 3; ++p) cp_async(bd + p * nrows * TIL + e, a.in_planes + p * a.plane + ge, 8);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const TC scale = pass_scale<TC>(a);
+  int64_t t = blockIdx.x;
+  if (t < ntiles) issue(t, stage[0]);
+  for (int k = 0; t < ntiles; t += gridDim.x, ++k) {
+    const int cur = k & 1;
+    if (t + gridDim.x < ntiles) issue(t + gridDim.x, stage[cur ^ 1]);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();  // tile t staged by every thread (and the twiddles, on the first pass)
+    const int64_t o = t / tiles_x;
+    const int64_t i0 = (t - o * tiles_x) * TIL;
+    const int ncol = static_cast<int>(std::min<int64_t>(TIL, a.inner - i0));
+    C<TO>* out = static_cast<C<TO>*>(a.out) + o * a.out_so + i0;
+    plan_stage<TC, TC, TO, kThreads, TIL, L, 1, kIn, Rs...>(a, nullptr, out, stage[cur], work, tw, ncol, scale);
+    __syncthreads();  // stage[cur] is refilled (tile t + 2 * gridDim.x) in the next iteration
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+inline int device_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// streaming launch for very large passes (TI == TC, no device-side offsets / partial sums / scatter);
+// returns -1 when the pass does not qualify
+template <typename TC, typename TO, int TIL, int... Rs>
+int try_stream(const PassArgs& a, cudaStream_t s) {
+  static const int64_t min_tiles = [] {
+    const char* e = std::getenv("TOEP_FFT_STREAM_MIN_TILES");
+    return e != nullptr ? std::atoll(e) : static_cast<int64_t>(1) << 15;
+  }();
+  const int64_t tiles_x = (a.inner + TIL - 1) / TIL;
+  const int64_t ntiles = tiles_x * a.outer;
+  // measured on cfg3 (L = 60, 432 000 tiles per pass): the 3M-plane input pass 1.74 -> 1.38 ms, but the
+  // complex-input passes 1.17 -> 1.30 / 2.45 -> 2.56 ms (fewer resident warps than the short-lived
+  // CTAs of fft_plan_kernel); TOEP_FFT_STREAM=all streams those too
+  static const bool all = [] {
+    const char* e = std::getenv("TOEP_FFT_STREAM");
+    return e != nullptr && std::strcmp(e, "all") == 0;
+  }();
+  if (min_tiles <= 0 || ntiles < min_tiles || a.in_idx != nullptr || a.out_idx != nullptr || a.part_count != nullptr ||
+      a.scatter != nullptr || (a.in_planes == nullptr && !all))
+    return -1;
+  constexpr int L = PlanLen<Rs...>::value;
+  auto launch_kin = [&](auto kin_tag) -> int {
+    constexpr int kIn = decltype(kin_tag)::value;
+    using SM = StreamSmem<TC, TIL, kIn, L>;
+    auto kern = fft_plan_stream_kernel<TC, TO, TIL, kIn, Rs...>;
+    static int per_sm = 0;
+    if (per_sm == 0) {
+      if (SM::bytes > 48 * 1024)
+        TOEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SM::bytes)));
+      TOEP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, SM::bytes));
+      if (per_sm <= 0) per_sm = 1;
+    }
+    const int64_t grid = std::min<int64_t>(ntiles, static_cast<int64_t>(device_sms()) * per_sm);
+    return launch_k(kern, dim3(static_cast<unsigned>(grid)), dim3(kThreads), SM::bytes, s, a, 2.0 / L, ntiles, tiles_x);
+  };
+  if (a.in_planes != nullptr) return launch_kin(std::integral_constant<int, 2>{});
+  return launch_kin(std::integral_constant<int, 1>{});
+}
+
 // compile-time plan for L (7, 32, 60, 128), or -1
 template <typename TI, typename TC, typename TO>
 int try_plan(const PassArgs& a, cudaStream_t s) {
   switch (a.L) {
-    case 60: if (a.inner >= 16) return launch_plan<TI, TC, TO, 16, 4, 3, 5>(a, s); break;
+    case 60:
+      if (a.inner >= 16) {
+        if constexpr (std::is_same_v<TI, TC>) {
+          const int rc = try_stream<TC, TO, 16, 4, 3, 5>(a, s);
+          if (rc >= 0) return rc;
+        }
+        return launch_plan<TI, TC, TO, 16, 4, 3, 5>(a, s);
+      }
+      break;
     case 128: if (a.inner >= 8) return launch_plan<TI, TC, TO, 8, 4, 4, 4, 2>(a, s); break;
     case 32: if (a.inner >= 32) return launch_plan<TI, TC, TO, 32, 4, 4, 2>(a, s); break;
     case 64: if (a.inner >= 16) return launch_plan<TI, TC, TO, 16, 4, 4, 4>(a, s); break;
@@ -355,7 +507,7 @@ template <int... Rs> struct Plan {
   template <typename TI, typename TC, typename TO, int NT, int TIL>
   __device__ static void run(const PassArgs& a, const C<TI>* gin, C<TO>* gout, C<TC>* b0, C<TC>* b1,
                              const C<TC>* tw, int ncol, TC scale) {
-    plan_stage<TI, TC, TO, NT, TIL, L, 1, Rs...>(a, gin, gout, b0, b1, tw, ncol, scale);
+    plan_stage<TI, TC, TO, NT, TIL, L, 1, 0, Rs...>(a, gin, gout, b0, b1, tw, ncol, scale);
   }
 };
 

@@ -234,3 +234,23 @@ def test_nb128_kernel_variants_vs_dense(wcols):
     op32 = precompute_spectral(gen, dtype=torch.complex64)
     got = matvec(op32, u.astype(np.complex64))
     assert rel_err(np.asarray(got, dtype=np.complex128), dense @ u.astype(np.complex64)) <= 1e-5
+
+
+@pytest.mark.parametrize("dims", [(16, 16, 32), (16, 16, 64), (30, 30, 16), (12, 16, 8), (16, 9, 8)])
+@pytest.mark.parametrize("dtype", [torch.complex128, torch.complex64])
+def test_fused_2d_dft_grids_vs_oracle(dims, dtype):
+    # single-RHS matvecs on the grids with a one-CTA-per-column 2-D DFT instantiation (32x32 with
+    # n2 <= 16, 60x60 with n2 <= 30) and neighbours that fall back to the pass chain; forward and
+    # transpose against the numpy restatement of the reference pipeline
+    ny, nx, nb = dims
+    s4 = seeded_stacked4(ny, nx, nb, seed=ny + nx)
+    gen = generator_from_stacked(s4)
+    op = precompute_spectral(gen, dtype=dtype)
+    u = dense_rhs(gen.dim, seed=nb)
+    dims5 = (ny, nx, nb, 2 * ny - 1, 2 * nx - 1)
+    diag = oracle.mlfft.precompute_spectral(s4)
+    tol = 1e-12 if dtype == torch.complex128 else 1e-5
+    uu = u if dtype == torch.complex128 else u.astype(np.complex64)
+    assert rel_err(np.asarray(matvec(op, uu), np.complex128), oracle.mlfft.matvec(diag, dims5, uu)) <= tol
+    assert rel_err(np.asarray(matvec_transpose(op, uu), np.complex128),
+                   oracle.mlfft.matvec_transpose(diag, dims5, uu)) <= tol
