@@ -369,7 +369,7 @@ __device__ __forceinline__ void cp_async(void* smem, const void* g, int nbytes) 
 }
 
 template <typename TC, typename TO, int TIL, int kIn, int... Rs>
-__global__ void __launch_bounds__(kThreads, kStreamBlocks) fft_plan_stream_kernel(PassArgs a, double two_over_L,
+__global__ void __launch_bounds__(kThreads, TIL <= 8 ? 2 * kStreamBlocks : kStreamBlocks) fft_plan_stream_kernel(PassArgs a, double two_over_L,
                                                                                  int64_t ntiles, int64_t tiles_x) {
   using Z = C<TC>;
   constexpr int L = PlanLen<Rs...>::value;
@@ -483,7 +483,11 @@ int try_plan(const PassArgs& a, cudaStream_t s) {
     case 60:
       if (a.inner >= 16) {
         if constexpr (std::is_same_v<TI, TC>) {
-          const int rc = try_stream<TC, TO, 16, 4, 3, 5>(a, s);
+          static const int til = [] {
+            const char* e = std::getenv("TOEP_FFT_STREAM_TIL");
+            return e != nullptr ? std::atoi(e) : 16;
+          }();
+          const int rc = til == 8 ? try_stream<TC, TO, 8, 4, 3, 5>(a, s) : try_stream<TC, TO, 16, 4, 3, 5>(a, s);
           if (rc >= 0) return rc;
         }
         return launch_plan<TI, TC, TO, 16, 4, 3, 5>(a, s);
