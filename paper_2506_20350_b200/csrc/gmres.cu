@@ -458,6 +458,7 @@ struct OrthArgs {
   double2* part2;   // [ldr][nblk] partials of V^H v_{m-1}
 };
 constexpr int kMaxOrthM = 1024;  // basis vectors per cycle handled by the cooperative kernel
+constexpr int kOrthGroupedMinChunk = 2048;  // elements per CTA from which the grouped dot sweep is used
 
 // Grid barrier on a monotonic arrival counter (zeroed once per solve): every CTA adds 1 and
 // waits until the counter reaches the next multiple of gridDim.x (one atomic per CTA, no reset).
@@ -522,9 +523,9 @@ __device__ __forceinline__ double orth_update(const OrthArgs& a, const double2* 
   return nrm;
 }
 
-// One-sweep CGS2 dots: warp l computes both V_l^H w and V_l^H V_{m-1} over the chunk (the last
+// One-sweep CGS2 dots, one warp per basis vector (short chunks): warp l computes both V_l^H w and V_l^H V_{m-1} over the chunk (the last
 // basis vector's Gram column), reading V_l once; warp NW-1 also accumulates ||w||^2
-__device__ __forceinline__ void orth_dots_gram(const OrthArgs& a, int64_t c0, int64_t c1) {
+__device__ __forceinline__ void orth_dots_gram_pv(const OrthArgs& a, int64_t c0, int64_t c1) {
   constexpr int NW = kCoopThreads / 32, U = 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nblk = gridDim.x;
@@ -573,6 +574,83 @@ __device__ __forceinline__ void orth_dots_gram(const OrthArgs& a, int64_t c0, in
       a.part[static_cast<int64_t>(l) * nblk + blockIdx.x] = s1;
       a.part2[static_cast<int64_t>(l) * nblk + blockIdx.x] = s2;
     }
+  }
+}
+
+// One-sweep CGS2 dots over the CTA's chunk: V_l^H w and V_l^H V_{m-1} (the last basis vector's
+// Gram column) for every l, plus ||w||^2.  Work items are (group of G basis vectors) x (sub-chunk):
+// a warp reads w and V_{m-1} once per group instead of once per vector, and with few basis vectors
+// (early steps) the chunk is split over several warps per group so that all 32 warps keep loads
+// in flight.  Sub-chunk partials are combined in shared memory in a fixed order (deterministic).
+__device__ __forceinline__ void orth_dots_gram(const OrthArgs& a, int64_t c0, int64_t c1) {
+  constexpr int NW = kCoopThreads / 32, G = 4;
+  __shared__ double2 dpart[2][NW * G];
+  __shared__ double nsub[NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nblk = gridDim.x, m = a.m;
+  const double2* vl = a.V + static_cast<int64_t>(m - 1) * a.N;
+  const int ngroups = (m + G - 1) / G;
+  const int64_t len = c1 - c0;
+  const int S = ngroups >= NW ? 1 : NW / ngroups;  // warps (sub-chunks) per group; S * m <= NW * G
+  for (int item = warp; item < ngroups * S; item += NW) {
+    const int g = item / S, sc = item - g * S;
+    const int64_t s0 = c0 + ((len * sc / S) / 32) * 32;
+    const int64_t s1 = (sc + 1 == S) ? c1 : c0 + ((len * (sc + 1) / S) / 32) * 32;
+    const int l0 = g * G;
+    const int nl = min(G, m - l0);
+    const double2* v0 = a.V + static_cast<int64_t>(l0) * a.N;
+    double2 acc[G], acg[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) acc[u] = acg[u] = make_double2(0, 0);
+    double wn = 0.0;
+    for (int64_t i = s0 + lane; i < s1; i += 32) {
+      const double2 wi = a.w[i], li = vl[i];
+      double2 vv[G];
+#pragma unroll
+      for (int u = 0; u < G; ++u) vv[u] = u < nl ? v0[u * a.N + i] : make_double2(0, 0);
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        cfmac(acc[u], vv[u], wi);
+        cfmac(acg[u], vv[u], li);
+      }
+      wn = fma(wi.x, wi.x, fma(wi.y, wi.y, wn));
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      if (u >= nl) break;
+      const double2 d1 = warp_sum(acc[u]);
+      const double2 d2 = warp_sum(acg[u]);
+      if (lane == 0) {
+        if (S == 1) {
+          a.part[static_cast<int64_t>(l0 + u) * nblk + blockIdx.x] = d1;
+          a.part2[static_cast<int64_t>(l0 + u) * nblk + blockIdx.x] = d2;
+        } else {
+          dpart[0][sc * m + l0 + u] = d1;
+          dpart[1][sc * m + l0 + u] = d2;
+        }
+      }
+    }
+    if (g == 0) {
+      wn = warp_sum(wn);
+      if (lane == 0) nsub[sc] = wn;
+    }
+  }
+  __syncthreads();
+  if (S > 1) {
+    for (int l = threadIdx.x; l < m; l += kCoopThreads) {
+      double2 d1 = dpart[0][l], d2 = dpart[1][l];
+      for (int sc = 1; sc < S; ++sc) {
+        d1 = cadd(d1, dpart[0][sc * m + l]);
+        d2 = cadd(d2, dpart[1][sc * m + l]);
+      }
+      a.part[static_cast<int64_t>(l) * nblk + blockIdx.x] = d1;
+      a.part2[static_cast<int64_t>(l) * nblk + blockIdx.x] = d2;
+    }
+  }
+  if (threadIdx.x == 0) {
+    double t = nsub[0];
+    for (int sc = 1; sc < S; ++sc) t += nsub[sc];
+    a.npart[blockIdx.x] = t;
   }
 }
 
@@ -734,7 +812,10 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
     // G = V^H V, the basis Gram matrix, whose new column comes out of the same sweep as h1; then
     // one update w'' = w - V (h1 + h2) and ||w''||^2 = ||w||^2 - 2 Re(h^H h1) + h^H G h.
     // One grid barrier and two basis sweeps per step instead of three barriers and four sweeps.
-    orth_dots_gram(a, c0, c1);
+    // grouped sweep for long chunks (cfg4: 3 567 elements per CTA, GMRES 23.4 -> 22.8 ms); per-vector
+    // warps for short ones (cfg1 / cfg2 chunks of 32 / 784 elements measured slower grouped)
+    if (a.N >= static_cast<int64_t>(kOrthGroupedMinChunk) * (gridDim.x - 1)) orth_dots_gram(a, c0, c1);
+    else orth_dots_gram_pv(a, c0, c1);
     grid_barrier(a.bar);
     const int m = a.m, nblk = gridDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
