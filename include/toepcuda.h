@@ -93,6 +93,10 @@ TOEP_API int toep_op_fold_left(toep_op_t op, const void* m_dev, void* stream, to
  * u, v: (n, w) device column blocks.  pad_rhs / extract_result (:256-284) are
  * fused into the first / last FFT pass.  v must not alias u. */
 TOEP_API int toep_matvec(toep_op_t op, const void* u, void* v, int64_t w, int flags, void* stream);
+/* toep_matvec with HOST u / v (pinned for overlap-free DMA; pageable works): copy in, apply, copy
+ * out and synchronise `stream` in one call (the numpy-in / numpy-out contract of toeplitz.py:287-303
+ * without per-call device allocations); device staging is owned by the operator, per stream. */
+TOEP_API int toep_matvec_host(toep_op_t op, const void* u_host, void* v_host, int64_t w, int flags, void* stream);
 
 /* Multi-GPU row / kx-slab decomposition (no reference counterpart:
  * the reference is single-process).  toep_op_slab: operator holding only the bins with

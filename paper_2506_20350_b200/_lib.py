@@ -92,6 +92,7 @@ SIGNATURES = {
     "toep_op_diag_blocks": (c_int, [c_vp, c_vp, c_vp]),
     "toep_op_fold_left": (c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(c_vp)]),
     "toep_matvec": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
+    "toep_matvec_host": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
     "toep_op_slab": (c_int, [c_vp, c_int, c_int, c_vp, ctypes.POINTER(c_vp)]),
     "toep_matvec_stage": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_int, c_vp]),
     "toep_matvec_stage_peer": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_int, c_vp]),

@@ -411,6 +411,7 @@ int toep_op_destroy(toep_op_t op) {
     cudaFree(kv.second.cnt);
     cudaFree(kv.second.hatp);
     cudaFree(kv.second.hat2p);
+    cudaFree(kv.second.io);
   }
   cudaFree(op->DT);
   cudaFree(op->DTp);
@@ -571,6 +572,41 @@ int toep_matvec(toep_op_t op, const void* u, void* v, int64_t w, int flags, void
   TOEP_REQUIRE(u != v, TOEP_ERR_ARG, "matvec output must not alias its input");
   return matvec_impl(op, u, v, w, (flags & TOEP_MV_TRANSPOSE) != 0, (flags & TOEP_MV_IO_C128) != 0, nullptr,
                      static_cast<cudaStream_t>(stream));
+}
+
+int toep_matvec_host(toep_op_t op, const void* u_host, void* v_host, int64_t w, int flags, void* stream) {
+  TOEP_REQUIRE(op != nullptr && (w == 0 || (u_host != nullptr && v_host != nullptr)), TOEP_ERR_ARG, "null argument");
+  TOEP_REQUIRE(op->slab_kxs == 0, TOEP_ERR_ARG, "a slab operator is applied through toep_matvec_stage");
+  TOEP_REQUIRE(w >= 0, TOEP_ERR_SHAPE, "negative column count");
+  TOEP_REQUIRE(u_host != v_host, TOEP_ERR_ARG, "matvec output must not alias its input");
+  if (w == 0) return TOEP_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool io_c128 = (flags & TOEP_MV_IO_C128) != 0;
+  const size_t bytes = static_cast<size_t>(toep::op_dim(op)) * w * (io_c128 ? 16 : toep::elt_size(op->dtype));
+  toep_op_s::Workspace* ws = nullptr;
+  {
+    toep::keep_pool();
+    std::lock_guard<std::mutex> lock(op->mu);
+    ws = &op->ws[s];
+    if (ws->io_cap < 2 * bytes) {
+      if (ws->io) TOEP_CUDA(cudaFreeAsync(ws->io, s));
+      ws->io = nullptr;
+      ws->io_cap = 0;
+      if (cudaMallocAsync(&ws->io, 2 * bytes, s) != cudaSuccess) {
+        cudaGetLastError();
+        toep::set_error("out of device memory for host matvec staging (w=%lld)", static_cast<long long>(w));
+        return TOEP_ERR_OOM;
+      }
+      ws->io_cap = 2 * bytes;
+    }
+  }
+  char* ud = static_cast<char*>(ws->io);
+  char* vd = ud + bytes;
+  TOEP_CUDA(cudaMemcpyAsync(ud, u_host, bytes, cudaMemcpyHostToDevice, s));
+  TOEP_TRY(toep::matvec_impl(op, ud, vd, w, (flags & TOEP_MV_TRANSPOSE) != 0, io_c128, nullptr, s));
+  TOEP_CUDA(cudaMemcpyAsync(v_host, vd, bytes, cudaMemcpyDeviceToHost, s));
+  TOEP_CUDA(cudaStreamSynchronize(s));
+  return TOEP_OK;
 }
 
 int toep_op_spectral_apply(toep_op_t op, const void* hat_in, void* hat_out, int64_t w, int flags, void* stream) {

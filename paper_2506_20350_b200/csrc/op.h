@@ -23,6 +23,8 @@ struct toep_op_s {
     double* hatp = nullptr;   // multi-RHS 3M: planes of u_hat (3 x K*n0*w)
     double* hat2p = nullptr;  // multi-RHS 3M: product planes T1, T2, T3
     int64_t p_cap = 0;
+    void* io = nullptr;  // toep_matvec_host: device copies of u and v
+    size_t io_cap = 0;
   };
   // kx-slab operator of the multi-GPU row/slab decomposition (toep_op_slab): bins
   // k' = ky*slab_kxs + (kx - slab_k0); 0 = full operator

@@ -260,6 +260,9 @@ def precompute_spectral(gen: BlockGenerator2L, dtype=torch.complex128, embedding
 
 
 def _apply(op: SpectralOperator, u, flags: int):
+    if isinstance(u, torch.Tensor) and not u.is_cuda and u.is_pinned() and u.ndim in (1, 2) and u.is_contiguous() \
+            and not u.is_conj() and not u.is_neg() and (u.dtype == op.dtype or u.dtype == torch.complex128):
+        return _apply_pinned(op, u, flags)
     x, origin = to_columns(u, keep_c64=(op.dtype == torch.complex64))
     if x.shape[0] != op.dim:
         raise ShapeError(f"rows {x.shape[0]} != operator dim {op.dim}")
@@ -269,6 +272,23 @@ def _apply(op: SpectralOperator, u, flags: int):
     _lib.check(_lib.lib().toep_matvec(op.handle, x.data_ptr(), out.data_ptr(), x.shape[1], flags,
                                       _lib.stream_handle()), "matvec")
     return restore(out, origin)
+
+
+def _apply_pinned(op: SpectralOperator, u: torch.Tensor, flags: int):
+    """Pinned host tensor in -> pinned host tensor out, one library call (copy in, apply, copy out,
+    synchronise): no device tensors are created per call."""
+    _lib.require_cuda()
+    rows = u.shape[0]
+    w = 1 if u.ndim == 1 else u.shape[1]
+    if rows != op.dim:
+        raise ShapeError(f"rows {rows} != operator dim {op.dim}")
+    if op.dtype == torch.complex64 and u.dtype == torch.complex128:
+        flags |= _lib.TOEP_MV_IO_C128
+    out = torch.empty(u.shape, dtype=u.dtype, pin_memory=True)
+    if w:
+        _lib.check(_lib.lib().toep_matvec_host(op.handle, u.data_ptr(), out.data_ptr(), w, flags,
+                                               _lib.stream_handle()), "matvec")
+    return out
 
 
 def matvec(op: SpectralOperator, u):

@@ -254,3 +254,21 @@ def test_fused_2d_dft_grids_vs_oracle(dims, dtype):
     assert rel_err(np.asarray(matvec(op, uu), np.complex128), oracle.mlfft.matvec(diag, dims5, uu)) <= tol
     assert rel_err(np.asarray(matvec_transpose(op, uu), np.complex128),
                    oracle.mlfft.matvec_transpose(diag, dims5, uu)) <= tol
+
+
+@pytest.mark.parametrize("dtype", [torch.complex128, torch.complex64])
+def test_pinned_host_matvec_single_call(dtype):
+    # pinned CPU tensors go through toep_matvec_host (copy in, apply, copy out in one call): same
+    # result as the device path, pinned CPU result, vector and column-block shapes, transpose
+    gen = generator_from_stacked(seeded_stacked4(6, 5, 16, seed=2))
+    op = precompute_spectral(gen, dtype=dtype)
+    tol = 1e-12 if dtype == torch.complex128 else 1e-5
+    for shape in [(gen.dim,), (gen.dim, 3)]:
+        u = torch.from_numpy(dense_rhs(gen.dim, 1 if len(shape) == 1 else shape[1], seed=4).reshape(shape))
+        for fn in (matvec, matvec_transpose):
+            want = fn(op, u.cuda()).cpu()
+            got = fn(op, u.pin_memory())
+            assert got.device.type == "cpu" and got.is_pinned() and got.shape == u.shape
+            assert rel_err(got.numpy(), want.numpy()) <= tol
+    with pytest.raises(ShapeError):
+        matvec(op, torch.zeros(gen.dim + 1, dtype=torch.complex128).pin_memory())
