@@ -254,14 +254,24 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
           if (row >= 0 && col < ncol) {
             const double* sp = reinterpret_cast<const double*>(src);
             const int nr = a.n_lo + a.n_hi;
-            const double t1 = sp[row * TIL + col], t2 = sp[(nr + row) * TIL + col], t3 = sp[(2 * nr + row) * TIL + col];
-            v[r] = mk<TC>(static_cast<TC>(t1 - t2), static_cast<TC>(t3 - t1 - t2));
+            const double t1 = sp[row * TIL + col], t2 = sp[(nr + row) * TIL + col];
+            if (a.planes2) {
+              v[r] = mk<TC>(static_cast<TC>(t1), static_cast<TC>(t2));
+            } else {
+              const double t3 = sp[(2 * nr + row) * TIL + col];
+              v[r] = mk<TC>(static_cast<TC>(t1 - t2), static_cast<TC>(t3 - t1 - t2));
+            }
           }
         } else if (row >= 0 && col < ncol) {
           if (a.in_planes != nullptr) {
             const int64_t e = (gin - static_cast<const C<TI>*>(a.in)) + row * a.in_sa + col * a.in_cs;
-            const double t1 = a.in_planes[e], t2 = a.in_planes[a.plane + e], t3 = a.in_planes[2 * a.plane + e];
-            v[r] = mk<TC>(static_cast<TC>(t1 - t2), static_cast<TC>(t3 - t1 - t2));
+            const double t1 = a.in_planes[e], t2 = a.in_planes[a.plane + e];
+            if (a.planes2) {
+              v[r] = mk<TC>(static_cast<TC>(t1), static_cast<TC>(t2));
+            } else {
+              const double t3 = a.in_planes[2 * a.plane + e];
+              v[r] = mk<TC>(static_cast<TC>(t1 - t2), static_cast<TC>(t3 - t1 - t2));
+            }
           } else if (a.part_count == nullptr) {
             v[r] = cvt<Z>(gin[row * a.in_sa + col * a.in_cs]);
           } else {
@@ -296,7 +306,7 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
               const Z val = cscale(v[q], scale);
               a.out_planes[e] = static_cast<double>(val.x);
               a.out_planes[a.plane + e] = static_cast<double>(val.y);
-              a.out_planes[2 * a.plane + e] = static_cast<double>(val.x) + static_cast<double>(val.y);
+              if (!a.planes2) a.out_planes[2 * a.plane + e] = static_cast<double>(val.x) + static_cast<double>(val.y);
             } else {
               gout[idx * a.out_sa + col * a.out_cs] = cvt<C<TO>>(cscale(v[q], scale));
             }
@@ -401,8 +411,8 @@ __global__ void __launch_bounds__(kThreads, TIL <= 8 ? 2 * kStreamBlocks : kStre
         cp_async(buf + e, static_cast<const Z*>(a.in) + ge, static_cast<int>(sizeof(Z)));
       } else {
         double* bd = reinterpret_cast<double*>(buf);
-#pragma unroll
-        for (int p = 0; p < 3; ++p) cp_async(bd + p * nrows * TIL + e, a.in_planes + p * a.plane + ge, 8);
+        const int np = a.planes2 ? 2 : 3;
+        for (int p = 0; p < np; ++p) cp_async(bd + p * nrows * TIL + e, a.in_planes + p * a.plane + ge, 8);
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");

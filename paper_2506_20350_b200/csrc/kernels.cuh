@@ -44,6 +44,7 @@ struct PassArgs {
   double* out_planes = nullptr;
   const double* in_planes = nullptr;
   int64_t plane = 0;
+  int planes2 = 0;  // 1: (re, im) planes only — out: no re+im plane; in: (T1, T2) = (re, im) directly
   // optional peer scatter (toep_matvec_stage_peer): device table routing output index a to the
   // destination rank's receive buffer, plus the arrival signal after the launch's last store
   const toep_peer_scatter* scatter = nullptr;
@@ -119,6 +120,16 @@ bool fft_plan_has_planes(int L, int64_t inner);
 int dgemm_tc_rm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t lda, int64_t a_bs,
                 const double* b, int64_t ldb, int64_t b_bs, double beta, double* c, int64_t ldc, int64_t c_bs,
                 int64_t batch, cudaStream_t s);
+
+// Ozaki-scheme FP64 per-bin products on the int8 tensor cores (ozaki.cu): operator slices once,
+// then per chunk of bins: slice the (re, im) planes of U and write the (re, im) planes of D U
+bool ozaki_supported(int n0);
+int64_t ozaki_a_bytes(int n0, int64_t K);
+int64_t ozaki_b_bytes(int n0, int64_t bins, int64_t w);
+int64_t ozaki_b_exps(int64_t bins, int64_t w);
+int ozaki_slice_a(const void* DT, int n0, int l2, int l1, int8_t* asl, int32_t* aexp, cudaStream_t s);
+int ozaki_products(const int8_t* asl, const int32_t* aexp, const double* re, const double* im, int n0, int64_t bins,
+                   int64_t w, int8_t* bsl, int32_t* bexp, double* out_re, double* out_im, cudaStream_t s);
 
 // batched transpose of complex matrices: out[b][c][r] = in[b][r][c]  (rows x cols)
 int transpose_batched(int dtype, const void* in, void* out, int64_t batch, int rows, int cols, cudaStream_t s);

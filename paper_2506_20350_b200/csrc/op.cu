@@ -118,10 +118,52 @@ bool mrhs_3m(const toep_op_s* op, int64_t w, bool transpose) {
          fft_plan_has_planes(op->l2, static_cast<int64_t>(op->n0) * w);
 }
 
-int ensure_planes(toep_op_s* op, toep_op_s::Workspace* ws, int64_t w, cudaStream_t s) {
+// Ozaki scheme for the multi-RHS per-bin products (ozaki.cu: int8 tensor cores, FP64-accurate);
+// TOEP_MRHS_OZAKI=0 keeps the 3M DMMA GEMMs
+bool mrhs_ozaki(const toep_op_s* op) {
+  static const bool on = [] {
+    const char* e = std::getenv("TOEP_MRHS_OZAKI");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on && ozaki_supported(op->n0);
+}
+
+int ensure_ozaki(toep_op_s* op, toep_op_s::Workspace* ws, int64_t w, int kc, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(op->mu);
+  if (op->oz_a == nullptr) {
+    const int64_t abytes = ozaki_a_bytes(op->n0, op->K);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&op->oz_a), abytes, s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&op->oz_aexp), op->K * 2 * op->n0 * sizeof(int32_t), s) !=
+            cudaSuccess) {
+      cudaGetLastError();
+      set_error("out of device memory for the operator's int8 slices");
+      return TOEP_ERR_OOM;
+    }
+    TOEP_TRY(ozaki_slice_a(op->DT, op->n0, op->l2, op->l1, op->oz_a, op->oz_aexp, s));
+  }
+  if (ws->oz_cap < w) {
+    if (ws->oz_b) TOEP_CUDA(cudaFreeAsync(ws->oz_b, s));
+    if (ws->oz_bexp) TOEP_CUDA(cudaFreeAsync(ws->oz_bexp, s));
+    ws->oz_b = nullptr;
+    ws->oz_bexp = nullptr;
+    ws->oz_cap = 0;
+    const int64_t bins = static_cast<int64_t>(kc) * op->l2;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&ws->oz_b), ozaki_b_bytes(op->n0, bins, w), s) != cudaSuccess ||
+        cudaMallocAsync(reinterpret_cast<void**>(&ws->oz_bexp), ozaki_b_exps(bins, w) * sizeof(int32_t), s) !=
+            cudaSuccess) {
+      cudaGetLastError();
+      set_error("out of device memory for the int8 right-hand-side slices (w=%lld)", static_cast<long long>(w));
+      return TOEP_ERR_OOM;
+    }
+    ws->oz_cap = w;
+  }
+  return TOEP_OK;
+}
+
+int ensure_planes(toep_op_s* op, toep_op_s::Workspace* ws, int64_t w, cudaStream_t s, bool need_dtp) {
   std::lock_guard<std::mutex> lock(op->mu);
   const int64_t kn = op->K * op->n0;
-  if (op->DTp == nullptr) {
+  if (need_dtp && op->DTp == nullptr) {
     const int64_t cnt = kn * op->n0;
     if (cudaMallocAsync(reinterpret_cast<void**>(&op->DTp), 3 * cnt * sizeof(double), s) != cudaSuccess) {
       cudaGetLastError();
@@ -224,8 +266,10 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
     // 3M in kx-chunks: level-2 DFT of the chunk's columns into split planes (bins kx-major within
     // the chunk), three real batched GEMMs against the operator planes, inverse level-2 DFT
     // recombining (T1 - T2) + i (T3 - T1 - T2) into x1
-    TOEP_TRY(ensure_planes(op, ws, w, s));
+    const bool oz = mrhs_ozaki(op);
+    TOEP_TRY(ensure_planes(op, ws, w, s, !oz));
     const int kc = mrhs_chunk(op, w);
+    if (oz) TOEP_TRY(ensure_ozaki(op, ws, w, kc, s));
     const int64_t n0 = op->n0, nw = n0 * w, dn = op->K * n0 * n0;
     const int64_t plane = static_cast<int64_t>(op->l2) * kc * nw;  // doubles per plane (one chunk)
     for (int kx0 = 0; kx0 < op->l1; kx0 += kc) {
@@ -235,19 +279,26 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
       b.out = ws->hatp; b.L = op->l2; b.n_lo = op->n2; b.n_hi = 0; b.n_out = op->l2;
       b.inner = inner; b.outer = cnt; b.in_sa = op->l1 * inner; b.in_so = inner; b.out_sa = inner;
       b.out_so = op->l2 * inner; b.sign = s1; b.scale = sc1y; b.stop = stop;
-      b.out_planes = ws->hatp; b.plane = plane;
+      b.out_planes = ws->hatp; b.plane = plane; b.planes2 = oz;
       TOEP_TRY(fft_pass(b, tc, tc, tc, s));
       const int64_t bins = static_cast<int64_t>(cnt) * op->l2;
-      const int64_t dofs = static_cast<int64_t>(kx0) * op->l2 * n0 * n0;
-      for (int q = 0; q < 3; ++q)
-        TOEP_TRY(dgemm_tc_crr(n0, w, n0, op->DTp + q * dn + dofs, n0, n0 * n0, ws->hatp + q * plane, w, nw,
-                              ws->hat2p + q * plane, w, nw, bins, s));
+      const int64_t bin0 = static_cast<int64_t>(kx0) * op->l2;  // kx-major bin index of the chunk
+      if (oz) {
+        TOEP_TRY(ozaki_products(op->oz_a + bin0 * ozaki_a_bytes(op->n0, 1), op->oz_aexp + bin0 * 2 * n0, ws->hatp,
+                                ws->hatp + plane, op->n0, bins, w, ws->oz_b, ws->oz_bexp, ws->hat2p,
+                                ws->hat2p + plane, s));
+      } else {
+        const int64_t dofs = bin0 * n0 * n0;
+        for (int q = 0; q < 3; ++q)
+          TOEP_TRY(dgemm_tc_crr(n0, w, n0, op->DTp + q * dn + dofs, n0, n0 * n0, ws->hatp + q * plane, w, nw,
+                                ws->hat2p + q * plane, w, nw, bins, s));
+      }
       PassArgs c;  // inverse level 2, keep rows y < n2 -> x1 columns [kx0, kx0+cnt)
       c.in = ws->hat2p; c.out = static_cast<char*>(ws->x1) + kx0 * inner * elt_size(op->dtype);
       c.L = op->l2; c.n_lo = op->l2; c.n_hi = 0; c.n_out = op->n2;
       c.inner = inner; c.outer = cnt; c.in_sa = inner; c.in_so = op->l2 * inner; c.out_sa = op->l1 * inner;
       c.out_so = inner; c.sign = -s1; c.scale = sc2y; c.stop = stop;
-      c.in_planes = ws->hat2p; c.plane = plane;
+      c.in_planes = ws->hat2p; c.plane = plane; c.planes2 = oz;
       TOEP_TRY(fft_pass(c, tc, tc, tc, s));
     }
   } else {
@@ -412,7 +463,11 @@ int toep_op_destroy(toep_op_t op) {
     cudaFree(kv.second.hatp);
     cudaFree(kv.second.hat2p);
     cudaFree(kv.second.io);
+    cudaFree(kv.second.oz_b);
+    cudaFree(kv.second.oz_bexp);
   }
+  cudaFree(op->oz_a);
+  cudaFree(op->oz_aexp);
   cudaFree(op->DT);
   cudaFree(op->DTp);
   cudaFree(op->part_count);

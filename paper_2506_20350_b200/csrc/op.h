@@ -25,7 +25,12 @@ struct toep_op_s {
     int64_t p_cap = 0;
     void* io = nullptr;  // toep_matvec_host: device copies of u and v
     size_t io_cap = 0;
+    int8_t* oz_b = nullptr;     // Ozaki path: int8 slices of one chunk's U planes
+    int32_t* oz_bexp = nullptr; // and their column exponents
+    int64_t oz_cap = 0;         // w the buffers were sized for
   };
+  int8_t* oz_a = nullptr;       // Ozaki path: int8 slices of [Dr -Di; Di Dr] per bin (kx-major)
+  int32_t* oz_aexp = nullptr;   // row exponents
   // kx-slab operator of the multi-GPU row/slab decomposition (toep_op_slab): bins
   // k' = ky*slab_kxs + (kx - slab_k0); 0 = full operator
   int slab_k0 = 0, slab_kxs = 0;
