@@ -41,7 +41,7 @@ constexpr int kBK = 32;          // K bytes per stage
 constexpr int kATile = kS * kBM * kBK;  // 28 672 B
 constexpr int kBTile = kS * kBN * kBK;  // 14 336 B
 constexpr int kStages = 4;
-constexpr int kOzThreads = 128;
+constexpr int kOzThreads = 256;  // 8 warps: warp w reads TMEM lane quarter w % 4, column half w / 4
 
 // element offset of (row, kk) inside one slice of a [g][c][r][16] tile (kk < kBK)
 __device__ __forceinline__ int core_off(int row, int kk) {
@@ -252,7 +252,8 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
   const uint32_t tmem = tmem_base;
   const int8_t* Ab = a.asl + (static_cast<int64_t>(b) * mtiles + mt) * kcs * kATile;
   const int8_t* Bb = a.bsl + static_cast<int64_t>(b) * nt_count * kcs * kBTile;
-  const int row = mt * kBM + warp * 32 + lane;  // this thread's output row (epilogue)
+  const int quarter = warp & 3, chalf = warp >> 2;
+  const int row = mt * kBM + quarter * 32 + lane;  // this thread's output row (epilogue)
   const double srow = ldexp(1.0, a.aexp[static_cast<int64_t>(b) * kdim + row]);
   __shared__ double scol[kBN];
   double* orow = (row < a.n0 ? a.out_re + (static_cast<int64_t>(b) * a.n0 + row) * a.w
@@ -306,10 +307,10 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
     const int32_t* fe = a.bexp + (static_cast<int64_t>(b) * nt_count + nt) * kBN;
     if (tid < kBN) scol[tid] = ldexp(1.0, __ldg(fe + tid));
     __syncthreads();
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
     const bool vec = (a.w & 1) == 0;
 #pragma unroll 1
-    for (int cc = 0; cc < (a.dbg == 1 ? 0 : kBN / 16); ++cc) {
+    for (int cc = chalf * (kBN / 32); cc < (a.dbg == 1 ? 0 : (chalf + 1) * (kBN / 32)); ++cc) {
       uint32_t v[kG][16];
 #pragma unroll
       for (int g = 0; g < kG; ++g) {

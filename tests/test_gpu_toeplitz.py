@@ -272,3 +272,17 @@ def test_pinned_host_matvec_single_call(dtype):
             assert rel_err(got.numpy(), want.numpy()) <= tol
     with pytest.raises(ShapeError):
         matvec(op, torch.zeros(gen.dim + 1, dtype=torch.complex128).pin_memory())
+
+
+@pytest.mark.parametrize("dims,w", [((16, 16, 64), 24), ((16, 16, 64), 70), ((16, 16, 128), 16)])
+def test_multi_rhs_int8_tensor_core_products_vs_oracle(dims, w):
+    # W >= 16 on a grid with a compiled level-2 plan (l2 = 32) routes the per-bin products through
+    # the Ozaki-scheme int8 tensor-core kernel (ozaki.cu); partial column tiles (w % 64 != 0)
+    ny, nx, nb = dims
+    s4 = seeded_stacked4(ny, nx, nb, seed=w)
+    gen = generator_from_stacked(s4)
+    op = precompute_spectral(gen)
+    assert op.l2 == 32
+    u = dense_rhs(gen.dim, w, seed=5)
+    want = oracle.mlfft.matvec(oracle.mlfft.precompute_spectral(s4), (ny, nx, nb, 2 * ny - 1, 2 * nx - 1), u)
+    assert rel_err(matvec(op, u), want) <= 1e-12
