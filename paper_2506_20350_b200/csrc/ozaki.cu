@@ -34,13 +34,12 @@ namespace toep {
 namespace {
 
 constexpr int kS = 7;            // slices per operand
-constexpr int kG = kS;           // accumulator groups t = 2 .. kS + 1
 constexpr int kBM = 128;         // rows per tile
-constexpr int kBN = 64;          // columns per tile
+constexpr int kBN = 128;         // columns per tile
 constexpr int kBK = 32;          // K bytes per stage
 constexpr int kATile = kS * kBM * kBK;  // 28 672 B
-constexpr int kBTile = kS * kBN * kBK;  // 14 336 B
-constexpr int kStages = 4;
+constexpr int kBTile = kS * kBN * kBK;  // 28 672 B
+constexpr int kStages = 3;
 constexpr int kOzThreads = 256;  // 8 warps: warp w reads TMEM lane quarter w % 4, column half w / 4
 
 // element offset of (row, kk) inside one slice of a [g][c][r][16] tile (kk < kBK)
@@ -223,17 +222,25 @@ struct OzArgs {
   int dbg;  // experiment switch (TOEP_OZ_DBG): 1 = no epilogue math / stores, 2 = no operand loads
 };
 
+// Groups t = 2..8 do not fit TMEM side by side at N = 128 (7 x 128 columns), so every column tile
+// runs two phases over K: phase 0 accumulates t = 2..5 (4 x 128 columns, digits 1..4 only) into the
+// exact integer G2 2^21 + G3 2^14 + G4 2^7 + G5, kept in registers; phase 1 accumulates t = 6..8,
+// adds 2^-56 (G6 2^14 + G7 2^7 + G8) to 2^-35 times it, scales and stores.  N = 128 halves the shared-memory operand reads per MAC of the
+// N = 64 single-phase tile (the tensor core's smem bandwidth is what bounds N = 64).
+__device__ __forceinline__ int phase_slices(int ph) { return ph == 0 ? 4 : kS; }
+
 __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
   extern __shared__ __align__(1024) unsigned char oz_smem[];
   int8_t* sA = reinterpret_cast<int8_t*>(oz_smem);              // [kStages][kATile]
   int8_t* sB = sA + kStages * kATile;                            // [kStages][kBTile]
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull;
   __shared__ uint32_t tmem_base;
+  __shared__ double scol[kBN];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.y, mt = blockIdx.x;  // the row tiles of one bin run together (B tiles reused from L2)
   const int kdim = 2 * a.n0, kcs = kdim / kBK, mtiles = kdim / kBM;
   const int nt_count = a.ntiles;
-  const int total = nt_count * kcs;
+  const int total = nt_count * 2 * kcs;  // steps: (column tile, phase, K chunk)
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -255,96 +262,122 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
   const int quarter = warp & 3, chalf = warp >> 2;
   const int row = mt * kBM + quarter * 32 + lane;  // this thread's output row (epilogue)
   const double srow = ldexp(1.0, a.aexp[static_cast<int64_t>(b) * kdim + row]);
-  __shared__ double scol[kBN];
   double* orow = (row < a.n0 ? a.out_re + (static_cast<int64_t>(b) * a.n0 + row) * a.w
                              : a.out_im + (static_cast<int64_t>(b) * a.n0 + row - a.n0) * a.w);
   const uint64_t pol = policy_evict_last();
-  int issued = 0;  // producer: next global step (nt * kcs + kc) to load
+  int issued = 0;  // producer: next step to load
   auto produce_until = [&](int limit) {
     for (; issued < limit && issued < total; ++issued) {
       const int st = issued % kStages;
       if (issued >= kStages) mbar_wait(&empty[st], ((issued / kStages) - 1) & 1);
-      const int nt = issued / kcs, kc = issued - nt * kcs;
+      const int tp = issued / kcs, kc = issued - tp * kcs;  // tp = nt * 2 + phase
+      const int nt = tp >> 1;
       if (a.dbg == 2) {
         mbar_arrive(&full[st]);
         continue;
       }
-      mbar_expect_tx(&full[st], kATile + kBTile);
-      bulk_g2s(sA + st * kATile, Ab + static_cast<int64_t>(kc) * kATile, kATile, &full[st], pol);
-      bulk_g2s(sB + st * kBTile, Bb + (static_cast<int64_t>(nt) * kcs + kc) * kBTile, kBTile, &full[st], pol);
+      const uint32_t bytes = static_cast<uint32_t>(phase_slices(tp & 1)) * (kBM * kBK);  // kBM == kBN
+      mbar_expect_tx(&full[st], 2 * bytes);
+      bulk_g2s(sA + st * kATile, Ab + static_cast<int64_t>(kc) * kATile, bytes, &full[st], pol);
+      bulk_g2s(sB + st * kBTile, Bb + (static_cast<int64_t>(nt) * kcs + kc) * kBTile, bytes, &full[st], pol);
     }
   };
+  const bool vec = (a.w & 1) == 0;
+  double part[kBN / 2];  // per-thread partial sums of its 64 output columns (registers)
   for (int nt = 0; nt < nt_count; ++nt) {
-    if (warp == 0 && lane == 0) produce_until((nt + 1) * kcs);
-    if (warp == 1 && lane == 0) {
-      for (int kc = 0; kc < kcs; ++kc) {
-        const int step = nt * kcs + kc, st = step % kStages;
-        mbar_wait(&full[st], (step / kStages) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
+    const int32_t* fe = a.bexp + (static_cast<int64_t>(b) * nt_count + nt) * kBN;
+    if (tid < kBN) scol[tid] = ldexp(1.0, __ldg(fe + tid));  // read after the phase-0 barrier below
+    for (int ph = 0; ph < 2; ++ph) {
+      const int tp = nt * 2 + ph;
+      if (warp == 0 && lane == 0) produce_until((tp + 1) * kcs);
+      if (warp == 1 && lane == 0) {
+        for (int kc = 0; kc < kcs; ++kc) {
+          const int step = tp * kcs + kc, st = step % kStages;
+          mbar_wait(&full[st], (step / kStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
+          if (ph == 0) {
 #pragma unroll
-        for (int p = 1; p <= kS; ++p) {
+            for (int p = 1; p <= 4; ++p) {
 #pragma unroll
-          for (int q = 1; q + p <= kS + 1; ++q) {
-            const uint32_t acc_col = tmem + static_cast<uint32_t>((p + q - 2) * kBN);
+              for (int q = 1; p + q <= 5; ++q)
+                mma_i8(tmem + static_cast<uint32_t>((p + q - 2) * kBN),
+                       umma_desc(a0 + (p - 1) * (kBM * kBK)), umma_desc(b0 + (q - 1) * (kBN * kBK)),
+                       (kc > 0 || p > 1) ? 1u : 0u);
+            }
+          } else {
 #pragma unroll
-            for (int k32 = 0; k32 < kBK / 32; ++k32) {
-              const uint64_t da = umma_desc(a0 + (p - 1) * (kBM * kBK) + k32 * 256);
-              const uint64_t db = umma_desc(b0 + (q - 1) * (kBN * kBK) + k32 * 256);
-              mma_i8(acc_col, da, db, (kc > 0 || k32 > 0 || p > 1) ? 1u : 0u);
+            for (int p = 1; p <= kS; ++p) {
+#pragma unroll
+              for (int q = (6 - p > 1 ? 6 - p : 1); p + q <= kS + 1; ++q)
+                mma_i8(tmem + static_cast<uint32_t>((p + q - 6) * kBN),
+                       umma_desc(a0 + (p - 1) * (kBM * kBK)), umma_desc(b0 + (q - 1) * (kBN * kBK)),
+                       (kc > 0 || p > 1) ? 1u : 0u);
+            }
+          }
+          umma_commit(&empty[st]);  // smem slot free once these MMAs have read it
+        }
+        umma_commit(&tfull);        // this phase's accumulators complete
+      }
+      // the producer runs ahead into the next phase before joining the epilogue
+      if (warp == 0 && lane == 0) produce_until((tp + 1) * kcs + kStages);
+      __syncwarp();
+      mbar_wait(&tfull, tp & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      __syncthreads();  // scol visible
+      const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+      if (a.dbg != 1) {
+        // this thread's 64 columns: the phase-0 partial stays in registers until phase 1 completes it
+#pragma unroll
+        for (int ci = 0; ci < kBN / 32; ++ci) {
+          const int cc = chalf * (kBN / 32) + ci;
+          uint32_t v[4][16];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            if (ph == 1 && g == 3) break;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(v[g][0]), "=r"(v[g][1]), "=r"(v[g][2]), "=r"(v[g][3]), "=r"(v[g][4]), "=r"(v[g][5]),
+                  "=r"(v[g][6]), "=r"(v[g][7]), "=r"(v[g][8]), "=r"(v[g][9]), "=r"(v[g][10]), "=r"(v[g][11]),
+                  "=r"(v[g][12]), "=r"(v[g][13]), "=r"(v[g][14]), "=r"(v[g][15])
+                : "r"(lane_base + static_cast<uint32_t>(g * kBN + cc * 16)));
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            auto G = [&](int g) { return static_cast<int64_t>(static_cast<int32_t>(v[g][jj])); };
+            if (ph == 0) {
+              part[ci * 16 + jj] = static_cast<double>((G(0) << 21) + (G(1) << 14) + (G(2) << 7) + G(3));
+            } else {
+              part[ci * 16 + jj] =
+                  fma(part[ci * 16 + jj], 0x1p-35, static_cast<double>((G(0) << 14) + (G(1) << 7) + G(2)) * 0x1p-56);
             }
           }
         }
-        umma_commit(&empty[st]);  // smem slot free once these MMAs have read it
+        if (ph == 1) {
+#pragma unroll
+          for (int ci = 0; ci < kBN / 32; ++ci) {
+            const int cc = chalf * (kBN / 32) + ci;
+            const int64_t j0 = static_cast<int64_t>(nt) * kBN + cc * 16;
+            double o[16];
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) o[jj] = part[ci * 16 + jj] * srow * scol[cc * 16 + jj];
+            if (vec && j0 + 16 <= a.w) {
+#pragma unroll
+              for (int jj = 0; jj < 16; jj += 2)
+                *reinterpret_cast<double2*>(orow + j0 + jj) = make_double2(o[jj], o[jj + 1]);
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj)
+                if (j0 + jj < a.w) orow[j0 + jj] = o[jj];
+            }
+          }
+        }
       }
-      umma_commit(&tfull);        // accumulators of this column tile complete
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();  // TMEM free for the next phase
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
-    // the producer runs ahead into the next column tile before joining the epilogue
-    if (warp == 0 && lane == 0) produce_until((nt + 1) * kcs + kStages);
-    __syncwarp();
-    mbar_wait(&tfull, nt & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int32_t* fe = a.bexp + (static_cast<int64_t>(b) * nt_count + nt) * kBN;
-    if (tid < kBN) scol[tid] = ldexp(1.0, __ldg(fe + tid));
-    __syncthreads();
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    const bool vec = (a.w & 1) == 0;
-#pragma unroll 1
-    for (int cc = chalf * (kBN / 32); cc < (a.dbg == 1 ? 0 : (chalf + 1) * (kBN / 32)); ++cc) {
-      uint32_t v[kG][16];
-#pragma unroll
-      for (int g = 0; g < kG; ++g) {
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[g][0]), "=r"(v[g][1]), "=r"(v[g][2]), "=r"(v[g][3]), "=r"(v[g][4]), "=r"(v[g][5]),
-              "=r"(v[g][6]), "=r"(v[g][7]), "=r"(v[g][8]), "=r"(v[g][9]), "=r"(v[g][10]), "=r"(v[g][11]),
-              "=r"(v[g][12]), "=r"(v[g][13]), "=r"(v[g][14]), "=r"(v[g][15])
-            : "r"(lane_base + static_cast<uint32_t>(g * kBN + cc * 16)));
-      }
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      const int64_t j0 = static_cast<int64_t>(nt) * kBN + cc * 16;
-      double o[16];
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
-        // sum_t 2^(-7t) G_t with two exact integer partial sums: hi = G2..G5, lo = G6..G8
-        auto G = [&](int t) { return static_cast<int64_t>(static_cast<int32_t>(v[t - 2][jj])); };
-        const int64_t hi = (G(2) << 21) + (G(3) << 14) + (G(4) << 7) + G(5);
-        const int64_t lo = (G(6) << 14) + (G(7) << 7) + G(8);
-        const double acc = fma(static_cast<double>(hi), 0x1p-35, static_cast<double>(lo) * 0x1p-56);
-        o[jj] = acc * srow * scol[cc * 16 + jj];
-      }
-      if (vec && j0 + 16 <= a.w) {
-#pragma unroll
-        for (int jj = 0; jj < 16; jj += 2) *reinterpret_cast<double2*>(orow + j0 + jj) = make_double2(o[jj], o[jj + 1]);
-      } else {
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj)
-          if (j0 + jj < a.w) orow[j0 + jj] = o[jj];
-      }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();  // TMEM free for the next column tile
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   }
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
