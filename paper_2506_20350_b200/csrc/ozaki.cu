@@ -190,14 +190,14 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   return d;
 }
 // kind::i8, D s32, A / B signed, K-major, N = 64, M = 128
-constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
-                            (static_cast<uint32_t>(kBM >> 4) << 24);
+constexpr uint32_t kIdescBase = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kBM >> 4) << 24);
+__host__ __device__ constexpr uint32_t idesc_n(int n) { return kIdescBase | (static_cast<uint32_t>(n >> 3) << 17); }
 
-__device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
+__device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc, uint32_t idesc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -291,6 +291,9 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
       const int tp = nt * 2 + ph;
       if (warp == 0 && lane == 0) produce_until((tp + 1) * kcs);
       if (warp == 1 && lane == 0) {
+        // the last column tile runs the narrowest N (multiple of 16 for M = 128) covering its live columns
+        const int64_t live = a.w - static_cast<int64_t>(nt) * kBN;
+        const uint32_t idesc = idesc_n(live >= kBN ? kBN : static_cast<int>((live + 15) / 16) * 16);
         for (int kc = 0; kc < kcs; ++kc) {
           const int step = tp * kcs + kc, st = step % kStages;
           mbar_wait(&full[st], (step / kStages) & 1);
@@ -303,7 +306,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
               for (int q = 1; p + q <= 5; ++q)
                 mma_i8(tmem + static_cast<uint32_t>((p + q - 2) * kBN),
                        umma_desc(a0 + (p - 1) * (kBM * kBK)), umma_desc(b0 + (q - 1) * (kBN * kBK)),
-                       (kc > 0 || p > 1) ? 1u : 0u);
+                       (kc > 0 || p > 1) ? 1u : 0u, idesc);
             }
           } else {
 #pragma unroll
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
               for (int q = (6 - p > 1 ? 6 - p : 1); p + q <= kS + 1; ++q)
                 mma_i8(tmem + static_cast<uint32_t>((p + q - 6) * kBN),
                        umma_desc(a0 + (p - 1) * (kBM * kBK)), umma_desc(b0 + (q - 1) * (kBN * kBK)),
-                       (kc > 0 || p > 1) ? 1u : 0u);
+                       (kc > 0 || p > 1) ? 1u : 0u, idesc);
             }
           }
           umma_commit(&empty[st]);  // smem slot free once these MMAs have read it
@@ -331,6 +334,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
 #pragma unroll
         for (int ci = 0; ci < kBN / 32; ++ci) {
           const int cc = chalf * (kBN / 32) + ci;
+          if (static_cast<int64_t>(nt) * kBN + cc * 16 >= a.w) break;  // beyond the live columns (warp-uniform)
           uint32_t v[4][16];
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
