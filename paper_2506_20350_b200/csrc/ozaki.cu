@@ -139,11 +139,26 @@ __global__ void __launch_bounds__(kSliceThreads) ozaki_slice_b_kernel(const doub
   const double* R = re + static_cast<int64_t>(b) * n0 * w;
   const double* I = im + static_cast<int64_t>(b) * n0 * w;
   const int tid = threadIdx.x, jl = tid % kSliceCols, part = tid / kSliceCols;
-  const bool live = j0 + jl < w;
-  for (int kk = part; kk < kdim; kk += kSliceThreads / kSliceCols) {
-    double* dst = tile + kk * kSliceCols + jl;
-    if (live) cp_async8(dst, (kk < n0 ? R + static_cast<int64_t>(kk) * w : I + static_cast<int64_t>(kk - n0) * w) + j0 + jl);
-    else *dst = 0.0;
+  if ((w & 1) == 0) {  // 16-byte copies: 8 threads per K row, two columns each
+    const int jp = 2 * (tid & 7);
+    const bool live2 = j0 + jp < w;  // w even: both columns live or both dead
+    for (int kk = tid >> 3; kk < kdim; kk += kSliceThreads / 8) {
+      double* dst = tile + kk * kSliceCols + jp;
+      const double* src = (kk < n0 ? R + static_cast<int64_t>(kk) * w : I + static_cast<int64_t>(kk - n0) * w) + j0 + jp;
+      if (live2) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+      } else {
+        dst[0] = 0.0;
+        dst[1] = 0.0;
+      }
+    }
+  } else {
+    const bool live = j0 + jl < w;
+    for (int kk = part; kk < kdim; kk += kSliceThreads / kSliceCols) {
+      double* dst = tile + kk * kSliceCols + jl;
+      if (live) cp_async8(dst, (kk < n0 ? R + static_cast<int64_t>(kk) * w : I + static_cast<int64_t>(kk - n0) * w) + j0 + jl);
+      else *dst = 0.0;
+    }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
