@@ -274,7 +274,7 @@ def test_pinned_host_matvec_single_call(dtype):
         matvec(op, torch.zeros(gen.dim + 1, dtype=torch.complex128).pin_memory())
 
 
-@pytest.mark.parametrize("dims,w", [((16, 16, 64), 24), ((16, 16, 64), 70), ((16, 16, 128), 16)])
+@pytest.mark.parametrize("dims,w", [((16, 16, 64), 24), ((16, 16, 64), 70), ((16, 16, 64), 17), ((16, 16, 128), 16)])
 def test_multi_rhs_int8_tensor_core_products_vs_oracle(dims, w):
     # W >= 16 on a grid with a compiled level-2 plan (l2 = 32) routes the per-bin products through
     # the Ozaki-scheme int8 tensor-core kernel (ozaki.cu); partial column tiles (w % 64 != 0)
