@@ -421,21 +421,14 @@ int ozaki_slice_a(const void* DT, int n0, int l2, int l1, int8_t* asl, int32_t* 
 
 int ozaki_products(const int8_t* asl, const int32_t* aexp, const double* re, const double* im, int n0, int64_t bins,
                    int64_t w, int8_t* bsl, int32_t* bexp, double* out_re, double* out_im, cudaStream_t s) {
-  TOEP_REQUIRE(ozaki_supported(n0) && bins <= 65535 * 64, TOEP_ERR_ARG, "ozaki: unsupported geometry");
+  TOEP_REQUIRE(ozaki_supported(n0), TOEP_ERR_ARG, "ozaki: unsupported block side %d", n0);
   if (bins == 0 || w == 0) return TOEP_OK;
   const int ntiles = static_cast<int>((w + kBN - 1) / kBN);
-  {
-    const size_t tsm = static_cast<size_t>(2 * n0) * kSliceCols * sizeof(double);
-    static size_t tattr = 0;
-    if (tattr < tsm) {
-      TOEP_CUDA(cudaFuncSetAttribute(ozaki_slice_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsm)));
-      tattr = tsm;
-    }
-    // zero the padded columns' slices / exponents of the last column tile once per call
-    const int64_t wpad = static_cast<int64_t>(ntiles) * kBN;
-    ozaki_slice_b_kernel<<<dim3(static_cast<unsigned>((wpad + kSliceCols - 1) / kSliceCols), static_cast<unsigned>(bins)),
-                           kSliceThreads, tsm, s>>>(re, im, n0, w, ntiles, bsl, bexp);
-    TOEP_LAUNCHED();
+  const size_t tsm = static_cast<size_t>(2 * n0) * kSliceCols * sizeof(double);
+  static size_t tattr = 0;
+  if (tattr < tsm) {
+    TOEP_CUDA(cudaFuncSetAttribute(ozaki_slice_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsm)));
+    tattr = tsm;
   }
   const size_t smem = kStages * (kATile + kBTile);
   static bool attr = false;
@@ -447,10 +440,20 @@ int ozaki_products(const int8_t* asl, const int32_t* aexp, const double* re, con
     const char* e = std::getenv("TOEP_OZ_DBG");
     return e != nullptr ? std::atoi(e) : 0;
   }();
-  OzArgs oa{asl, aexp, bsl, bexp, out_re, out_im, n0, w, ntiles, dbg};
-  ozaki_tile_kernel<<<dim3(static_cast<unsigned>(2 * n0 / kBM), static_cast<unsigned>(bins)), kOzThreads, smem, s>>>(
-      oa);
-  TOEP_LAUNCHED();
+  const int64_t wpad = static_cast<int64_t>(ntiles) * kBN;
+  const int64_t a_bin = ozaki_a_bytes(n0, 1), b_bin = ozaki_b_bytes(n0, 1, w), plane_bin = static_cast<int64_t>(n0) * w;
+  for (int64_t b0 = 0; b0 < bins; b0 += 65535) {  // grid.y limit
+    const unsigned nb = static_cast<unsigned>(std::min<int64_t>(65535, bins - b0));
+    // digits of the right-hand sides (padded columns get zero digits / exponents every call)
+    ozaki_slice_b_kernel<<<dim3(static_cast<unsigned>((wpad + kSliceCols - 1) / kSliceCols), nb), kSliceThreads, tsm,
+                           s>>>(re + b0 * plane_bin, im + b0 * plane_bin, n0, w, ntiles, bsl + b0 * b_bin,
+                                bexp + b0 * wpad);
+    TOEP_LAUNCHED();
+    OzArgs oa{asl + b0 * a_bin, aexp + b0 * 2 * n0, bsl + b0 * b_bin, bexp + b0 * wpad, out_re + b0 * plane_bin,
+              out_im + b0 * plane_bin, n0, w, ntiles, dbg};
+    ozaki_tile_kernel<<<dim3(static_cast<unsigned>(2 * n0 / kBM), nb), kOzThreads, smem, s>>>(oa);
+    TOEP_LAUNCHED();
+  }
   return TOEP_OK;
 }
 
