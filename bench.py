@@ -194,7 +194,7 @@ def run_ours(args):
 
     from paper_2506_20350_b200.problems import dense_rhs, seeded_stacked4, system_from_generator, unit_feed_rhs
     from paper_2506_20350_b200.solvers import BorderedOperator, GmresConfig, build_pk, solve_multi_rhs_vectorized
-    from paper_2506_20350_b200.toeplitz import generator_from_stacked, matvec
+    from paper_2506_20350_b200.toeplitz import generator_from_stacked, matvec, pin
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -259,7 +259,9 @@ def run_ours(args):
     k_ms = k0.elapsed_time(k1) / nk
 
     # ---- end to end through the public API, pinned host buffers
-    u_host = torch.from_numpy(dense_rhs(DIM, seed=1)[:, None]).pin_memory()
+    # page-locked through the library allocator (toeplitz.pin): the copy engines read torch's own
+    # pinned blocks at 17-19 GB/s on these boxes, cudaHostAlloc blocks at 50 GB/s (tools/hostbuf_probe.py)
+    u_host = pin(dense_rhs(DIM, seed=1)[:, None])
     for _ in range(max(2, args.warmup // 2)):
         matvec(spec, u_host)
     torch.cuda.synchronize()

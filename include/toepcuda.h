@@ -98,6 +98,12 @@ TOEP_API int toep_matvec(toep_op_t op, const void* u, void* v, int64_t w, int fl
  * without per-call device allocations); device staging is owned by the operator, per stream. */
 TOEP_API int toep_matvec_host(toep_op_t op, const void* u_host, void* v_host, int64_t w, int flags, void* stream);
 
+/* Page-locked host memory for the host vectors of toep_matvec_host (the numpy in/out buffers of
+ * toeplitz.py:287-303 when the caller keeps them pinned).  cudaHostAlloc(Portable); `bytes` == 0
+ * yields NULL.  No reference counterpart (the reference never leaves host memory). */
+TOEP_API int toep_host_alloc(uint64_t bytes, void** out);
+TOEP_API int toep_host_free(void* p);
+
 /* Multi-GPU row / kx-slab decomposition (no reference counterpart:
  * the reference is single-process).  toep_op_slab: operator holding only the bins with
  * level-1 frequency kx in [kx0, kx1).  toep_matvec_stage: the local steps of one distributed

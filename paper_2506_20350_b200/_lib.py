@@ -93,6 +93,8 @@ SIGNATURES = {
     "toep_op_fold_left": (c_int, [c_vp, c_vp, c_vp, ctypes.POINTER(c_vp)]),
     "toep_matvec": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
     "toep_matvec_host": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
+    "toep_host_alloc": (c_int, [ctypes.c_uint64, ctypes.POINTER(c_vp)]),
+    "toep_host_free": (c_int, [c_vp]),
     "toep_op_slab": (c_int, [c_vp, c_int, c_int, c_vp, ctypes.POINTER(c_vp)]),
     "toep_matvec_stage": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_int, c_vp]),
     "toep_matvec_stage_peer": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_int, c_vp]),

@@ -28,6 +28,7 @@ import torch
 
 from . import _lib
 from ._tensor import restore, to_columns
+from .hostmem import pin, pinned_empty  # noqa: F401 - public: host vectors for the host-in/out calls
 from .errors import BlockShapeMismatch, MissingOffset, ShapeError
 
 __all__ = [
@@ -284,7 +285,7 @@ def _apply_pinned(op: SpectralOperator, u: torch.Tensor, flags: int):
         raise ShapeError(f"rows {rows} != operator dim {op.dim}")
     if op.dtype == torch.complex64 and u.dtype == torch.complex128:
         flags |= _lib.TOEP_MV_IO_C128
-    out = torch.empty(u.shape, dtype=u.dtype, pin_memory=True)
+    out = pinned_empty(u.shape, u.dtype)
     if w:
         _lib.check(_lib.lib().toep_matvec_host(op.handle, u.data_ptr(), out.data_ptr(), w, flags,
                                                _lib.stream_handle()), "matvec")

@@ -274,6 +274,27 @@ def test_pinned_host_matvec_single_call(dtype):
         matvec(op, torch.zeros(gen.dim + 1, dtype=torch.complex128).pin_memory())
 
 
+def test_library_pinned_host_buffers():
+    # toeplitz.pin / pinned_empty: cudaHostAlloc blocks seen by torch as pinned, routed through
+    # toep_matvec_host; the result lands in the same kind of memory; freed blocks are reused
+    from paper_2506_20350_b200 import hostmem
+    from paper_2506_20350_b200.toeplitz import pin, pinned_empty
+    gen = generator_from_stacked(seeded_stacked4(5, 4, 8, seed=3))
+    op = precompute_spectral(gen)
+    u = dense_rhs(gen.dim, 2, seed=5)
+    uh = pin(u)
+    assert uh.is_pinned() and uh.dtype == torch.complex128 and tuple(uh.shape) == u.shape
+    assert np.array_equal(uh.numpy(), u)
+    got = matvec(op, uh)
+    assert got.is_pinned() and got.device.type == "cpu"
+    assert rel_err(got.numpy(), np.asarray(matvec(op, u))) <= 1e-13
+    e = pinned_empty((3, 7), torch.complex64)
+    assert e.shape == (3, 7) and e.dtype == torch.complex64 and e.is_pinned()
+    addr = uh.data_ptr()
+    del uh
+    assert pinned_empty(u.shape).data_ptr() == addr  # cached block handed back
+
+
 @pytest.mark.parametrize("dims,w", [((16, 16, 64), 24), ((16, 16, 64), 70), ((16, 16, 64), 17), ((16, 16, 128), 16)])
 def test_multi_rhs_int8_tensor_core_products_vs_oracle(dims, w):
     # W >= 16 on a grid with a compiled level-2 plan (l2 = 32) routes the per-bin products through
