@@ -222,7 +222,7 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
                                            C<TC>* __restrict__ src, C<TC>* __restrict__ dst,
                                            const C<TC>* __restrict__ tw, int ncol, TC scale) {
   using Z = C<TC>;
-  static_assert(kIn >= 0 && kIn <= 2, "plan_stage input mode");
+  static_assert(kIn >= 0 && kIn <= 3, "plan_stage input mode");
   static_assert(Ns * R * PlanLen<Rest...>::value == L, "plan radices must multiply to L");
   constexpr bool kFirst = (Ns == 1);
   constexpr bool kLast = sizeof...(Rest) == 0;
@@ -250,12 +250,12 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
         v[r] = mk<TC>(0, 0);
         if constexpr (kIn == 1) {  // staged by the streaming kernel: rows [n_lo + n_hi][TIL] in `src`
           if (row >= 0 && col < ncol) v[r] = src[row * TIL + col];
-        } else if constexpr (kIn == 2) {  // staged (T1, T2, T3) planes [3][n_lo + n_hi][TIL] doubles
+        } else if constexpr (kIn >= 2) {  // staged planes [3 or 2][n_lo + n_hi][TIL] doubles
           if (row >= 0 && col < ncol) {
             const double* sp = reinterpret_cast<const double*>(src);
             const int nr = a.n_lo + a.n_hi;
             const double t1 = sp[row * TIL + col], t2 = sp[(nr + row) * TIL + col];
-            if (a.planes2) {
+            if (kIn == 3 || a.planes2) {
               v[r] = mk<TC>(static_cast<TC>(t1), static_cast<TC>(t2));
             } else {
               const double t3 = sp[(2 * nr + row) * TIL + col];
@@ -368,7 +368,8 @@ constexpr int kStreamBlocks = 4;
 
 template <typename TC, int TIL, int kIn, int L>
 struct StreamSmem {
-  static constexpr int kStageZ = kIn == 2 ? (3 * L * TIL + 1) / 2 : L * TIL;  // complex slots per staging buffer
+  // complex slots per staging buffer: kIn 2 = three double planes, kIn 3 = two (Re, Im: the Ozaki path)
+  static constexpr int kStageZ = kIn == 2 ? (3 * L * TIL + 1) / 2 : L * TIL;
   static constexpr size_t bytes = sizeof(C<TC>) * (L + 2 * static_cast<size_t>(kStageZ) + L * TIL);
 };
 
@@ -411,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, TIL <= 8 ? 2 * kStreamBlocks : kStre
         cp_async(buf + e, static_cast<const Z*>(a.in) + ge, static_cast<int>(sizeof(Z)));
       } else {
         double* bd = reinterpret_cast<double*>(buf);
-        const int np = a.planes2 ? 2 : 3;
+        const int np = (kIn == 3 || a.planes2) ? 2 : 3;
         for (int p = 0; p < np; ++p) cp_async(bd + p * nrows * TIL + e, a.in_planes + p * a.plane + ge, 8);
       }
     }
@@ -482,6 +483,8 @@ int try_stream(const PassArgs& a, cudaStream_t s) {
     const int64_t grid = std::min<int64_t>(ntiles, static_cast<int64_t>(device_sms()) * per_sm);
     return launch_k(kern, dim3(static_cast<unsigned>(grid)), dim3(kThreads), SM::bytes, s, a, 2.0 / L, ntiles, tiles_x);
   };
+  // two planes: 47 KB of shared memory per CTA (4 resident per SM) instead of the 3-plane 62 KB (3)
+  if (a.in_planes != nullptr && a.planes2) return launch_kin(std::integral_constant<int, 3>{});
   if (a.in_planes != nullptr) return launch_kin(std::integral_constant<int, 2>{});
   return launch_kin(std::integral_constant<int, 1>{});
 }

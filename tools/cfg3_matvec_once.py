@@ -13,3 +13,8 @@ for _ in range(2):
     matvec(op.spectral, B)
 torch.cuda.synchronize()
 print("ok")
+if os.environ.get("NCU_RANGE"):  # ncu --profile-from-start off: capture one steady-state matvec only
+    torch.cuda.profiler.start()
+    matvec(op.spectral, B)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
