@@ -81,14 +81,39 @@ __global__ void __launch_bounds__(kCols) kb_dots_gram(const double2* const* __re
   const double2* vl = Vp[m - 1];
   for (int l0 = 0; l0 < m; l0 += kLGG) {
     double2 acc[kLGG], acg[kLGG];
+    const double2* vp[kLGG];
 #pragma unroll
-    for (int g = 0; g < kLGG; ++g) acc[g] = acg[g] = make_double2(0, 0);
-    for (int64_t i = r0; i < r1; ++i) {
+    for (int g = 0; g < kLGG; ++g) {
+      acc[g] = acg[g] = make_double2(0, 0);
+      vp[g] = Vp[l0 + g < m ? l0 + g : m - 1];
+    }
+    int64_t i = r0;
+    // two rows per iteration, every load issued before the first use (the sweep is latency-bound:
+    // ncu long-scoreboard stalls at 32 resident warps per SM); same accumulation order as one row
+    for (; i + 1 < r1; i += 2) {
+      const int64_t o0 = i * W + c, o1 = o0 + W;
+      const double2 w0 = w[o0], w1 = w[o1], a0 = vl[o0], a1 = vl[o1];
+      double2 x0[kLGG], x1[kLGG];
+#pragma unroll
+      for (int g = 0; g < kLGG; ++g) {
+        x0[g] = l0 + g < m ? __ldg(vp[g] + o0) : make_double2(0, 0);
+        x1[g] = l0 + g < m ? __ldg(vp[g] + o1) : make_double2(0, 0);
+      }
+#pragma unroll
+      for (int g = 0; g < kLGG; ++g)
+        if (l0 + g < m) {
+          cfmac(acc[g], x0[g], w0);
+          cfmac(acg[g], x0[g], a0);
+          cfmac(acc[g], x1[g], w1);
+          cfmac(acg[g], x1[g], a1);
+        }
+    }
+    for (; i < r1; ++i) {
       const double2 wi = w[i * W + c], li = vl[i * W + c];
 #pragma unroll
       for (int g = 0; g < kLGG; ++g)
         if (l0 + g < m) {
-          const double2 v = Vp[l0 + g][i * W + c];
+          const double2 v = vp[g][i * W + c];
           cfmac(acc[g], v, wi);
           cfmac(acg[g], v, li);
         }
@@ -180,11 +205,37 @@ __global__ void __launch_bounds__(kCols) kb_upd(const double2* const* __restrict
       cl[g] = make_double2(-hv.x, -hv.y);
     }
     const bool last = (l0 + kLG >= m);
-    for (int64_t i = r0; i < r1; ++i) {
+    const double2* vp[kLG];
+#pragma unroll
+    for (int g = 0; g < kLG; ++g) vp[g] = Vp[l0 + g < m ? l0 + g : m - 1];
+    int64_t i = r0;
+    for (; i + 1 < r1; i += 2) {  // two rows per iteration, loads first (as kb_dots_gram)
+      const int64_t o0 = i * W + c, o1 = o0 + W;
+      double2 acc0 = w[o0], acc1 = w[o1];
+      double2 x0[kLG], x1[kLG];
+#pragma unroll
+      for (int g = 0; g < kLG; ++g) {
+        x0[g] = l0 + g < m ? __ldg(vp[g] + o0) : make_double2(0, 0);
+        x1[g] = l0 + g < m ? __ldg(vp[g] + o1) : make_double2(0, 0);
+      }
+#pragma unroll
+      for (int g = 0; g < kLG; ++g)
+        if (l0 + g < m) {
+          cfma(acc0, x0[g], cl[g]);
+          cfma(acc1, x1[g], cl[g]);
+        }
+      w[o0] = acc0;
+      w[o1] = acc1;
+      if (last) {
+        nrm = fma(acc0.x, acc0.x, fma(acc0.y, acc0.y, nrm));
+        nrm = fma(acc1.x, acc1.x, fma(acc1.y, acc1.y, nrm));
+      }
+    }
+    for (; i < r1; ++i) {
       double2 acc = w[i * W + c];
 #pragma unroll
       for (int g = 0; g < kLG; ++g)
-        if (l0 + g < m) cfma(acc, Vp[l0 + g][i * W + c], cl[g]);
+        if (l0 + g < m) cfma(acc, vp[g][i * W + c], cl[g]);
       w[i * W + c] = acc;
       if (last) nrm = fma(acc.x, acc.x, fma(acc.y, acc.y, nrm));
     }
