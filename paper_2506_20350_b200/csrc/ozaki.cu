@@ -52,27 +52,31 @@ __device__ __forceinline__ int row_exponent(double mx) {
   return ilogb(mx) + 1;  // mx * 2^-e in [0.5, 1)
 }
 
-// 16 values (already scaled by 2^(49 - e)) -> kS int4 slices of signed base-128 digits
+// 16 values (already scaled by 2^(49 - e)) -> kS int4 slices of signed base-128 digits.  The
+// 49-bit magnitude is split into 32-bit halves (digits 0-2 from bits 28-48, 3-6 from bits 0-27) so
+// every digit is one 32-bit shift-and (the kernel is ALU-bound on the 64-bit shifts otherwise);
+// the sign is applied as (d ^ s) - s with s = 0 / -1.
 __device__ __forceinline__ void digits16(const double* x, int4* out) {
-  int64_t m[16];
-  uint32_t neg = 0;
+  uint32_t hi[16], lo[16], sg[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     // round to nearest (unbiased truncation error, unlike chopping); |x| < 2^49 so |t| <= 2^49, and
     // the one value that can round up to 2^49 is clamped to the largest 7-digit magnitude
     const int64_t t = __double2ll_rn(x[i]);
-    neg |= (t < 0 ? 1u : 0u) << i;
-    const int64_t a = t < 0 ? -t : t;
-    m[i] = a < (int64_t{1} << (7 * kS)) ? a : (int64_t{1} << (7 * kS)) - 1;
+    const int64_t a0 = t < 0 ? -t : t;
+    const int64_t a = a0 < (int64_t{1} << (7 * kS)) ? a0 : (int64_t{1} << (7 * kS)) - 1;
+    hi[i] = static_cast<uint32_t>(a >> 28);
+    lo[i] = static_cast<uint32_t>(a) & ((1u << 28) - 1u);
+    sg[i] = t < 0 ? 0xffffffffu : 0u;
   }
+  static_assert(kS == 7, "digit split assumes 7 base-128 digits");
 #pragma unroll
   for (int p = 0; p < kS; ++p) {
     uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      int32_t d = static_cast<int32_t>((m[i] >> (7 * (kS - 1 - p))) & 127);
-      if ((neg >> i) & 1u) d = -d;
-      w[i >> 2] |= (static_cast<uint32_t>(d) & 0xffu) << (8 * (i & 3));
+      const uint32_t d = p < 3 ? (hi[i] >> (7 * (2 - p))) & 127u : (lo[i] >> (7 * (6 - p))) & 127u;
+      w[i >> 2] |= (((d ^ sg[i]) - sg[i]) & 0xffu) << (8 * (i & 3));
     }
     out[p] = make_int4(static_cast<int>(w[0]), static_cast<int>(w[1]), static_cast<int>(w[2]), static_cast<int>(w[3]));
   }
