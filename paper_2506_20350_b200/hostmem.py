@@ -65,15 +65,31 @@ def _acquire(nbytes: int) -> int:
     return int(out.value)
 
 
+_layouts: dict = {}
+
+
+def _layout(shape, dtype):
+    key = (shape, dtype)
+    lay = _layouts.get(key)
+    if lay is None:
+        shp = (int(shape),) if isinstance(shape, (int, np.integer)) else tuple(int(s) for s in shape)
+        count = int(np.prod(shp, dtype=np.int64)) if shp else 1
+        nbytes = max(_ALIGN, -(-count * torch.empty((), dtype=dtype).element_size() // _ALIGN) * _ALIGN)
+        lay = (shp, count, nbytes, _block_type(nbytes))
+        if len(_layouts) < 4096:
+            _layouts[key] = lay
+    return lay
+
+
 def pinned_empty(shape, dtype=torch.complex128) -> torch.Tensor:
     """Uninitialised page-locked CPU tensor (``is_pinned()`` is True) from the library allocator."""
     _lib.require_cuda()
-    shape = (int(shape),) if isinstance(shape, (int, np.integer)) else tuple(int(s) for s in shape)
-    count = int(np.prod(shape, dtype=np.int64)) if shape else 1
-    itemsize = torch.empty((), dtype=dtype).element_size()
-    nbytes = max(_ALIGN, -(-count * itemsize // _ALIGN) * _ALIGN)
-    block = _block_type(nbytes).from_address(_acquire(nbytes))
-    return torch.frombuffer(block, dtype=dtype, count=count).view(shape)
+    try:
+        shp, count, nbytes, btype = _layout(shape, dtype)
+    except TypeError:  # unhashable shape (e.g. a list)
+        shp, count, nbytes, btype = _layout(tuple(shape), dtype)
+    block = btype.from_address(_acquire(nbytes))
+    return torch.frombuffer(block, dtype=dtype, count=count).view(shp)
 
 
 def pin(x, dtype=None) -> torch.Tensor:
