@@ -398,10 +398,14 @@ __global__ void kb_scale(double2* __restrict__ x, const double* __restrict__ inv
   pdl_wait();
   pdl_trigger();
   const int64_t total = n * W;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int c = static_cast<int>(t % W);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int cstep = static_cast<int>(stride % W);  // column advances by a constant: no 64-bit % per element
+  int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  int c = static_cast<int>(t % W);
+  for (; t < total; t += stride) {
     x[t] = cscale(src[t], inv[c]);
+    c += cstep;
+    if (c >= W) c -= W;
   }
 }
 
