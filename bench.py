@@ -2,7 +2,7 @@
 30x30, N_b = 128, complex128 (BASELINE.json configs[1]), with the HBM
 roofline fraction of the dominant kernel.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--scale|--no-scale]
 
 A step is one MLFFT matvec (pad -> 2-D DFT -> per-bin 128x128 product ->
 inverse DFT -> crop) of one dense seeded vector against the resident
@@ -10,10 +10,18 @@ spectral operator.  The spectral blocks (944 MB) exceed the 126 MB L2, so
 every step streams them from HBM (no L2 flush needed).  N > 1 runs one
 independent replica per GPU (the single-RHS path does not shard; DESIGN.md
 "replicas only"); value = total matvecs over all ranks / max-over-ranks time.
+``--gpus N`` without a launcher (no WORLD_SIZE in the environment) spawns the
+N ranks itself (NCCL, 127.0.0.1), and refuses cleanly if fewer than N GPUs exist.
 
-``--impl reference`` times the reference algorithm's CPU implementation on
-the host cores: the numpy restatement in ``oracle/`` (the reference itself
-is pure Python and is not installed on the GPU box), on the same config.
+``config.scale`` (on by default when N > 1, ``--scale`` at N = 1) adds the
+paths that do shard: the cfg3 900-column multi-RHS solve
+sharded by columns, and the cfg4 64x64 slab-decomposed matvec / GMRES with
+both exchanges (``all_to_all_single`` and NVLink peer stores).
+
+``--impl reference`` times the reference's own CPU implementation: the
+unmodified ``toepsolve`` package installed into ``oracle/_ref`` by
+``oracle/build_ref.sh`` (its public ``toeplitz.matvec``), on all host threads;
+the numpy restatement in ``oracle/`` stands in only if that install is absent.
 """
 
 from __future__ import annotations
@@ -115,59 +123,121 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def cpu_baseline(max_seconds: float = 20.0) -> dict:
-    """Oracle (numpy restatement of the reference, pocketfft + OpenBLAS) on the host cores."""
-    import oracle
+def _reference_module():
+    """The unmodified reference (toepsolve from oracle/_ref), or None if it was not installed."""
+    ref = os.path.join(REPO, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref, "toepsolve")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import toepsolve.toeplitz as tz
+    return tz
+
+
+def cpu_matvecs(seconds: float, warmup: int, max_steps: int) -> dict:
+    """cfg2 matvecs of the reference's own CPU path in THIS process (threads as the environment
+    sets them): setup (generator + precompute_spectral) untimed, then `warmup` untimed calls, then
+    timed calls until `seconds` or `max_steps`.  The port (oracle/) stands in if oracle/_ref is absent."""
     from paper_2506_20350_b200.problems import dense_rhs, seeded_stacked4
 
-    cores = os.cpu_count() or 1
     s4 = seeded_stacked4(NY, NX, NB, seed=0)
-    d = oracle.precompute_spectral(s4)
+    u = dense_rhs(DIM, seed=1)
+    tz = _reference_module()
+    if tz is not None:
+        k2, k1 = 2 * NY - 1, 2 * NX - 1
+        blocks = {(p, q): s4[p % k2, q % k1] for p in range(-(NY - 1), NY) for q in range(-(NX - 1), NX)}
+        gen = tz.embed_2l(blocks, NY, NX, NB)
+        del blocks
+        op = tz.precompute_spectral(gen)
+        del gen
+
+        def step():
+            return tz.matvec(op, u)
+        kind, what = "reference", "toepsolve.toeplitz.matvec (unmodified reference, oracle/_ref)"
+    else:
+        import oracle
+
+        d = oracle.precompute_spectral(s4)
+        dims = (NY, NX, NB, 2 * NY - 1, 2 * NX - 1)
+        uc = u[:, None]
+
+        def step():
+            return oracle.matvec(d, dims, uc)
+        kind, what = "port", "oracle/mlfft.py (numpy restatement; oracle/_ref not installed)"
     del s4
-    dims = (NY, NX, NB, 2 * NY - 1, 2 * NX - 1)
-    u = dense_rhs(DIM, seed=1)[:, None]
-    oracle.matvec(d, dims, u)  # warm-up (FFT plans, pools)
+    for _ in range(warmup):
+        step()
     times = []
-    t_end = time.perf_counter() + max_seconds
-    while time.perf_counter() < t_end and len(times) < 200:
+    t_end = time.perf_counter() + seconds
+    while len(times) < max(1, max_steps) and (not times or time.perf_counter() < t_end):
         t0 = time.perf_counter()
-        oracle.matvec(d, dims, u)
+        step()
         times.append(time.perf_counter() - t0)
-    best = min(times)
-    return {"value": 1.0 / best, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{len(times)} cfg2 matvecs (best-of, after warm-up) of oracle/mlfft.py "
-                      f"(numpy pocketfft + OpenBLAS, {cores} threads), precompute excluded",
-            "mean_s": float(np.mean(times))}
+    return {"kind": kind, "what": what, "times": times}
+
+
+def cpu_baseline_subprocess(threads: int, seconds: float) -> dict:
+    """One bounded CPU sample in a fresh process with BLAS threads pinned to `threads`."""
+    env = dict(os.environ)
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        env[k] = str(threads)
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-sample", "--cpu-seconds", str(seconds),
+           "--warmup", "2", "--steps", "200"]
+    try:
+        out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+        line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1]
+        r = json.loads(line)
+    except Exception as exc:  # noqa: BLE001
+        return {"error": f"cpu sample failed: {exc!r}"}
+    t = r["times"]
+    return {"value": 1.0 / min(t), "unit": UNIT, "cores": threads, "kind": r["kind"],
+            "sample": f"{len(t)} cfg2 matvecs (best-of, after 2 warm-up) of {r['what']}, "
+                      f"{threads} BLAS thread(s), generator + precompute excluded",
+            "mean_s": float(np.mean(t)), "median_s": float(np.median(t))}
+
+
+def cpu_baseline() -> dict:
+    """Reference CPU path on the box's host cores: all threads (headline) and one thread."""
+    cores = os.cpu_count() or 1
+    allc = cpu_baseline_subprocess(cores, 10.0)
+    one = cpu_baseline_subprocess(1, 10.0)
+    if "error" in allc:
+        return allc
+    allc["single_thread"] = one
+    try:
+        allc["cpu_model"] = [ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo")
+                             if ln.startswith("model name")][0]
+    except Exception:  # noqa: BLE001
+        pass
+    return allc
+
+
+def run_cpu_sample(args):
+    r = cpu_matvecs(args.cpu_seconds, args.warmup, args.steps)
+    print(json.dumps(r), flush=True)
 
 
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    import oracle
-    from paper_2506_20350_b200.problems import dense_rhs, seeded_stacked4
-
-    s4 = seeded_stacked4(NY, NX, NB, seed=0)
-    d = oracle.precompute_spectral(s4)
-    del s4
-    dims = (NY, NX, NB, 2 * NY - 1, 2 * NX - 1)
-    u = dense_rhs(DIM, seed=1)[:, None]
-    for _ in range(args.warmup):
-        oracle.matvec(d, dims, u)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle.matvec(d, dims, u)
-    dt = time.perf_counter() - t0
-    value = args.steps / dt
     cores = os.cpu_count() or 1
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+    # bounded: at ~0.1 s per reference matvec, K steps of the driver's run are timed in full up to
+    # 120 s; beyond that the first steps that fit are the sample
+    r = cpu_matvecs(120.0, args.warmup, args.steps)
+    t = r["times"]
+    dt = float(np.sum(t))
+    value = len(t) / dt
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(t),
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / len(t), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (BASELINE seeded generator)",
             "config": {"workload": WORKLOAD, "embedding": "59x59 circulant (3481 bins, the reference's 2N-1)",
-                       "n_bins": (2 * NY - 1) * (2 * NX - 1), "dim": DIM},
+                       "n_bins": (2 * NY - 1) * (2 * NX - 1), "dim": DIM, "steps_requested": args.steps},
             "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} timed matvecs of oracle/mlfft.py on {cores} host threads"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": r["kind"],
+                             "sample": f"{len(t)} timed cfg2 matvecs of {r['what']} on {cores} host threads "
+                                       f"(generator + precompute_spectral excluded)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -188,13 +258,130 @@ def count_launches(step, reps: int = 4) -> int:
     return round(n / reps)
 
 
+def _percall(fn, n):
+    """Per-call host wall times (each call ends with its own synchronisation) plus the total."""
+    ts = []
+    for _ in range(n):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return ts
+
+
+def _broadcast_stacked(ny, nx, nb, dev, world):
+    """Seeded generator made once on rank 0 and broadcast to every rank's device (NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_20350_b200.problems import seeded_stacked4
+
+    shape = (2 * ny - 1, 2 * nx - 1, nb, nb)
+    if world == 1 or dist.get_rank() == 0:
+        t = torch.from_numpy(seeded_stacked4(ny, nx, nb, seed=0)).to(dev)
+    else:
+        t = torch.empty(shape, dtype=torch.complex128, device=dev)
+    if world > 1:
+        dist.broadcast(torch.view_as_real(t), src=0)
+    return t
+
+
+def scale_legs(dev, world, rank):
+    """The paths that shard, timed on the device, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_20350_b200.distributed import SlabOperator, column_range, gmres_slab, solve_columns_sharded
+    from paper_2506_20350_b200.problems import unit_feed_rhs
+    from paper_2506_20350_b200.solvers import GmresConfig
+    from paper_2506_20350_b200.toeplitz import precompute_spectral_stacked
+
+    def tmax(ms):
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    out = {}
+    # ---- cfg3: 900 unit right-hand sides, columns sharded, no collective in the data path
+    s4 = _broadcast_stacked(30, 30, 256, dev, world)
+    op3 = precompute_spectral_stacked(s4)
+    del s4
+    W = 900
+    b = torch.from_numpy(unit_feed_rhs(30, 30, 256, columns="each")).to(dev)
+    cfg = GmresConfig(tol=1e-6)
+    c0, c1 = column_range(W, world, rank)
+    from paper_2506_20350_b200.solvers import solve_multi_rhs_sequential
+    solve_multi_rhs_sequential(op3, None, b[:, c0:c1].contiguous(), cfg)  # warm: workspaces, slices
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    local = b[:, c0:c1].contiguous()
+    x, reps = solve_multi_rhs_sequential(op3, None, local, cfg)
+    e1.record()
+    barrier()
+    solve_ms = tmax(e0.elapsed_time(e1))
+    xs = None
+    if world > 1:  # the public sharded entry point (same solve + gather of X to rank 0)
+        xs, _ = solve_columns_sharded(op3, None, b, cfg)
+    its = [r.iterations for r in reps]
+    out["cfg3_columns"] = {"columns_total": W, "columns_per_rank": c1 - c0, "solve_ms_max_over_ranks": solve_ms,
+                           "columns_per_s": W / (solve_ms * 1e-3), "iterations_min_max_rank0": [min(its), max(its)],
+                           "note": "batched per-column GMRES(1e-6) of this rank's columns, no data-path "
+                                   "collective; X gathered to rank 0 afterwards (solve_columns_sharded)"}
+    del op3, b, x, xs
+    torch.cuda.empty_cache()
+    if world == 1:
+        return out
+    # ---- cfg4: 64x64 slab decomposition, both exchanges
+    s4 = _broadcast_stacked(64, 64, 128, dev, world)
+    from paper_2506_20350_b200.problems import dense_rhs
+    u_full = torch.from_numpy(dense_rhs(64 * 64 * 128, seed=1)).to(dev)
+    b_full = torch.from_numpy(unit_feed_rhs(64, 64, 128)).to(dev)
+    for exchange in ("collective", "peer"):
+        sop = SlabOperator.from_generator(s4, exchange=exchange)
+        y0, y1 = sop.rows
+        n_loc = sop.local_dim
+        u = u_full[y0 * 64 * 128:y1 * 64 * 128].contiguous()
+        for _ in range(3):
+            sop.matvec_local(u)
+        barrier()
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record()
+        for _ in range(20):
+            sop.matvec_local(u)
+        k1.record()
+        barrier()
+        mv_us = tmax(k0.elapsed_time(k1) / 20) * 1e3
+        bl = b_full[y0 * 64 * 128:y1 * 64 * 128].contiguous()
+        gmres_slab(sop, None, bl, GmresConfig(tol=1e-6, restart=50))
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        _, rep = gmres_slab(sop, None, bl, GmresConfig(tol=1e-6, restart=50))
+        g1.record()
+        barrier()
+        out[f"cfg4_slab_{exchange}"] = {
+            "matvec_us_max_over_ranks": mv_us, "gmres_ms_max_over_ranks": tmax(g0.elapsed_time(g1)),
+            "gmres_iterations": rep.iterations, "reference_iterations": 28, "local_rows": n_loc // (64 * 128),
+            "resident_spectral_bytes_per_rank": sop.stages.op.resident_bytes,
+            "exchange_bytes_per_matvec_per_rank": 2 * 64 * 128 * 128 * 16 * (world - 1) // (world * world)}
+        del sop
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_2506_20350_b200.problems import dense_rhs, seeded_stacked4, system_from_generator, unit_feed_rhs
     from paper_2506_20350_b200.solvers import BorderedOperator, GmresConfig, build_pk, solve_multi_rhs_vectorized
-    from paper_2506_20350_b200.toeplitz import generator_from_stacked, matvec, pin
+    from paper_2506_20350_b200.toeplitz import generator_from_stacked, matvec, pin, pinned_empty
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -257,28 +444,42 @@ def run_ours(args):
     k1.record(stream)
     torch.cuda.synchronize()
     k_ms = k0.elapsed_time(k1) / nk
+    del hat_in, hat_out
 
-    # ---- end to end through the public API, pinned host buffers
-    # page-locked through the library allocator (toeplitz.pin): the copy engines read torch's own
+    # ---- end to end through the public API, pinned host buffers, steady state: the result goes
+    # into a preallocated pinned tensor (out=), so no host allocation happens inside the timed loop.
+    # Page-locked through the library allocator (toeplitz.pin): the copy engines read torch's own
     # pinned blocks at 17-19 GB/s on these boxes, cudaHostAlloc blocks at 50 GB/s (tools/hostbuf_probe.py)
     u_host = pin(dense_rhs(DIM, seed=1)[:, None])
-    for _ in range(max(2, args.warmup // 2)):
-        matvec(spec, u_host)
+    out_host = pinned_empty(u_host.shape, u_host.dtype)
+    for _ in range(args.warmup):
+        matvec(spec, u_host, out=out_host)
     torch.cuda.synchronize()
     barrier()
-    t0 = time.perf_counter()
     x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     x0.record(stream)
-    n_e2e = args.steps
-    for _ in range(n_e2e):
-        out_host = matvec(spec, u_host)
+    per_call = _percall(lambda: matvec(spec, u_host, out=out_host), args.steps)
     x1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = x0.elapsed_time(x1)
     t_e2e = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_value = world * n_e2e / (float(t_e2e.item()) * 1e-3)
+    e2e_value = world * args.steps / (float(t_e2e.item()) * 1e-3)
+    # the reference's own calling convention: numpy in, numpy out (fresh result per call)
+    u_np = dense_rhs(DIM, seed=1)
+    r_np = None
+    for _ in range(args.warmup):
+        r_np = matvec(spec, u_np)
+    torch.cuda.synchronize()
+    barrier()
+
+    def np_call():
+        nonlocal r_np
+        r_np = matvec(spec, u_np)
+    per_call_np = _percall(np_call, args.steps)
+    np_value = args.steps / float(np.sum(per_call_np))
+    assert isinstance(r_np, np.ndarray) and r_np.shape == (DIM,)
 
     # ---- GMRES(50) to 1e-8, none and PK (BASELINE cfg2)
     gm = {}
@@ -307,6 +508,14 @@ def run_ours(args):
                    "algorithmic_bytes": gbytes, "achieved_GBps": gbytes / (med * 1e-3) / 1e9}
     clocks = sampler.stop()
     launches_per_step = count_launches(lambda: matvec(spec, u))
+    scale = None
+    if args.scale or (world > 1 and not args.no_scale):
+        del op, spec, pk, sys_
+        torch.cuda.empty_cache()
+        try:
+            scale = scale_legs(dev, world, rank)
+        except Exception as exc:  # noqa: BLE001 - the headline line must still be printed
+            scale = {"error": repr(exc)}
 
     if rank != 0:
         if world > 1:
@@ -316,7 +525,7 @@ def run_ours(args):
     for g in gm.values():
         g["roofline_frac_measured_peak"] = g["achieved_GBps"] / peak
         g["roofline_frac_nominal_8TBps"] = g["achieved_GBps"] / 8000.0
-    by = algorithmic_bytes(spec.bins)
+    by = algorithmic_bytes(3600)
     achieved_k = by["kernel"] / (k_ms * 1e-3) / 1e9
     achieved_mv = by["matvec"] * (args.steps / (ms * 1e-3)) / 1e9
     traffic = None
@@ -324,6 +533,8 @@ def run_ours(args):
     if os.path.exists(prof):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
+    pc = np.array(per_call) * 1e6
+    pcn = np.array(per_call_np) * 1e6
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -337,20 +548,49 @@ def run_ours(args):
                    "2-D DFT of the blocks; the reference takes 7.4 s (BASELINE.md)",
                    "gmres": gm},
         "roofline": {"bound": "hbm", "achieved": achieved_k, "peak": peak, "unit": "GB/s", "frac": achieved_k / peak,
-                     "traffic": traffic, "kernel": "binprod_tma_kernel (per-bin D_k u_k)", "kernel_ms": k_ms,
+                     "traffic": traffic,
+                     "traffic_source": "profiles/binprod_traffic.json: ncu --set full capture of this kernel "
+                                       "(dram__bytes_read.sum + dram__bytes_write.sum per launch), not measured "
+                                       "in this run",
+                     "kernel": "binprod_tma_kernel (per-bin D_k u_k)", "kernel_ms": k_ms,
                      "kernel_share_of_step": k_ms / (ms / args.steps),
                      "bytes_per_launch": by["kernel"], "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": DIM * 16, "d2h_bytes_per_step": DIM * 16,
-                "path": "toeplitz.matvec(op, pinned CPU tensor) -> pinned CPU tensor"},
+                "path": "toeplitz.matvec(op, pinned CPU tensor, out=pinned CPU tensor): one library call per "
+                        "step (H2D copy, matvec, D2H copy, synchronise)",
+                "per_call_us_min": float(pc.min()), "per_call_us_median": float(np.median(pc)),
+                "numpy": {"value": np_value, "unit": UNIT,
+                          "path": "toeplitz.matvec(op, numpy array) -> numpy array (the reference's calling "
+                                  "convention; staged through a library page-locked block)",
+                          "per_call_us_min": float(pcn.min()), "per_call_us_median": float(np.median(pcn))}},
         "gpu_launches": launches_per_step * args.steps,
         "gpu_launches_per_step": launches_per_step,
         "clocks": clocks,
     }
+    if scale is not None:
+        line["config"]["scale"] = scale
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _spawned(local_rank, args, world, port):
+    os.environ.update({"RANK": str(local_rank), "LOCAL_RANK": str(local_rank), "WORLD_SIZE": str(world),
+                       "LOCAL_WORLD_SIZE": str(world), "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
 
 
 def main():
@@ -360,9 +600,32 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scale", action="store_true", help="add config.scale (cfg3 column / cfg4 slab legs) at N=1")
+    ap.add_argument("--no-scale", action="store_true", help="skip config.scale at N>1")
+    ap.add_argument("--cpu-sample", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.cpu_sample:
+        run_cpu_sample(args)
+        return
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # no launcher: spawn the N ranks here (one process per GPU, NCCL over 127.0.0.1)
+        if args.impl == "reference":
+            run_reference(args)  # rank 0 only does work; nothing to spawn
+            return
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} requested but only {have} CUDA "
+                              f"device(s) are visible", "n_gpus": args.gpus}), flush=True)
+            sys.exit(2)
+        import torch.multiprocessing as mp
+
+        mp.spawn(_spawned, args=(args, args.gpus, _free_port()), nprocs=args.gpus, join=True)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -80,6 +80,8 @@ TOEP_API int toep_fnv1a64(const void* data, uint64_t bytes, uint64_t* out);
  * n0 x n0 block per bin, stored transposed (column-major) for streaming. */
 TOEP_API int toep_op_create(const void* stacked4, int on_device, int n2, int n1, int n0, int l2, int l1,
                    int dtype, void* stream, toep_op_t* out);
+/* Releases the operator.  Waits for the streams the operator was used on (each entry point
+ * registers its stream), not the whole device: those streams must still be valid here. */
 TOEP_API int toep_op_destroy(toep_op_t op);
 TOEP_API int toep_op_info(toep_op_t op, toep_op_info_t* info);
 /* SpectralOperator.diag_blocks (toeplitz.py:153): copy the (bins, n0, n0) blocks, row-major. */
@@ -113,6 +115,12 @@ TOEP_API int toep_host_free(void* p);
  *            in/out (n2, count = slab width, n0*w)
  *   stage 2: level-1 inverse DFT + crop + 1/(l1*l2) of `count` rows, (count, l1, n0*w) -> (count, n1, n0*w) */
 TOEP_API int toep_op_slab(toep_op_t op, int kx0, int kx1, void* stream, toep_op_t* out);
+/* The slab operator built straight from the generator (toeplitz.py:248-253 restricted to the
+ * rank's level-1 frequencies): level-1 DFT of all generator rows, level-2 DFT of columns
+ * [kx0, kx1) only; the full spectral operator never exists on the rank (resident bytes = D * kxs / l1).
+ * kx1 <= kx0 builds the full operator (= toep_op_create). */
+TOEP_API int toep_op_create_slab(const void* stacked4, int on_device, int n2, int n1, int n0, int l2, int l1,
+                                 int dtype, int kx0, int kx1, void* stream, toep_op_t* out);
 TOEP_API int toep_matvec_stage(toep_op_t op, int stage, const void* in, void* out, int64_t w, int count,
                                void* stream);
 

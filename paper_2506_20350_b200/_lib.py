@@ -96,6 +96,8 @@ SIGNATURES = {
     "toep_host_alloc": (c_int, [ctypes.c_uint64, ctypes.POINTER(c_vp)]),
     "toep_host_free": (c_int, [c_vp]),
     "toep_op_slab": (c_int, [c_vp, c_int, c_int, c_vp, ctypes.POINTER(c_vp)]),
+    "toep_op_create_slab": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
+                                    ctypes.POINTER(c_vp)]),
     "toep_matvec_stage": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_int, c_vp]),
     "toep_matvec_stage_peer": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_int, c_vp]),
     "toep_peer_wait": (c_int, [c_vp, ctypes.c_uint64, c_vp]),

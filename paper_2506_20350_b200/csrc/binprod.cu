@@ -413,33 +413,12 @@ int launch_cm(const void* DT, const void* U, void* V, int64_t K, int n0, int64_t
   return TOEP_OK;
 }
 
-// TOEP_BINPROD selects the single-RHS streaming kernel (A/B measurement):
-//   simple (LDG, 4 rows in flight), simple8 (LDG, 8 rows), tma64 (bulk copies of 64-column row
-//   segments), tmafull (default: one bulk copy of whole DT rows per stage)
-int binprod_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("TOEP_BINPROD");
-    if (e == nullptr) return 3;
-    if (std::strcmp(e, "simple") == 0) return 0;
-    if (std::strcmp(e, "simple8") == 0) return 1;
-    if (std::strcmp(e, "tma64") == 0) return 2;
-    if (std::strcmp(e, "tmafull4") == 0) return 4;
-    if (std::strcmp(e, "tmafull3") == 0) return 5;
-    return 3;
-  }();
-  return v;
-}
-
 template <typename T, int MT, int STAGES = 6>
 int launch_tma(const void* DT, const void* U, void* V, int64_t K, int n0, const int* stop, cudaStream_t s) {
   constexpr int RB = 32768 / (MT * sizeof(C<T>));  // 32 KB per stage
   using Cfg = TmaCfg<T, MT, RB, STAGES>;
   auto kern = binprod_tma_kernel<T, MT, RB, STAGES>;
-  static bool attr = false;
-  if (!attr) {
-    TOEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
-    attr = true;
-  }
+  TOEP_CUDA(ensure_smem(kern, Cfg::kSmem));
   const int mtiles = n0 / MT;
   const int64_t items = K * mtiles;
   const int grid = static_cast<int>(std::min<int64_t>(items, sm_count()));
@@ -472,12 +451,10 @@ int bin_product_t(const void* DT, const void* U, void* V, int64_t K, int n0, int
                 static_cast<int64_t>(n0) * w, K, s, stop);
   }
   if (w == 1) {
-    const int var = binprod_variant();
-    if (var == 3 && n0 == 128) return launch_tma<T, 128>(DT, U, V, K, n0, stop, s);
-    if (var == 4 && n0 == 128) return launch_tma<T, 128, 4>(DT, U, V, K, n0, stop, s);
-    if (var == 5 && n0 == 128) return launch_tma<T, 128, 3>(DT, U, V, K, n0, stop, s);
-    if (var >= 2 && n0 % 64 == 0 && n0 <= 256) return launch_tma<T, 64>(DT, U, V, K, n0, stop, s);
-    if (var == 1) return launch_cm<T, 1, 8>(DT, U, V, K, n0, w, stop, s);
+    // whole-row bulk-copy stream (N_b = 128: one 32 KB DT row pair per stage), 64-column row
+    // segments for the other multiples of 64, the SIMT column kernel otherwise
+    if (n0 == 128) return launch_tma<T, 128>(DT, U, V, K, n0, stop, s);
+    if (n0 % 64 == 0 && n0 <= 256) return launch_tma<T, 64>(DT, U, V, K, n0, stop, s);
     return launch_cm<T, 1>(DT, U, V, K, n0, w, stop, s);
   }
   if (w == 2) return launch_cm<T, 2>(DT, U, V, K, n0, w, stop, s);
@@ -489,13 +466,11 @@ int bin_product_t(const void* DT, const void* U, void* V, int64_t K, int n0, int
 
 L2Prefetch binprod_prefetch_plan(int dtype, const void* DT, int64_t K, int n0, int side) {
   L2Prefetch pf;
-  if (n0 != 128 || binprod_variant() != 3) return pf;  // only the whole-row TMA stream has this bin order
-  auto env_mb = [](const char* name, int64_t dflt) {
-    const char* e = std::getenv(name);
-    return static_cast<int64_t>(e != nullptr ? std::atoll(e) : dflt) << 20;
-  };
-  static const int64_t budget[3] = {env_mb("TOEP_PREFETCH_MB", 48), env_mb("TOEP_PREFETCH_INV_MB", 0),
-                                    env_mb("TOEP_PREFETCH_ORTH_MB", 0)};
+  if (n0 != 128) return pf;  // only the whole-row TMA stream has this bin order
+  // L2 prefetch of the head of every CTA's bin range, issued by the forward DFT (side 0) while it
+  // computes: 48 MB measured best (+4 %); from the inverse DFT (side 1) or the GMRES
+  // orthogonalisation (side 2) it measured no gain, so those budgets are 0
+  constexpr int64_t budget[3] = {int64_t{48} << 20, 0, 0};
   const int64_t bin_bytes = static_cast<int64_t>(n0) * n0 * (dtype == TOEP_C64 ? 8 : 16);
   pf.ranges = static_cast<int>(std::min<int64_t>(K, sm_count()));
   const int64_t range_min = bin_bytes * (K / pf.ranges);

@@ -44,6 +44,14 @@ template <typename Z, typename S> __host__ __device__ __forceinline__ Z cscale(Z
 void set_error(const char* fmt, ...);
 const char* last_error();
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize >= bytes for `func` on the CURRENT device.
+// Function attributes belong to a device context, so the cache is keyed by (device, function);
+// thread-safe.  Cheap on the hit path (one lock + map lookup).
+cudaError_t ensure_smem_attr(const void* func, size_t bytes);
+template <typename F> inline cudaError_t ensure_smem(F* func, size_t bytes) {
+  return ensure_smem_attr(reinterpret_cast<const void*>(func), bytes);
+}
+
 struct Status {
   int code = TOEP_OK;
 };

@@ -272,11 +272,8 @@ __device__ __forceinline__ void plan_stage(const PassArgs& a, const C<TI>* __res
               const double t3 = a.in_planes[2 * a.plane + e];
               v[r] = mk<TC>(static_cast<TC>(t1 - t2), static_cast<TC>(t3 - t1 - t2));
             }
-          } else if (a.part_count == nullptr) {
-            v[r] = cvt<Z>(gin[row * a.in_sa + col * a.in_cs]);
           } else {
-            const int np = a.part_count[row];
-            for (int p = 0; p < np; ++p) v[r] = cadd(v[r], cvt<Z>(gin[row * a.in_sa + p * a.part_stride + col * a.in_cs]));
+            v[r] = cvt<Z>(gin[row * a.in_sa + col * a.in_cs]);
           }
         }
       } else {
@@ -465,7 +462,7 @@ int try_stream(const PassArgs& a, cudaStream_t s) {
     const char* e = std::getenv("TOEP_FFT_STREAM");
     return e != nullptr && std::strcmp(e, "all") == 0;
   }();
-  if (min_tiles <= 0 || ntiles < min_tiles || a.in_idx != nullptr || a.out_idx != nullptr || a.part_count != nullptr ||
+  if (min_tiles <= 0 || ntiles < min_tiles || a.in_idx != nullptr || a.out_idx != nullptr ||
       a.scatter != nullptr || (a.in_planes == nullptr && !all))
     return -1;
   constexpr int L = PlanLen<Rs...>::value;
@@ -473,10 +470,9 @@ int try_stream(const PassArgs& a, cudaStream_t s) {
     constexpr int kIn = decltype(kin_tag)::value;
     using SM = StreamSmem<TC, TIL, kIn, L>;
     auto kern = fft_plan_stream_kernel<TC, TO, TIL, kIn, Rs...>;
-    static int per_sm = 0;
+    static int per_sm = 0;  // identical devices: same occupancy; the attribute itself is per device
+    TOEP_CUDA(ensure_smem(kern, SM::bytes));
     if (per_sm == 0) {
-      if (SM::bytes > 48 * 1024)
-        TOEP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SM::bytes)));
       TOEP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, SM::bytes));
       if (per_sm <= 0) per_sm = 1;
     }
@@ -628,12 +624,7 @@ int launch2d(bool inverse, const Fft2dArgs& f, cudaStream_t s) {
   auto kf = fft2d_kernel<TI, TC, TO, TILX, TILY, PX, PY, false>;
   auto ki = fft2d_kernel<TI, TC, TO, TILX, TILY, PX, PY, true>;
   auto k = inverse ? ki : kf;
-  static size_t attr_f = 0, attr_i = 0;
-  size_t& attr = inverse ? attr_i : attr_f;
-  if (attr < smem) {
-    TOEP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  TOEP_CUDA(ensure_smem(k, smem));
   return launch_k(k, dim3(static_cast<unsigned>(f.inner)), dim3(k2dThreads), smem, s, f);
 }
 
@@ -783,11 +774,11 @@ int launch(const PassArgs& a, const Radices& rad, bool direct, cudaStream_t s) {
   case T: {                                                                                      \
     if (direct) {                                                                                \
       auto k = dft_direct_kernel<TI, TC, TO, T>;                                                 \
-      if (smem > 48 * 1024) TOEP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      TOEP_CUDA(ensure_smem(k, smem)); \
       k<<<grid, kThreads, smem, s>>>(a, two_over_L);                                             \
     } else {                                                                                     \
       auto k = fft_pass_kernel<TI, TC, TO, T>;                                                   \
-      if (smem > 48 * 1024) TOEP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      TOEP_CUDA(ensure_smem(k, smem)); \
       k<<<grid, kThreads, smem, s>>>(a, rad, two_over_L);                                        \
     }                                                                                            \
     break;                                                                                       \

@@ -474,7 +474,15 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
     unsigned old;
     asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
     const unsigned target = (old / gridDim.x + 1) * gridDim.x;
-    while (static_cast<int>(ld_acquire_gpu(bar) - target) < 0) {
+    // a CTA that never arrives (a fault elsewhere in the grid) must not hang the device forever:
+    // trap after 10 s, which surfaces as a CUDA error on the host
+    long long t0 = 0;
+    for (unsigned spins = 1; static_cast<int>(ld_acquire_gpu(bar) - target) < 0; ++spins) {
+      if ((spins & 1023u) == 0) {
+        const long long t = global_ns();
+        if (t0 == 0) t0 = t;
+        else if (t - t0 > 10000000000ll) __trap();
+      }
     }
   }
   __syncthreads();
@@ -1139,11 +1147,21 @@ struct Trace {
   // spin on the event: cudaEventSynchronize may yield the thread and wake it up
   // hundreds of microseconds late, which starves the launch queue
   // spin until the device has completed `target` steps overall (or stopped)
-  void wait_total(const HostFlags* hf, int target) {
+  // Every 4096 spins the stream is queried: a device fault returns TOEP_ERR_CUDA instead of
+  // spinning forever, and a drained stream (nothing left that could advance the word) ends the wait.
+  int wait_total(const HostFlags* hf, int target, cudaStream_t s) {
     const auto a = clk::now();
-    while (hf->total < target && !hf->stop) {
+    for (unsigned spins = 1; hf->total < target && !hf->stop; ++spins) {
+      if ((spins & 4095u) != 0) continue;
+      const cudaError_t e = cudaStreamQuery(s);
+      if (e == cudaSuccess) break;
+      if (e != cudaErrorNotReady) {
+        set_error("gmres: device error while waiting for step %d: %s", target, cudaGetErrorString(e));
+        return TOEP_ERR_CUDA;
+      }
     }
     if (on) wait += std::chrono::duration<double, std::milli>(clk::now() - a).count();
+    return TOEP_OK;
   }
 };
 
@@ -1557,7 +1575,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       // record would break their programmatic-dependent-launch chain)
       constexpr int kLag = 2;
       if (j > kLag) {
-        tr.wait_total(hf, total + (j - kLag));
+        G_TRY(tr.wait_total(hf, total + (j - kLag), s));
         if (hf->stop) break;
       }
     }

@@ -31,10 +31,6 @@ struct PassArgs {
   int64_t out_idx_stride = 0;
   const int* stop = nullptr;  // if non-null and *stop != 0 the launch is a no-op
   const double* in_scale = nullptr;  // optional device scalar multiplying the input
-  // optional: input row a is the sum of part_count[a] slabs spaced part_stride apart
-  // (the per-CTA inverse level-2 partials of the fused spectral kernel)
-  const int* part_count = nullptr;
-  int64_t part_stride = 0;
   // stride of the batch ("column") index; 1 = contiguous batch (all standalone passes)
   int64_t in_cs = 1, out_cs = 1;
   // optional split-plane I/O (3M products of the multi-RHS path): out_planes receives (re, im,

@@ -19,6 +19,20 @@ void set_error(const char* fmt, ...) {
 }
 const char* last_error() { return g_err; }
 
+cudaError_t ensure_smem_attr(const void* func, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{dev, func}];
+  if (have >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
 size_t elt_size(int dtype) { return dtype == TOEP_C64 ? sizeof(float2) : sizeof(double2); }
 int64_t op_dim(const toep_op_s* op) { return static_cast<int64_t>(op->n2) * op->n1 * op->n0; }
 
@@ -46,6 +60,12 @@ void keep_pool() {
   }
   cudaGetLastError();
   done_dev = dev;
+}
+
+// Register `s` as a stream with work reading the operator (toep_op_destroy synchronises it)
+void note_stream(toep_op_s* op, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(op->mu);
+  op->ws[s];
 }
 
 int op_workspace(toep_op_s* op, int64_t w, cudaStream_t s, toep_op_s::Workspace** out, bool need_hat) {
@@ -128,6 +148,38 @@ bool mrhs_ozaki(const toep_op_s* op) {
   return on && ozaki_supported(op->n0);
 }
 
+// Publish a lazily built operator-wide buffer: record an event on the building stream (op->mu held)
+static int mark_lazy_build(toep_op_s* op, cudaStream_t s) {
+  if (op->lazy_ev == nullptr) TOEP_CUDA(cudaEventCreateWithFlags(&op->lazy_ev, cudaEventDisableTiming));
+  TOEP_CUDA(cudaEventRecord(op->lazy_ev, s));
+  op->lazy_stream = s;
+  return TOEP_OK;
+}
+
+// A stream other than the one that built the lazy buffers waits for that build (op->mu held)
+static int order_after_lazy_build(toep_op_s* op, cudaStream_t s) {
+  if (op->lazy_ev != nullptr && op->lazy_stream != s) TOEP_CUDA(cudaStreamWaitEvent(s, op->lazy_ev, 0));
+  return TOEP_OK;
+}
+
+// (Re)size a per-stream device buffer to at least `need` bytes; capacity tracked in bytes because
+// the per-call size depends on w through the chunking (mrhs_chunk), not monotonically
+template <typename T>
+static int ensure_bytes(T** buf, size_t* cap, size_t need, cudaStream_t s, const char* what) {
+  if (*cap >= need && *buf != nullptr) return TOEP_OK;
+  if (*buf) TOEP_CUDA(cudaFreeAsync(*buf, s));
+  *buf = nullptr;
+  *cap = 0;
+  if (cudaMallocAsync(reinterpret_cast<void**>(buf), need, s) != cudaSuccess) {
+    cudaGetLastError();
+    *buf = nullptr;
+    set_error("out of device memory for %s (%zu bytes)", what, need);
+    return TOEP_ERR_OOM;
+  }
+  *cap = need;
+  return TOEP_OK;
+}
+
 int ensure_ozaki(toep_op_s* op, toep_op_s::Workspace* ws, int64_t w, int kc, cudaStream_t s) {
   std::lock_guard<std::mutex> lock(op->mu);
   if (op->oz_a == nullptr) {
@@ -136,27 +188,22 @@ int ensure_ozaki(toep_op_s* op, toep_op_s::Workspace* ws, int64_t w, int kc, cud
         cudaMallocAsync(reinterpret_cast<void**>(&op->oz_aexp), op->K * 2 * op->n0 * sizeof(int32_t), s) !=
             cudaSuccess) {
       cudaGetLastError();
+      if (op->oz_a) cudaFreeAsync(op->oz_a, s);
+      op->oz_a = nullptr;
+      op->oz_aexp = nullptr;
       set_error("out of device memory for the operator's int8 slices");
       return TOEP_ERR_OOM;
     }
     TOEP_TRY(ozaki_slice_a(op->DT, op->n0, op->l2, op->l1, op->oz_a, op->oz_aexp, s));
+    TOEP_TRY(mark_lazy_build(op, s));
+  } else {
+    TOEP_TRY(order_after_lazy_build(op, s));
   }
-  if (ws->oz_cap < w) {
-    if (ws->oz_b) TOEP_CUDA(cudaFreeAsync(ws->oz_b, s));
-    if (ws->oz_bexp) TOEP_CUDA(cudaFreeAsync(ws->oz_bexp, s));
-    ws->oz_b = nullptr;
-    ws->oz_bexp = nullptr;
-    ws->oz_cap = 0;
-    const int64_t bins = static_cast<int64_t>(kc) * op->l2;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&ws->oz_b), ozaki_b_bytes(op->n0, bins, w), s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&ws->oz_bexp), ozaki_b_exps(bins, w) * sizeof(int32_t), s) !=
-            cudaSuccess) {
-      cudaGetLastError();
-      set_error("out of device memory for the int8 right-hand-side slices (w=%lld)", static_cast<long long>(w));
-      return TOEP_ERR_OOM;
-    }
-    ws->oz_cap = w;
-  }
+  const int64_t bins = static_cast<int64_t>(kc) * op->l2;
+  TOEP_TRY(ensure_bytes(&ws->oz_b, &ws->oz_b_bytes, static_cast<size_t>(ozaki_b_bytes(op->n0, bins, w)), s,
+                        "the int8 right-hand-side slices"));
+  TOEP_TRY(ensure_bytes(&ws->oz_bexp, &ws->oz_bexp_bytes, static_cast<size_t>(ozaki_b_exps(bins, w)) * sizeof(int32_t),
+                        s, "the int8 right-hand-side exponents"));
   return TOEP_OK;
 }
 
@@ -175,20 +222,20 @@ int ensure_planes(toep_op_s* op, toep_op_s::Workspace* ws, int64_t w, cudaStream
     k_split_planes<<<grid, 256, 0, s>>>(static_cast<const double2*>(op->DT), cnt, op->l2, op->l1,
                                         static_cast<int64_t>(op->n0) * op->n0, op->DTp);
     TOEP_LAUNCHED();
+    TOEP_TRY(mark_lazy_build(op, s));
+  } else if (need_dtp) {
+    TOEP_TRY(order_after_lazy_build(op, s));
   }
-  if (ws->p_cap < w) {
+  const size_t bytes = 3 * static_cast<size_t>(op->l2) * mrhs_chunk(op, w) * op->n0 * w * sizeof(double);
+  if (ws->p_bytes < bytes || ws->hatp == nullptr || ws->hat2p == nullptr) {
+    size_t c1 = 0, c2 = 0;
     if (ws->hatp) TOEP_CUDA(cudaFreeAsync(ws->hatp, s));
     if (ws->hat2p) TOEP_CUDA(cudaFreeAsync(ws->hat2p, s));
     ws->hatp = ws->hat2p = nullptr;
-    ws->p_cap = 0;
-    const size_t bytes = 3 * static_cast<size_t>(op->l2) * mrhs_chunk(op, w) * op->n0 * w * sizeof(double);
-    if (cudaMallocAsync(reinterpret_cast<void**>(&ws->hatp), bytes, s) != cudaSuccess ||
-        cudaMallocAsync(reinterpret_cast<void**>(&ws->hat2p), bytes, s) != cudaSuccess) {
-      cudaGetLastError();
-      set_error("out of device memory for the 3M workspace (w=%lld)", static_cast<long long>(w));
-      return TOEP_ERR_OOM;
-    }
-    ws->p_cap = w;
+    ws->p_bytes = 0;
+    TOEP_TRY(ensure_bytes(&ws->hatp, &c1, bytes, s, "the 3M workspace"));
+    TOEP_TRY(ensure_bytes(&ws->hat2p, &c2, bytes, s, "the 3M workspace"));
+    ws->p_bytes = bytes;
   }
   return TOEP_OK;
 }
@@ -206,37 +253,6 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
   const int s1 = transpose ? +1 : -1;
   const double sc1y = transpose ? 1.0 / op->l2 : 1.0, sc1x = transpose ? 1.0 / op->l1 : 1.0;
   const double sc2y = transpose ? 1.0 : 1.0 / op->l2, sc2x = transpose ? 1.0 : 1.0 / op->l1;
-
-  if (fused_eligible(op, w, transpose)) {
-    // level-1 pass -> fused (level-2 DFT + per-bin product + inverse level-2 DFT) -> inverse level-1 pass
-    TOEP_TRY(fused_prepare(op, s));
-    {
-      std::lock_guard<std::mutex> lock(op->mu);
-      if (ws->parts == nullptr) {
-        const size_t bytes = static_cast<size_t>(op->l1) * op->fused_maxp * op->n2 * op->n0 * elt_size(op->dtype);
-        if (cudaMallocAsync(&ws->parts, bytes, s) != cudaSuccess ||
-            cudaMallocAsync(reinterpret_cast<void**>(&ws->cnt), sizeof(int) * op->l1, s) != cudaSuccess) {
-          cudaGetLastError();
-          set_error("out of device memory for fused matvec workspace");
-          return TOEP_ERR_OOM;
-        }
-        TOEP_CUDA(cudaMemsetAsync(ws->cnt, 0, sizeof(int) * op->l1, s));
-      }
-    }
-    PassArgs a;
-    a.in = u; a.out = ws->x1; a.L = op->l1; a.n_lo = op->n1; a.n_hi = 0; a.n_out = op->l1;
-    a.inner = inner; a.outer = op->n2; a.in_sa = inner; a.in_so = op->n1 * inner; a.out_sa = inner;
-    a.out_so = op->l1 * inner; a.sign = -1; a.scale = 1.0; a.stop = stop; a.in_scale = in_scale;
-    TOEP_TRY(fft_pass(a, tio, tc, tc, s));
-    // X2 [n2][l1][n0] reuses the (otherwise idle) spectral workspace
-    TOEP_TRY(fused_spectral(op, ws->x1, ws->parts, ws->hat, ws->cnt, stop, s));
-    PassArgs d;  // inverse level-1 DFT of the combined columns, crop, 1/(l1 l2)
-    d.in = ws->hat; d.out = v; d.L = op->l1; d.n_lo = op->l1; d.n_hi = 0; d.n_out = op->n1;
-    d.inner = inner; d.outer = op->n2; d.in_sa = inner; d.in_so = op->l1 * inner;
-    d.out_sa = inner; d.out_so = op->n1 * inner; d.sign = +1; d.scale = 1.0 / (static_cast<double>(op->l1) * op->l2);
-    d.stop = stop;
-    return fft_pass(d, tc, tc, tio, s);
-  }
 
   // one-CTA-per-column 2-D transforms when a compiled 2-D plan covers the grid
   if (w == 1) {
@@ -357,6 +373,13 @@ int toep_version(void) { return 100; }
 
 int toep_op_create(const void* stacked4, int on_device, int n2, int n1, int n0, int l2, int l1, int dtype,
                    void* stream, toep_op_t* out) {
+  return toep_op_create_slab(stacked4, on_device, n2, n1, n0, l2, l1, dtype, 0, 0, stream, out);
+}
+
+// kx1 <= kx0 (e.g. 0, 0): the full operator; else only the bins of level-1 frequencies [kx0, kx1)
+// are transformed and kept (the slab operator of the row / kx-slab decomposition)
+int toep_op_create_slab(const void* stacked4, int on_device, int n2, int n1, int n0, int l2, int l1, int dtype,
+                        int kx0, int kx1, void* stream, toep_op_t* out) {
   TOEP_REQUIRE(out != nullptr && stacked4 != nullptr, TOEP_ERR_ARG, "null argument");
   TOEP_REQUIRE(n2 >= 1 && n1 >= 1 && n0 >= 1, TOEP_ERR_SHAPE, "n2, n1, n0 must be positive");
   TOEP_REQUIRE(dtype == TOEP_C128 || dtype == TOEP_C64, TOEP_ERR_ARG, "dtype must be TOEP_C128 or TOEP_C64");
@@ -366,10 +389,15 @@ int toep_op_create(const void* stacked4, int on_device, int n2, int n1, int n0, 
   TOEP_REQUIRE(l2 >= k2 && l1 >= k1, TOEP_ERR_SHAPE, "embedding (%d,%d) shorter than 2n-1 (%d,%d)", l2, l1, k2, k1);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
 
+  const bool slab = kx1 > kx0;
+  if (!slab) { kx0 = 0; kx1 = l1; }
+  TOEP_REQUIRE(0 <= kx0 && kx1 <= l1, TOEP_ERR_SHAPE, "slab [%d,%d) outside [0,%d)", kx0, kx1, l1);
+  const int kxs = kx1 - kx0;
   auto* op = new (std::nothrow) toep_op_s();
   TOEP_REQUIRE(op != nullptr, TOEP_ERR_OOM, "host allocation failed");
   op->n2 = n2; op->n1 = n1; op->n0 = n0; op->l2 = l2; op->l1 = l1; op->dtype = dtype;
-  op->K = static_cast<int64_t>(l2) * l1;
+  op->K = static_cast<int64_t>(l2) * kxs;
+  if (slab) { op->slab_k0 = kx0; op->slab_kxs = kxs; }
   cudaGetDevice(&op->device);
 
   const int64_t nn = static_cast<int64_t>(n0) * n0;
@@ -417,9 +445,10 @@ int toep_op_create(const void* stacked4, int on_device, int n2, int n1, int n0, 
   if (!on_device) { cudaFreeAsync(gen, s); }
   gen = nullptr;
   TOEP_ALLOC(d, d_bytes);
-  PassArgs b;  // level-2 DFT, embedded at offset % l2 -> D [l2][l1][n0][n0]
-  b.in = x; b.out = d; b.L = l2; b.n_lo = n2; b.n_hi = n2 - 1; b.n_out = l2; b.inner = nn; b.outer = l1;
-  b.in_sa = static_cast<int64_t>(l1) * nn; b.in_so = nn; b.out_sa = static_cast<int64_t>(l1) * nn; b.out_so = nn;
+  PassArgs b;  // level-2 DFT of columns [kx0, kx1), embedded at offset % l2 -> D [l2][kxs][n0][n0]
+  b.in = static_cast<const double2*>(x) + static_cast<int64_t>(kx0) * nn; b.out = d; b.L = l2; b.n_lo = n2;
+  b.n_hi = n2 - 1; b.n_out = l2; b.inner = nn; b.outer = kxs;
+  b.in_sa = static_cast<int64_t>(l1) * nn; b.in_so = nn; b.out_sa = static_cast<int64_t>(kxs) * nn; b.out_so = nn;
   b.sign = -1;
   TOEP_STEP(fft_pass(b, 0, 0, 0, s));
   cudaFreeAsync(x, s);
@@ -440,6 +469,7 @@ int toep_op_create(const void* stacked4, int on_device, int n2, int n1, int n0, 
     dt = dt32;
   }
   op->DT = dt;
+  op->ws[s];
   if (cudaStreamSynchronize(s) != cudaSuccess) {
     set_error("precompute_spectral failed: %s", cudaGetErrorString(cudaGetLastError()));
     dt = op->DT;
@@ -453,24 +483,24 @@ int toep_op_create(const void* stacked4, int on_device, int n2, int n1, int n0, 
 
 int toep_op_destroy(toep_op_t op) {
   if (op == nullptr) return TOEP_OK;
-  cudaDeviceSynchronize();
+  // Wait only for the streams this operator was used on (each entry point registers its stream in
+  // op->ws), not the whole device; then return every buffer to the stream-ordered pool.
+  cudaStream_t fs = cudaStreamPerThread;
+  for (auto& kv : op->ws) cudaStreamSynchronize(kv.first);
+  if (op->lazy_ev) cudaEventSynchronize(op->lazy_ev);
+  cudaGetLastError();
+  auto rel = [&](void* p) {
+    if (p) cudaFreeAsync(p, fs);
+  };
   for (auto& kv : op->ws) {
-    cudaFree(kv.second.x1);
-    cudaFree(kv.second.hat);
-    cudaFree(kv.second.hat2);
-    cudaFree(kv.second.parts);
-    cudaFree(kv.second.cnt);
-    cudaFree(kv.second.hatp);
-    cudaFree(kv.second.hat2p);
-    cudaFree(kv.second.io);
-    cudaFree(kv.second.oz_b);
-    cudaFree(kv.second.oz_bexp);
+    auto& w = kv.second;
+    for (void* p : {w.x1, w.hat, w.hat2, static_cast<void*>(w.hatp),
+                    static_cast<void*>(w.hat2p), w.io, static_cast<void*>(w.oz_b), static_cast<void*>(w.oz_bexp)})
+      rel(p);
   }
-  cudaFree(op->oz_a);
-  cudaFree(op->oz_aexp);
-  cudaFree(op->DT);
-  cudaFree(op->DTp);
-  cudaFree(op->part_count);
+  for (void* p : {static_cast<void*>(op->oz_a), static_cast<void*>(op->oz_aexp), op->DT, static_cast<void*>(op->DTp)})
+    rel(p);
+  if (op->lazy_ev) cudaEventDestroy(op->lazy_ev);
   delete op;
   TOEP_LAUNCHED();
   return TOEP_OK;
@@ -487,6 +517,7 @@ int toep_op_info(toep_op_t op, toep_op_info_t* info) {
 int toep_op_diag_blocks(toep_op_t op, void* dst, void* stream) {
   TOEP_REQUIRE(op != nullptr && dst != nullptr, TOEP_ERR_ARG, "null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  note_stream(op, s);
   const int64_t nn = static_cast<int64_t>(op->n0) * op->n0;
   const size_t es = elt_size(op->dtype);
   for (int64_t k0 = 0; k0 < op->K; k0 += 65535) {
@@ -500,6 +531,7 @@ int toep_op_diag_blocks(toep_op_t op, void* dst, void* stream) {
 int toep_op_fold_left(toep_op_t op, const void* m_dev, void* stream, toep_op_t* out) {
   TOEP_REQUIRE(op != nullptr && m_dev != nullptr && out != nullptr, TOEP_ERR_ARG, "null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  note_stream(op, s);
   auto* f = new (std::nothrow) toep_op_s();
   TOEP_REQUIRE(f != nullptr, TOEP_ERR_OOM, "host allocation failed");
   f->n2 = op->n2; f->n1 = op->n1; f->n0 = op->n0; f->l2 = op->l2; f->l1 = op->l1; f->dtype = op->dtype;
@@ -524,10 +556,11 @@ int toep_op_fold_left(toep_op_t op, const void* m_dev, void* stream, toep_op_t* 
                 make_double2(0, 0), f->DT, 1, n0, 0, 1, s);
   if (m32) cudaFreeAsync(m32, s);
   if (rc != TOEP_OK) {
-    cudaFree(f->DT);
+    cudaFreeAsync(f->DT, s);
     delete f;
     return rc;
   }
+  f->ws[s];  // the build stream: toep_op_destroy(f) synchronises it
   *out = f;
   return TOEP_OK;
 }
@@ -536,6 +569,7 @@ int toep_op_slab(toep_op_t op, int kx0, int kx1, void* stream, toep_op_t* out) {
   TOEP_REQUIRE(op != nullptr && out != nullptr && op->slab_kxs == 0, TOEP_ERR_ARG, "slab of a full operator only");
   TOEP_REQUIRE(0 <= kx0 && kx0 < kx1 && kx1 <= op->l1, TOEP_ERR_SHAPE, "slab [%d,%d) outside [0,%d)", kx0, kx1, op->l1);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  note_stream(op, s);
   auto* f = new (std::nothrow) toep_op_s();
   TOEP_REQUIRE(f != nullptr, TOEP_ERR_OOM, "host allocation failed");
   f->n2 = op->n2; f->n1 = op->n1; f->n0 = op->n0; f->l2 = op->l2; f->l1 = op->l1; f->dtype = op->dtype;
@@ -552,11 +586,12 @@ int toep_op_slab(toep_op_t op, int kx0, int kx1, void* stream, toep_op_t* out) {
   const cudaError_t e = cudaMemcpy2DAsync(f->DT, f->slab_kxs * blk, static_cast<const char*>(op->DT) + kx0 * blk,
                                           op->l1 * blk, f->slab_kxs * blk, op->l2, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) {
-    cudaFree(f->DT);
+    cudaFreeAsync(f->DT, s);
     delete f;
     set_error("slab copy failed: %s", cudaGetErrorString(e));
     return TOEP_ERR_CUDA;
   }
+  f->ws[s];  // the build stream: toep_op_destroy(f) synchronises it
   *out = f;
   return TOEP_OK;
 }
@@ -667,6 +702,7 @@ int toep_matvec_host(toep_op_t op, const void* u_host, void* v_host, int64_t w, 
 int toep_op_spectral_apply(toep_op_t op, const void* hat_in, void* hat_out, int64_t w, int flags, void* stream) {
   TOEP_REQUIRE(op != nullptr && hat_in != nullptr && hat_out != nullptr && hat_in != hat_out, TOEP_ERR_ARG,
                "bad spectral_apply arguments");
+  note_stream(op, static_cast<cudaStream_t>(stream));
   return bin_product(op->dtype, op->DT, hat_in, hat_out, op->K, op->n0, w, (flags & TOEP_MV_TRANSPOSE) != 0, nullptr,
                      static_cast<cudaStream_t>(stream));
 }

@@ -18,26 +18,24 @@ struct toep_op_s {
     void* x1 = nullptr;    // [n2][l1][n0*w]
     void* hat = nullptr;   // [K][n0][w]
     void* hat2 = nullptr;  // [K][n0][w]
-    void* parts = nullptr; // fused path: [l1][maxp][n2][n0] inverse level-2 partial slabs
-    int* cnt = nullptr;    // fused path: [l1] slab arrival counters
     double* hatp = nullptr;   // multi-RHS 3M: planes of u_hat (3 x K*n0*w)
     double* hat2p = nullptr;  // multi-RHS 3M: product planes T1, T2, T3
-    int64_t p_cap = 0;
+    size_t p_bytes = 0;       // capacity of hatp / hat2p in bytes (the chunking depends on w)
     void* io = nullptr;  // toep_matvec_host: device copies of u and v
     size_t io_cap = 0;
     int8_t* oz_b = nullptr;     // Ozaki path: int8 slices of one chunk's U planes
     int32_t* oz_bexp = nullptr; // and their column exponents
-    int64_t oz_cap = 0;         // w the buffers were sized for
+    size_t oz_b_bytes = 0, oz_bexp_bytes = 0;  // capacities in bytes
   };
   int8_t* oz_a = nullptr;       // Ozaki path: int8 slices of [Dr -Di; Di Dr] per bin (kx-major)
   int32_t* oz_aexp = nullptr;   // row exponents
+  // operator-wide buffers built lazily (oz_a / oz_aexp, DTp) on the first caller's stream: an
+  // event recorded after the build orders every other stream's first use after it
+  cudaEvent_t lazy_ev = nullptr;
+  cudaStream_t lazy_stream = nullptr;
   // kx-slab operator of the multi-GPU row/slab decomposition (toep_op_slab): bins
   // k' = ky*slab_kxs + (kx - slab_k0); 0 = full operator
   int slab_k0 = 0, slab_kxs = 0;
-  // fused single-RHS path (fused.cu): kx-major persistent partition
-  int fused_grid = 0;
-  int fused_maxp = 0;
-  int* part_count = nullptr;  // device [l1]
   std::mutex mu;
   std::map<cudaStream_t, Workspace> ws;
 };
@@ -59,11 +57,6 @@ void keep_pool();
 // the local stages of the slab-decomposed matvec (toep_matvec_stage / toep_matvec_stage_peer)
 int matvec_stage_impl(toep_op_s* op, int stage, const void* in, void* out, int64_t w, int count,
                       const toep_peer_scatter* scatter, cudaStream_t s);
-
-// fused.cu
-bool fused_eligible(const toep_op_s* op, int64_t w, bool transpose);
-int fused_prepare(toep_op_s* op, cudaStream_t s);
-int fused_spectral(toep_op_s* op, const void* x1, void* parts, void* x2, int* cnt, const int* stop, cudaStream_t s);
 
 int block_apply_impl(const void* m, int n0, const void* in, void* out, int64_t segments, int64_t w, int dtype,
                      cudaStream_t s, const int* stop);

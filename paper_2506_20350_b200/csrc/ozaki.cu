@@ -429,17 +429,9 @@ int ozaki_products(const int8_t* asl, const int32_t* aexp, const double* re, con
   if (bins == 0 || w == 0) return TOEP_OK;
   const int ntiles = static_cast<int>((w + kBN - 1) / kBN);
   const size_t tsm = static_cast<size_t>(2 * n0) * kSliceCols * sizeof(double);
-  static size_t tattr = 0;
-  if (tattr < tsm) {
-    TOEP_CUDA(cudaFuncSetAttribute(ozaki_slice_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tsm)));
-    tattr = tsm;
-  }
+  TOEP_CUDA(ensure_smem(ozaki_slice_b_kernel, tsm));
   const size_t smem = kStages * (kATile + kBTile);
-  static bool attr = false;
-  if (!attr) {
-    TOEP_CUDA(cudaFuncSetAttribute(ozaki_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  TOEP_CUDA(ensure_smem(ozaki_tile_kernel, smem));
   static const int dbg = [] {
     const char* e = std::getenv("TOEP_OZ_DBG");
     return e != nullptr ? std::atoi(e) : 0;

@@ -116,11 +116,7 @@ void trsm(const double2* LU, int lda, double2* X, int64_t ldx, int r0, int nb, i
           cudaStream_t s) {
   static_assert(NB % kTrsmWarps == 0 && NB % 32 == 0, "trsm block");
   constexpr int smem = NB * (NB + 1) * static_cast<int>(sizeof(double2));
-  static bool configured = false;  // opt-in above 48 KB, once per process
-  if (!configured) {
-    cudaFuncSetAttribute(trsm_block<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
-  }
+  ensure_smem(trsm_block<NB>, smem);
   trsm_block<NB><<<(ncols + kTrsmWarps - 1) / kTrsmWarps, kTrsmWarps * 32, smem, s>>>(LU, lda, X, ldx, r0, nb, c0, ncols,
                                                                                   upper);
 }
@@ -529,13 +525,9 @@ int getrf_batched(double2* A, int64_t mstride, int batch, int n, int* ipiv, int*
   const int rpc = (n + kCL - 1) / kCL;
   TOEP_REQUIRE(rpc <= 4 * kRowsPass, TOEP_ERR_ARG, "lu_factor: n = %d exceeds the cluster-resident panel (n <= 4096)",
                n);
-  static size_t attr = 0;
-  if (psmem > 40 * 1024 && attr < psmem) {
-    TOEP_CUDA(cudaFuncSetAttribute(lu_panel_cluster<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
-    TOEP_CUDA(cudaFuncSetAttribute(lu_panel_cluster<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
-    TOEP_CUDA(cudaFuncSetAttribute(lu_panel_cluster<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
-    attr = psmem;
-  }
+  TOEP_CUDA(ensure_smem(lu_panel_cluster<1>, psmem));
+  TOEP_CUDA(ensure_smem(lu_panel_cluster<2>, psmem));
+  TOEP_CUDA(ensure_smem(lu_panel_cluster<4>, psmem));
   int* moves = nullptr;
   TOEP_REQUIRE(cudaMallocAsync(reinterpret_cast<void**>(&moves), sizeof(int) * kMovesStride * batch, s) == cudaSuccess,
                TOEP_ERR_OOM, "out of device memory in lu_factor");

@@ -50,14 +50,23 @@ row_range = column_range
 slab_ranges = column_range
 
 
-def _gather_cols(x_local: torch.Tensor, w: int, world: int, group) -> torch.Tensor:
-    """All-gather column shards (n, w_r) into (n, w) on every rank."""
+def _gather_cols(x_local: torch.Tensor, w: int, world: int, group, root: int | None) -> torch.Tensor | None:
+    """Column shards (n, w_r) -> (n, w) on ``root`` (``None``: on every rank); other ranks get None."""
     n = x_local.shape[0]
     per = -(-w // world)
     buf = torch.zeros((n, per), dtype=x_local.dtype, device=x_local.device)
     buf[:, : x_local.shape[1]] = x_local
-    parts = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(parts, buf.contiguous(), group=group)
+    rank = dist.get_rank(group)
+    rv = torch.view_as_real if buf.is_complex() else (lambda t: t)  # gloo has no complex collectives
+    if root is None:
+        parts = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather([rv(t) for t in parts], rv(buf), group=group)
+    else:
+        parts = [torch.empty_like(buf) for _ in range(world)] if rank == root else None
+        dist.gather(rv(buf), [rv(t) for t in parts] if parts is not None else None,
+                    dst=dist.get_global_rank(group, root) if group is not None else root, group=group)
+        if rank != root:
+            return None
     cols = []
     for r in range(world):
         c0, c1 = column_range(w, world, r)
@@ -65,14 +74,19 @@ def _gather_cols(x_local: torch.Tensor, w: int, world: int, group) -> torch.Tens
     return torch.cat(cols, dim=1)
 
 
-def solve_columns_sharded(op, p, rhs, cfg, group=None, solver=None, method: str = "sequential"):
+def solve_columns_sharded(op, p, rhs, cfg, group=None, solver=None, method: str = "sequential",
+                          gather: str = "root"):
     """Column-sharded ``solve_multi_rhs_sequential`` (gmres.py:304-336) over the process group.
 
-    Every rank passes the full (n, W) right-hand side (or just its own columns via
-    ``rhs_is_local``-free convention: the full block is sliced here); each solves its column
-    range, then X and the reports are all-gathered, so every rank returns the full result.
+    Every rank passes the full (n, W) right-hand side (the rank's column range is sliced here) and
+    solves its columns with no communication in the data path.  ``gather="root"`` (default):
+    rank 0 receives X (n, W) and every column's report, the other ranks return their own column
+    block and reports; ``gather="all"``: every rank returns the full result.  A column that did not
+    converge raises ``NoConvergence`` on every rank (one all-reduced flag).
     ``solver(op, p, block, cfg, method)`` defaults to the device batched solver.
     """
+    if gather not in ("root", "all"):
+        raise ValueError(f"gather must be 'root' or 'all', got {gather!r}")
     if solver is None:
         from .solvers.gmres import solve_multi_rhs_sequential as solver
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -83,27 +97,41 @@ def solve_columns_sharded(op, p, rhs, cfg, group=None, solver=None, method: str 
     w = full.shape[1]
     c0, c1 = column_range(w, world, rank)
     local = full[:, c0:c1].contiguous()
-    failed_local = False
     try:
         x_local, reports = solver(op, p, local, cfg, method)
     except NoConvergence as exc:
-        x_local, reports, failed_local = exc.solution, exc.reports, True
+        x_local, reports = exc.solution, exc.reports
     x_local = torch.as_tensor(x_local)
     if world == 1:
-        if failed_local:
-            raise NoConvergence("columns did not converge", solution=x_local, reports=reports)
+        if any(not r.converged for r in reports):
+            bad = [i for i, r in enumerate(reports) if not r.converged]
+            raise NoConvergence(f"columns {bad} did not converge within {cfg.max_iter} iterations",
+                                solution=x_local, reports=reports)
         return x_local, reports
     backend = dist.get_backend(group)
     dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-    x_all = _gather_cols(x_local.to(dev), w, world, group)
-    gathered = [None] * world
-    dist.all_gather_object(gathered, reports, group=group)
-    all_reports = [r for part in gathered for r in part]
-    if any(not r.converged for r in all_reports):
-        bad = [i for i, r in enumerate(all_reports) if not r.converged]
-        raise NoConvergence(f"columns {bad} did not converge within {cfg.max_iter} iterations", solution=x_all,
-                            reports=all_reports)
-    return x_all, all_reports
+    root = None if gather == "all" else 0
+    x_all = _gather_cols(x_local.to(dev), w, world, group, root)
+    if root is None:
+        got = [None] * world
+        dist.all_gather_object(got, reports, group=group)
+    else:
+        got = [None] * world if rank == root else None
+        dist.gather_object(reports, got, dst=dist.get_global_rank(group, root) if group is not None else root,
+                           group=group)
+    failed = torch.tensor([sum(1 for r in reports if not r.converged)], dtype=torch.int64, device=dev)
+    dist.all_reduce(failed, group=group)
+    if got is not None:
+        all_reports = [r for part in got for r in part]
+        x_out = x_all
+    else:
+        all_reports, x_out = reports, x_local
+    if int(failed.item()):
+        bad = [c0 + i for i, r in enumerate(reports) if not r.converged] if got is None else \
+            [i for i, r in enumerate(all_reports) if not r.converged]
+        raise NoConvergence(f"{int(failed.item())} columns did not converge within {cfg.max_iter} iterations "
+                            f"(this rank's view: {bad})", solution=x_out, reports=all_reports)
+    return x_out, all_reports
 
 
 class SlabOperator:
@@ -136,11 +164,12 @@ class SlabOperator:
 
     @classmethod
     def from_generator(cls, gen, group=None, dtype=torch.complex128, exchange: str = "collective"):
-        """Device slab operator: each rank keeps only its kx slab of the spectral blocks."""
+        """Device slab operator: each rank transforms and keeps only its kx slab of the spectral
+        blocks.  ``gen``: a generator, or the stacked blocks (host array / CUDA tensor)."""
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         st = DeviceSlabStages(gen, world, rank, dtype)
-        return cls(gen.n2, gen.n1, gen.n0, st.l2, st.l1, st, group, exchange)
+        return cls(st.n2, st.n1, st.n0, st.l2, st.l1, st, group, exchange)
 
     @property
     def local_dim(self) -> int:
@@ -246,23 +275,24 @@ def gmres_slab(op: SlabOperator, p, b_local, cfg):
 
 
 class DeviceSlabStages:
-    """The three local stages of SlabOperator on the device (toep_matvec_stage)."""
+    """The three local stages of SlabOperator on the device (toep_matvec_stage).
 
-    def __init__(self, gen, world: int, rank: int, dtype):
-        from .toeplitz import precompute_spectral
+    The rank's slab operator is built straight from the generator (``toep_op_create_slab``): the
+    level-2 DFT runs only over the rank's level-1 frequencies, so no rank ever holds the full
+    spectral operator (resident bytes = D * kxs / l1).  ``gen`` may be a generator, a host stacked
+    array or a CUDA tensor of the stacked blocks (e.g. broadcast from rank 0).
+    """
 
-        self.l2 = self.l1 = None
-        full = precompute_spectral(gen, dtype=dtype)
-        self.l2, self.l1 = full.l2, full.l1
-        k0, k1 = slab_ranges(full.l1, world, rank)
-        out = ctypes.c_void_p()
-        _lib.check(_lib.lib().toep_op_slab(full.handle, k0, k1, _lib.stream_handle(), ctypes.byref(out)), "op_slab")
-        from .toeplitz import _wrap
+    def __init__(self, gen, world: int, rank: int, dtype, embedding=None):
+        from .toeplitz import _smooth7, precompute_spectral_stacked
 
-        self.op = _wrap(out.value, full.device)
-        del full
-        self.k0, self.k1 = k0, k1
-        self.n2, self.n1, self.n0 = gen.n2, gen.n1, gen.n0
+        stacked = gen if isinstance(gen, (np.ndarray, torch.Tensor)) else gen.stacked4()
+        k2, k1, n0 = int(stacked.shape[0]), int(stacked.shape[1]), int(stacked.shape[2])
+        self.n2, self.n1, self.n0 = (k2 + 1) // 2, (k1 + 1) // 2, n0
+        self.l2, self.l1 = embedding if embedding is not None else (_smooth7(k2), _smooth7(k1))
+        k0, k1_ = slab_ranges(self.l1, world, rank)
+        self.op = precompute_spectral_stacked(stacked, dtype=dtype, embedding=(self.l2, self.l1), slab=(k0, k1_))
+        self.k0, self.k1 = k0, k1_
 
     def _stage(self, stage: int, x: torch.Tensor, out_shape, count: int):
         x = x.contiguous()

@@ -25,6 +25,7 @@ from . import _lib
 _ALIGN = 4096
 _CACHE_CAP = int(os.environ.get("TOEP_HOST_CACHE_MB", "1024")) << 20
 _cache: dict[int, list[int]] = {}
+_live: dict[int, int] = {}  # start address -> bytes of every block handed out and not yet released
 _cached_bytes = 0
 _mu = threading.Lock()
 _types: dict[int, type] = {}
@@ -33,6 +34,7 @@ _types: dict[int, type] = {}
 def _release(addr: int, nbytes: int) -> None:
     global _cached_bytes
     with _mu:
+        _live.pop(addr, None)
         if _cached_bytes + nbytes <= _CACHE_CAP:
             _cache.setdefault(nbytes, []).append(addr)
             _cached_bytes += nbytes
@@ -59,9 +61,13 @@ def _acquire(nbytes: int) -> int:
         free = _cache.get(nbytes)
         if free:
             _cached_bytes -= nbytes
-            return free.pop()
+            addr = free.pop()
+            _live[addr] = nbytes
+            return addr
     out = ctypes.c_void_p()
     _lib.check(_lib.lib().toep_host_alloc(ctypes.c_uint64(nbytes), ctypes.byref(out)), "pinned_empty")
+    with _mu:
+        _live[int(out.value)] = nbytes
     return int(out.value)
 
 
@@ -88,6 +94,8 @@ def pinned_empty(shape, dtype=torch.complex128) -> torch.Tensor:
         shp, count, nbytes, btype = _layout(shape, dtype)
     except TypeError:  # unhashable shape (e.g. a list)
         shp, count, nbytes, btype = _layout(tuple(shape), dtype)
+    if count == 0:  # torch.frombuffer rejects count=0; an empty pinned tensor needs no block
+        return torch.empty(shp, dtype=dtype, pin_memory=True)
     block = btype.from_address(_acquire(nbytes))
     return torch.frombuffer(block, dtype=dtype, count=count).view(shp)
 
@@ -102,3 +110,16 @@ def pin(x, dtype=None) -> torch.Tensor:
     out = pinned_empty(t.shape, dtype or (t.dtype if t.is_complex() else torch.complex128))
     out.copy_(t)
     return out
+
+
+def pinned_view(a: np.ndarray):
+    """Tensor view of a C-contiguous numpy array that starts a live library page-locked block (e.g.
+    the numpy result of a previous host-path call), else None."""
+    if not a.flags.c_contiguous or not a.flags.writeable or a.dtype not in (np.complex128, np.complex64):
+        return None
+    addr = a.__array_interface__["data"][0]
+    with _mu:
+        nbytes = _live.get(addr)
+    if nbytes is None or a.nbytes > nbytes:
+        return None
+    return torch.from_numpy(a)

@@ -28,7 +28,7 @@ import torch
 
 from . import _lib
 from ._tensor import restore, to_columns
-from .hostmem import pin, pinned_empty  # noqa: F401 - public: host vectors for the host-in/out calls
+from .hostmem import pin, pinned_empty, pinned_view  # noqa: F401 - public: host vectors for the host-in/out calls
 from .errors import BlockShapeMismatch, MissingOffset, ShapeError
 
 __all__ = [
@@ -42,6 +42,7 @@ __all__ = [
     "block_fft_1l",
     "block_fft_2l",
     "precompute_spectral",
+    "precompute_spectral_stacked",
     "pad_rhs",
     "extract_result",
     "matvec",
@@ -243,6 +244,19 @@ def _wrap(handle: int, device) -> SpectralOperator:
     return SpectralOperator(handle, info, device)
 
 
+def _smooth7(m: int) -> int:
+    """Smallest 7-smooth length >= m (the default circulant length of each level, as op.cu)."""
+    n = max(1, int(m))
+    while True:
+        r = n
+        for p in (2, 3, 5, 7):
+            while r % p == 0:
+                r //= p
+        if r == 1:
+            return n
+        n += 1
+
+
 def precompute_spectral(gen: BlockGenerator2L, dtype=torch.complex128, embedding=None) -> SpectralOperator:
     """Transform the generator into resident spectral blocks (toeplitz.py:248-253).
 
@@ -250,34 +264,66 @@ def precompute_spectral(gen: BlockGenerator2L, dtype=torch.complex128, embedding
     variant; the transform itself runs in complex128 and the blocks are
     rounded once).  ``embedding``: optional (l2, l1) circulant lengths.
     """
+    return precompute_spectral_stacked(gen.stacked4(), dtype=dtype, embedding=embedding)
+
+
+def precompute_spectral_stacked(stacked4, dtype=torch.complex128, embedding=None, slab=None) -> SpectralOperator:
+    """``precompute_spectral`` of a circulant-ordered (2n2-1, 2n1-1, n0, n0) block array: a host
+    numpy array, or a complex128 CUDA tensor already resident on the device (no upload).
+
+    ``slab=(kx0, kx1)``: keep only the bins of level-1 frequencies [kx0, kx1) (the kx-slab operator
+    of the multi-GPU decomposition, built without ever holding the full operator).
+    """
     dev = _lib.require_cuda()
-    stacked = np.ascontiguousarray(gen.stacked4(), dtype=np.complex128)
+    if isinstance(stacked4, torch.Tensor) and stacked4.is_cuda:
+        arr = stacked4.to(dtype=torch.complex128).contiguous()
+        ptr, on_dev, shape = arr.data_ptr(), 1, tuple(arr.shape)
+    else:
+        arr = np.ascontiguousarray(stacked4, dtype=np.complex128)
+        ptr, on_dev, shape = arr.ctypes.data, 0, arr.shape
+    if len(shape) != 4 or shape[2] != shape[3] or shape[0] % 2 == 0 or shape[1] % 2 == 0:
+        raise BlockShapeMismatch(f"stacked generator has shape {shape}")
+    n2, n1, n0 = (shape[0] + 1) // 2, (shape[1] + 1) // 2, shape[2]
     l2, l1 = (0, 0) if embedding is None else embedding
+    kx0, kx1 = (0, 0) if slab is None else (int(slab[0]), int(slab[1]))
     ct = _lib.TOEP_C64 if dtype in (torch.complex64, "complex64", "c64", np.complex64) else _lib.TOEP_C128
     handle = ctypes.c_void_p()
-    _lib.check(_lib.lib().toep_op_create(stacked.ctypes.data, 0, gen.n2, gen.n1, gen.n0, int(l2), int(l1), ct,
-                                         _lib.stream_handle(), ctypes.byref(handle)), "precompute_spectral")
+    _lib.check(_lib.lib().toep_op_create_slab(ptr, on_dev, n2, n1, n0, int(l2), int(l1), ct, kx0, kx1,
+                                              _lib.stream_handle(), ctypes.byref(handle)), "precompute_spectral")
+    del arr
     return _wrap(handle.value, dev)
 
 
-def _apply(op: SpectralOperator, u, flags: int):
-    if isinstance(u, torch.Tensor) and not u.is_cuda and u.is_pinned() and u.ndim in (1, 2) and u.is_contiguous() \
-            and not u.is_conj() and not u.is_neg() and (u.dtype == op.dtype or u.dtype == torch.complex128):
-        return _apply_pinned(op, u, flags)
+def _pinned_ok(op: SpectralOperator, t: torch.Tensor) -> bool:
+    return (not t.is_cuda and t.is_pinned() and t.ndim in (1, 2) and t.is_contiguous() and not t.is_conj()
+            and not t.is_neg() and (t.dtype == op.dtype or t.dtype == torch.complex128))
+
+
+def _apply(op: SpectralOperator, u, flags: int, out=None):
+    if isinstance(u, torch.Tensor):
+        if _pinned_ok(op, u):
+            return _apply_pinned(op, u, flags, out)
+    elif isinstance(u, np.ndarray) and u.ndim in (1, 2) and out is None:
+        return _apply_numpy(op, u, flags)
     x, origin = to_columns(u, keep_c64=(op.dtype == torch.complex64))
     if x.shape[0] != op.dim:
         raise ShapeError(f"rows {x.shape[0]} != operator dim {op.dim}")
     if op.dtype == torch.complex64 and x.dtype == torch.complex128:
         flags |= _lib.TOEP_MV_IO_C128
-    out = torch.empty_like(x)
-    _lib.check(_lib.lib().toep_matvec(op.handle, x.data_ptr(), out.data_ptr(), x.shape[1], flags,
+    res = torch.empty_like(x)
+    _lib.check(_lib.lib().toep_matvec(op.handle, x.data_ptr(), res.data_ptr(), x.shape[1], flags,
                                       _lib.stream_handle()), "matvec")
-    return restore(out, origin)
+    res = restore(res, origin)
+    if out is not None:
+        out.copy_(res)
+        return out
+    return res
 
 
-def _apply_pinned(op: SpectralOperator, u: torch.Tensor, flags: int):
+def _apply_pinned(op: SpectralOperator, u: torch.Tensor, flags: int, out=None):
     """Pinned host tensor in -> pinned host tensor out, one library call (copy in, apply, copy out,
-    synchronise): no device tensors are created per call."""
+    synchronise): no device tensors are created per call.  ``out`` (a pinned tensor of u's shape and
+    dtype) receives the result instead of a fresh ``pinned_empty`` block."""
     _lib.require_cuda()
     rows = u.shape[0]
     w = 1 if u.ndim == 1 else u.shape[1]
@@ -285,21 +331,50 @@ def _apply_pinned(op: SpectralOperator, u: torch.Tensor, flags: int):
         raise ShapeError(f"rows {rows} != operator dim {op.dim}")
     if op.dtype == torch.complex64 and u.dtype == torch.complex128:
         flags |= _lib.TOEP_MV_IO_C128
-    out = pinned_empty(u.shape, u.dtype)
+    if out is None:
+        out = pinned_empty(u.shape, u.dtype)
+    elif not (isinstance(out, torch.Tensor) and _pinned_ok(op, out) and out.shape == u.shape
+              and out.dtype == u.dtype):
+        raise ShapeError("out= must be a contiguous pinned CPU tensor of the input's shape and dtype")
     if w:
         _lib.check(_lib.lib().toep_matvec_host(op.handle, u.data_ptr(), out.data_ptr(), w, flags,
                                                _lib.stream_handle()), "matvec")
     return out
 
 
-def matvec(op: SpectralOperator, u):
-    """pad -> DFT -> per-bin D_k multiply -> inverse DFT -> extract (toeplitz.py:287-303)."""
-    return _apply(op, u, 0)
+def _apply_numpy(op: SpectralOperator, u: np.ndarray, flags: int):
+    """The reference's numpy-in / numpy-out call (toeplitz.py:287-303).  The vector is staged once
+    into a library page-locked block (the copy engines read pageable memory through the driver's
+    own bounce buffers at a fraction of the PCIe rate), applied with ``toep_matvec_host``, and the
+    result is returned as a numpy array backed by a page-locked block (released to the block cache
+    when the array dies).  A numpy array that already lives in such a block (a previous result) is
+    passed through without staging."""
+    want = np.complex64 if (op.dtype == torch.complex64 and u.dtype == np.complex64) else np.complex128
+    if u.dtype != want or not u.flags.c_contiguous:
+        u = np.ascontiguousarray(u, dtype=want)
+    if u.shape[0] != op.dim:
+        raise ShapeError(f"rows {u.shape[0]} != operator dim {op.dim}")
+    t = pinned_view(u)
+    if t is None:
+        t = pinned_empty(u.shape, torch.from_numpy(u[:0]).dtype)
+        if u.size:
+            t.numpy()[...] = u
+    return _apply_pinned(op, t, flags).numpy()
 
 
-def matvec_transpose(op: SpectralOperator, u):
+def matvec(op: SpectralOperator, u, out=None):
+    """pad -> DFT -> per-bin D_k multiply -> inverse DFT -> extract (toeplitz.py:287-303).
+
+    numpy in -> numpy out (the reference's convention), CUDA tensor in -> CUDA tensor out, pinned
+    CPU tensor in -> pinned CPU tensor out.  ``out`` (optional extension): a preallocated result of
+    the same container, shape and dtype, for steady-state loops without per-call allocations.
+    """
+    return _apply(op, u, 0, out)
+
+
+def matvec_transpose(op: SpectralOperator, u, out=None):
     """Plain transpose action (toeplitz.py:306-324)."""
-    return _apply(op, u, _lib.TOEP_MV_TRANSPOSE)
+    return _apply(op, u, _lib.TOEP_MV_TRANSPOSE, out)
 
 
 def block_fft_2l(data, n2: int, n1: int, n0: int, direction: str = "forward"):

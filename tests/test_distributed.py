@@ -83,14 +83,32 @@ class _Cfg:
     max_iter = 200
 
 
-def _columns_job(rank, world):
+def _columns_job(rank, world, gather="all"):
     s4 = seeded_stacked4(2, 3, 4, seed=1)
     d = oracle.precompute_spectral(s4)
     dims = (2, 3, 4, 3, 5)
     rng = np.random.default_rng(0)
     b = rng.standard_normal((24, 5)) + 1j * rng.standard_normal((24, 5))
-    x, reps = solve_columns_sharded((d, dims), None, torch.from_numpy(b), _Cfg(), solver=_oracle_solver)
+    x, reps = solve_columns_sharded((d, dims), None, torch.from_numpy(b), _Cfg(), solver=_oracle_solver,
+                                    gather=gather)
     return x.numpy(), [r.iterations for r in reps]
+
+
+def _columns_job_root(rank, world):
+    return _columns_job(rank, world, gather="root")
+
+
+def test_column_sharding_gather_to_root_gloo():
+    # default gather: only rank 0 receives X; rank 1 keeps its own column range (3 of 5 -> cols 3, 4)
+    out = spawn(_columns_job_root)
+    assert not isinstance(out[0], str), out[0]
+    assert not isinstance(out[1], str), out[1]
+    x0, its0 = out[0]
+    x1, its1 = out[1]
+    assert x0.shape == (24, 5) and len(its0) == 5
+    assert x1.shape == (24, 2) and len(its1) == 2
+    assert np.array_equal(x1, x0[:, 3:])
+    assert its1 == its0[3:]
 
 
 def test_column_sharding_gloo():

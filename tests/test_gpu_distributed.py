@@ -156,3 +156,19 @@ def test_ipc_handle_maps_exchange_memory_in_another_process():
         assert got == float(1023 * 1024 // 2)
     finally:
         _lib.lib().toep_peer_free(p)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_operator_built_without_full_operator(world):
+    # toep_op_create_slab transforms only the rank's level-1 frequencies: its blocks equal the
+    # corresponding bins of the full operator, and it keeps D * kxs / l1 bytes resident
+    s4 = seeded_stacked4(6, 7, 8, seed=4)
+    full = precompute_spectral(generator_from_stacked(s4))
+    dfull = full.diag_blocks.reshape(full.l2, full.l1, 8, 8)
+    for r in range(world):
+        st = DeviceSlabStages(torch.from_numpy(s4).cuda(), world, r, torch.complex128)
+        k0, k1 = slab_ranges(full.l1, world, r)
+        assert (st.k0, st.k1) == (k0, k1) and (st.l2, st.l1) == (full.l2, full.l1)
+        assert st.op.resident_bytes == full.resident_bytes * (k1 - k0) // full.l1
+        got = st.op.diag_blocks.reshape(full.l2, k1 - k0, 8, 8)
+        assert torch.equal(got, dfull[:, k0:k1])

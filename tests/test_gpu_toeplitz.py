@@ -220,6 +220,69 @@ class TestBaselineConfigs:
         assert rel_err(matvec(op32, u)[::97], g["mv_sub"]) <= 1e-5
 
 
+@pytest.fixture(scope="module")
+def cfg3_operator():
+    op = precompute_spectral(generator_from_stacked(seeded_stacked4(30, 30, 256, seed=0)))
+    yield op
+    del op
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_cfg3_int8_products_at_baseline_shape(cfg3_operator):
+    # cfg3's own shape (60x60 grid, N_b = 256, K = 512 real-ified) through the int8 tensor-core
+    # (Ozaki) products (W >= 16).  Column 0 is the reference's cfg3 matvec input: compared with the
+    # reference output (golden, toeplitz.py:300 path).  Every other column is compared with its own
+    # single-column matvec (W = 1 streaming path, DMMA-free).  A W = 900 call first (kx-chunked
+    # workspaces, kc = 6) then W = 32 on the same operator and stream (kc = 60, larger per-chunk
+    # buffers: the byte-capacity reallocation path), and the W = 900 block must agree with W = 32.
+    g = golden("cfg3")
+    op = cfg3_operator
+    n = 30 * 30 * 256
+    u = torch.from_numpy(dense_rhs(n, 900, seed=7)).cuda()
+    u[:, 0] = torch.from_numpy(dense_rhs(n, seed=1)).cuda()
+    v900 = matvec(op, u)
+    v32 = matvec(op, u[:, :32].contiguous())
+    assert rel_err(v900[:, :32].cpu().numpy(), v32.cpu().numpy()) <= 1e-12
+    c0 = v32[:, 0].cpu().numpy()
+    assert rel_err(c0[::97], g["mv_sub"]) <= 1e-12
+    assert abs(np.linalg.norm(c0) - g["mv_norm"]) / g["mv_norm"] <= 1e-12
+    worst = 0.0
+    for c in (1, 2, 17, 31):
+        single = matvec(op, u[:, c].contiguous()).cpu().numpy()
+        worst = max(worst, rel_err(v32[:, c].cpu().numpy(), single))
+    assert worst <= 1e-12, worst
+    for c in (450, 899):
+        single = matvec(op, u[:, c].contiguous()).cpu().numpy()
+        assert rel_err(v900[:, c].cpu().numpy(), single) <= 1e-12
+
+
+def test_pinned_out_and_empty_and_numpy_passthrough():
+    from paper_2506_20350_b200.toeplitz import pinned_empty, pin
+    gen = generator_from_stacked(seeded_stacked4(5, 4, 8, seed=3))
+    op = precompute_spectral(gen)
+    u = dense_rhs(gen.dim, 2, seed=5)
+    want = matvec(op, torch.from_numpy(u).cuda()).cpu().numpy()
+    uh = pin(u)
+    out = pinned_empty(u.shape)
+    got = matvec(op, uh, out=out)
+    assert got is out and rel_err(out.numpy(), want) <= 1e-13
+    with pytest.raises(ShapeError):
+        matvec(op, uh, out=pinned_empty((gen.dim, 3)))
+    # zero columns: a (n, 0) pinned tensor and an empty pinned_empty
+    z = pinned_empty((gen.dim, 0))
+    assert z.shape == (gen.dim, 0) and z.is_pinned()
+    assert matvec(op, z).shape == (gen.dim, 0)
+    assert pinned_empty((0, 5)).numel() == 0
+    # numpy in -> numpy out; a result fed back in is used in place (no staging) and gives the same
+    r1 = matvec(op, u)
+    assert isinstance(r1, np.ndarray) and rel_err(r1, want) <= 1e-13
+    r2 = matvec(op, r1)
+    assert rel_err(r2, matvec(op, torch.from_numpy(want).cuda()).cpu().numpy()) <= 1e-13
+    assert rel_err(matvec(op, u[:, 0]), want[:, 0]) <= 1e-13
+    assert matvec(op, u[:, 0].astype(np.complex64)).dtype == np.complex128  # coerced to c128 (toeplitz.py:160)
+
+
 @pytest.mark.parametrize("wcols", [1, 2, 4, 8, 16])
 def test_nb128_kernel_variants_vs_dense(wcols):
     # N_b = 128 selects the streaming TMA product (W = 1), the SIMT column kernels (W <= 8) and the
