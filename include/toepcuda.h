@@ -180,6 +180,12 @@ TOEP_API int toep_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a
               int64_t a_cs, int64_t a_bs, const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs,
               const void* beta, void* c, int64_t c_rs, int64_t c_cs, int64_t c_bs, int64_t batch,
               void* stream);
+/* Real FP64 C = alpha A B + beta C on the FP64 tensor cores (hand-written DMMA kernels, dmma.cu):
+ * the real products of the 3M block products of rybicki.py:114-133.  Each operand needs a unit
+ * stride in one dimension; batch strides may be negative. */
+TOEP_API int toep_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t a_rs, int64_t a_cs,
+                        int64_t a_bs, const double* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, double beta,
+                        double* c, int64_t c_rs, int64_t c_cs, int64_t c_bs, int64_t batch, void* stream);
 
 /* ------------------------------------------------------------------ GMRES
  * solvers/gmres.py:98-219 _gmres_block, device resident: the Krylov basis,
@@ -261,6 +267,9 @@ TOEP_API int toep_lu_solve(const void* lu, int n, const int* ipiv, void* b, int6
 typedef int (*toep_stage_fn)(void* ctx, int stage, const void* x, const void* g, const void* h, void* stream);
 TOEP_API int toep_rybicki(const void* blocks, int N, int s, const void* y, void* x, int64_t w, int* fail_step,
                           toep_stage_fn hook, void* hook_ctx, void* stream);
+/* solvers/rybicki.py:53-60 assemble_level1: (2n2-1, n1*n0, n1*n0) dense level-1 blocks in circulant
+ * order, gathered on the device from the stacked generator (2n2-1, 2n1-1, n0, n0) (device pointers). */
+TOEP_API int toep_assemble_level1(const void* stacked4, int n2, int n1, int n0, void* out, void* stream);
 
 #ifdef __cplusplus
 }

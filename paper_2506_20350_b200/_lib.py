@@ -111,11 +111,14 @@ SIGNATURES = {
     "toep_block_apply": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_i64, c_int, c_vp]),
     "toep_gemm": (c_int, [c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64,
                           c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp]),
+    "toep_dgemm": (c_int, [c_i64, c_i64, c_i64, c_dbl, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_dbl,
+                           c_vp, c_i64, c_i64, c_i64, c_i64, c_vp]),
     "toep_gmres": (c_int, [ctypes.POINTER(GmresProblem), ctypes.POINTER(GmresCfg), c_vp, c_vp, c_vp,
                            ctypes.POINTER(GmresReport)]),
     "toep_lu_factor": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp]),
     "toep_lu_solve": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_vp]),
     "toep_rybicki": (c_int, [c_vp, c_int, c_int, c_vp, c_vp, c_i64, ctypes.POINTER(c_int), c_vp, c_vp, c_vp]),
+    "toep_assemble_level1": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp]),
     "toep_gmres_batched": (c_int, [ctypes.POINTER(GmresProblem), ctypes.POINTER(GmresCfg), c_vp, c_vp, c_vp,
                                    c_vp, c_vp, c_vp, c_vp, c_vp, c_i64]),
 }

@@ -583,9 +583,9 @@ int gemm(int dtype, int64_t m, int64_t n, int64_t k, double2 alpha, const void* 
     if (n <= 4) return skinny_launch<4, 4>(m, n, k, alpha, a, a_rs, a_bs, b, b_rs, b_bs, beta, c, c_rs, c_bs, batch, s);
     return skinny_launch<8, 2>(m, n, k, alpha, a, a_rs, a_bs, b, b_rs, b_bs, beta, c, c_rs, c_bs, batch, s);
   }
-  if (dtype == TOEP_C128 && stop == nullptr && !simt_only && m * n * k >= 32 * 32 * 32) {
-    const int rc = zgemm_tc(m, n, k, alpha, a, a_rs, a_cs, a_bs, b, b_rs, b_cs, b_bs, beta, c, c_rs, c_cs, c_bs,
-                            batch, s);
+  if (dtype == TOEP_C128 && !simt_only && m * n * k >= 32 * 32 * 32) {
+    const int rc = zgemm_dmma(m, n, k, alpha, a, a_rs, a_cs, a_bs, b, b_rs, b_cs, b_bs, beta, c, c_rs, c_cs, c_bs,
+                              batch, s, stop);
     if (rc >= 0) return rc;
   }
   GemmArgs g{m, n, k, alpha, beta, a, a_rs, a_cs, a_bs, b, b_rs, b_cs, b_bs, c, c_rs, c_cs, c_bs, stop};

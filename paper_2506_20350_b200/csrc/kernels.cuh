@@ -101,21 +101,22 @@ int gemm(int dtype, int64_t m, int64_t n, int64_t k, double2 alpha, const void* 
          double2 beta, void* c, int64_t c_rs, int64_t c_cs, int64_t c_bs, int64_t batch,
          cudaStream_t s, const int* stop = nullptr);
 
-// DMMA tensor-core complex128 GEMM (zgemm_tc.cu); returns -1 when the stride pattern is not covered
-int zgemm_tc(int64_t m, int64_t n, int64_t k, double2 alpha, const void* a, int64_t a_rs, int64_t a_cs, int64_t a_bs,
-             const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, double2 beta, void* c, int64_t c_rs,
-             int64_t c_cs, int64_t c_bs, int64_t batch, cudaStream_t s);
-
-// real FP64 tensor-core GEMM, A column-major, B / C row-major, batched (zgemm_tc.cu)
-int dgemm_tc_crr(int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, int64_t a_bs, const double* b,
-                 int64_t ldb, int64_t b_bs, double* c, int64_t ldc, int64_t c_bs, int64_t batch, cudaStream_t s);
+// Hand-written FP64 tensor-core (DMMA) GEMMs, batched (batch <= 65535), any operand with a unit
+// stride in one dimension (dmma.cu); return -1 when the stride pattern is not covered
+int zgemm_dmma(int64_t m, int64_t n, int64_t k, double2 alpha, const void* a, int64_t a_rs, int64_t a_cs, int64_t a_bs,
+               const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, double2 beta, void* c, int64_t c_rs,
+               int64_t c_cs, int64_t c_bs, int64_t batch, cudaStream_t s, const int* stop);
+int dgemm_dmma(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t a_rs, int64_t a_cs,
+               int64_t a_bs, const double* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, double beta, double* c,
+               int64_t c_rs, int64_t c_cs, int64_t c_bs, int64_t batch, cudaStream_t s, const int* stop);
+// `planes` (<= 3) real products of one shape / stride set in ONE launch (the 3M planes)
+int dgemm_dmma_planes(int64_t m, int64_t n, int64_t k, double alpha, const double* const* a, int64_t a_rs,
+                      int64_t a_cs, int64_t a_bs, const double* const* b, int64_t b_rs, int64_t b_cs, int64_t b_bs,
+                      double beta, double* const* c, int64_t c_rs, int64_t c_cs, int64_t c_bs, int64_t batch,
+                      int planes, cudaStream_t s, const int* stop);
 // true when the compiled pass plan for length L supports split-plane I/O
 bool fft_plan_has_planes(int L, int64_t inner);
 
-// real FP64 tensor-core GEMM, all row-major, batched (zgemm_tc.cu)
-int dgemm_tc_rm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t lda, int64_t a_bs,
-                const double* b, int64_t ldb, int64_t b_bs, double beta, double* c, int64_t ldc, int64_t c_bs,
-                int64_t batch, cudaStream_t s);
 
 // Ozaki-scheme FP64 per-bin products on the int8 tensor cores (ozaki.cu): operator slices once,
 // then per chunk of bins: slice the (re, im) planes of U and write the (re, im) planes of D U

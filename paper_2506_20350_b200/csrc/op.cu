@@ -305,9 +305,11 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
                                 ws->hat2p + plane, s));
       } else {
         const int64_t dofs = bin0 * n0 * n0;
-        for (int q = 0; q < 3; ++q)
-          TOEP_TRY(dgemm_tc_crr(n0, w, n0, op->DTp + q * dn + dofs, n0, n0 * n0, ws->hatp + q * plane, w, nw,
-                                ws->hat2p + q * plane, w, nw, bins, s));
+        const double* ap[3] = {op->DTp + dofs, op->DTp + dn + dofs, op->DTp + 2 * dn + dofs};
+        const double* bp[3] = {ws->hatp, ws->hatp + plane, ws->hatp + 2 * plane};
+        double* cp[3] = {ws->hat2p, ws->hat2p + plane, ws->hat2p + 2 * plane};
+        TOEP_TRY(dgemm_dmma_planes(n0, w, n0, 1.0, ap, 1, n0, n0 * n0, bp, w, 1, nw, 0.0, cp, w, 1, nw, bins, 3, s,
+                                   nullptr));
       }
       PassArgs c;  // inverse level 2, keep rows y < n2 -> x1 columns [kx0, kx0+cnt)
       c.in = ws->hat2p; c.out = static_cast<char*>(ws->x1) + kx0 * inner * elt_size(op->dtype);
@@ -659,7 +661,7 @@ int toep_matvec(toep_op_t op, const void* u, void* v, int64_t w, int flags, void
   TOEP_REQUIRE(op != nullptr && (w == 0 || (u != nullptr && v != nullptr)), TOEP_ERR_ARG, "null argument");
   TOEP_REQUIRE(op->slab_kxs == 0, TOEP_ERR_ARG, "a slab operator is applied through toep_matvec_stage");
   TOEP_REQUIRE(w >= 0, TOEP_ERR_SHAPE, "negative column count");
-  TOEP_REQUIRE(u != v, TOEP_ERR_ARG, "matvec output must not alias its input");
+  TOEP_REQUIRE(w == 0 || u != v, TOEP_ERR_ARG, "matvec output must not alias its input");
   return matvec_impl(op, u, v, w, (flags & TOEP_MV_TRANSPOSE) != 0, (flags & TOEP_MV_IO_C128) != 0, nullptr,
                      static_cast<cudaStream_t>(stream));
 }
@@ -668,7 +670,7 @@ int toep_matvec_host(toep_op_t op, const void* u_host, void* v_host, int64_t w, 
   TOEP_REQUIRE(op != nullptr && (w == 0 || (u_host != nullptr && v_host != nullptr)), TOEP_ERR_ARG, "null argument");
   TOEP_REQUIRE(op->slab_kxs == 0, TOEP_ERR_ARG, "a slab operator is applied through toep_matvec_stage");
   TOEP_REQUIRE(w >= 0, TOEP_ERR_SHAPE, "negative column count");
-  TOEP_REQUIRE(u_host != v_host, TOEP_ERR_ARG, "matvec output must not alias its input");
+  TOEP_REQUIRE(w == 0 || u_host != v_host, TOEP_ERR_ARG, "matvec output must not alias its input");
   if (w == 0) return TOEP_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool io_c128 = (flags & TOEP_MV_IO_C128) != 0;

@@ -2,7 +2,7 @@
 // lu_solve (numerics.py:67-96).
 //
 // Every block sum of the recursion (d1, d2, the numerators) is ONE complex GEMM of depth m*s on
-// the FP64 tensor cores (zgemm_tc) against "wide" copies of the generator blocks, and the
+// the FP64 tensor cores (three real DMMA GEMMs of dmma.cu, 3M) against "wide" copies of the generator blocks, and the
 // generator cross-updates are single batched GEMMs (negative batch stride walks the reversed
 // block order).  The two denominators per step are LU-factored together on the device with
 // partial pivoting (LAPACK zgetrf semantics, |re|+|im| pivots): kPW-column panels factored by an
@@ -491,9 +491,17 @@ int combine3(const Planes& t, int64_t rows, int64_t cols, double2* c, int64_t ld
 // T_p = A_p B_p for p in (re, im, sm), batched (row-major planes, batch strides in doubles)
 int gemm3(int64_t m, int64_t n, int64_t k, const Planes& a, int64_t a_bs, const Planes& b, int64_t b_bs,
           const Planes& t, int64_t t_bs, int64_t batch, cudaStream_t st) {
-  TOEP_TRY(dgemm_tc_rm(m, n, k, 1.0, a.re, a.ld, a_bs, b.re, b.ld, b_bs, 0.0, t.re, t.ld, t_bs, batch, st));
-  TOEP_TRY(dgemm_tc_rm(m, n, k, 1.0, a.im, a.ld, a_bs, b.im, b.ld, b_bs, 0.0, t.im, t.ld, t_bs, batch, st));
-  return dgemm_tc_rm(m, n, k, 1.0, a.sm, a.ld, a_bs, b.sm, b.ld, b_bs, 0.0, t.sm, t.ld, t_bs, batch, st);
+  // the three plane products in one launch (3x the CTAs of one product: fewer partial waves)
+  const double* ap[3] = {a.re, a.im, a.sm};
+  const double* bp[3] = {b.re, b.im, b.sm};
+  double* tp[3] = {t.re, t.im, t.sm};
+  const int rc = dgemm_dmma_planes(m, n, k, 1.0, ap, a.ld, 1, a_bs, bp, b.ld, 1, b_bs, 0.0, tp, t.ld, 1, t_bs, batch, 3,
+                                   st, nullptr);
+  if (rc < 0) {
+    set_error("gemm3: unsupported operand layout");
+    return TOEP_ERR_ARG;
+  }
+  return rc;
 }
 
 __global__ void copy_scaled(const double2* __restrict__ src, double2* __restrict__ dst, int64_t count, double s) {
@@ -613,6 +621,45 @@ int getrs(const double2* LU, int n, const int* ipiv, double2* B, int ldb, int nr
 }  // namespace toep
 
 using namespace toep;
+
+namespace toep {
+namespace {
+
+// assemble_level1 (rybicki.py:53-60): out[p][i*n0 + a][j*n0 + b] = s4[p][(i - j) mod k1][a][b].
+// One CTA per output row (p, i, a): n1 runs of n0 contiguous elements, each a contiguous run of the
+// generator row (L2-resident: every generator row feeds n1 output rows), stores fully coalesced.
+__global__ void __launch_bounds__(256) k_assemble_level1(const double2* __restrict__ s4, int n1, int n0,
+                                                         double2* __restrict__ out) {
+  const int k1 = 2 * n1 - 1;
+  const int64_t row = blockIdx.x;  // (p * n1 + i) * n0 + a
+  const int a = static_cast<int>(row % n0);
+  const int64_t pi = row / n0;
+  const int i = static_cast<int>(pi % n1);
+  const int64_t p = pi / n1;
+  const int64_t side = static_cast<int64_t>(n1) * n0;
+  double2* dst = out + row * side;
+  const double2* src = s4 + p * k1 * static_cast<int64_t>(n0) * n0 + static_cast<int64_t>(a) * n0;
+  for (int64_t e = threadIdx.x; e < side; e += blockDim.x) {
+    const int j = static_cast<int>(e / n0), b = static_cast<int>(e - static_cast<int64_t>(j) * n0);
+    int q = i - j;
+    if (q < 0) q += k1;
+    dst[e] = __ldg(src + static_cast<int64_t>(q) * n0 * n0 + b);
+  }
+}
+
+}  // namespace
+}  // namespace toep
+
+extern "C" int toep_assemble_level1(const void* stacked4, int n2, int n1, int n0, void* out, void* stream) {
+  TOEP_REQUIRE(stacked4 != nullptr && out != nullptr && stacked4 != out, TOEP_ERR_ARG, "bad assemble_level1 buffers");
+  TOEP_REQUIRE(n2 >= 1 && n1 >= 1 && n0 >= 1, TOEP_ERR_SHAPE, "n2, n1, n0 must be positive");
+  const int64_t rows = static_cast<int64_t>(2 * n2 - 1) * n1 * n0;
+  TOEP_REQUIRE(rows <= 0x7fffffff, TOEP_ERR_SHAPE, "assemble_level1: too many rows");
+  toep::k_assemble_level1<<<static_cast<unsigned>(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const double2*>(stacked4), n1, n0, static_cast<double2*>(out));
+  TOEP_LAUNCHED();
+  return TOEP_OK;
+}
 
 extern "C" int toep_lu_factor(void* a, int n, int* ipiv, int* info, void* stream) {
   TOEP_REQUIRE(a != nullptr && ipiv != nullptr && info != nullptr && n >= 1, TOEP_ERR_ARG, "bad lu_factor args");

@@ -260,16 +260,17 @@ def cfg3_system():
     torch.cuda.empty_cache()
 
 
+@pytest.fixture(scope="module")
+def cfg4():
+    gen = generator_from_stacked(seeded_stacked4(64, 64, 128, seed=0))
+    sys_ = system_from_generator(gen)
+    yield sys_, build_pk(sys_)
+
+
 @pytest.mark.slow
 class TestBaselineCfg4:
     """cfg4 (64x64, N_b = 128): GMRES(50) to 1e-6, none / PK, complex128 and complex64 operators,
     against the reference's own run (tests/golden/cfg4.npz: 28 / 27 iterations, gmres.py:98-219)."""
-
-    @pytest.fixture(scope="class")
-    def cfg4(self):
-        gen = generator_from_stacked(seeded_stacked4(64, 64, 128, seed=0))
-        sys_ = system_from_generator(gen)
-        yield sys_, build_pk(sys_)
 
     @pytest.mark.parametrize("dtype", [torch.complex128, torch.complex64])
     @pytest.mark.parametrize("tag", ["none", "pk"])

@@ -270,8 +270,8 @@ def test_pinned_out_and_empty_and_numpy_passthrough():
     with pytest.raises(ShapeError):
         matvec(op, uh, out=pinned_empty((gen.dim, 3)))
     # zero columns: a (n, 0) pinned tensor and an empty pinned_empty
-    z = pinned_empty((gen.dim, 0))
-    assert z.shape == (gen.dim, 0) and z.is_pinned()
+    z = pinned_empty((gen.dim, 0))  # no block behind an empty tensor (torch reports it unpinned)
+    assert z.shape == (gen.dim, 0)
     assert matvec(op, z).shape == (gen.dim, 0)
     assert pinned_empty((0, 5)).numel() == 0
     # numpy in -> numpy out; a result fed back in is used in place (no staging) and gives the same
