@@ -426,7 +426,10 @@ __global__ void k_givens(GState* st, const double* norm_partial, int nblk, doubl
 // (every CTA reduces the per-CTA partials in the same order) -> update + dots -> barrier ->
 // update + norm -> barrier -> Givens on CTA 0.  Replaces 4 launches and their drain / ramp
 // gaps; 32 warps per SM keep enough L2 requests in flight for the basis sweeps.
-constexpr int kCoopThreads = 1024;
+#ifndef TOEP_COOP_THREADS
+#define TOEP_COOP_THREADS 512
+#endif
+constexpr int kCoopThreads = TOEP_COOP_THREADS;
 
 struct OrthArgs {
   const double2* V;
@@ -456,6 +459,7 @@ struct OrthArgs {
   int direct_norm;  // 1: h_{j+1,j} = ||w''|| from a third sweep + barrier (TOEP_DIRECT_NORM=1)
   double2* gram;    // one-sweep CGS2: Gram matrix of the cycle's basis [ldr][ldr] (col-major), or null
   double2* part2;   // [ldr][nblk] partials of V^H v_{m-1}
+  int gram_smem;    // 1: the Gram block is staged in shared memory (small cycles, see coop_smem)
 };
 constexpr int kMaxOrthM = 1024;  // basis vectors per cycle handled by the cooperative kernel
 constexpr int kOrthGroupedMinChunk = 2048;  // elements per CTA from which the grouped dot sweep is used
@@ -512,17 +516,17 @@ __device__ __forceinline__ void orth_coefs(const OrthArgs& a, double2* coef, int
 }
 
 __device__ __forceinline__ double orth_update(const OrthArgs& a, const double2* coef, int64_t c0, int64_t c1) {
+  constexpr int U = 8;  // basis loads issued together (latency-bound sweep over L2-resident vectors)
   double nrm = 0.0;
   for (int64_t i = c0 + threadIdx.x; i < c1; i += kCoopThreads) {
     double2 acc = a.w[i];
     int l = 0;
-    for (; l + 3 < a.m; l += 4) {
-      const double2 v0 = a.V[l * a.N + i], v1 = a.V[(l + 1) * a.N + i], v2 = a.V[(l + 2) * a.N + i],
-                    v3 = a.V[(l + 3) * a.N + i];
-      cfma(acc, v0, make_double2(-coef[l].x, -coef[l].y));
-      cfma(acc, v1, make_double2(-coef[l + 1].x, -coef[l + 1].y));
-      cfma(acc, v2, make_double2(-coef[l + 2].x, -coef[l + 2].y));
-      cfma(acc, v3, make_double2(-coef[l + 3].x, -coef[l + 3].y));
+    for (; l + U - 1 < a.m; l += U) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = a.V[(l + u) * a.N + i];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cfma(acc, v[u], make_double2(-coef[l + u].x, -coef[l + u].y));
     }
     for (; l < a.m; ++l) cfma(acc, a.V[l * a.N + i], make_double2(-coef[l].x, -coef[l].y));
     a.w[i] = acc;
@@ -531,57 +535,87 @@ __device__ __forceinline__ double orth_update(const OrthArgs& a, const double2* 
   return nrm;
 }
 
-// One-sweep CGS2 dots, one warp per basis vector (short chunks): warp l computes both V_l^H w and V_l^H V_{m-1} over the chunk (the last
-// basis vector's Gram column), reading V_l once; warp NW-1 also accumulates ||w||^2
+// One-sweep CGS2 dots for short chunks: V_l^H w and V_l^H V_{m-1} (the last basis vector's Gram
+// column) over the CTA's chunk, reading V_l once.  Work item = (basis vector l, sub-chunk): with m
+// basis vectors and NW warps, S = NW / m warps split each vector's chunk so that every warp has
+// loads in flight (all of a lane's U iterations issued before any use); the items of vector 0
+// also accumulate ||w||^2 from the w values they load anyway.  Sub-chunk partials are combined in
+// shared memory in a fixed order (deterministic).
 __device__ __forceinline__ void orth_dots_gram_pv(const OrthArgs& a, int64_t c0, int64_t c1) {
   constexpr int NW = kCoopThreads / 32, U = 4;
+  __shared__ double2 sp1[NW], sp2[NW];
+  __shared__ double spn[NW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nblk = gridDim.x;
-  const double2* vl = a.V + static_cast<int64_t>(a.m - 1) * a.N;
-  if (warp == NW - 1) {
-    double t = 0.0;
-    for (int64_t i = c0 + lane; i < c1; i += 32) {
-      const double2 v = a.w[i];
-      t = fma(v.x, v.x, fma(v.y, v.y, t));
-    }
-    t = warp_sum(t);
-    if (lane == 0) a.npart[blockIdx.x] = t;
-  }
-  for (int l = warp; l < a.m; l += NW) {
-    const double2* v = a.V + static_cast<int64_t>(l) * a.N;
+  const int nblk = gridDim.x, m = a.m;
+  const double2* vl = a.V + static_cast<int64_t>(m - 1) * a.N;
+  const int S = m >= NW ? 1 : NW / m;  // warps per basis vector
+  const int per_round = NW / S;        // vectors per round
+  const int64_t len = c1 - c0;
+  for (int l0 = 0; l0 < m; l0 += per_round) {
+    const int l = l0 + warp / S, sc = warp - (warp / S) * S;
     double2 acc[U], acg[U];
+    double wn = 0.0;
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = acg[u] = make_double2(0, 0);
-    int64_t i = c0 + lane;
-    for (; i + 32 * (U - 1) < c1; i += 32 * U) {
-      double2 vv[U], ww[U], ll[U];
+    if (l < m && warp / S < per_round) {
+      const int64_t s0 = c0 + ((len * sc / S) / 32) * 32;
+      const int64_t s1 = (sc + 1 == S) ? c1 : c0 + ((len * (sc + 1) / S) / 32) * 32;
+      const double2* v = a.V + static_cast<int64_t>(l) * a.N;
+      int64_t i = s0 + lane;
+      for (; i + 32 * (U - 1) < s1; i += 32 * U) {
+        double2 vv[U], ww[U], ll[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        vv[u] = v[i + 32 * u];
-        ww[u] = a.w[i + 32 * u];
-        ll[u] = vl[i + 32 * u];
+        for (int u = 0; u < U; ++u) {
+          vv[u] = v[i + 32 * u];
+          ww[u] = a.w[i + 32 * u];
+          ll[u] = vl[i + 32 * u];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          cfmac(acc[u], vv[u], ww[u]);
+          cfmac(acg[u], vv[u], ll[u]);
+          if (l == 0) wn = fma(ww[u].x, ww[u].x, fma(ww[u].y, ww[u].y, wn));
+        }
+      }
+      for (; i < s1; i += 32) {
+        const double2 vi = v[i], wi = a.w[i];
+        cfmac(acc[0], vi, wi);
+        cfmac(acg[0], vi, vl[i]);
+        if (l == 0) wn = fma(wi.x, wi.x, fma(wi.y, wi.y, wn));
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        cfmac(acc[u], vv[u], ww[u]);
-        cfmac(acg[u], vv[u], ll[u]);
+      for (int u = 1; u < U; ++u) {
+        acc[0] = cadd(acc[0], acc[u]);
+        acg[0] = cadd(acg[0], acg[u]);
       }
     }
-    for (; i < c1; i += 32) {
-      cfmac(acc[0], v[i], a.w[i]);
-      cfmac(acg[0], v[i], vl[i]);
-    }
-#pragma unroll
-    for (int u = 1; u < U; ++u) {
-      acc[0] = cadd(acc[0], acc[u]);
-      acg[0] = cadd(acg[0], acg[u]);
-    }
-    const double2 s1 = warp_sum(acc[0]);
-    const double2 s2 = warp_sum(acg[0]);
+    const double2 t1 = warp_sum(acc[0]);
+    const double2 t2 = warp_sum(acg[0]);
+    if (l0 == 0) wn = warp_sum(wn);
     if (lane == 0) {
-      a.part[static_cast<int64_t>(l) * nblk + blockIdx.x] = s1;
-      a.part2[static_cast<int64_t>(l) * nblk + blockIdx.x] = s2;
+      sp1[warp] = t1;
+      sp2[warp] = t2;
+      if (l0 == 0) spn[warp] = wn;
     }
+    __syncthreads();
+    if (threadIdx.x < per_round) {
+      const int lv = l0 + static_cast<int>(threadIdx.x);
+      if (lv < m) {
+        double2 u1 = sp1[threadIdx.x * S], u2 = sp2[threadIdx.x * S];
+        for (int q = 1; q < S; ++q) {
+          u1 = cadd(u1, sp1[threadIdx.x * S + q]);
+          u2 = cadd(u2, sp2[threadIdx.x * S + q]);
+        }
+        a.part[static_cast<int64_t>(lv) * nblk + blockIdx.x] = u1;
+        a.part2[static_cast<int64_t>(lv) * nblk + blockIdx.x] = u2;
+      }
+      if (l0 == 0 && threadIdx.x == 0) {
+        double t = spn[0];
+        for (int q = 1; q < S; ++q) t += spn[q];
+        a.npart[blockIdx.x] = t;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -786,7 +820,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
   long long pt[8];
   int np = 0;
 #define OPROBE() \
-  if (blockIdx.x == 0 && threadIdx.x == 0) pt[np++] = global_ns()
+  if (blockIdx.x == (gridDim.x > 1 ? 1 : 0) && threadIdx.x == 0) pt[np++] = global_ns()
 #else
 #define OPROBE()
 #endif
@@ -822,33 +856,94 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
     // One grid barrier and two basis sweeps per step instead of three barriers and four sweeps.
     // grouped sweep for long chunks (cfg4: 3 567 elements per CTA, GMRES 23.4 -> 22.8 ms); per-vector
     // warps for short ones (cfg1 / cfg2 chunks of 32 / 784 elements measured slower grouped)
+    // the previous steps' Gram block G[0..m-2][0..m-2] (written by earlier launches, complete at
+    // pdl_wait) is staged into shared memory with cp.async while the dots sweep runs
+    // (and the basis scale factors vs[0..m-1], read by every coefficient below)
+    const int mp = a.m - 1;
+    double2* gs = osm + 7 * a.ldr;  // column-major [mp][mp] when a.gram_smem
+    double* vss = reinterpret_cast<double*>(osm + 7 * a.ldr + (a.gram_smem ? a.ldr * a.ldr : 0));
+    if (a.gram_smem) {
+      for (int e = threadIdx.x; e < mp * mp; e += kCoopThreads) {
+        const int k = e / mp, l = e - k * mp;
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(gs + e));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(a.gram + static_cast<int64_t>(k) * a.ldr + l)
+                     : "memory");
+      }
+    }
+    for (int l = threadIdx.x; l < a.m; l += kCoopThreads) {
+      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(vss + l));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(a.vs + l) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     if (a.N >= static_cast<int64_t>(kOrthGroupedMinChunk) * (gridDim.x - 1)) orth_dots_gram(a, c0, c1);
     else orth_dots_gram_pv(a, c0, c1);
+    OPROBE();
     grid_barrier(a.bar);
+    OPROBE();
     const int m = a.m, nblk = gridDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double2* h1s = osm + 4 * a.ldr;
     double2* gcol = osm + 5 * a.ldr;
     double2* gh = osm + 6 * a.ldr;
-    const double vlast = a.vs[m - 1];
-    for (int l = warp; l < m; l += kCoopThreads / 32) {
-      double2 s1 = make_double2(0, 0), s2 = make_double2(0, 0);
-      for (int b = lane; b < nblk; b += 32) {
-        s1 = cadd(s1, __ldcg(a.part + static_cast<int64_t>(l) * nblk + b));
-        s2 = cadd(s2, __ldcg(a.part2 + static_cast<int64_t>(l) * nblk + b));
+    // ||w||^2 partials: issued now, consumed by the norm below (one round trip for everything)
+    double wnq[5];
+    if (threadIdx.x < 32) {
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        const int b = static_cast<int>(threadIdx.x) + 32 * j;
+        wnq[j] = b < nblk ? __ldcg(a.npart + b) : 0.0;
       }
-      s1 = warp_sum(s1);
-      s2 = warp_sum(s2);
-      if (lane == 0) {
-        h1s[l] = cscale(s1, a.vs[l]);
-        gcol[l] = cscale(s2, a.vs[l] * vlast);  // G[l][m-1]
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const double vlast = vss[m - 1];
+    // cross-CTA partials: one warp per (vector, sum) item, up to 4 items per warp with all of their
+    // loads issued before any is summed (one L2 round trip); each item is summed in a fixed order,
+    // identical in every CTA (the decisions below are uniform across the grid)
+    {
+      constexpr int NWc = kCoopThreads / 32, IT = 4, Q = 5;
+      const int items = 2 * m;
+      auto item_ptr = [&](int it) {
+        return ((it & 1) ? a.part2 : a.part) + static_cast<int64_t>(it >> 1) * nblk;
+      };
+      auto finish = [&](int it, double2 sacc) {
+        sacc = warp_sum(sacc);
+        if (lane == 0) {
+          const int l = it >> 1;
+          if (it & 1) gcol[l] = cscale(sacc, vss[l] * vlast);  // G[l][m-1]
+          else h1s[l] = cscale(sacc, vss[l]);
+        }
+      };
+      if (nblk <= 32 * Q && items <= IT * NWc) {
+        double2 q[IT][Q];
+#pragma unroll
+        for (int r = 0; r < IT; ++r) {
+          const int it = warp + r * NWc;
+#pragma unroll
+          for (int j = 0; j < Q; ++j)
+            q[r][j] = (it < items && lane + 32 * j < nblk) ? __ldcg(item_ptr(it) + lane + 32 * j) : make_double2(0, 0);
+        }
+#pragma unroll
+        for (int r = 0; r < IT; ++r) {
+          const int it = warp + r * NWc;
+          double2 sacc = make_double2(0, 0);
+#pragma unroll
+          for (int j = 0; j < Q; ++j) sacc = cadd(sacc, q[r][j]);
+          if (it < items) finish(it, sacc);
+        }
+      } else {
+        for (int it = warp; it < items; it += NWc) {
+          double2 sacc = make_double2(0, 0);
+          for (int b = lane; b < nblk; b += 32) sacc = cadd(sacc, __ldcg(item_ptr(it) + b));
+          finish(it, sacc);
+        }
       }
     }
     __syncthreads();
     auto G = [&](int l, int k) -> double2 {  // G[l][k], Hermitian; column m-1 from this step
       if (k == m - 1) return gcol[l];
       if (l == m - 1) return make_double2(gcol[k].x, -gcol[k].y);
-      return a.gram[static_cast<int64_t>(k) * a.ldr + l];
+      return a.gram_smem ? gs[k * mp + l] : a.gram[static_cast<int64_t>(k) * a.ldr + l];
     };
     // h2 = h1 - G h1, h = h1 + h2; gh = G h (for the norm)
     for (int l = warp; l < m; l += kCoopThreads / 32) {
@@ -857,7 +952,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
       t = warp_sum(t);
       if (lane == 0) {
         const double2 h = csub(cscale(h1s[l], 2.0), t);
-        coef[l] = cscale(h, a.vs[l]);
+        coef[l] = cscale(h, vss[l]);
         hsm[l] = h;
       }
     }
@@ -874,7 +969,12 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
     __syncthreads();
     if (threadIdx.x < 32) {
       double wn = 0.0;
-      for (int b = threadIdx.x; b < nblk; b += 32) wn += __ldcg(a.npart + b);
+      if (nblk <= 160) {
+#pragma unroll
+        for (int j = 0; j < 5; ++j) wn += wnq[j];
+      } else {
+        for (int b = threadIdx.x; b < nblk; b += 32) wn += __ldcg(a.npart + b);
+      }
       double t = 0.0;
       for (int l = threadIdx.x; l < m; l += 32)
         t += -2.0 * (hsm[l].x * h1s[l].x + hsm[l].y * h1s[l].y) + (hsm[l].x * gh[l].x + hsm[l].y * gh[l].y);
@@ -902,7 +1002,15 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
       }
     }
     if (!direct) {
+      OPROBE();
       orth_update(a, coef, c0, c1);
+#ifdef TOEP_ORTH_PROBE
+      __syncthreads();
+      OPROBE();
+      if (blockIdx.x == 1 && threadIdx.x == 0 && (a.m == 8 || a.m == 16 || a.m == 24 || a.m == 31))
+        printf("orth-gram m=%d: dots %lld bar %lld coef+norm %lld upd %lld ns\n", a.m, pt[1] - pt[0], pt[2] - pt[1],
+               pt[3] - pt[2], pt[4] - pt[3]);
+#endif
       return;
     }
     double nrm = orth_update(a, coef, c0, c1);
@@ -1356,8 +1464,12 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   G_ALLOC(ts, 2 * max_total + 4);
   G_ALLOC(gram, (int64_t)ldr * ldr);
   TOEP_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s));
-  const size_t coop_smem = std::max(sizeof(double2) * ldr * (1 + kCoopThreads / 32),
-                                    (2 * sizeof(double2) + sizeof(double)) * ldr);
+  // Gram block staged in shared memory for cycles up to 64 vectors (64 KB); larger cycles read it from L2
+  const bool gram_smem = ldr <= 64;
+  const size_t coop_smem = std::max({sizeof(double2) * ldr * (1 + kCoopThreads / 32),
+                                     (2 * sizeof(double2) + sizeof(double)) * ldr,
+                                     sizeof(double2) * (7 * ldr + (gram_smem ? ldr * ldr : 0)) +
+                                         sizeof(double) * ldr});
   const int coop_grid = nblk;
   // TOEP_COOP_LAUNCH=0: plain PDL launch of the grid-barrier kernel (co-residency from the
   // resource budget: one CTA per SM, fits next to either 2-D DFT kernel)
@@ -1370,8 +1482,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     return !(v != nullptr && v[0] == '0');
   }();
   if (use_coop) {
-    if (coop_smem > 48 * 1024)
-      cudaFuncSetAttribute(k_orth_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem);
+    ensure_smem(k_orth_coop, coop_smem + 8 * 1024);  // + headroom: the kernel's static shared memory
     // same (maximal) shared-memory carveout as the 2-D DFT kernels, so the next forward DFT can
     // become resident next to this kernel without an SM reconfiguration
     cudaFuncSetAttribute(k_orth_coop, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1530,7 +1641,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       if (use_coop) {
         OrthArgs oa{V, N, m, vs, w, part1, e.norm_partial, h1, st, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
                     static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev, orth_pf, force_cgs2, reorth_eta2,
-                    direct_norm, gram_form ? gram : nullptr, part2};
+                    direct_norm, gram_form ? gram : nullptr, part2, (gram_form && gram_smem) ? 1 : 0};
         rc = coop_attr ? launch_coop(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa,
                                      (const int*)stop_dev)
                        : launch_k(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa,
