@@ -574,16 +574,12 @@ int gemm(int dtype, int64_t m, int64_t n, int64_t k, double2 alpha, const void* 
          int64_t a_bs, const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, double2 beta, void* c, int64_t c_rs,
          int64_t c_cs, int64_t c_bs, int64_t batch, cudaStream_t s, const int* stop) {
   if (m == 0 || n == 0 || batch == 0) return TOEP_OK;
-  static const bool simt_only = [] {
-    const char* e = std::getenv("TOEP_ZGEMM");
-    return e != nullptr && std::strcmp(e, "simt") == 0;
-  }();
-  if (dtype == TOEP_C128 && stop == nullptr && !simt_only && n <= 8 && k >= 256 && a_cs == 1 && b_cs == 1 &&
+  if (dtype == TOEP_C128 && stop == nullptr && n <= 8 && k >= 256 && a_cs == 1 && b_cs == 1 &&
       c_cs == 1 && batch <= 65535 && (m + 3) / 4 <= 0x7fffffff) {
     if (n <= 4) return skinny_launch<4, 4>(m, n, k, alpha, a, a_rs, a_bs, b, b_rs, b_bs, beta, c, c_rs, c_bs, batch, s);
     return skinny_launch<8, 2>(m, n, k, alpha, a, a_rs, a_bs, b, b_rs, b_bs, beta, c, c_rs, c_bs, batch, s);
   }
-  if (dtype == TOEP_C128 && !simt_only && m * n * k >= 32 * 32 * 32) {
+  if (dtype == TOEP_C128 && m * n * k >= 32 * 32 * 32) {
     const int rc = zgemm_dmma(m, n, k, alpha, a, a_rs, a_cs, a_bs, b, b_rs, b_cs, b_bs, beta, c, c_rs, c_cs, c_bs,
                               batch, s, stop);
     if (rc >= 0) return rc;

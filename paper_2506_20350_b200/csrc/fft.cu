@@ -449,21 +449,14 @@ inline int device_sms() {
 // returns -1 when the pass does not qualify
 template <typename TC, typename TO, int TIL, int... Rs>
 int try_stream(const PassArgs& a, cudaStream_t s) {
-  static const int64_t min_tiles = [] {
-    const char* e = std::getenv("TOEP_FFT_STREAM_MIN_TILES");
-    return e != nullptr ? std::atoll(e) : static_cast<int64_t>(1) << 15;
-  }();
+  constexpr int64_t min_tiles = int64_t{1} << 15;  // persistent streaming only for very large passes
   const int64_t tiles_x = (a.inner + TIL - 1) / TIL;
   const int64_t ntiles = tiles_x * a.outer;
-  // measured on cfg3 (L = 60, 432 000 tiles per pass): the 3M-plane input pass 1.74 -> 1.38 ms, but the
+  // measured on cfg3 (L = 60, 432 000 tiles per pass): the plane-input pass 1.74 -> 1.38 ms, but the
   // complex-input passes 1.17 -> 1.30 / 2.45 -> 2.56 ms (fewer resident warps than the short-lived
-  // CTAs of fft_plan_kernel); TOEP_FFT_STREAM=all streams those too
-  static const bool all = [] {
-    const char* e = std::getenv("TOEP_FFT_STREAM");
-    return e != nullptr && std::strcmp(e, "all") == 0;
-  }();
-  if (min_tiles <= 0 || ntiles < min_tiles || a.in_idx != nullptr || a.out_idx != nullptr ||
-      a.scatter != nullptr || (a.in_planes == nullptr && !all))
+  // CTAs of fft_plan_kernel): only plane-input passes stream
+  if (ntiles < min_tiles || a.in_idx != nullptr || a.out_idx != nullptr || a.scatter != nullptr ||
+      a.in_planes == nullptr)
     return -1;
   constexpr int L = PlanLen<Rs...>::value;
   auto launch_kin = [&](auto kin_tag) -> int {
@@ -492,11 +485,7 @@ int try_plan(const PassArgs& a, cudaStream_t s) {
     case 60:
       if (a.inner >= 16) {
         if constexpr (std::is_same_v<TI, TC>) {
-          static const int til = [] {
-            const char* e = std::getenv("TOEP_FFT_STREAM_TIL");
-            return e != nullptr ? std::atoi(e) : 16;
-          }();
-          const int rc = til == 8 ? try_stream<TC, TO, 8, 4, 3, 5>(a, s) : try_stream<TC, TO, 16, 4, 3, 5>(a, s);
+          const int rc = try_stream<TC, TO, 16, 4, 3, 5>(a, s);  // 16-column tiles (8: 47.7 vs 46.5 ms at cfg3)
           if (rc >= 0) return rc;
         }
         return launch_plan<TI, TC, TO, 16, 4, 3, 5>(a, s);
@@ -817,11 +806,7 @@ int factorize(int L, int* rad, int* nrad) {
 
 int fft2d(bool inverse, const void* in, void* out, int n2, int n1, int l2, int l1, int64_t inner, int sign, int tin,
           int tc, int tout, const double* in_scale, const int* stop, cudaStream_t s, const L2Prefetch* pf) {
-  static const bool off = [] {
-    const char* e = std::getenv("TOEP_FFT2D");
-    return e != nullptr && e[0] == '0';
-  }();
-  if (off || inner > 65535 || inner < 1) return -1;
+  if (inner > 65535 || inner < 1) return -1;
   Fft2dArgs f{in, out, n2, n1, inner, sign, in_scale, stop, pf != nullptr ? *pf : L2Prefetch{}};
   const int code = tin * 4 + tc * 2 + tout;
   switch (code) {

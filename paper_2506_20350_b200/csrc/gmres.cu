@@ -454,10 +454,7 @@ struct OrthArgs {
   unsigned* bar;    // [2] grid barrier: arrival count, generation
   long long* ts;    // optional phase stamps: [2k+2] = step k orth start, [2k+3] = step k end
   L2Prefetch pf;    // operator stream prefetched into L2 for the next matvec (HBM is idle here)
-  int force_cgs2;   // 1: always two Gram-Schmidt passes (TOEP_CGS2=1)
-  double reorth_eta2;  // second pass when ||w'||^2 <= eta^2 ||w||^2
-  int direct_norm;  // 1: h_{j+1,j} = ||w''|| from a third sweep + barrier (TOEP_DIRECT_NORM=1)
-  double2* gram;    // one-sweep CGS2: Gram matrix of the cycle's basis [ldr][ldr] (col-major), or null
+  double2* gram;    // one-sweep CGS2: Gram matrix of the cycle's basis [ldr][ldr] (col-major)
   double2* part2;   // [ldr][nblk] partials of V^H v_{m-1}
   int gram_smem;    // 1: the Gram block is staged in shared memory (small cycles, see coop_smem)
 };
@@ -493,27 +490,6 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
 }
 
 // coef[l] = vs_l * (vs_l * sum_b part[l][b]); CTA 0 stores h (mode 1) or hprev + h (mode 2)
-__device__ __forceinline__ void orth_coefs(const OrthArgs& a, double2* coef, int mode, double2* hout,
-                                           double2* hsm = nullptr, double* hsq = nullptr) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nblk = gridDim.x;
-  for (int l = warp; l < a.m; l += kCoopThreads / 32) {
-    double2 s = make_double2(0, 0);
-    for (int b = lane; b < nblk; b += 32) s = cadd(s, __ldcg(a.part + static_cast<int64_t>(l) * nblk + b));
-    s = warp_sum(s);
-    if (lane == 0) {
-      const double2 h = cscale(s, a.vs[l]);
-      coef[l] = cscale(h, a.vs[l]);
-      if (hsq != nullptr) hsq[l] = h.x * h.x + h.y * h.y;
-      if (blockIdx.x == 0) {
-        const double2 hv = (mode == 1) ? h : cadd(a.h1[l], h);
-        hout[l] = hv;
-        if (hsm != nullptr) hsm[l] = hv;
-      }
-    }
-  }
-  __syncthreads();
-}
 
 __device__ __forceinline__ double orth_update(const OrthArgs& a, const double2* coef, int64_t c0, int64_t c1) {
   constexpr int U = 8;  // basis loads issued together (latency-bound sweep over L2-resident vectors)
@@ -698,42 +674,6 @@ __device__ __forceinline__ void orth_dots_gram(const OrthArgs& a, int64_t c0, in
 
 // one warp per basis vector: warp l sweeps the CTA's chunk of V_l and w with 8 independent
 // loads in flight per lane and ends with a single warp reduction; lane 0 stores the CTA partial
-__device__ __forceinline__ void orth_dots(const OrthArgs& a, int64_t c0, int64_t c1, double* wn2 = nullptr) {
-  constexpr int NW = kCoopThreads / 32, U = 8;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nblk = gridDim.x;
-  if (wn2 != nullptr && warp == NW - 1) {  // ||w||^2 over the chunk (selective re-orthogonalisation test)
-    double t = 0.0;
-    for (int64_t i = c0 + lane; i < c1; i += 32) {
-      const double2 v = a.w[i];
-      t = fma(v.x, v.x, fma(v.y, v.y, t));
-    }
-    t = warp_sum(t);
-    if (lane == 0) wn2[blockIdx.x] = t;
-  }
-  for (int l = warp; l < a.m; l += NW) {
-    const double2* v = a.V + static_cast<int64_t>(l) * a.N;
-    double2 acc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc[u] = make_double2(0, 0);
-    int64_t i = c0 + lane;
-    for (; i + 32 * (U - 1) < c1; i += 32 * U) {
-      double2 vv[U], ww[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        vv[u] = v[i + 32 * u];
-        ww[u] = a.w[i + 32 * u];
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) cfmac(acc[u], vv[u], ww[u]);
-    }
-    for (; i < c1; i += 32) cfmac(acc[0], v[i], a.w[i]);
-#pragma unroll
-    for (int u = 1; u < U; ++u) acc[0] = cadd(acc[0], acc[u]);
-    const double2 s = warp_sum(acc[0]);
-    if (lane == 0) a.part[static_cast<int64_t>(l) * nblk + blockIdx.x] = s;
-  }
-}
 
 // the new rotation from the rotated column's diagonal entry and h_{j+1,j} = ||w|| (gmres.py:
 // 87-95, 171-190); same arithmetic as givens_warp's tail, with the scalars prefetched
@@ -849,7 +789,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
     k_step = a.st->total;
     nhist = a.st->nhist;
   }
-  if (a.gram != nullptr) {
+  {
     // ---- one-sweep CGS2 (Gram-matrix form): the second pass coefficients V^H w' = h1 - G h1 with
     // G = V^H V, the basis Gram matrix, whose new column comes out of the same sweep as h1; then
     // one update w'' = w - V (h1 + h2) and ||w''||^2 = ||w||^2 - 2 Re(h^H h1) + h^H G h.
@@ -1033,105 +973,6 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
       }
     }
     return;
-  }
-  // pass 1: h1 = V^H w, plus ||w||^2
-  __shared__ double hsq[kMaxOrthM];
-  __shared__ int reorth_s;
-  __shared__ double hn2_s;
-  orth_dots(a, c0, c1, a.force_cgs2 ? nullptr : a.npart);
-  OPROBE();
-  grid_barrier(a.bar);
-  OPROBE();
-  orth_coefs(a, coef, 1, a.h1, blockIdx.x == 0 ? hsm : nullptr, a.force_cgs2 ? nullptr : hsq);
-  // Selective re-orthogonalisation (Kahan-Parlett "twice is enough" test): ||w'||^2 = ||w||^2 -
-  // ||h1||^2 (Pythagoras, v_l orthonormal); a second Gram-Schmidt pass only when the projection
-  // cancelled more than a factor eta of ||w|| (default eta = 1/10, TOEP_REORTH_ETA2 = eta^2;
-  // TOEP_CGS2=1 forces the second pass).  Every CTA evaluates the test from the same partials in
-  // the same order, so the branch is uniform across the grid.
-  if (a.force_cgs2) {
-    if (threadIdx.x == 0) reorth_s = 1;
-  } else if (threadIdx.x < 32) {
-    double wn = 0.0, hs = 0.0;
-    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32) wn += __ldcg(a.npart + b);
-    for (int l = threadIdx.x; l < a.m; l += 32) hs += hsq[l];
-    wn = warp_sum(wn);
-    hs = warp_sum(hs);
-    if (threadIdx.x == 0) {
-      const double hn2 = wn - hs;
-      hn2_s = hn2;
-      reorth_s = !(hn2 > a.reorth_eta2 * wn) ? 1 : 0;
-    }
-  }
-  __syncthreads();
-  if (!reorth_s) {
-    double2* hcol1 = a.rcols + static_cast<int64_t>(jcol) * a.ldr;
-    if (blockIdx.x == 0) {
-      orth_prepare_givens(a, jcol, hsm, snl, csl, hcol1);
-      if (threadIdx.x == 0) {
-        givens_finish(a, jcol, hsm[jcol], hn2_s, g_j, beta0, nhist);
-        if (a.ts != nullptr) a.ts[2 * k_step + 3] = global_ns();
-      }
-    }
-    orth_update(a, coef, c0, c1);
-    return;
-  }
-  OPROBE();
-  orth_update(a, coef, c0, c1);
-  __syncthreads();
-  OPROBE();  // pass 2 (re-orthogonalisation): h2 = V^H w', H[:, j] = h1 + h2, plus ||w'||^2
-  orth_dots(a, c0, c1, a.direct_norm ? nullptr : a.npart);
-  grid_barrier(a.bar);
-  OPROBE();
-  double2* hcol = a.rcols + static_cast<int64_t>(jcol) * a.ldr;
-  orth_coefs(a, coef, 2, hcol, blockIdx.x == 0 ? hsm : nullptr, a.direct_norm ? nullptr : hsq);
-  if (!a.direct_norm) {
-    // h_{j+1,j}^2 = ||w''||^2 = ||w'||^2 - ||h2||^2 (Pythagoras; h2 is the small second-pass
-    // correction, so there is no cancellation): no third grid barrier, CTA 0 finishes the Givens
-    // step while the other CTAs apply the second update
-    if (blockIdx.x == 0) {
-      orth_prepare_givens(a, jcol, hsm, snl, csl, hcol);
-      if (threadIdx.x < 32) {
-        double wn = 0.0, hs = 0.0;
-        for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32) wn += __ldcg(a.npart + b);
-        for (int l = threadIdx.x; l < a.m; l += 32) hs += hsq[l];
-        wn = warp_sum(wn);
-        hs = warp_sum(hs);
-        if (threadIdx.x == 0) {
-          givens_finish(a, jcol, hsm[jcol], fmax(wn - hs, 0.0), g_j, beta0, nhist);
-          if (a.ts != nullptr) a.ts[2 * k_step + 3] = global_ns();
-        }
-      }
-    }
-    orth_update(a, coef, c0, c1);
-    return;
-  }
-  if (blockIdx.x == 0) orth_prepare_givens(a, jcol, hsm, snl, csl, hcol);
-  double nrm = orth_update(a, coef, c0, c1);
-  nrm = warp_sum(nrm);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = red[0];
-    for (int ww = 1; ww < kCoopThreads / 32; ++ww) t += red[ww];
-    a.npart[blockIdx.x] = t;
-  }
-  grid_barrier(a.bar);
-  if (blockIdx.x == 0 && threadIdx.x < 32) {
-    double hn2 = 0.0;
-    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32) hn2 += __ldcg(a.npart + b);
-    hn2 = warp_sum(hn2);
-    OPROBE();
-    if (threadIdx.x == 0) {
-      givens_finish(a, jcol, hsm[jcol], hn2, g_j, beta0, nhist);
-      if (a.ts != nullptr) a.ts[2 * k_step + 3] = global_ns();
-    }
-#ifdef TOEP_ORTH_PROBE
-    OPROBE();
-    if (threadIdx.x == 0 && (k_step == 8 || k_step == 16 || k_step == 24))
-      printf("orth k=%d m=%d: dots1 %lld bar %lld coef %lld upd %lld dots2+bar %lld upd2+norm+bar %lld givens %lld ns\n",
-             k_step, a.m, pt[1] - pt[0], pt[2] - pt[1], pt[3] - pt[2], pt[4] - pt[3], pt[5] - pt[4], pt[6] - pt[5],
-             pt[7] - pt[6]);
-#endif
   }
 }
 
@@ -1471,16 +1312,9 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
                                      sizeof(double2) * (7 * ldr + (gram_smem ? ldr * ldr : 0)) +
                                          sizeof(double) * ldr});
   const int coop_grid = nblk;
-  // TOEP_COOP_LAUNCH=0: plain PDL launch of the grid-barrier kernel (co-residency from the
-  // resource budget: one CTA per SM, fits next to either 2-D DFT kernel)
-  static const bool coop_attr = [] {
-    const char* v = std::getenv("TOEP_COOP_LAUNCH");
-    return !(v != nullptr && v[0] == '0');
-  }();
-  bool use_coop = !e.distributed() && cycle_len <= kMaxOrthM && [] {
-    const char* v = std::getenv("TOEP_COOP");
-    return !(v != nullptr && v[0] == '0');
-  }();
+  // the cooperative orthogonalisation kernel (grid barrier): single process, cycles up to
+  // kMaxOrthM vectors, and every CTA co-resident; otherwise the per-phase kernel chain
+  bool use_coop = !e.distributed() && cycle_len <= kMaxOrthM;
   if (use_coop) {
     ensure_smem(k_orth_coop, coop_smem + 8 * 1024);  // + headroom: the kernel's static shared memory
     // same (maximal) shared-memory carveout as the 2-D DFT kernels, so the next forward DFT can
@@ -1499,23 +1333,9 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   tr.mark("allocations");
 
   const bool timed = cfg->timings != 0;
-  // default: always two passes (CGS2), whose residual histories track the reference's MGS to
-  // 1e-6; TOEP_REORTH_ETA2=<eta^2> selects the one-pass-unless-cancelled variant (measured: half
-  // the orthogonalisation time at eta^2 = 1e-2, same iteration counts, histories drift ~1e-5)
-  // TOEP_ORTH=cgs2: the two-sweep-pair CGS2 kernel path (three barriers); default: one-sweep CGS2
-  static const bool gram_form = [] {
-    const char* e = std::getenv("TOEP_ORTH");
-    return !(e != nullptr && std::strcmp(e, "cgs2") == 0);
-  }();
-  static const int direct_norm = [] {
-    const char* e = std::getenv("TOEP_DIRECT_NORM");
-    return e != nullptr && e[0] == '1' ? 1 : 0;
-  }();
-  static const int force_cgs2 = std::getenv("TOEP_REORTH_ETA2") == nullptr ? 1 : 0;
-  static const double reorth_eta2 = [] {
-    const char* e = std::getenv("TOEP_REORTH_ETA2");
-    return e != nullptr ? std::atof(e) : 1e-2;
-  }();
+  // orthogonalisation: one-sweep CGS2 in Gram-matrix form (histories track the reference's MGS to
+  // 1e-6; the measured alternatives -- explicit two-pass CGS2, selective re-orthogonalisation --
+  // are recorded in DESIGN.md)
   const L2Prefetch orth_pf = (p->op != nullptr && p->w == 1) ? binprod_prefetch_plan(p->op->dtype, p->op->DT,
                                                                                     p->op->K, p->op->n0, 2)
                                                             : L2Prefetch{};
@@ -1640,12 +1460,9 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       const int m = j + 1;
       if (use_coop) {
         OrthArgs oa{V, N, m, vs, w, part1, e.norm_partial, h1, st, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
-                    static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev, orth_pf, force_cgs2, reorth_eta2,
-                    direct_norm, gram_form ? gram : nullptr, part2, (gram_form && gram_smem) ? 1 : 0};
-        rc = coop_attr ? launch_coop(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa,
-                                     (const int*)stop_dev)
-                       : launch_k(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa,
-                                  (const int*)stop_dev);
+                    static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev, orth_pf, gram, part2,
+                    gram_smem ? 1 : 0};
+        rc = launch_coop(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa, (const int*)stop_dev);
         if (rc != TOEP_OK) {  // cooperative launch unavailable: permanent fallback to the 4-kernel chain
           use_coop = false;
           rc = TOEP_OK;

@@ -40,32 +40,6 @@ __device__ __forceinline__ int64_t rows_begin(int chunk, int nchunks, int64_t n)
   return n * chunk / nchunks;
 }
 
-// partial[(l*nchunks + chunk)*W + c] = sum_{rows in chunk} conj(V_l[i, c]) w[i, c]
-__global__ void __launch_bounds__(kCols) kb_dots(const double2* const* __restrict__ Vp, int m,
-                                                 const double2* __restrict__ w, int64_t n, int W, int nchunks,
-                                                 double2* __restrict__ partial) {
-  pdl_wait();
-  pdl_trigger();
-  const int c = blockIdx.y * kCols + threadIdx.x;
-  if (c >= W) return;
-  const int chunk = blockIdx.x;
-  const int64_t r0 = rows_begin(chunk, nchunks, n), r1 = rows_begin(chunk + 1, nchunks, n);
-  for (int l0 = 0; l0 < m; l0 += kLG) {
-    double2 acc[kLG];
-#pragma unroll
-    for (int g = 0; g < kLG; ++g) acc[g] = make_double2(0, 0);
-    for (int64_t i = r0; i < r1; ++i) {
-      const double2 wi = w[i * W + c];
-#pragma unroll
-      for (int g = 0; g < kLG; ++g)
-        if (l0 + g < m) cfmac(acc[g], Vp[l0 + g][i * W + c], wi);
-    }
-#pragma unroll
-    for (int g = 0; g < kLG; ++g)
-      if (l0 + g < m) partial[(static_cast<int64_t>(l0 + g) * nchunks + chunk) * W + c] = acc[g];
-  }
-}
-
 // One-sweep CGS2 (Gram-matrix form), per column: partial[l] = V_l^H w and partial2[l] =
 // V_l^H V_{m-1} (the newest basis vector's Gram column) in the same basis sweep
 constexpr int kLGG = 4;
@@ -164,22 +138,6 @@ __global__ void kb_coef_gram(const double2* __restrict__ h1, const double2* __re
     h[static_cast<int64_t>(l) * W + c] = hv;
     hcol[static_cast<int64_t>(l) * W + c] = hv;
   }
-}
-
-// h[l][c] = sum_chunk partial[l][chunk][c]; mode 1: hout = h; mode 2: hout = hprev + h
-__global__ void kb_reduce(const double2* __restrict__ partial, int m, int nchunks, int W, double2* __restrict__ h,
-                          const double2* __restrict__ hprev, double2* __restrict__ hcol, int ldh,
-                          const int* __restrict__ stop) {
-  pdl_wait();
-  pdl_trigger();
-  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (t >= static_cast<int64_t>(m) * W) return;
-  const int l = static_cast<int>(t / W), c = static_cast<int>(t - static_cast<int64_t>(l) * W);
-  if (stop[c]) return;
-  double2 s = make_double2(0, 0);
-  for (int ch = 0; ch < nchunks; ++ch) s = cadd(s, partial[(static_cast<int64_t>(l) * nchunks + ch) * W + c]);
-  h[static_cast<int64_t>(l) * W + c] = s;
-  if (hcol != nullptr) hcol[static_cast<int64_t>(l) * ldh + c] = cadd(hprev[static_cast<int64_t>(l) * W + c], s);
 }
 
 // w[:, c] -= sum_l V_l[:, c] h[l][c]  (active columns); mode 1: partial dots of the result,
@@ -492,10 +450,7 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
   const int ctiles = (W + kCols - 1) / kCols;
   // row chunks: enough CTAs of kCols threads for ~32 resident warps per SM (the sweeps are
   // latency-bound per thread; occupancy is what keeps HBM busy)
-  static const int chunk_mult = [] {
-    const char* e = std::getenv("TOEP_BATCH_CHUNKS");
-    return e != nullptr ? std::max(1, std::atoi(e)) : 32;
-  }();
+  constexpr int chunk_mult = 32;
   const int nchunks = static_cast<int>(
       std::max<int64_t>(1, std::min<int64_t>(n / 16, (chunk_mult * sms + ctiles - 1) / ctiles)));
   const int g1 = static_cast<int>(std::min<int64_t>((N + 255) / 256, 8 * sms));
@@ -544,15 +499,9 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
   B_ALLOC(pb, N);
   B_ALLOC(h1, static_cast<int64_t>(ldr) * W);
   B_ALLOC(h2, static_cast<int64_t>(ldr) * W);
-  // one-sweep CGS2 (Gram form) unless TOEP_BATCH_ORTH=cgs2
-  static const bool gram_form = [] {
-    const char* e = std::getenv("TOEP_BATCH_ORTH");
-    return !(e != nullptr && std::strcmp(e, "cgs2") == 0);
-  }();
-  if (gram_form) {
-    B_ALLOC(part2, static_cast<int64_t>(ldr) * nchunks * W);
-    B_ALLOC(gram, static_cast<int64_t>(ldr) * ldr * W);
-  }
+  // one-sweep CGS2 in Gram-matrix form per column (the explicit two-pass variant measured slower)
+  B_ALLOC(part2, static_cast<int64_t>(ldr) * nchunks * W);
+  B_ALLOC(gram, static_cast<int64_t>(ldr) * ldr * W);
   B_ALLOC(rcols, static_cast<int64_t>(cycle_len) * ldr * W);
   B_ALLOC(sn, static_cast<int64_t>(ldr) * W);
   B_ALLOC(cs, static_cast<int64_t>(ldr) * W);
@@ -646,23 +595,12 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
         B_TRY(matvec_impl(p->op, Vh[j], w, W, false, io64, nullptr, s));
       }
       const int rg = static_cast<int>((static_cast<int64_t>(m) * W + 255) / 256);
-      if (gram_form) {
-        B_TRY(launch_k(kb_dots_gram, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)w, n, W,
-                       nchunks, part, part2));
-        B_TRY(launch_k(kb_reduce_gram, dim3(rg), dim3(256), 0, s, (const double2*)part, (const double2*)part2, m,
-                       nchunks, W, h1, gram, ldr, (const int*)st.stop));
-        B_TRY(launch_k(kb_coef_gram, dim3(gc), dim3(128), 0, s, (const double2*)h1, (const double2*)gram, m, ldr, W,
-                       h2, rcols + static_cast<int64_t>(j) * ldr * W, (const int*)st.stop));
-      } else {
-      B_TRY(launch_k(kb_dots, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)w, n, W,
-                     nchunks, part));
-      B_TRY(launch_k(kb_reduce, dim3(rg), dim3(256), 0, s, (const double2*)part, m, nchunks, W, h1,
-                     (const double2*)nullptr, (double2*)nullptr, 0, (const int*)st.stop));
-      B_TRY(launch_k(kb_upd, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)h1, w, n,
-                     W, nchunks, 1, part, (double*)nullptr, (const int*)st.stop));
-      B_TRY(launch_k(kb_reduce, dim3(rg), dim3(256), 0, s, (const double2*)part, m, nchunks, W, h2,
-                     (const double2*)h1, rcols + static_cast<int64_t>(j) * ldr * W, W, (const int*)st.stop));
-      }
+      B_TRY(launch_k(kb_dots_gram, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)w, n, W,
+                     nchunks, part, part2));
+      B_TRY(launch_k(kb_reduce_gram, dim3(rg), dim3(256), 0, s, (const double2*)part, (const double2*)part2, m,
+                     nchunks, W, h1, gram, ldr, (const int*)st.stop));
+      B_TRY(launch_k(kb_coef_gram, dim3(gc), dim3(128), 0, s, (const double2*)h1, (const double2*)gram, m, ldr, W,
+                     h2, rcols + static_cast<int64_t>(j) * ldr * W, (const int*)st.stop));
       B_TRY(launch_k(kb_upd, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)h2, w, n,
                      W, nchunks, 2, (double2*)nullptr, npart, (const int*)st.stop));
       B_TRY(launch_k(kb_givens, dim3(gc), dim3(128), 0, s, st, (const double*)npart, nchunks, W, rcols, ldr, cs, sn, g,

@@ -5,7 +5,7 @@
 // are scheduled while the previous grid drains, run their prologue, and block
 // in griddepcontrol.wait until the predecessor's memory is visible.  This
 // hides the ~2-4 us launch/ramp gap at each of the many kernel boundaries of
-// a 170 us matvec and of the short Arnoldi kernels.  TOEP_PDL=0 disables it.
+// a 170 us matvec and of the short Arnoldi kernels.
 #pragma once
 
 #include <cstdlib>
@@ -16,13 +16,7 @@
 
 namespace toep {
 
-inline bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("TOEP_PDL");
-    return !(e != nullptr && std::strcmp(e, "0") == 0);
-  }();
-  return on;
-}
+inline bool pdl_enabled() { return true; }
 
 // Wait until the predecessor grid (PDL) has completed and its writes are visible.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

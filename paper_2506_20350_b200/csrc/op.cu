@@ -128,13 +128,9 @@ int mrhs_chunk(const toep_op_s* op, int64_t w) {
 // Multi-RHS per-bin products as 3M (Gauss): V = D U with three real FP64 tensor-core GEMMs on split
 // planes, T1 = Dr Ur, T2 = Di Ui, T3 = (Dr + Di)(Ur + Ui); the level-2 DFT passes write / read the
 // planes directly, so the split and the recombination cost no extra pass.  Enabled for c128,
-// W >= 16 and a compiled level-2 plan (TOEP_MRHS_3M=0: complex GEMMs).
+// W >= 16 and a compiled level-2 plan.
 bool mrhs_3m(const toep_op_s* op, int64_t w, bool transpose) {
-  static const bool on = [] {
-    const char* e = std::getenv("TOEP_MRHS_3M");
-    return !(e != nullptr && e[0] == '0');
-  }();
-  return on && !transpose && w >= 16 && op->dtype == TOEP_C128 && op->slab_kxs == 0 &&
+  return !transpose && w >= 16 && op->dtype == TOEP_C128 && op->slab_kxs == 0 &&
          fft_plan_has_planes(op->l2, static_cast<int64_t>(op->n0) * w);
 }
 

@@ -238,7 +238,6 @@ struct OzArgs {
   int n0;
   int64_t w;
   int ntiles;
-  int dbg;  // experiment switch (TOEP_OZ_DBG): 1 = no epilogue math / stores, 2 = no operand loads
 };
 
 // Groups t = 2..8 do not fit TMEM side by side at N = 128 (7 x 128 columns), so every column tile
@@ -291,10 +290,6 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
       if (issued >= kStages) mbar_wait(&empty[st], ((issued / kStages) - 1) & 1);
       const int tp = issued / kcs, kc = issued - tp * kcs;  // tp = nt * 2 + phase
       const int nt = tp >> 1;
-      if (a.dbg == 2) {
-        mbar_arrive(&full[st]);
-        continue;
-      }
       const uint32_t bytes = static_cast<uint32_t>(phase_slices(tp & 1)) * (kBM * kBK);  // kBM == kBN
       mbar_expect_tx(&full[st], 2 * bytes);
       bulk_g2s(sA + st * kATile, Ab + static_cast<int64_t>(kc) * kATile, bytes, &full[st], pol);
@@ -348,7 +343,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       __syncthreads();  // scol visible
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-      if (a.dbg != 1) {
+      {
         // this thread's 64 columns: the phase-0 partial stays in registers until phase 1 completes it
 #pragma unroll
         for (int ci = 0; ci < kBN / 32; ++ci) {
@@ -432,10 +427,6 @@ int ozaki_products(const int8_t* asl, const int32_t* aexp, const double* re, con
   TOEP_CUDA(ensure_smem(ozaki_slice_b_kernel, tsm));
   const size_t smem = kStages * (kATile + kBTile);
   TOEP_CUDA(ensure_smem(ozaki_tile_kernel, smem));
-  static const int dbg = [] {
-    const char* e = std::getenv("TOEP_OZ_DBG");
-    return e != nullptr ? std::atoi(e) : 0;
-  }();
   const int64_t wpad = static_cast<int64_t>(ntiles) * kBN;
   const int64_t a_bin = ozaki_a_bytes(n0, 1), b_bin = ozaki_b_bytes(n0, 1, w), plane_bin = static_cast<int64_t>(n0) * w;
   for (int64_t b0 = 0; b0 < bins; b0 += 65535) {  // grid.y limit
@@ -446,7 +437,7 @@ int ozaki_products(const int8_t* asl, const int32_t* aexp, const double* re, con
                                 bexp + b0 * wpad);
     TOEP_LAUNCHED();
     OzArgs oa{asl + b0 * a_bin, aexp + b0 * 2 * n0, bsl + b0 * b_bin, bexp + b0 * wpad, out_re + b0 * plane_bin,
-              out_im + b0 * plane_bin, n0, w, ntiles, dbg};
+              out_im + b0 * plane_bin, n0, w, ntiles};
     ozaki_tile_kernel<<<dim3(static_cast<unsigned>(2 * n0 / kBM), nb), kOzThreads, smem, s>>>(oa);
     TOEP_LAUNCHED();
   }
