@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/toepcuda.h"
 
 namespace toep {
@@ -56,6 +58,14 @@ struct Status {
   int code = TOEP_OK;
 };
 
+// NVTX range over a C-ABI entry point (header-only NVTX v3: a no-op unless a tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 }  // namespace toep
 
 #define TOEP_CUDA(call)                                                                  \
@@ -81,6 +91,8 @@ struct Status {
     int _s = (expr);                   \
     if (_s != TOEP_OK) return _s;      \
   } while (0)
+
+#define TOEP_NVTX(name) ::toep::NvtxRange _toep_nvtx_range(name)
 
 #define TOEP_REQUIRE(cond, code, ...)         \
   do {                                        \

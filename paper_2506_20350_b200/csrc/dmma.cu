@@ -597,6 +597,7 @@ int zgemm_dmma(int64_t m, int64_t n, int64_t k, double2 alpha, const void* a, in
 extern "C" int toep_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t a_rs, int64_t a_cs,
                           int64_t a_bs, const double* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, double beta,
                           double* c, int64_t c_rs, int64_t c_cs, int64_t c_bs, int64_t batch, void* stream) {
+  TOEP_NVTX("toep_dgemm");
   TOEP_REQUIRE(m >= 0 && n >= 0 && k >= 0 && batch >= 0, TOEP_ERR_SHAPE, "negative gemm size");
   int64_t done = 0;
   while (done < batch) {

@@ -1590,6 +1590,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
 
 extern "C" int toep_gmres(const toep_gmres_problem_t* prob, const toep_gmres_cfg_t* cfg, const void* b, void* x,
                           void* stream, toep_gmres_report_t* rep) {
+  TOEP_NVTX("toep_gmres");
   TOEP_REQUIRE(prob != nullptr && cfg != nullptr && b != nullptr && x != nullptr && rep != nullptr, TOEP_ERR_ARG,
                "null argument");
   return toep::gmres_run(prob, cfg, static_cast<const double2*>(b), static_cast<double2*>(x),

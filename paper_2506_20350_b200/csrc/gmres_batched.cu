@@ -667,6 +667,7 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
 extern "C" int toep_gmres_batched(const toep_gmres_problem_t* prob, const toep_gmres_cfg_t* cfg, const void* b,
                                   void* x, void* stream, int32_t* iterations, int32_t* converged,
                                   double* final_residual, int32_t* n_history, double* history, int64_t history_rows) {
+  TOEP_NVTX("toep_gmres_batched");
   TOEP_REQUIRE(prob != nullptr && cfg != nullptr && b != nullptr && x != nullptr && iterations != nullptr &&
                    converged != nullptr && final_residual != nullptr && n_history != nullptr,
                TOEP_ERR_ARG, "null argument");

@@ -378,6 +378,7 @@ int toep_op_create(const void* stacked4, int on_device, int n2, int n1, int n0, 
 // are transformed and kept (the slab operator of the row / kx-slab decomposition)
 int toep_op_create_slab(const void* stacked4, int on_device, int n2, int n1, int n0, int l2, int l1, int dtype,
                         int kx0, int kx1, void* stream, toep_op_t* out) {
+  TOEP_NVTX("toep_op_create");
   TOEP_REQUIRE(out != nullptr && stacked4 != nullptr, TOEP_ERR_ARG, "null argument");
   TOEP_REQUIRE(n2 >= 1 && n1 >= 1 && n0 >= 1, TOEP_ERR_SHAPE, "n2, n1, n0 must be positive");
   TOEP_REQUIRE(dtype == TOEP_C128 || dtype == TOEP_C64, TOEP_ERR_ARG, "dtype must be TOEP_C128 or TOEP_C64");
@@ -527,6 +528,7 @@ int toep_op_diag_blocks(toep_op_t op, void* dst, void* stream) {
 }
 
 int toep_op_fold_left(toep_op_t op, const void* m_dev, void* stream, toep_op_t* out) {
+  TOEP_NVTX("toep_op_fold_left");
   TOEP_REQUIRE(op != nullptr && m_dev != nullptr && out != nullptr, TOEP_ERR_ARG, "null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   note_stream(op, s);
@@ -595,6 +597,7 @@ int toep_op_slab(toep_op_t op, int kx0, int kx1, void* stream, toep_op_t* out) {
 }
 
 int toep_matvec_stage(toep_op_t op, int stage, const void* in, void* out, int64_t w, int count, void* stream) {
+  TOEP_NVTX("toep_matvec_stage");
   TOEP_REQUIRE(op != nullptr && in != nullptr && out != nullptr && in != out && w >= 1 && count >= 0, TOEP_ERR_ARG,
                "bad matvec_stage arguments");
   return toep::matvec_stage_impl(op, stage, in, out, w, count, nullptr, static_cast<cudaStream_t>(stream));
@@ -602,6 +605,7 @@ int toep_matvec_stage(toep_op_t op, int stage, const void* in, void* out, int64_
 
 int toep_matvec_stage_peer(toep_op_t op, int stage, const void* in, const toep_peer_scatter* scatter, int64_t w,
                            int count, void* stream) {
+  TOEP_NVTX("toep_matvec_stage_peer");
   TOEP_REQUIRE(op != nullptr && in != nullptr && scatter != nullptr && w >= 1 && count >= 0, TOEP_ERR_ARG,
                "bad matvec_stage_peer arguments");
   TOEP_REQUIRE(stage == 0 || stage == 1, TOEP_ERR_ARG, "peer scatter is defined for stages 0 and 1, not %d", stage);
@@ -654,6 +658,7 @@ int matvec_stage_impl(toep_op_s* op, int stage, const void* in, void* out, int64
 extern "C" {
 
 int toep_matvec(toep_op_t op, const void* u, void* v, int64_t w, int flags, void* stream) {
+  TOEP_NVTX("toep_matvec");
   TOEP_REQUIRE(op != nullptr && (w == 0 || (u != nullptr && v != nullptr)), TOEP_ERR_ARG, "null argument");
   TOEP_REQUIRE(op->slab_kxs == 0, TOEP_ERR_ARG, "a slab operator is applied through toep_matvec_stage");
   TOEP_REQUIRE(w >= 0, TOEP_ERR_SHAPE, "negative column count");
@@ -663,6 +668,7 @@ int toep_matvec(toep_op_t op, const void* u, void* v, int64_t w, int flags, void
 }
 
 int toep_matvec_host(toep_op_t op, const void* u_host, void* v_host, int64_t w, int flags, void* stream) {
+  TOEP_NVTX("toep_matvec_host");
   TOEP_REQUIRE(op != nullptr && (w == 0 || (u_host != nullptr && v_host != nullptr)), TOEP_ERR_ARG, "null argument");
   TOEP_REQUIRE(op->slab_kxs == 0, TOEP_ERR_ARG, "a slab operator is applied through toep_matvec_stage");
   TOEP_REQUIRE(w >= 0, TOEP_ERR_SHAPE, "negative column count");
@@ -732,6 +738,7 @@ int toep_block_dft(const void* in, void* out, int n2, int n1, int64_t inner, int
 
 int toep_block_apply(const void* m, int n0, const void* in, void* out, int64_t segments, int64_t w, int dtype,
                      void* stream) {
+  TOEP_NVTX("toep_block_apply");
   TOEP_REQUIRE(m != nullptr && in != nullptr && out != nullptr, TOEP_ERR_ARG, "null argument");
   TOEP_REQUIRE(in != out, TOEP_ERR_ARG, "block_apply output must not alias its input");
   return block_apply_impl(m, n0, in, out, segments, w, dtype, static_cast<cudaStream_t>(stream), nullptr);
@@ -740,6 +747,7 @@ int toep_block_apply(const void* m, int n0, const void* in, void* out, int64_t s
 int toep_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* alpha, const void* a, int64_t a_rs,
               int64_t a_cs, int64_t a_bs, const void* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, const void* beta,
               void* c, int64_t c_rs, int64_t c_cs, int64_t c_bs, int64_t batch, void* stream) {
+  TOEP_NVTX("toep_gemm");
   TOEP_REQUIRE(alpha != nullptr && beta != nullptr, TOEP_ERR_ARG, "null alpha/beta");
   const double2 al = *static_cast<const double2*>(alpha);
   const double2 be = *static_cast<const double2*>(beta);

@@ -651,6 +651,7 @@ __global__ void __launch_bounds__(256) k_assemble_level1(const double2* __restri
 }  // namespace toep
 
 extern "C" int toep_assemble_level1(const void* stacked4, int n2, int n1, int n0, void* out, void* stream) {
+  TOEP_NVTX("toep_assemble_level1");
   TOEP_REQUIRE(stacked4 != nullptr && out != nullptr && stacked4 != out, TOEP_ERR_ARG, "bad assemble_level1 buffers");
   TOEP_REQUIRE(n2 >= 1 && n1 >= 1 && n0 >= 1, TOEP_ERR_SHAPE, "n2, n1, n0 must be positive");
   const int64_t rows = static_cast<int64_t>(2 * n2 - 1) * n1 * n0;
@@ -662,6 +663,7 @@ extern "C" int toep_assemble_level1(const void* stacked4, int n2, int n1, int n0
 }
 
 extern "C" int toep_lu_factor(void* a, int n, int* ipiv, int* info, void* stream) {
+  TOEP_NVTX("toep_lu_factor");
   TOEP_REQUIRE(a != nullptr && ipiv != nullptr && info != nullptr && n >= 1, TOEP_ERR_ARG, "bad lu_factor args");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return getrf(static_cast<double2*>(a), n, ipiv, info, s);
@@ -675,6 +677,7 @@ extern "C" int toep_lu_solve(const void* lu, int n, const int* ipiv, void* b, in
 
 extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v, void* x_v, int64_t w,
                             int* fail_step, toep_stage_fn hook, void* hook_ctx, void* stream) {
+  TOEP_NVTX("toep_rybicki");
   TOEP_REQUIRE(blocks_v != nullptr && y_v != nullptr && x_v != nullptr && N >= 1 && s >= 1 && w >= 1, TOEP_ERR_ARG,
                "bad rybicki arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
