@@ -452,7 +452,7 @@ def run_ours(args):
     # pinned blocks at 17-19 GB/s on these boxes, cudaHostAlloc blocks at 50 GB/s (tools/hostbuf_probe.py)
     u_host = pin(dense_rhs(DIM, seed=1)[:, None])
     out_host = pinned_empty(u_host.shape, u_host.dtype)
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 50)):  # host path warm-up: page-locked blocks, driver state
         matvec(spec, u_host, out=out_host)
     torch.cuda.synchronize()
     barrier()
@@ -559,6 +559,7 @@ def run_ours(args):
                 "path": "toeplitz.matvec(op, pinned CPU tensor, out=pinned CPU tensor): one library call per "
                         "step (H2D copy, matvec, D2H copy, synchronise)",
                 "per_call_us_min": float(pc.min()), "per_call_us_median": float(np.median(pc)),
+                "per_call_us_p90": float(np.percentile(pc, 90)),
                 "numpy": {"value": np_value, "unit": UNIT,
                           "path": "toeplitz.matvec(op, numpy array) -> numpy array (the reference's calling "
                                   "convention; staged through a library page-locked block)",

@@ -52,6 +52,10 @@ extern "C" {
 #define TOEP_MV_TRANSPOSE 1   /* matvec_transpose (toeplitz.py:306-324)                */
 #define TOEP_MV_IO_C128 2     /* c64 operator, but u / v are complex128 (cast in the   */
                               /* first / last FFT pass; the GMRES Krylov space is c128) */
+#define TOEP_MV_STAGE_INPUT 4 /* toep_matvec_host: u_host is pageable (e.g. a numpy      */
+                              /* array): the library's copy threads stage it through a  */
+                              /* page-locked buffer in chunks, each chunk's DMA issued  */
+                              /* as soon as it is staged (copies overlap the transfer)  */
 
 typedef struct toep_op_s* toep_op_t;
 

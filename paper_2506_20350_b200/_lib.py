@@ -33,6 +33,7 @@ TOEP_C64 = 1
 
 TOEP_MV_TRANSPOSE = 1
 TOEP_MV_IO_C128 = 2
+TOEP_MV_STAGE_INPUT = 4
 
 TOEP_PC_NONE = 0
 TOEP_PC_BLOCK = 1

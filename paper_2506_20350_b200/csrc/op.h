@@ -23,6 +23,8 @@ struct toep_op_s {
     size_t p_bytes = 0;       // capacity of hatp / hat2p in bytes (the chunking depends on w)
     void* io = nullptr;  // toep_matvec_host: device copies of u and v
     size_t io_cap = 0;
+    void* pin_in = nullptr;  // toep_matvec_host + TOEP_MV_STAGE_INPUT: page-locked staging of u
+    size_t pin_cap = 0;
     int8_t* oz_b = nullptr;     // Ozaki path: int8 slices of one chunk's U planes
     int32_t* oz_bexp = nullptr; // and their column exponents
     size_t oz_b_bytes = 0, oz_bexp_bytes = 0;  // capacities in bytes
@@ -53,6 +55,12 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
                 const int* stop, cudaStream_t s, const double* in_scale = nullptr);
 
 void keep_pool();
+
+// hostio.cu: copy `bytes` from pageable `src` to page-locked `dst` with the library's copy threads
+// in chunks, enqueueing each chunk's H2D copy (dst -> dev) on `s` as soon as it is staged
+int staged_h2d(const void* src, void* dst_pinned, void* dev, size_t bytes, cudaStream_t s);
+// keep the copy threads spinning for `us` microseconds (host-path calls: see hostio.cu)
+void keep_host_threads_warm(int us);
 
 // the local stages of the slab-decomposed matvec (toep_matvec_stage / toep_matvec_stage_peer)
 int matvec_stage_impl(toep_op_s* op, int stage, const void* in, void* out, int64_t w, int count,

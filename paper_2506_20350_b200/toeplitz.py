@@ -28,6 +28,7 @@ import torch
 
 from . import _lib
 from ._tensor import restore, to_columns
+from . import hostmem as _hostmem
 from .hostmem import pin, pinned_empty, pinned_view  # noqa: F401 - public: host vectors for the host-in/out calls
 from .errors import BlockShapeMismatch, MissingOffset, ShapeError
 
@@ -295,8 +296,11 @@ def precompute_spectral_stacked(stacked4, dtype=torch.complex128, embedding=None
 
 
 def _pinned_ok(op: SpectralOperator, t: torch.Tensor) -> bool:
-    return (not t.is_cuda and t.is_pinned() and t.ndim in (1, 2) and t.is_contiguous() and not t.is_conj()
-            and not t.is_neg() and (t.dtype == op.dtype or t.dtype == torch.complex128))
+    if t.is_cuda or t.ndim not in (1, 2) or not (t.dtype == op.dtype or t.dtype == torch.complex128):
+        return False
+    if not (t.is_contiguous() and not t.is_conj() and not t.is_neg()):
+        return False
+    return _hostmem.is_library_block(t) or t.is_pinned()
 
 
 def _apply(op: SpectralOperator, u, flags: int, out=None):
@@ -343,11 +347,11 @@ def _apply_pinned(op: SpectralOperator, u: torch.Tensor, flags: int, out=None):
 
 
 def _apply_numpy(op: SpectralOperator, u: np.ndarray, flags: int):
-    """The reference's numpy-in / numpy-out call (toeplitz.py:287-303).  The vector is staged once
-    into a library page-locked block (the copy engines read pageable memory through the driver's
-    own bounce buffers at a fraction of the PCIe rate), applied with ``toep_matvec_host``, and the
-    result is returned as a numpy array backed by a page-locked block (released to the block cache
-    when the array dies).  A numpy array that already lives in such a block (a previous result) is
+    """The reference's numpy-in / numpy-out call (toeplitz.py:287-303).  The array is handed to
+    ``toep_matvec_host`` as is (``TOEP_MV_STAGE_INPUT``: the library's copy threads stage it into
+    page-locked memory in chunks, each chunk's DMA issued as soon as it is staged), and the result is
+    returned as a numpy array backed by a library page-locked block (released to the block cache when
+    the array dies).  A numpy array that already lives in such a block (a previous result) is
     passed through without staging."""
     want = np.complex64 if (op.dtype == torch.complex64 and u.dtype == np.complex64) else np.complex128
     if u.dtype != want or not u.flags.c_contiguous:
@@ -355,11 +359,17 @@ def _apply_numpy(op: SpectralOperator, u: np.ndarray, flags: int):
     if u.shape[0] != op.dim:
         raise ShapeError(f"rows {u.shape[0]} != operator dim {op.dim}")
     t = pinned_view(u)
-    if t is None:
-        t = pinned_empty(u.shape, torch.from_numpy(u[:0]).dtype)
-        if u.size:
-            t.numpy()[...] = u
-    return _apply_pinned(op, t, flags).numpy()
+    if t is not None:
+        return _apply_pinned(op, t, flags).numpy()
+    _lib.require_cuda()
+    w = 1 if u.ndim == 1 else u.shape[1]
+    if op.dtype == torch.complex64 and u.dtype == np.complex128:
+        flags |= _lib.TOEP_MV_IO_C128
+    out = pinned_empty(u.shape, torch.from_numpy(u[:0]).dtype)
+    if w:
+        _lib.check(_lib.lib().toep_matvec_host(op.handle, u.__array_interface__["data"][0], out.data_ptr(), w,
+                                               flags | _lib.TOEP_MV_STAGE_INPUT, _lib.stream_handle()), "matvec")
+    return out.numpy()
 
 
 def matvec(op: SpectralOperator, u, out=None):
