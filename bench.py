@@ -411,7 +411,9 @@ def run_ours(args):
     sampler = ClockSampler(local)
     sampler.start()
 
-    # ---- device-resident matvecs (value)
+    # ---- device-resident matvecs (value).  Exactly W warm-up steps: a longer warm-up (0.5 s of
+    # matvecs) measured slower, not faster -- the sustained HBM stream brings the board to its power
+    # cap (sw_power_cap, SM clock 1 905-1 920 MHz: 6 255 vs 6 350-6 480 matvec/s at 20 steps)
     for _ in range(args.warmup):
         v = matvec(spec, u)
     torch.cuda.synchronize()

@@ -676,7 +676,6 @@ int toep_matvec_host(toep_op_t op, const void* u_host, void* v_host, int64_t w, 
   TOEP_REQUIRE(w == 0 || u_host != v_host, TOEP_ERR_ARG, "matvec output must not alias its input");
   if (w == 0) return TOEP_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  toep::keep_host_threads_warm(2000);
   const bool io_c128 = (flags & TOEP_MV_IO_C128) != 0;
   const size_t bytes = static_cast<size_t>(toep::op_dim(op)) * w * (io_c128 ? 16 : toep::elt_size(op->dtype));
   toep_op_s::Workspace* ws = nullptr;
