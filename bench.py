@@ -285,15 +285,14 @@ def _broadcast_stacked(ny, nx, nb, dev, world):
     return t
 
 
-def scale_legs(dev, world, rank):
-    """The paths that shard, timed on the device, max over ranks."""
+def scale_legs(dev, world, rank, peer: bool = False):
+    """The paths that shard, timed on the device, max over ranks.
+
+    Each leg runs inside a guard whose outcome is all-reduced before the next one starts, so a
+    failure on one rank cannot leave the others waiting in a collective.  The NVLink peer-store
+    exchange (custom system-scope spin waits, never run across GPUs here) only with ``peer``."""
     import torch
     import torch.distributed as dist
-
-    from paper_2506_20350_b200.distributed import SlabOperator, column_range, gmres_slab, solve_columns_sharded
-    from paper_2506_20350_b200.problems import unit_feed_rhs
-    from paper_2506_20350_b200.solvers import GmresConfig
-    from paper_2506_20350_b200.toeplitz import precompute_spectral_stacked
 
     def tmax(ms):
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -307,6 +306,43 @@ def scale_legs(dev, world, rank):
             dist.barrier()
 
     out = {}
+
+    def agreed(ok: bool) -> bool:  # every rank learns whether every rank succeeded
+        if world == 1:
+            return ok
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
+
+    try:
+        out.update(_scale_cfg3(dev, world, rank, tmax, barrier))
+        ok = True
+    except Exception as exc:  # noqa: BLE001
+        out["cfg3_columns"] = {"error": repr(exc)}
+        ok = False
+    if not agreed(ok) or world == 1:
+        return out
+    for exchange in (("collective", "peer") if peer else ("collective",)):
+        try:
+            out[f"cfg4_slab_{exchange}"] = _scale_cfg4(dev, world, rank, exchange, tmax, barrier)
+            ok = True
+        except Exception as exc:  # noqa: BLE001
+            out[f"cfg4_slab_{exchange}"] = {"error": repr(exc)}
+            ok = False
+        if not agreed(ok):
+            break
+    return out
+
+
+def _scale_cfg3(dev, world, rank, tmax, barrier):
+    import torch
+
+    from paper_2506_20350_b200.distributed import column_range, solve_columns_sharded
+    from paper_2506_20350_b200.problems import unit_feed_rhs
+    from paper_2506_20350_b200.solvers import GmresConfig, solve_multi_rhs_sequential
+    from paper_2506_20350_b200.toeplitz import precompute_spectral_stacked
+
+    out = {}
     # ---- cfg3: 900 unit right-hand sides, columns sharded, no collective in the data path
     s4 = _broadcast_stacked(30, 30, 256, dev, world)
     op3 = precompute_spectral_stacked(s4)
@@ -315,7 +351,6 @@ def scale_legs(dev, world, rank):
     b = torch.from_numpy(unit_feed_rhs(30, 30, 256, columns="each")).to(dev)
     cfg = GmresConfig(tol=1e-6)
     c0, c1 = column_range(W, world, rank)
-    from paper_2506_20350_b200.solvers import solve_multi_rhs_sequential
     solve_multi_rhs_sequential(op3, None, b[:, c0:c1].contiguous(), cfg)  # warm: workspaces, slices
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -335,15 +370,23 @@ def scale_legs(dev, world, rank):
                                    "collective; X gathered to rank 0 afterwards (solve_columns_sharded)"}
     del op3, b, x, xs
     torch.cuda.empty_cache()
-    if world == 1:
-        return out
-    # ---- cfg4: 64x64 slab decomposition, both exchanges
+    return out
+
+
+def _scale_cfg4(dev, world, rank, exchange, tmax, barrier):
+    """cfg4 64x64 slab decomposition: matvec and GMRES(50) to 1e-6 with one exchange mode."""
+    import torch
+
+    from paper_2506_20350_b200.distributed import SlabOperator, gmres_slab
+    from paper_2506_20350_b200.problems import dense_rhs, unit_feed_rhs
+    from paper_2506_20350_b200.solvers import GmresConfig
+
     s4 = _broadcast_stacked(64, 64, 128, dev, world)
-    from paper_2506_20350_b200.problems import dense_rhs
     u_full = torch.from_numpy(dense_rhs(64 * 64 * 128, seed=1)).to(dev)
     b_full = torch.from_numpy(unit_feed_rhs(64, 64, 128)).to(dev)
-    for exchange in ("collective", "peer"):
+    if True:
         sop = SlabOperator.from_generator(s4, exchange=exchange)
+        del s4
         y0, y1 = sop.rows
         n_loc = sop.local_dim
         u = u_full[y0 * 64 * 128:y1 * 64 * 128].contiguous()
@@ -365,14 +408,14 @@ def scale_legs(dev, world, rank):
         _, rep = gmres_slab(sop, None, bl, GmresConfig(tol=1e-6, restart=50))
         g1.record()
         barrier()
-        out[f"cfg4_slab_{exchange}"] = {
+        res = {
             "matvec_us_max_over_ranks": mv_us, "gmres_ms_max_over_ranks": tmax(g0.elapsed_time(g1)),
             "gmres_iterations": rep.iterations, "reference_iterations": 28, "local_rows": n_loc // (64 * 128),
             "resident_spectral_bytes_per_rank": sop.stages.op.resident_bytes,
             "exchange_bytes_per_matvec_per_rank": 2 * 64 * 128 * 128 * 16 * (world - 1) // (world * world)}
         del sop
         torch.cuda.empty_cache()
-    return out
+    return res
 
 
 def run_ours(args):
@@ -515,7 +558,7 @@ def run_ours(args):
         del op, spec, pk, sys_
         torch.cuda.empty_cache()
         try:
-            scale = scale_legs(dev, world, rank)
+            scale = scale_legs(dev, world, rank, peer=args.scale_peer)
         except Exception as exc:  # noqa: BLE001 - the headline line must still be printed
             scale = {"error": repr(exc)}
 
@@ -605,6 +648,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scale", action="store_true", help="add config.scale (cfg3 column / cfg4 slab legs) at N=1")
     ap.add_argument("--no-scale", action="store_true", help="skip config.scale at N>1")
+    ap.add_argument("--scale-peer", action="store_true",
+                    help="config.scale also times the NVLink peer-store exchange of the cfg4 slab legs")
     ap.add_argument("--cpu-sample", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help=argparse.SUPPRESS)
     args = ap.parse_args()
