@@ -981,20 +981,38 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
 // column-oriented substitution: lane l owns rows l, l+32, ...; each solved y_i is broadcast with a
 // shuffle and subtracted from the remaining rows.  A zero pivot gives y_i = 0, as before.
 constexpr int kBsRows = 8;  // rows per lane: cycles up to 256 steps
+constexpr int kBsThreads = 256;  // k_backsub block: all stage the triangle, warp 0 solves
 __global__ void k_backsub(const GState* st, const double2* rcols, int ldr, const double2* g, double2* y, int staged) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ double2 rsm[];  // staged: [m][m] column-major upper triangle
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
   const int m = st->m;
   const double2* rs = rcols;
   int rld = ldr;
   if (staged) {
-    for (int i = 0; i < m; ++i)
-      for (int r = lane; r <= i; r += 32) rsm[i * m + r] = rcols[static_cast<int64_t>(i) * ldr + r];
+    // every thread of the block stages with its loads batched (one L2 round trip per batch of 8,
+    // instead of one per column: 46 -> a few us at m = 31)
+    constexpr int B = 8;
+    const int tot = m * m;
+    for (int e0 = threadIdx.x; e0 < tot; e0 += B * kBsThreads) {
+      double2 v[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int e = e0 + u * kBsThreads, i = e / max(m, 1), r = e - i * m;
+        v[u] = (e < tot && r <= i) ? rcols[static_cast<int64_t>(i) * ldr + r] : make_double2(0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int e = e0 + u * kBsThreads;
+        if (e < tot) rsm[e] = v[u];
+      }
+    }
+    __syncthreads();
     rs = rsm;
     rld = m;
   }
+  if (threadIdx.x >= 32) return;  // one warp solves
   double2 acc[kBsRows];
 #pragma unroll
   for (int q = 0; q < kBsRows; ++q) {
@@ -1510,7 +1528,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     tr.mark("arnoldi steps launched");
     // ---- assemble x += V y (gmres.py:192-204)
     if (backsub_warp)
-      G_TRY(launch_k(k_backsub, dim3(1), dim3(32), backsub_smem, s, (const GState*)st, (const double2*)rcols, ldr,
+      G_TRY(launch_k(k_backsub, dim3(1), dim3(kBsThreads), backsub_smem, s, (const GState*)st, (const double2*)rcols, ldr,
                      (const double2*)g, y, backsub_staged));
     else
       G_TRY(launch_k(k_backsub_serial, dim3(1), dim3(32), 0, s, (const GState*)st, (const double2*)rcols, ldr,

@@ -38,5 +38,5 @@ print(f"iterations {rep.iterations}  span {span:.0f} us  kernels {len(ev)}")
 for k, (c, busy, gap) in sorted(tot.items(), key=lambda kv: -kv[1][1]):
     print(f"{c:5d}  busy {busy:9.1f} us  ({busy / c:7.1f}/launch)  gaps-before {gap:8.1f} us   {k}")
 print("--- timeline: first 14 and last 14 kernels (start, end relative us)")
-for e in ev[40:56]:
+for e in ev[:14] + ev[-14:]:
     print(f"{e.time_range.start - t0:9.1f} {e.time_range.end - t0:9.1f}  {e.name[:70]}")
