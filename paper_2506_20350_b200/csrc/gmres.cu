@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
   if (a.ts != nullptr && blockIdx.x == 0 && threadIdx.x == 0) a.ts[2 * a.st->total + 2] = global_ns();
   if (threadIdx.x >= kCoopThreads - 32) l2_prefetch_heads(a.pf, blockIdx.x, gridDim.x, threadIdx.x & 31);
 #ifdef TOEP_ORTH_PROBE
-  long long pt[8];
+  long long pt[12];
   int np = 0;
 #define OPROBE() \
   if (blockIdx.x == (gridDim.x > 1 ? 1 : 0) && threadIdx.x == 0) pt[np++] = global_ns()
@@ -825,14 +825,22 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
     double2* h1s = osm + 4 * a.ldr;
     double2* gcol = osm + 5 * a.ldr;
     double2* gh = osm + 6 * a.ldr;
-    // ||w||^2 partials: issued now, consumed by the norm below (one round trip for everything)
-    double wnq[5];
-    if (threadIdx.x < 32) {
+    // ||w||^2 partials: the last warp sums them now (their L2 round trip overlaps the partials'
+    // loads of the other warps); the norm below reads the total from shared memory
+    __shared__ double wn_s, hn2_g;
+    if (warp == kCoopThreads / 32 - 1) {
+      double wn = 0.0;
+      if (nblk <= 160) {
+        double q[5];
 #pragma unroll
-      for (int j = 0; j < 5; ++j) {
-        const int b = static_cast<int>(threadIdx.x) + 32 * j;
-        wnq[j] = b < nblk ? __ldcg(a.npart + b) : 0.0;
+        for (int j = 0; j < 5; ++j) q[j] = lane + 32 * j < nblk ? __ldcg(a.npart + lane + 32 * j) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) wn += q[j];
+      } else {
+        for (int b = lane; b < nblk; b += 32) wn += __ldcg(a.npart + b);
       }
+      wn = warp_sum(wn);
+      if (lane == 0) wn_s = wn;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
@@ -880,6 +888,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
       }
     }
     __syncthreads();
+    OPROBE();
     auto G = [&](int l, int k) -> double2 {  // G[l][k], Hermitian; column m-1 from this step
       if (k == m - 1) return gcol[l];
       if (l == m - 1) return make_double2(gcol[k].x, -gcol[k].y);
@@ -897,6 +906,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
       }
     }
     __syncthreads();
+    OPROBE();
     // (G h)_l, then ||w''||^2 = ||w||^2 - 2 Re(h^H h1) + h^H G h -- every CTA evaluates it (same
     // data, same order), so the precision test below is uniform across the grid
     for (int l = warp; l < m; l += kCoopThreads / 32) {
@@ -905,27 +915,17 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
       t = warp_sum(t);
       if (lane == 0) gh[l] = t;
     }
-    __shared__ double wn_s, hn2_g;
     __syncthreads();
+    OPROBE();
     if (threadIdx.x < 32) {
-      double wn = 0.0;
-      if (nblk <= 160) {
-#pragma unroll
-        for (int j = 0; j < 5; ++j) wn += wnq[j];
-      } else {
-        for (int b = threadIdx.x; b < nblk; b += 32) wn += __ldcg(a.npart + b);
-      }
       double t = 0.0;
       for (int l = threadIdx.x; l < m; l += 32)
         t += -2.0 * (hsm[l].x * h1s[l].x + hsm[l].y * h1s[l].y) + (hsm[l].x * gh[l].x + hsm[l].y * gh[l].y);
-      wn = warp_sum(wn);
       t = warp_sum(t);
-      if (threadIdx.x == 0) {
-        wn_s = wn;
-        hn2_g = wn + t;
-      }
+      if (threadIdx.x == 0) hn2_g = wn_s + t;
     }
     __syncthreads();
+    OPROBE();
     // below ~1e-13 of ||w||^2 the formula is cancellation noise (e.g. a lucky breakdown): measure
     // ||w''|| directly instead (third sweep + barrier)
     const bool direct = !(hn2_g > 1e-13 * wn_s);
@@ -948,8 +948,9 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
       __syncthreads();
       OPROBE();
       if (blockIdx.x == 1 && threadIdx.x == 0 && (a.m == 8 || a.m == 16 || a.m == 24 || a.m == 31))
-        printf("orth-gram m=%d: dots %lld bar %lld coef+norm %lld upd %lld ns\n", a.m, pt[1] - pt[0], pt[2] - pt[1],
-               pt[3] - pt[2], pt[4] - pt[3]);
+        printf("orth-gram m=%d: dots %lld bar %lld partials %lld Gh1 %lld Gh %lld norm %lld ->upd %lld upd %lld ns\n",
+               a.m, pt[1] - pt[0], pt[2] - pt[1], pt[3] - pt[2], pt[4] - pt[3], pt[5] - pt[4], pt[6] - pt[5],
+               pt[7] - pt[6], pt[8] - pt[7]);
 #endif
       return;
     }
