@@ -46,9 +46,11 @@ extern "C" int toep_host_free(void* p) {
 // A pageable buffer (a numpy array) cannot be read by the copy engines directly: the driver
 // bounces it through its own pinned buffers (1.84 MB in 115-140 us on the B200 boxes against 45 us
 // from page-locked memory, tools/hoststage_probe.cu).  Here the library's copy threads memcpy it
-// into a page-locked staging buffer in parallel slices (5 threads: 1.84 MB in ~10 us), then one DMA.  The workers spin for up to 2 ms after a job (back-to-back calls
-// find them awake; a condition-variable wake-up costs tens of microseconds), then sleep.
+// into a page-locked staging buffer in parallel slices (5 threads: 1.84 MB in ~10 us, non-temporal
+// stores), then one DMA.  The workers spin for up to 2 ms after a job (back-to-back calls find them
+// awake; a condition-variable wake-up costs tens of microseconds), then sleep.
 #include <immintrin.h>
+#include <unistd.h>
 
 #include <atomic>
 #include <chrono>
@@ -64,28 +66,23 @@ namespace {
 class CopyPool {
  public:
   static constexpr int kWorkers = 4;
+  // never destroyed: the workers live as long as the process (a destructor would have to join them
+  // at exit, and a forked child holds thread handles that are not its own)
   static CopyPool& get() {
-    static CopyPool pool;
-    return pool;
-  }
-  // keep the workers awake (spinning) until now + `us` microseconds; wakes sleeping ones without
-  // waiting for them (the host-path calls keep a busy core set around their PCIe transfers: on the
-  // B200 VMs an idle host measurably delays the call's completion, 280-306 vs 257-287 us per cfg2 call)
-  void keep_warm(int us) {
-    const int64_t until = now_ns() + int64_t{us} * 1000;
-    int64_t cur = warm_until_.load(std::memory_order_relaxed);
-    while (cur < until && !warm_until_.compare_exchange_weak(cur, until, std::memory_order_relaxed)) {
-    }
-    if (sleepers_.load(std::memory_order_relaxed) > 0) {
-      {
-        std::lock_guard<std::mutex> lk(mu_);
-      }
-      cv_.notify_all();
-    }
+    static CopyPool* pool = new CopyPool();
+    return *pool;
   }
   // chunk c of [0, n) is copied by participant c % (kWorkers + 1) (0 = the caller); on_ready(c) runs
   // on the caller, in chunk order, once chunks 0..c are staged.  Returns on_ready's first error.
   int run(int n, const std::function<void(int)>& job, const std::function<int(int)>& on_ready) {
+    if (getpid() != pid_) {  // a forked child inherits no threads: copy on the caller alone
+      int rc = TOEP_OK;
+      for (int c = 0; c < n; ++c) {
+        job(c);
+        if (rc == TOEP_OK) rc = on_ready(c);
+      }
+      return rc;
+    }
     std::lock_guard<std::mutex> run_lock(run_mu_);  // one staged copy at a time
     std::vector<std::atomic<int>> done(static_cast<size_t>(n));
     for (auto& d : done) d.store(0, std::memory_order_relaxed);
@@ -122,16 +119,8 @@ class CopyPool {
   struct alignas(64) Slot {
     std::atomic<uint64_t> v{0};
   };
-  CopyPool() {
+  CopyPool() : pid_(getpid()) {
     for (int i = 0; i < kWorkers; ++i) threads_.emplace_back([this, i] { loop(i); });
-  }
-  ~CopyPool() {
-    stop_.store(true);
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-    }
-    cv_.notify_all();
-    for (auto& t : threads_) t.join();
   }
   static int64_t now_ns() {
     return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
@@ -146,19 +135,11 @@ class CopyPool {
         if (stop_.load(std::memory_order_acquire)) return;
         g = gen_.load(std::memory_order_acquire);
         if (g != seen) break;
-        if ((spins & 1023u) == 0) {
-          const int64_t t = now_ns();
-          if (t - t0 > 2000000 && t > warm_until_.load(std::memory_order_relaxed)) {
-            std::unique_lock<std::mutex> lk(mu_);
-            sleepers_.fetch_add(1, std::memory_order_relaxed);
-            cv_.wait(lk, [&] {
-              return stop_.load() || gen_.load(std::memory_order_acquire) != seen ||
-                     warm_until_.load(std::memory_order_relaxed) > now_ns();
-            });
-            sleepers_.fetch_sub(1, std::memory_order_relaxed);
-            t0 = now_ns();
-            continue;
-          }
+        if ((spins & 1023u) == 0 && now_ns() - t0 > 2000000) {
+          std::unique_lock<std::mutex> lk(mu_);
+          cv_.wait(lk, [&] { return stop_.load() || gen_.load(std::memory_order_acquire) != seen; });
+          t0 = now_ns();
+          continue;
         }
         _mm_pause();
       }
@@ -178,9 +159,8 @@ class CopyPool {
   std::atomic<int>* done_ = nullptr;
   int n_ = 0;
   std::atomic<uint64_t> gen_{0};
-  std::atomic<bool> stop_{false};
-  std::atomic<int64_t> warm_until_{0};
-  std::atomic<int> sleepers_{0};
+  std::atomic<bool> stop_{false};  // (never set: the pool lives for the whole process)
+  pid_t pid_;
   Slot finished_[kWorkers];
 };
 
@@ -206,8 +186,6 @@ void stream_copy(char* dst, const char* src, size_t n) {
   }
   if (i < n) std::memcpy(dst + i, src + i, n - i);
 }
-
-void keep_host_threads_warm(int us) { CopyPool::get().keep_warm(us); }
 
 int staged_h2d(const void* src, void* dst_pinned, void* dev, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return TOEP_OK;

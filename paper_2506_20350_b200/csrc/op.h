@@ -59,8 +59,7 @@ void keep_pool();
 // hostio.cu: copy `bytes` from pageable `src` to page-locked `dst` with the library's copy threads
 // in chunks, enqueueing each chunk's H2D copy (dst -> dev) on `s` as soon as it is staged
 int staged_h2d(const void* src, void* dst_pinned, void* dev, size_t bytes, cudaStream_t s);
-// keep the copy threads spinning for `us` microseconds (host-path calls: see hostio.cu)
-void keep_host_threads_warm(int us);
+
 
 // the local stages of the slab-decomposed matvec (toep_matvec_stage / toep_matvec_stage_peer)
 int matvec_stage_impl(toep_op_s* op, int stage, const void* in, void* out, int64_t w, int count,

@@ -257,6 +257,32 @@ def test_cfg3_int8_products_at_baseline_shape(cfg3_operator):
         assert rel_err(v900[:, c].cpu().numpy(), single) <= 1e-12
 
 
+@pytest.mark.parametrize("dtype", [torch.complex128, torch.complex64])
+def test_numpy_staged_host_path(dtype):
+    # numpy in -> numpy out through toep_matvec_host with library-staged input (TOEP_MV_STAGE_INPUT):
+    # vectors and column blocks, transpose, c64 operator with c128 / c64 arrays, non-contiguous input
+    gen = generator_from_stacked(seeded_stacked4(7, 6, 24, seed=8))
+    op = precompute_spectral(gen, dtype=dtype)
+    tol = 1e-12 if dtype == torch.complex128 else 1e-5
+    for w in (1, 3):
+        u = dense_rhs(gen.dim, w, seed=9)
+        u = u[:, 0] if w == 1 else u
+        for fn in (matvec, matvec_transpose):
+            want = fn(op, torch.from_numpy(np.ascontiguousarray(u)).cuda()).cpu().numpy()
+            got = fn(op, u)
+            assert isinstance(got, np.ndarray) and got.shape == u.shape
+            assert rel_err(got, want) <= tol
+    ub = dense_rhs(gen.dim, 4, seed=10)
+    strided = ub[:, ::2]  # not C-contiguous: copied once, then staged
+    want = matvec(op, torch.from_numpy(np.ascontiguousarray(strided)).cuda()).cpu().numpy()
+    assert rel_err(matvec(op, strided), want) <= tol
+    if dtype == torch.complex64:
+        u32 = dense_rhs(gen.dim, seed=11).astype(np.complex64)
+        want = matvec(op, torch.from_numpy(u32).cuda()).cpu().numpy()
+        got = matvec(op, u32)
+        assert got.dtype == np.complex64 and rel_err(got, want) <= 1e-6
+
+
 def test_pinned_out_and_empty_and_numpy_passthrough():
     from paper_2506_20350_b200.toeplitz import pinned_empty, pin
     gen = generator_from_stacked(seeded_stacked4(5, 4, 8, seed=3))
