@@ -534,21 +534,20 @@ struct Fft2dSmem {
   static size_t bytes(int n2) { return sizeof(C<TC>) * (PX::L + PY::L + 2 * kBuf + static_cast<size_t>(n2) * kGs); }
 };
 
+// The 2-D transform of batch column `b`, shared-memory workspace at `smem_raw`.  Every thread of the
+// block calls it (threads >= k2dThreads only take part in the barriers).  With `wait` the PDL
+// wait / stop check happens inside (after the twiddles); returns false when the stop flag is set.
 template <typename TI, typename TC, typename TO, int TILX, int TILY, typename PX, typename PY, bool INV>
-__global__ void __launch_bounds__(k2dThreads, 1) fft2d_kernel(Fft2dArgs f) {
+__device__ __forceinline__ bool fft2d_body(const Fft2dArgs& f, unsigned char* smem_raw, int64_t b, bool wait) {
   using Z = C<TC>;
   using S = Fft2dSmem<TC, TILX, TILY, PX, PY>;
   constexpr int L1 = PX::L, L2 = PY::L;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   Z* twx = reinterpret_cast<Z*>(smem_raw);
   Z* twy = twx + L1;
   Z* b0 = twy + L2;
   Z* b1 = b0 + S::kBuf;
   Z* G = b1 + S::kBuf;  // [n2][kGs]
   constexpr int Gs = S::kGs;
-  pdl_trigger();
-  if (threadIdx.x < 32)  // constant operator data: no dependency to wait for
-    l2_prefetch_heads(f.pf, blockIdx.x, gridDim.x, threadIdx.x);
   for (int t = threadIdx.x; t < L1 + L2; t += k2dThreads) {
     const int L = t < L1 ? L1 : L2;
     const int tt = t < L1 ? t : t - L1;
@@ -556,10 +555,11 @@ __global__ void __launch_bounds__(k2dThreads, 1) fft2d_kernel(Fft2dArgs f) {
     sincospi_t<TC>(static_cast<TC>(2.0 * tt / L), &s, &c);
     (t < L1 ? twx[tt] : twy[tt]) = mk<TC>(c, f.sign * s);
   }
-  pdl_wait();
-  if (f.stop != nullptr && *f.stop != 0) return;
+  if (wait) {
+    pdl_wait();
+    if (f.stop != nullptr && *f.stop != 0) return false;
+  }
   __syncthreads();
-  const int64_t b = blockIdx.x;
   const int64_t inner = f.inner;
   const int n2 = f.n2, n1 = f.n1;
   // each level runs over its columns in tiles of TILX (level 1: array rows y) / TILY (level 2:
@@ -603,6 +603,16 @@ __global__ void __launch_bounds__(k2dThreads, 1) fft2d_kernel(Fft2dArgs f) {
                                                      static_cast<TC>(1.0 / (static_cast<double>(L1) * L2)));
     }
   }
+  return true;
+}
+
+template <typename TI, typename TC, typename TO, int TILX, int TILY, typename PX, typename PY, bool INV>
+__global__ void __launch_bounds__(k2dThreads, 1) fft2d_kernel(Fft2dArgs f) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  pdl_trigger();
+  if (threadIdx.x < 32)  // constant operator data: no dependency to wait for
+    l2_prefetch_heads(f.pf, blockIdx.x, gridDim.x, threadIdx.x);
+  fft2d_body<TI, TC, TO, TILX, TILY, PX, PY, INV>(f, smem_raw, blockIdx.x, true);
 }
 
 template <typename TI, typename TC, typename TO, int TILX, int TILY, typename PX, typename PY>
@@ -615,6 +625,236 @@ int launch2d(bool inverse, const Fft2dArgs& f, cudaStream_t s) {
   auto k = inverse ? ki : kf;
   TOEP_CUDA(ensure_smem(k, smem));
   return launch_k(k, dim3(static_cast<unsigned>(f.inner)), dim3(k2dThreads), smem, s, f);
+}
+
+// ------------------------------------------------------------------------------------------
+// Fused single-RHS matvec for N_b = 128 on the 60 x 60 grid (cfg2): forward 2-D DFT -> per-bin
+// product D_k u_k -> inverse 2-D DFT in ONE cooperative launch (148 CTAs, one per SM), phases
+// separated by grid barriers.  The operator blocks do not depend on the vector, so the product's
+// bulk-copy ring is filled while the forward DFT computes (3 stages of 32 KB per SM, plus the L2
+// prefetch of every CTA's first bins): the DFT runs under the HBM stream instead of in front of it.
+// In the product phase the ring grows to 6 stages (the DFT's shared memory is free by then).
+// Warps 0-15 run the DFTs; warps 0-7 consume and warp 16 produces in the product phase, exactly
+// as binprod_tma_kernel (csrc/binprod.cu): a bin's 128 x 128 block streams in 8 whole-row stages.
+#ifndef TOEP_FUSED_PF_MB
+#define TOEP_FUSED_PF_MB 48  // L2 prefetch of the first bins in hand-out order
+#endif
+constexpr int kFusedThreads = k2dThreads + 32;
+constexpr int kFusedN0 = 128;
+constexpr int kFusedRB = 16;                                 // rows per 32 KB stage
+constexpr int kFusedStageElems = kFusedRB * kFusedN0;
+constexpr int kFusedStages = 6;                              // 3 in the ring region + 3 in the DFT region
+constexpr int kFusedEarly = 3;                               // stages filled during the forward DFT
+constexpr int kFusedConsumers = 8;
+using FusedPX = Plan<4, 3, 5>;
+using FusedPY = Plan<4, 3, 5>;
+constexpr int kFusedTILX = 32, kFusedTILY = 32;
+using FusedSmem = Fft2dSmem<double, kFusedTILX, kFusedTILY, FusedPX, FusedPY>;
+
+struct FusedArgs {
+  Fft2dArgs fwd, inv;
+  const double2* DT;  // [K][n0][n0], DT[k][j][m] = D_k[m][j]
+  double2* hat;       // [K][n0] forward DFT output
+  double2* hat2;      // [K][n0] product output
+  int64_t K;
+  unsigned* bar;      // grid barrier arrival counter (monotonic, zeroed once)
+  int* work;          // dynamic bin hand-out counter (zero between launches)
+  int64_t pf_bytes;   // L2 prefetch budget of the first bins in hand-out order
+};
+
+__host__ __device__ constexpr size_t fused_dft_bytes(int n2) {
+  return ((sizeof(double2) * (FusedPX::L + FusedPY::L + 2 * (FusedPX::L * kFusedTILX > FusedPY::L * kFusedTILY
+                                                                 ? FusedPX::L * kFusedTILX
+                                                                 : FusedPY::L * kFusedTILY) +
+                              static_cast<size_t>(n2) * (FusedPX::L | 1)) +
+           127) / 128) * 128;
+}
+__host__ __device__ constexpr size_t fused_region0(int n2) {  // DFT workspace / late ring stages
+  return fused_dft_bytes(n2) > sizeof(double2) * 3 * kFusedStageElems ? fused_dft_bytes(n2)
+                                                                      : sizeof(double2) * 3 * kFusedStageElems;
+}
+__host__ __device__ constexpr size_t fused_smem_bytes(int n2) {
+  return fused_region0(n2) + sizeof(double2) * (3 * kFusedStageElems + kFusedN0 + kFusedConsumers * kFusedN0) +
+         2 * kFusedStages * sizeof(uint64_t);
+}
+
+__device__ __forceinline__ void fused_grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    const unsigned target = (old / gridDim.x + 1) * gridDim.x;
+    long long t0 = 0;
+    for (unsigned spins = 1;; ++spins) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (static_cast<int>(v - target) >= 0) break;
+      if ((spins & 1023u) == 0) {  // a CTA that never arrives must not hang the device: trap after 10 s
+        long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t0 == 0) t0 = t;
+        else if (t - t0 > 10000000000ll) __trap();
+      }
+    }
+  }
+  __syncthreads();
+}
+
+#ifdef TOEP_ORTH_PROBE
+__device__ unsigned g_fused_calls;
+#define FPROBE(i) \
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fpt[i]))
+#else
+#define FPROBE(i)
+#endif
+
+__global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a) {
+  using Z = double2;
+#ifdef TOEP_ORTH_PROBE
+  long long fpt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+  FPROBE(0);
+  extern __shared__ __align__(128) unsigned char fsm[];
+  const int n2 = a.fwd.n2;
+  unsigned char* region0 = fsm;                                      // DFT workspace, later stages 3..5
+  Z* ring0 = reinterpret_cast<Z*>(fsm + fused_region0(n2));           // stages 0..2
+  Z* us = ring0 + 3 * kFusedStageElems;
+  Z* red = us + kFusedN0;
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + kFusedConsumers * kFusedN0);
+  uint64_t* empty = full + kFusedStages;
+  auto stage_ptr = [&](int st) -> Z* {
+    return st < 3 ? ring0 + st * kFusedStageElems : reinterpret_cast<Z*>(region0) + (st - 3) * kFusedStageElems;
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int nrb = kFusedN0 / kFusedRB;
+  // Bins are handed out dynamically: CTA b starts with bin b (its first stages stream under the
+  // forward DFT), later bins come from a device counter as the CTA's producer needs them, so CTAs
+  // that draw more HBM bandwidth take more bins and the grid finishes together (a static partition
+  // left a ~10 us spread at the closing barrier).  item_of[stage] tells the consumers which bin a
+  // stage belongs to (-1: no more bins).
+  __shared__ int item_of[kFusedStages];
+  const int64_t first = blockIdx.x < a.K ? static_cast<int64_t>(blockIdx.x) : -1;
+  auto issue = [&](int64_t q, int64_t k, uint64_t pol) {
+    const int st = static_cast<int>(q % kFusedStages);
+    const int rb = static_cast<int>(q % nrb);
+    item_of[st] = static_cast<int>(k);
+    mbar_expect_tx(&full[st], static_cast<uint32_t>(sizeof(Z) * kFusedStageElems));
+    bulk_g2s(stage_ptr(st), a.DT + k * kFusedN0 * kFusedN0 + static_cast<int64_t>(rb) * kFusedStageElems,
+             sizeof(Z) * kFusedStageElems, &full[st], pol);
+  };
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kFusedStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kFusedConsumers);
+    }
+    mbar_init_fence();
+  }
+  __syncthreads();
+  // the operator stream starts now: the early stages of the first bin, and the L2 prefetch of the
+  // next bins in hand-out order (bin b + j * grid for this CTA)
+  const int64_t early = first >= 0 ? kFusedEarly : 0;
+  if (threadIdx.x == 0) {
+    const uint64_t pol = policy_evict_first();
+    for (int64_t q = 0; q < early; ++q) issue(q, first, pol);
+  }
+  if (warp == 1) {
+    const int64_t bin_bytes = sizeof(Z) * kFusedN0 * kFusedN0;
+    const int64_t pf_bins = std::min<int64_t>(a.K, a.pf_bytes / bin_bytes);
+    for (int64_t k = blockIdx.x; k < pf_bins; k += gridDim.x)
+      for (int64_t off = lane * 32768; off < bin_bytes; off += 32 * 32768)
+        bulk_prefetch_l2(reinterpret_cast<const char*>(a.DT + k * kFusedN0 * kFusedN0) + off, 32768);
+  }
+  pdl_wait();
+  FPROBE(1);
+  if (a.fwd.stop != nullptr && *a.fwd.stop != 0) {  // uniform across the grid: no barrier is reached
+    if (threadIdx.x == 0)
+      for (int64_t q = 0; q < early; ++q) mbar_wait(&full[q % kFusedStages], 0);  // no copy outlives the CTA
+    return;
+  }
+  // ---- phase 1: forward 2-D DFT of batch column b (CTAs beyond the batch only take the barriers)
+  if (blockIdx.x < a.fwd.inner)
+    fft2d_body<double, double, double, kFusedTILX, kFusedTILY, FusedPX, FusedPY, false>(a.fwd, region0, blockIdx.x,
+                                                                                         false);
+  FPROBE(2);
+  fused_grid_barrier(a.bar);
+  FPROBE(3);
+  // ---- phase 2: per-bin product, bins handed out dynamically
+  if (warp == kFusedThreads / 32 - 1) {  // producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int64_t k = first;
+      for (int64_t q = early;; ++q) {
+        const int st = static_cast<int>(q % kFusedStages);
+        if (q % nrb == 0) {  // next bin
+          if (q > 0 || k < 0) k = gridDim.x + static_cast<int64_t>(atomicAdd(a.work, 1));
+          if (q == 0 && first >= 0) k = first;
+        }
+        if (q >= kFusedStages) mbar_wait(&empty[st], static_cast<uint32_t>(((q / kFusedStages) - 1) & 1));
+        if (k >= a.K) {  // no more bins: wake the consumers on this stage with the end marker
+          item_of[st] = -1;
+          mbar_arrive(&full[st]);
+          break;
+        }
+        issue(q, k, pol);
+      }
+    }
+  } else if (warp < kFusedConsumers) {  // consumers: lane = output row m (4 per lane), warp = row slice
+    constexpr int MPL = kFusedN0 / 32;
+    for (int64_t q = 0;; q += nrb) {
+      const int st0 = static_cast<int>(q % kFusedStages);
+      mbar_wait(&full[st0], static_cast<uint32_t>((q / kFusedStages) & 1));
+      const int it = item_of[st0];
+      if (it < 0) break;
+      for (int t = threadIdx.x; t < kFusedN0; t += kFusedConsumers * 32)
+        us[t] = __ldcg(a.hat + static_cast<int64_t>(it) * kFusedN0 + t);
+      consumers_sync();
+      Z acc[MPL];
+#pragma unroll
+      for (int i = 0; i < MPL; ++i) acc[i] = make_double2(0, 0);
+      for (int rb = 0; rb < nrb; ++rb) {
+        const int64_t qq = q + rb;
+        const int st = static_cast<int>(qq % kFusedStages);
+        if (rb > 0) mbar_wait(&full[st], static_cast<uint32_t>((qq / kFusedStages) & 1));
+        const Z* tile = stage_ptr(st);
+#pragma unroll
+        for (int r = warp; r < kFusedRB; r += kFusedConsumers) {
+          const Z uj = us[rb * kFusedRB + r];
+#pragma unroll
+          for (int i = 0; i < MPL; ++i) cfma(acc[i], tile[r * kFusedN0 + lane + 32 * i], uj);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
+#pragma unroll
+      for (int i = 0; i < MPL; ++i) red[warp * kFusedN0 + lane + 32 * i] = acc[i];
+      consumers_sync();
+      for (int t = threadIdx.x; t < kFusedN0; t += kFusedConsumers * 32) {
+        Z sum = red[t];
+#pragma unroll
+        for (int ww = 1; ww < kFusedConsumers; ++ww) sum = cadd(sum, red[ww * kFusedN0 + t]);
+        a.hat2[static_cast<int64_t>(it) * kFusedN0 + t] = sum;
+      }
+      consumers_sync();
+    }
+  }
+  FPROBE(4);
+  fused_grid_barrier(a.bar);
+  FPROBE(5);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(a.work, 0);  // every CTA is past phase 2
+  // ---- phase 3: inverse 2-D DFT, crop, 1/(l1 l2) of batch column b
+  if (blockIdx.x < a.inv.inner)
+    fft2d_body<double, double, double, kFusedTILX, kFusedTILY, FusedPX, FusedPY, true>(a.inv, region0, blockIdx.x,
+                                                                                        false);
+#ifdef TOEP_ORTH_PROBE
+  FPROBE(6);
+  __shared__ unsigned fcall;
+  if (threadIdx.x == 0 && blockIdx.x == 0) fcall = atomicAdd(&g_fused_calls, 1);
+  __syncthreads();
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 140) && (fcall % 200) == 150)
+    printf("fused cta %d: start->pdl %lld dft %lld bar1 %lld product %lld bar2 %lld inv %lld ns\n", blockIdx.x,
+           fpt[1] - fpt[0], fpt[2] - fpt[1], fpt[3] - fpt[2], fpt[4] - fpt[3], fpt[5] - fpt[4], fpt[6] - fpt[5]);
+#endif
 }
 
 template <typename TI, typename TC, typename TO>
@@ -816,6 +1056,47 @@ int fft2d(bool inverse, const void* in, void* out, int n2, int n1, int l2, int l
     case 3: return fft2d_t<double, float, float>(inverse, f, l2, l1, s);
     default: return -1;
   }
+}
+
+// The fused cfg2 matvec (mv_fused_kernel) when it applies: complex128 operator and vectors, N_b = 128,
+// a 60 x 60 embedding with n2 <= 30, forward product (not transpose), every SM co-resident.
+// Returns -1 when it does not apply (the caller uses the three-kernel path).
+int matvec_fused(const void* DT, int64_t K, int n2, int n1, int l2, int l1, int n0, const void* u, void* hat,
+                 void* hat2, void* v, unsigned* bar, const double* in_scale, const int* stop, const L2Prefetch& pf,
+                 cudaStream_t s) {
+  if (n0 != kFusedN0 || l2 != 60 || l1 != 60 || n2 > 30 || n1 > 30 || bar == nullptr) return -1;
+  const size_t smem = fused_smem_bytes(n2);
+  if (smem > 227 * 1024) return -1;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  TOEP_CUDA(ensure_smem(mv_fused_kernel, smem));
+  static int fits = -1;  // every SM must hold one CTA (cooperative launch)
+  if (fits < 0) {
+    int per_sm = 0;
+    fits = (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mv_fused_kernel, kFusedThreads, smem) ==
+                cudaSuccess &&
+            per_sm >= 1)
+               ? 1
+               : 0;
+    cudaGetLastError();
+  }
+  if (!fits) return -1;
+  FusedArgs a;
+  a.fwd = Fft2dArgs{u, hat, n2, n1, kFusedN0, -1, in_scale, stop, pf};
+  a.inv = Fft2dArgs{hat2, v, n2, n1, kFusedN0, +1, nullptr, nullptr, L2Prefetch{}};
+  a.DT = static_cast<const double2*>(DT);
+  a.hat = static_cast<double2*>(hat);
+  a.hat2 = static_cast<double2*>(hat2);
+  a.K = K;
+  a.bar = bar;
+  a.work = reinterpret_cast<int*>(bar + 1);
+  a.pf_bytes = pf.bytes > 0 ? int64_t{TOEP_FUSED_PF_MB} << 20 : 0;
+  return launch_coop(mv_fused_kernel, dim3(static_cast<unsigned>(std::min<int64_t>(sms, K))), dim3(kFusedThreads),
+                     smem, s, a);
 }
 
 bool fft_plan_has_planes(int L, int64_t inner) {

@@ -76,6 +76,11 @@ __device__ __forceinline__ void l2_prefetch_heads(const L2Prefetch& pf, int cta,
     }
   }
 }
+// fused forward DFT -> per-bin product -> inverse DFT (one cooperative launch) for the cfg2 shape;
+// -1 when it does not apply (fft.cu)
+int matvec_fused(const void* DT, int64_t K, int n2, int n1, int l2, int l1, int n0, const void* u, void* hat,
+                 void* hat2, void* v, unsigned* bar, const double* in_scale, const int* stop, const L2Prefetch& pf,
+                 cudaStream_t s);
 int fft2d(bool inverse, const void* in, void* out, int n2, int n1, int l2, int l1, int64_t inner, int sign,
           int tin, int tc, int tout, const double* in_scale, const int* stop, cudaStream_t s,
           const L2Prefetch* pf = nullptr);

@@ -253,6 +253,19 @@ int matvec_impl(toep_op_s* op, const void* u, void* v, int64_t w, bool transpose
   // one-CTA-per-column 2-D transforms when a compiled 2-D plan covers the grid
   if (w == 1) {
     const L2Prefetch pf = transpose ? L2Prefetch{} : binprod_prefetch_plan(op->dtype, op->DT, op->K, op->n0);
+    if (!transpose && op->dtype == TOEP_C128 && tio == 0 && op->slab_kxs == 0 && op->n0 == 128) {
+      // the three stages in one cooperative launch: the operator stream starts under the forward DFT
+      {
+        std::lock_guard<std::mutex> lock(op->mu);
+        if (ws->bar == nullptr) {
+          TOEP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws->bar), 2 * sizeof(unsigned), s));
+          TOEP_CUDA(cudaMemsetAsync(ws->bar, 0, 2 * sizeof(unsigned), s));
+        }
+      }
+      const int rc = matvec_fused(op->DT, op->K, op->n2, op->n1, op->l2, op->l1, op->n0, u, ws->hat, ws->hat2, v,
+                                  ws->bar, in_scale, stop, pf, s);
+      if (rc != -1) return rc;
+    }
     const int rf =
         fft2d(false, u, ws->hat, op->n2, op->n1, op->l2, op->l1, inner, s1, tio, tc, tc, in_scale, stop, s, &pf);
     if (rf == TOEP_OK) {
@@ -494,7 +507,7 @@ int toep_op_destroy(toep_op_t op) {
   for (auto& kv : op->ws) {
     auto& w = kv.second;
     if (w.pin_in) cudaFreeHost(w.pin_in);
-    for (void* p : {w.x1, w.hat, w.hat2, static_cast<void*>(w.hatp),
+    for (void* p : {w.x1, w.hat, w.hat2, static_cast<void*>(w.bar), static_cast<void*>(w.hatp),
                     static_cast<void*>(w.hat2p), w.io, static_cast<void*>(w.oz_b), static_cast<void*>(w.oz_bexp)})
       rel(p);
   }

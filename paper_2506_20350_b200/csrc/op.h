@@ -25,6 +25,7 @@ struct toep_op_s {
     size_t io_cap = 0;
     void* pin_in = nullptr;  // toep_matvec_host + TOEP_MV_STAGE_INPUT: page-locked staging of u
     size_t pin_cap = 0;
+    unsigned* bar = nullptr;  // fused single-RHS matvec: [0] grid-barrier counter, [1] bin hand-out counter
     int8_t* oz_b = nullptr;     // Ozaki path: int8 slices of one chunk's U planes
     int32_t* oz_bexp = nullptr; // and their column exponents
     size_t oz_b_bytes = 0, oz_bexp_bytes = 0;  // capacities in bytes
