@@ -31,6 +31,7 @@
 // and no step waits on a host round trip.
 #include <chrono>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "launch.cuh"
@@ -318,7 +319,7 @@ __global__ void k_cycle_start(GState* st, const double* partial, int nblk, doubl
     const double beta = sqrt(s);
     st->beta = beta;
     st->m = 0;
-    if (beta / st->beta0 <= tol) {
+    if (st->beta0 == 0.0 || beta / st->beta0 <= tol) {  // b = 0: x = 0 is the solution
       st->converged = 1;
       st->stop = 1;
     } else {
@@ -1072,6 +1073,22 @@ struct HostRes {
   HostFlags* hf_dev = nullptr;
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
+  // page-locked landing area of the solve's single exit read-back (state, norm partials, history)
+  unsigned char* stage = nullptr;
+  size_t stage_cap = 0;
+  unsigned char* stage_bytes(size_t bytes) {
+    if (bytes > stage_cap) {
+      if (stage != nullptr) cudaFreeHost(stage);
+      stage_cap = 0;
+      if (cudaHostAlloc(reinterpret_cast<void**>(&stage), bytes, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        stage = nullptr;
+        return nullptr;
+      }
+      stage_cap = bytes;
+    }
+    return stage;
+  }
   cudaEvent_t event() {
     if (used == pool.size()) {
       cudaEvent_t ev;
@@ -1209,18 +1226,6 @@ struct Engine {
     *count = 1;
     return TOEP_OK;
   }
-  double host_norm(const double2* x) {
-    if (norm2_partials(x) != TOEP_OK) return -1.0;
-    const double* ptr = nullptr;
-    int cnt = 0;
-    if (finish_norm(&ptr, &cnt) != TOEP_OK) return -1.0;
-    std::vector<double> h(cnt);
-    cudaMemcpyAsync(h.data(), ptr, cnt * sizeof(double), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    double t = 0.0;
-    for (double v : h) t += v;
-    return std::sqrt(t);
-  }
 };
 
 int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const double2* b, double2* x,
@@ -1259,7 +1264,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   const int nblk = e.nblk;
   const int grid1 = e.grid1();
 
-  double2 *V = nullptr, *tmp = nullptr, *tmp2 = nullptr, *pb = nullptr, *h1 = nullptr;
+  double2 *V = nullptr, *tmp = nullptr, *tmp2 = nullptr, *pb = nullptr, *h1 = nullptr, *rres = nullptr;
   double2 *rcols = nullptr, *sn = nullptr, *g = nullptr, *y = nullptr, *part1 = nullptr, *part2 = nullptr;
   double *cs = nullptr, *hist = nullptr, *vs = nullptr;
   GState* st = nullptr;
@@ -1272,7 +1277,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   HostFlags* hf_dev = res.hf_dev;
   int rc = TOEP_OK;
   auto cleanup = [&]() {
-    for (void* q : {(void*)V, (void*)tmp, (void*)tmp2, (void*)pb, (void*)h1, (void*)rcols, (void*)sn, (void*)g,
+    for (void* q : {(void*)V, (void*)tmp, (void*)tmp2, (void*)rres, (void*)pb, (void*)h1, (void*)rcols, (void*)sn, (void*)g,
                     (void*)y, (void*)part1, (void*)part2, (void*)cs, (void*)hist, (void*)vs, (void*)st,
                     (void*)e.norm_partial, (void*)e.nred, (void*)e.hred, (void*)bar, (void*)ts,
                     (void*)gram})
@@ -1298,10 +1303,20 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       return rc;         \
     }                    \
   } while (0)
+#define G_CUDA(call)                                                                 \
+  do {                                                                               \
+    const cudaError_t _ge = (call);                                                  \
+    if (_ge != cudaSuccess) {                                                        \
+      set_error("gmres: %s: %s", #call, cudaGetErrorString(_ge));                    \
+      cleanup();                                                                     \
+      return TOEP_ERR_CUDA;                                                          \
+    }                                                                                \
+  } while (0)
   G_ALLOC(V, (int64_t)(cycle_len + 1) * N);
   G_ALLOC(tmp, N);
   G_ALLOC(pb, N);
   G_ALLOC(tmp2, N);
+  G_ALLOC(rres, N);
   e.tmp2 = tmp2;
   G_ALLOC(h1, ldr);
   G_ALLOC(rcols, (int64_t)cycle_len * ldr);
@@ -1402,33 +1417,41 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     }
     if (timed) mark(1, t0);
   }
+  // every value the host needs back (state, exit-residual and ||b|| partials, history) lands in
+  // one page-locked block read back by ONE copy + sync at the end of each cycle; the start of the
+  // solve does not wait for the device at all (b = 0 is caught by k_cycle_start)
+  const int hist_copy = static_cast<int>(std::min<int64_t>(rep->history != nullptr ? rep->history_cap : 0,
+                                                           max_total + 2));
+  const size_t off_r = (sizeof(GState) + 15) & ~size_t(15);
+  const size_t off_b = off_r + sizeof(double) * nblk;
+  const size_t off_h = off_b + sizeof(double) * nblk;
+  unsigned char* stage = res.stage_bytes(off_h + sizeof(double) * (hist_copy + 1));
+  if (stage == nullptr) {
+    set_error("pinned allocation failed");
+    cleanup();
+    return TOEP_ERR_OOM;
+  }
+  GState& hst = *reinterpret_cast<GState*>(stage);
+  double* h_rpart = reinterpret_cast<double*>(stage + off_r);
+  double* h_bpart = reinterpret_cast<double*>(stage + off_b);
+  double* h_hist = reinterpret_cast<double*>(stage + off_h);
+  int rcnt = 0, bcnt = 0;
   const double* nptr = nullptr;
   int ncnt = 0;
   G_TRY(e.norm2_partials(zb));
   G_TRY(e.finish_norm(&nptr, &ncnt));
   G_TRY(launch_k(k_init, dim3(1), dim3(32), 0, s, st, nptr, ncnt, hist));
-  GState hst{};
-  if (cudaMemcpyAsync(&hst, st, sizeof(GState), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaStreamSynchronize(s) != cudaSuccess) {
-    set_error("gmres init failed: %s", cudaGetErrorString(cudaGetLastError()));
-    cleanup();
-    return TOEP_ERR_CUDA;
+  if (zb != b) {  // ||b|| for the exit residual (unpreconditioned)
+    G_TRY(e.norm2_partials(b));
+    G_TRY(e.finish_norm(&nptr, &ncnt));
   }
-  tr.mark("init (P^-1 b, beta0) synced");
+  bcnt = ncnt;
+  G_CUDA(cudaMemcpyAsync(h_bpart, nptr, sizeof(double) * ncnt, cudaMemcpyDeviceToHost, s));
+  tr.mark("init (P^-1 b, beta0) queued");
   rep->iterations = 0;
   rep->converged = 1;
   rep->breakdown = 0;
   rep->t_matvec = rep->t_precond = rep->t_orth = 0.0;
-  if (hst.beta0 == 0.0) {
-    cudaMemsetAsync(x, 0, N * sizeof(double2), s);
-    cudaStreamSynchronize(s);
-    if (rep->history != nullptr && rep->history_cap >= 1) rep->history[0] = 0.0;
-    rep->n_history = 1;
-    rep->final_residual = 0.0;
-    cleanup();
-    rep->t_total = std::chrono::duration<double>(clk::now() - t_start).count();
-    return TOEP_OK;
-  }
   cudaMemsetAsync(x, 0, N * sizeof(double2), s);
 
   int* stop_dev = &st->stop;
@@ -1438,15 +1461,12 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   while (true) {
     // ---- cycle start (gmres.py:123-144): V[0] = P^-1 (b - A x), vs[0] = 1 / ||.||
     double2* v0 = V;
-    if (!first) {
+    if (!first) {  // tmp = A x (P^-1 A x when folded) from the previous cycle's exit block
       cudaEvent_t t0 = timed ? start_mark() : nullptr;
-      G_TRY(e.apply_a(x, nullptr, tmp, nullptr));
-      if (timed) t0 = mark(0, t0);
       if (p->precond == TOEP_PC_FOLDED) {
         G_TRY(launch_k(k_sub, dim3(grid1), dim3(kThreads), 0, s, (const double2*)pb, (const double2*)tmp, v0, N));
       } else if (e.precond_per_step()) {
-        G_TRY(launch_k(k_sub, dim3(grid1), dim3(kThreads), 0, s, b, (const double2*)tmp, tmp2, N));
-        G_TRY(e.apply_p(tmp2, v0, nullptr));
+        G_TRY(e.apply_p(rres, v0, nullptr));  // rres = b - A x
       } else {
         G_TRY(launch_k(k_sub, dim3(grid1), dim3(kThreads), 0, s, b, (const double2*)tmp, v0, N));
       }
@@ -1536,8 +1556,27 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
                      (const double2*)g, y));
     G_TRY(launch_k(k_axpy_basis, dim3(grid1), dim3(kThreads), coef_smem, s, (const double2*)V, N, cycle_len,
                    (const int*)m_dev, (const double*)vs, (const double2*)y, x, N));
-    if (cudaMemcpyAsync(&hst, st, sizeof(GState), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess) {
+    // ---- exit residual ||b - A x|| (gmres.py:209-216), unpreconditioned, queued before the host
+    // learns whether the solve ends here: A x is also the next cycle's start on a restart
+    {
+      cudaEvent_t t0 = timed ? start_mark() : nullptr;
+      G_TRY(e.apply_a(x, nullptr, tmp, nullptr));
+      const double2* ax = tmp;
+      if (p->precond == TOEP_PC_FOLDED) {  // A x = P (P^-1 A x)
+        G_TRY(block_apply_impl(p->pmat, p->pside, tmp, rres, p->n / p->pside, p->w, TOEP_C128, s, nullptr));
+        ax = rres;
+      }
+      if (timed) mark(0, t0);
+      G_TRY(launch_k(k_sub, dim3(grid1), dim3(kThreads), 0, s, b, ax, rres, N));
+      G_TRY(e.norm2_partials(rres));
+      G_TRY(e.finish_norm(&nptr, &ncnt));
+      rcnt = ncnt;
+      G_CUDA(cudaMemcpyAsync(h_rpart, nptr, sizeof(double) * ncnt, cudaMemcpyDeviceToHost, s));
+    }
+    G_CUDA(cudaMemcpyAsync(&hst, st, sizeof(GState), cudaMemcpyDeviceToHost, s));
+    if (hist_copy > 0)  // the whole history window: its length is only known after the sync
+      G_CUDA(cudaMemcpyAsync(h_hist, hist, sizeof(double) * hist_copy, cudaMemcpyDeviceToHost, s));
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
       set_error("gmres cycle failed: %s", cudaGetErrorString(cudaGetLastError()));
       cleanup();
       return TOEP_ERR_CUDA;
@@ -1547,34 +1586,26 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     if (hst.converged || hst.breakdown || total >= max_total) break;
   }
 
-  // ---- exit residual ||b - A x|| / ||b|| (gmres.py:209-216), unpreconditioned
-  {
-    cudaEvent_t t0 = timed ? start_mark() : nullptr;
-    G_TRY(e.apply_a(x, nullptr, tmp, nullptr));
-    double2* ax = tmp;
-    if (p->precond == TOEP_PC_FOLDED) {  // A x = P (P^-1 A x)
-      G_TRY(block_apply_impl(p->pmat, p->pside, tmp, pb, p->n / p->pside, p->w, TOEP_C128, s, nullptr));
-      ax = pb;
-    }
-    if (timed) mark(0, t0);
-    G_TRY(launch_k(k_sub, dim3(grid1), dim3(kThreads), 0, s, b, (const double2*)ax, tmp, N));
-  }
-  const double rn = e.host_norm(tmp);
-  const double bn = e.host_norm(b);
+  auto host_sum = [](const double* v, int n) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += v[i];
+    return std::sqrt(t);
+  };
   tr.mark("exit residual synced");
-  rep->final_residual = rn / bn;
-  rep->iterations = hst.total;
-  rep->converged = hst.converged;
-  rep->breakdown = hst.breakdown;
-  const int nh = std::min(hst.nhist, rep->history_cap);
-  if (rep->history != nullptr && nh > 0)
-    cudaMemcpyAsync(rep->history, hist, nh * sizeof(double), cudaMemcpyDeviceToHost, s);
-  rep->n_history = hst.nhist;
-  if (cudaStreamSynchronize(s) != cudaSuccess) {
-    set_error("gmres exit failed: %s", cudaGetErrorString(cudaGetLastError()));
-    cleanup();
-    return TOEP_ERR_CUDA;
+  if (hst.beta0 == 0.0) {  // b = 0 (P^-1 b = 0): x = 0, residual 0
+    rep->final_residual = 0.0;
+    rep->iterations = 0;
+    rep->converged = 1;
+    rep->breakdown = 0;
+  } else {
+    rep->final_residual = host_sum(h_rpart, rcnt) / host_sum(h_bpart, bcnt);
+    rep->iterations = hst.total;
+    rep->converged = hst.converged;
+    rep->breakdown = hst.breakdown;
   }
+  const int nh = std::min(hst.nhist, hist_copy);
+  if (nh > 0) std::memcpy(rep->history, h_hist, nh * sizeof(double));
+  rep->n_history = hst.nhist;
   if (timed && stamped) {
     std::vector<long long> hts(2 * static_cast<size_t>(hst.total) + 2);
     if (cudaMemcpy(hts.data(), ts, hts.size() * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess) {
@@ -1601,6 +1632,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   rep->t_total = std::chrono::duration<double>(clk::now() - t_start).count();
 #undef G_ALLOC
 #undef G_TRY
+#undef G_CUDA
   return TOEP_OK;
 }
 
