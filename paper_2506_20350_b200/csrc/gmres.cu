@@ -29,6 +29,7 @@
 // launches; after launching step j it waits for step j-1 and reads the stop
 // flag from mapped pinned memory, so the launch queue stays one step ahead
 // and no step waits on a host round trip.
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -330,6 +331,36 @@ __global__ void k_cycle_start(GState* st, const double* partial, int nblk, doubl
     hf->stop = st->stop;
     hf->converged = st->converged;
     hf->total = st->total;
+  }
+}
+
+// end-of-cycle report straight into mapped page-locked host memory: the solver state, the exit
+// residual's partials, the history written so far and (timed solves) the step stamps, then the
+// sequence word the host spins on (written last, after a system-scope fence).  Replaces the
+// device-to-host copies and the stream synchronisation of each cycle end.
+struct ReportLayout {
+  size_t st, r, b, h, t, bytes;
+};
+__global__ void k_report(const GState* st, const double* rpart, int rcnt, const double* hist, int hist_cap,
+                         const long long* ts, unsigned char* out, ReportLayout lay, unsigned seq) {
+  pdl_wait();
+  pdl_trigger();
+  const int nh = min(st->nhist, hist_cap);
+  double* orp = reinterpret_cast<double*>(out + lay.r);
+  double* oh = reinterpret_cast<double*>(out + lay.h);
+  for (int i = threadIdx.x; i < rcnt; i += blockDim.x) orp[i] = __ldcg(rpart + i);
+  for (int i = threadIdx.x; i < nh; i += blockDim.x) oh[i] = __ldcg(hist + i);
+  if (ts != nullptr) {
+    long long* ot = reinterpret_cast<long long*>(out + lay.t);
+    const int nt = 2 * st->total + 2;
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) ot[i] = __ldcg(ts + i);
+  }
+  if (threadIdx.x == 0) *reinterpret_cast<GState*>(out + lay.st) = *st;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned*>(out) = seq;
   }
 }
 
@@ -979,70 +1010,117 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_orth_coop(OrthArgs a, const
 }
 
 // y = R^-1 g (gmres.py:193-204), R upper triangular from the rotated columns (rcols[j][0..j]).
-// One warp: R is staged in shared memory by all lanes at once (one load latency), then a
-// column-oriented substitution: lane l owns rows l, l+32, ...; each solved y_i is broadcast with a
-// shuffle and subtracted from the remaining rows.  A zero pivot gives y_i = 0, as before.
+// One warp, column-oriented substitution: lane l owns rows l, l+32, ...; the pivots' reciprocals
+// are formed for all rows at once up front (the divisions leave the serial chain), then each solved
+// y_i is broadcast with a shuffle and subtracted from the remaining rows.  A zero pivot gives
+// y_i = 0.  rs: column i of R at rs[i * rld + 0..i]; out[i] = y_i * (scale ? scale[i] : 1).
+template <int ROWS>
+__device__ __forceinline__ void tri_solve_warp(const double2* rs, int rld, const double2* g, int m, const double* scale,
+                                               double2* out) {
+  const int lane = threadIdx.x & 31;
+  double2 acc[ROWS], pinv[ROWS];
+#pragma unroll
+  for (int q = 0; q < ROWS; ++q) {
+    const int r = lane + 32 * q;
+    acc[q] = make_double2(0, 0);
+    pinv[q] = make_double2(0, 0);
+    if (r < m) {
+      acc[q] = g[r];
+      const double2 d = rs[static_cast<int64_t>(r) * rld + r];
+      if (!(d.x == 0.0 && d.y == 0.0)) {
+        const double inv = 1.0 / (d.x * d.x + d.y * d.y);
+        pinv[q] = make_double2(d.x * inv, -d.y * inv);  // 1 / d = conj(d) / |d|^2
+      }
+    }
+  }
+  for (int i = m - 1; i >= 0; --i) {
+    const int qi = i >> 5;
+    double2 yi = make_double2(0, 0);
+#pragma unroll
+    for (int q = 0; q < ROWS; ++q)
+      if (q == qi) yi = cmul(acc[q], pinv[q]);
+    yi.x = __shfl_sync(0xffffffffu, yi.x, i & 31);
+    yi.y = __shfl_sync(0xffffffffu, yi.y, i & 31);
+    if (lane == (i & 31)) out[i] = scale != nullptr ? cscale(yi, scale[i]) : yi;
+    const double2 ny = make_double2(-yi.x, -yi.y);
+#pragma unroll
+    for (int q = 0; q < ROWS; ++q) {
+      const int r = lane + 32 * q;
+      if (r < i) cfma(acc[q], rs[static_cast<int64_t>(i) * rld + r], ny);
+    }
+  }
+}
+
+// every thread of the block stages the m x m upper triangle of R into shared memory (column-major,
+// leading dimension m) with its loads batched: one L2 round trip per batch of 8
+template <int NT>
+__device__ __forceinline__ void stage_triangle(const double2* rcols, int ldr, int m, double2* rsm) {
+  constexpr int B = 8;
+  const int tot = m * m;
+  for (int e0 = threadIdx.x; e0 < tot; e0 += B * NT) {
+    double2 v[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int e = e0 + u * NT, i = e / max(m, 1), r = e - i * m;
+      v[u] = (e < tot && r <= i) ? rcols[static_cast<int64_t>(i) * ldr + r] : make_double2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int e = e0 + u * NT;
+      if (e < tot) rsm[e] = v[u];
+    }
+  }
+}
+
 constexpr int kBsRows = 8;  // rows per lane: cycles up to 256 steps
 constexpr int kBsThreads = 256;  // k_backsub block: all stage the triangle, warp 0 solves
 __global__ void k_backsub(const GState* st, const double2* rcols, int ldr, const double2* g, double2* y, int staged) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ double2 rsm[];  // staged: [m][m] column-major upper triangle
-  const int lane = threadIdx.x & 31;
   const int m = st->m;
   const double2* rs = rcols;
   int rld = ldr;
   if (staged) {
-    // every thread of the block stages with its loads batched (one L2 round trip per batch of 8,
-    // instead of one per column: 46 -> a few us at m = 31)
-    constexpr int B = 8;
-    const int tot = m * m;
-    for (int e0 = threadIdx.x; e0 < tot; e0 += B * kBsThreads) {
-      double2 v[B];
-#pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int e = e0 + u * kBsThreads, i = e / max(m, 1), r = e - i * m;
-        v[u] = (e < tot && r <= i) ? rcols[static_cast<int64_t>(i) * ldr + r] : make_double2(0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int e = e0 + u * kBsThreads;
-        if (e < tot) rsm[e] = v[u];
-      }
-    }
+    stage_triangle<kBsThreads>(rcols, ldr, m, rsm);
     __syncthreads();
     rs = rsm;
     rld = m;
   }
   if (threadIdx.x >= 32) return;  // one warp solves
-  double2 acc[kBsRows];
+  tri_solve_warp<kBsRows>(rs, rld, g, m, nullptr, y);
+}
+
+// cycles up to kSolveAxpyMax steps: the triangular solve and x += V (vs y) in one kernel -- every
+// CTA stages R (L2-resident, m^2 * 16 bytes) and solves it redundantly, then updates its elements
+constexpr int kSolveAxpyMax = 64;
+__global__ void __launch_bounds__(kThreads)
+k_solve_axpy(const GState* st, const double2* __restrict__ rcols, int ldr, const double2* __restrict__ g,
+             const double* __restrict__ vs, const double2* __restrict__ V, int64_t ld, int m_max,
+             double2* __restrict__ x, int64_t N) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ double2 ssm[];  // [m_max][m_max] triangle | coef [m_max]
+  const int m = min(m_max, st->m);
+  double2* rsm = ssm;
+  double2* coef = ssm + static_cast<int64_t>(m_max) * m_max;
+  stage_triangle<kThreads>(rcols, ldr, m, rsm);
+  __syncthreads();
+  if (threadIdx.x < 32) tri_solve_warp<(kSolveAxpyMax + 31) / 32>(rsm, m, g, m, vs, coef);
+  __syncthreads();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < N;
+       i += static_cast<int64_t>(gridDim.x) * kThreads) {
+    double2 acc = x[i];
+    int l = 0;
+    for (; l + 7 < m; l += 8) {  // 8 independent basis loads in flight
+      double2 v[8];
 #pragma unroll
-  for (int q = 0; q < kBsRows; ++q) {
-    const int r = lane + 32 * q;
-    acc[q] = r < m ? g[r] : make_double2(0, 0);
-  }
-  __syncwarp();
-  for (int i = m - 1; i >= 0; --i) {
-    const int qi = i >> 5;
-    double2 yi = make_double2(0, 0);
+      for (int u = 0; u < 8; ++u) v[u] = V[(l + u) * ld + i];
 #pragma unroll
-    for (int q = 0; q < kBsRows; ++q)
-      if (q == qi && lane == (i & 31)) {
-        const double2 d = rs[static_cast<int64_t>(i) * rld + i];
-        if (!(d.x == 0.0 && d.y == 0.0)) {
-          const double den = d.x * d.x + d.y * d.y;
-          yi = make_double2((acc[q].x * d.x + acc[q].y * d.y) / den, (acc[q].y * d.x - acc[q].x * d.y) / den);
-        }
-        y[i] = yi;
-      }
-    yi.x = __shfl_sync(0xffffffffu, yi.x, i & 31);
-    yi.y = __shfl_sync(0xffffffffu, yi.y, i & 31);
-    const double2 ny = make_double2(-yi.x, -yi.y);
-#pragma unroll
-    for (int q = 0; q < kBsRows; ++q) {
-      const int r = lane + 32 * q;
-      if (r < i) cfma(acc[q], rs[static_cast<int64_t>(i) * rld + r], ny);
+      for (int u = 0; u < 8; ++u) cfma(acc, v[u], coef[l + u]);
     }
+    for (; l < m; ++l) cfma(acc, V[l * ld + i], coef[l]);
+    x[i] = acc;
   }
 }
 
@@ -1073,18 +1151,24 @@ struct HostRes {
   HostFlags* hf_dev = nullptr;
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
-  // page-locked landing area of the solve's single exit read-back (state, norm partials, history)
+  // mapped page-locked block the device writes each cycle's report into (k_report)
   unsigned char* stage = nullptr;
+  unsigned char* stage_dev = nullptr;
   size_t stage_cap = 0;
+  unsigned seq = 0;
   unsigned char* stage_bytes(size_t bytes) {
     if (bytes > stage_cap) {
       if (stage != nullptr) cudaFreeHost(stage);
+      stage = stage_dev = nullptr;
       stage_cap = 0;
-      if (cudaHostAlloc(reinterpret_cast<void**>(&stage), bytes, cudaHostAllocDefault) != cudaSuccess) {
+      if (cudaHostAlloc(reinterpret_cast<void**>(&stage), bytes, cudaHostAllocMapped) != cudaSuccess ||
+          cudaHostGetDevicePointer(reinterpret_cast<void**>(&stage_dev), stage, 0) != cudaSuccess) {
         cudaGetLastError();
-        stage = nullptr;
+        if (stage != nullptr) cudaFreeHost(stage);
+        stage = stage_dev = nullptr;
         return nullptr;
       }
+      std::memset(stage, 0, bytes);
       stage_cap = bytes;
     }
     return stage;
@@ -1276,25 +1360,21 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   HostFlags* hf = res.hf;
   HostFlags* hf_dev = res.hf_dev;
   int rc = TOEP_OK;
-  auto cleanup = [&]() {
-    for (void* q : {(void*)V, (void*)tmp, (void*)tmp2, (void*)rres, (void*)pb, (void*)h1, (void*)rcols, (void*)sn, (void*)g,
-                    (void*)y, (void*)part1, (void*)part2, (void*)cs, (void*)hist, (void*)vs, (void*)st,
-                    (void*)e.norm_partial, (void*)e.nred, (void*)e.hred, (void*)bar, (void*)ts,
-                    (void*)gram})
-      if (q) cudaFreeAsync(q, s);
-    cudaStreamSynchronize(s);
+  // stream-ordered frees; error paths also drain the stream (success: the last report already
+  // proved every kernel done)
+  // every device buffer of the solve is carved from ONE stream-ordered allocation (two pool calls
+  // per solve instead of ~40)
+  unsigned char* arena = nullptr;
+  // error paths also drain the stream (success: the last report already proved every kernel done)
+  auto cleanup = [&](bool sync = true) {
+    if (arena != nullptr) cudaFreeAsync(arena, s);
+    arena = nullptr;
+    if (sync) cudaStreamSynchronize(s);
     res.used = 0;
   };
   TOEP_REQUIRE(hf != nullptr, TOEP_ERR_OOM, "pinned allocation failed");
-#define G_ALLOC(ptr, count)                                                                                      \
-  do {                                                                                                           \
-    if (cudaMallocAsync(reinterpret_cast<void**>(&(ptr)), sizeof(*(ptr)) * (size_t)(count), s) != cudaSuccess) { \
-      cudaGetLastError();                                                                                        \
-      set_error("out of device memory in gmres");                                                                \
-      cleanup();                                                                                                 \
-      return TOEP_ERR_OOM;                                                                                       \
-    }                                                                                                            \
-  } while (0)
+  std::vector<std::pair<void**, size_t>> plan;
+#define G_ALLOC(ptr, count) plan.emplace_back(reinterpret_cast<void**>(&(ptr)), sizeof(*(ptr)) * (size_t)(count))
 #define G_TRY(expr)      \
   do {                   \
     rc = (expr);         \
@@ -1317,7 +1397,6 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   G_ALLOC(pb, N);
   G_ALLOC(tmp2, N);
   G_ALLOC(rres, N);
-  e.tmp2 = tmp2;
   G_ALLOC(h1, ldr);
   G_ALLOC(rcols, (int64_t)cycle_len * ldr);
   G_ALLOC(sn, cycle_len + 1);
@@ -1334,10 +1413,26 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     G_ALLOC(e.nred, 1);
     G_ALLOC(e.hred, ldr);
   }
-  // single-kernel cooperative orthogonalisation when all CTAs fit co-resident
-  G_ALLOC(bar, 2);
+  G_ALLOC(bar, 2);  // grid barrier of the cooperative orthogonalisation kernel
   G_ALLOC(ts, 2 * max_total + 4);
   G_ALLOC(gram, (int64_t)ldr * ldr);
+  {
+    size_t bytes = 0;
+    for (auto& pp : plan) bytes += (pp.second + 255) & ~size_t(255);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&arena), bytes, s) != cudaSuccess) {
+      cudaGetLastError();
+      arena = nullptr;
+      set_error("out of device memory in gmres (%zu bytes)", bytes);
+      cleanup();
+      return TOEP_ERR_OOM;
+    }
+    size_t off = 0;
+    for (auto& pp : plan) {
+      *pp.first = arena + off;
+      off += (pp.second + 255) & ~size_t(255);
+    }
+  }
+  e.tmp2 = tmp2;
   TOEP_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s));
   // Gram block staged in shared memory for cycles up to 64 vectors (64 KB); larger cycles read it from L2
   const bool gram_smem = ldr <= 64;
@@ -1391,6 +1486,9 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     return a;
   };
   const size_t coef_smem = sizeof(double2) * ldr;
+  const bool solve_axpy = cycle_len <= kSolveAxpyMax;  // else backsub kernel + axpy kernel
+  const size_t solve_axpy_smem = sizeof(double2) * static_cast<size_t>(cycle_len) * (cycle_len + 1);
+  if (solve_axpy) ensure_smem(k_solve_axpy, solve_axpy_smem);
   const bool backsub_warp = cycle_len <= 32 * kBsRows;  // else the serial kernel
   const int backsub_staged = sizeof(double2) * static_cast<size_t>(cycle_len) * cycle_len <= 200 * 1024 ? 1 : 0;
   const size_t backsub_smem = backsub_staged ? sizeof(double2) * static_cast<size_t>(cycle_len) * cycle_len : 0;
@@ -1422,19 +1520,44 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   // solve does not wait for the device at all (b = 0 is caught by k_cycle_start)
   const int hist_copy = static_cast<int>(std::min<int64_t>(rep->history != nullptr ? rep->history_cap : 0,
                                                            max_total + 2));
-  const size_t off_r = (sizeof(GState) + 15) & ~size_t(15);
-  const size_t off_b = off_r + sizeof(double) * nblk;
-  const size_t off_h = off_b + sizeof(double) * nblk;
-  unsigned char* stage = res.stage_bytes(off_h + sizeof(double) * (hist_copy + 1));
+  ReportLayout lay{};
+  lay.st = 16;
+  lay.r = (lay.st + sizeof(GState) + 15) & ~size_t(15);
+  lay.b = lay.r + sizeof(double) * nblk;
+  lay.h = lay.b + sizeof(double) * nblk;
+  lay.t = lay.h + sizeof(double) * (hist_copy + 1);
+  lay.bytes = lay.t + sizeof(long long) * (2 * max_total + 4);
+  unsigned char* stage = res.stage_bytes(lay.bytes);
   if (stage == nullptr) {
     set_error("pinned allocation failed");
     cleanup();
     return TOEP_ERR_OOM;
   }
-  GState& hst = *reinterpret_cast<GState*>(stage);
-  double* h_rpart = reinterpret_cast<double*>(stage + off_r);
-  double* h_bpart = reinterpret_cast<double*>(stage + off_b);
-  double* h_hist = reinterpret_cast<double*>(stage + off_h);
+  const GState& hst = *reinterpret_cast<const GState*>(stage + lay.st);
+  const double* h_rpart = reinterpret_cast<const double*>(stage + lay.r);
+  double* h_bpart = reinterpret_cast<double*>(stage + lay.b);
+  const double* h_hist = reinterpret_cast<const double*>(stage + lay.h);
+  const long long* h_ts = reinterpret_cast<const long long*>(stage + lay.t);
+  // wait for report `want` (spin on the mapped sequence word; a device fault or a stream that
+  // drained without writing it ends the wait with an error)
+  auto wait_report = [&](unsigned want) -> int {
+    volatile const unsigned* sq = reinterpret_cast<volatile const unsigned*>(stage);
+    for (unsigned spins = 1; *sq != want; ++spins) {
+      if ((spins & 4095u) != 0) continue;
+      const cudaError_t ce = cudaStreamQuery(s);
+      if (ce == cudaSuccess) {
+        if (*sq == want) break;
+        set_error("gmres: cycle report missing");
+        return TOEP_ERR_CUDA;
+      }
+      if (ce != cudaErrorNotReady) {
+        set_error("gmres cycle failed: %s", cudaGetErrorString(ce));
+        return TOEP_ERR_CUDA;
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return TOEP_OK;
+  };
   int rcnt = 0, bcnt = 0;
   const double* nptr = nullptr;
   int ncnt = 0;
@@ -1540,7 +1663,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       // keep up to kLag steps queued ahead of the one the host last saw finish.  Progress is read
       // from the mapped flag word the Givens step writes (no events between the kernels: an event
       // record would break their programmatic-dependent-launch chain)
-      constexpr int kLag = 2;
+      constexpr int kLag = 1;
       if (j > kLag) {
         G_TRY(tr.wait_total(hf, total + (j - kLag), s));
         if (hf->stop) break;
@@ -1548,14 +1671,19 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     }
     tr.mark("arnoldi steps launched");
     // ---- assemble x += V y (gmres.py:192-204)
-    if (backsub_warp)
+    if (solve_axpy)
+      G_TRY(launch_k(k_solve_axpy, dim3(grid1), dim3(kThreads), solve_axpy_smem, s, (const GState*)st,
+                     (const double2*)rcols, ldr, (const double2*)g, (const double*)vs, (const double2*)V, N, cycle_len,
+                     x, N));
+    else if (backsub_warp)
       G_TRY(launch_k(k_backsub, dim3(1), dim3(kBsThreads), backsub_smem, s, (const GState*)st, (const double2*)rcols, ldr,
                      (const double2*)g, y, backsub_staged));
     else
       G_TRY(launch_k(k_backsub_serial, dim3(1), dim3(32), 0, s, (const GState*)st, (const double2*)rcols, ldr,
                      (const double2*)g, y));
-    G_TRY(launch_k(k_axpy_basis, dim3(grid1), dim3(kThreads), coef_smem, s, (const double2*)V, N, cycle_len,
-                   (const int*)m_dev, (const double*)vs, (const double2*)y, x, N));
+    if (!solve_axpy)
+      G_TRY(launch_k(k_axpy_basis, dim3(grid1), dim3(kThreads), coef_smem, s, (const double2*)V, N, cycle_len,
+                     (const int*)m_dev, (const double*)vs, (const double2*)y, x, N));
     // ---- exit residual ||b - A x|| (gmres.py:209-216), unpreconditioned, queued before the host
     // learns whether the solve ends here: A x is also the next cycle's start on a restart
     {
@@ -1571,16 +1699,11 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
       G_TRY(e.norm2_partials(rres));
       G_TRY(e.finish_norm(&nptr, &ncnt));
       rcnt = ncnt;
-      G_CUDA(cudaMemcpyAsync(h_rpart, nptr, sizeof(double) * ncnt, cudaMemcpyDeviceToHost, s));
     }
-    G_CUDA(cudaMemcpyAsync(&hst, st, sizeof(GState), cudaMemcpyDeviceToHost, s));
-    if (hist_copy > 0)  // the whole history window: its length is only known after the sync
-      G_CUDA(cudaMemcpyAsync(h_hist, hist, sizeof(double) * hist_copy, cudaMemcpyDeviceToHost, s));
-    if (cudaStreamSynchronize(s) != cudaSuccess) {
-      set_error("gmres cycle failed: %s", cudaGetErrorString(cudaGetLastError()));
-      cleanup();
-      return TOEP_ERR_CUDA;
-    }
+    const unsigned want = ++res.seq;
+    G_TRY(launch_k(k_report, dim3(1), dim3(256), 0, s, (const GState*)st, nptr, rcnt, (const double*)hist, hist_copy,
+                   (const long long*)ts_dev, res.stage_dev, lay, want));
+    G_TRY(wait_report(want));
     total = hst.total;
     tr.mark("cycle synced");
     if (hst.converged || hst.breakdown || total >= max_total) break;
@@ -1607,16 +1730,13 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
   if (nh > 0) std::memcpy(rep->history, h_hist, nh * sizeof(double));
   rep->n_history = hst.nhist;
   if (timed && stamped) {
-    std::vector<long long> hts(2 * static_cast<size_t>(hst.total) + 2);
-    if (cudaMemcpy(hts.data(), ts, hts.size() * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess) {
-      for (int k = 0; k < hst.total; ++k) {
-        rep->t_matvec += 1e-9 * static_cast<double>(hts[2 * k + 2] - hts[2 * k + 1]);
-        rep->t_orth += 1e-9 * static_cast<double>(hts[2 * k + 3] - hts[2 * k + 2]);
-      }
+    for (int k = 0; k < hst.total; ++k) {
+      rep->t_matvec += 1e-9 * static_cast<double>(h_ts[2 * k + 2] - h_ts[2 * k + 1]);
+      rep->t_orth += 1e-9 * static_cast<double>(h_ts[2 * k + 3] - h_ts[2 * k + 2]);
     }
-    cudaGetLastError();
   }
-  if (timed) {
+  if (timed && !phases.empty()) {
+    cudaStreamSynchronize(s);
     for (auto& ph : phases) {
       float ms = 0.f;
       if (cudaEventElapsedTime(&ms, ph.a, ph.b) == cudaSuccess) {
@@ -1627,7 +1747,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
     }
     cudaGetLastError();
   }
-  cleanup();
+  cleanup(false);
   tr.mark("cleanup");
   rep->t_total = std::chrono::duration<double>(clk::now() - t_start).count();
 #undef G_ALLOC
