@@ -506,6 +506,7 @@ int try_plan(const PassArgs& a, cudaStream_t s) {
 // footprint fits (cfg2 60x60, cfg5 32x32).
 template <int... Rs> struct Plan {
   static constexpr int L = PlanLen<Rs...>::value;
+  static constexpr int kStages = sizeof...(Rs);
   template <typename TI, typename TC, typename TO, int NT, int TIL>
   __device__ static void run(const PassArgs& a, const C<TI>* gin, C<TO>* gout, C<TC>* b0, C<TC>* b1,
                              const C<TC>* tw, int ncol, TC scale) {
@@ -534,21 +535,50 @@ struct Fft2dSmem {
   static size_t bytes(int n2) { return sizeof(C<TC>) * (PX::L + PY::L + 2 * kBuf + static_cast<size_t>(n2) * kGs); }
 };
 
+#ifdef TOEP_ORTH_PROBE
+__device__ long long g_dft_ts[2][160][8];
+#define DPROBE(i)                                                                            \
+  if (threadIdx.x == 0 && b < 160) {                                                         \
+    long long t_;                                                                            \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
+    g_dft_ts[INV ? 1 : 0][b][i] = t_;                                                        \
+  }
+#else
+#define DPROBE(i)
+#endif
+
 // The 2-D transform of batch column `b`, shared-memory workspace at `smem_raw`.  Every thread of the
 // block calls it (threads >= k2dThreads only take part in the barriers).  With `wait` the PDL
 // wait / stop check happens inside (after the twiddles); returns false when the stop flag is set.
-template <typename TI, typename TC, typename TO, int TILX, int TILY, typename PX, typename PY, bool INV>
-__device__ __forceinline__ bool fft2d_body(const Fft2dArgs& f, unsigned char* smem_raw, int64_t b, bool wait) {
+struct NoHook {
+  __device__ void operator()() const {}
+};
+
+// kAliasG: the (n2 x l1) intermediate G lives in ping-pong buffer b1 instead of a buffer of its own
+// (the caller guarantees n2 * kGs <= kBuf).  Both plans have three stages, so the first pass ends
+// reading b0 (b1 is free for G) and the second pass runs with the buffers swapped (its first stage
+// reads G = b1 and writes b0).
+// kHatT: the spectral side (forward output / inverse input) is stored column-major, [b][ky][kx], so
+// the CTA of batch column b reads / writes one contiguous run of l2 * l1 values (coalesced) instead of
+// l2 * l1 values 16 * inner bytes apart.
+template <typename TI, typename TC, typename TO, int TILX, int TILY, typename PX, typename PY, bool INV,
+          bool kAliasG = false, int NT = k2dThreads, bool kHatT = false, typename AfterL1 = NoHook>
+__device__ __forceinline__ bool fft2d_body(const Fft2dArgs& f, unsigned char* smem_raw, int64_t b, bool wait,
+                                           AfterL1 after_l1 = {}) {
   using Z = C<TC>;
   using S = Fft2dSmem<TC, TILX, TILY, PX, PY>;
   constexpr int L1 = PX::L, L2 = PY::L;
+  static_assert(!kAliasG || (PX::kStages == 3 && PY::kStages == 3), "G aliasing assumes three-stage plans");
+  static_assert(!kAliasG || TILY >= PX::L, "G aliasing needs single-tile level-2 passes (the caller keeps n2 <= TILX)");
   Z* twx = reinterpret_cast<Z*>(smem_raw);
   Z* twy = twx + L1;
   Z* b0 = twy + L2;
   Z* b1 = b0 + S::kBuf;
-  Z* G = b1 + S::kBuf;  // [n2][kGs]
+  Z* G = kAliasG ? b1 : b1 + S::kBuf;  // [n2][kGs]
+  Z* p0 = kAliasG ? b1 : b0;  // ping-pong order of the second pass
+  Z* p1 = kAliasG ? b0 : b1;
   constexpr int Gs = S::kGs;
-  for (int t = threadIdx.x; t < L1 + L2; t += k2dThreads) {
+  for (int t = threadIdx.x; t < L1 + L2; t += NT) {
     const int L = t < L1 ? L1 : L2;
     const int tt = t < L1 ? t : t - L1;
     TC s, c;
@@ -560,6 +590,7 @@ __device__ __forceinline__ bool fft2d_body(const Fft2dArgs& f, unsigned char* sm
     if (f.stop != nullptr && *f.stop != 0) return false;
   }
   __syncthreads();
+  DPROBE(0);
   const int64_t inner = f.inner;
   const int n2 = f.n2, n1 = f.n1;
   // each level runs over its columns in tiles of TILX (level 1: array rows y) / TILY (level 2:
@@ -571,26 +602,32 @@ __device__ __forceinline__ bool fft2d_body(const Fft2dArgs& f, unsigned char* sm
     const TC sc = static_cast<TC>(f.in_scale != nullptr ? *f.in_scale : 1.0);
     for (int y0 = 0; y0 < n2; y0 += TILX) {
       if (y0) __syncthreads();
-      PX::template run<TI, TC, TC, k2dThreads, TILX>(ax, static_cast<const C<TI>*>(f.in) + y0 * n1 * inner + b,
+      PX::template run<TI, TC, TC, NT, TILX>(ax, static_cast<const C<TI>*>(f.in) + y0 * n1 * inner + b,
                                                      G + y0 * Gs, b0, b1, twx, min(TILX, n2 - y0), sc);
     }
     __syncthreads();
+    after_l1();
+    DPROBE(1);
     PassArgs ay;  // level 2: slots y (n2 non-zero rows), columns kx -> u_hat[ky][kx][b]
     ay.L = L2; ay.n_lo = n2; ay.n_hi = 0; ay.n_out = L2; ay.in_sa = Gs; ay.in_cs = 1;
-    ay.out_sa = static_cast<int64_t>(L1) * inner; ay.out_cs = inner; ay.sign = f.sign;
+    ay.out_sa = kHatT ? L1 : static_cast<int64_t>(L1) * inner; ay.out_cs = kHatT ? 1 : inner; ay.sign = f.sign;
+    C<TO>* hat_b = static_cast<C<TO>*>(f.out) + (kHatT ? b * L1 * L2 : b);
     for (int k0 = 0; k0 < L1; k0 += TILY) {
       if (k0) __syncthreads();
-      PY::template run<TC, TC, TO, k2dThreads, TILY>(ay, G + k0, static_cast<C<TO>*>(f.out) + k0 * inner + b, b0,
-                                                     b1, twy, min(TILY, L1 - k0), static_cast<TC>(1));
+      PY::template run<TC, TC, TO, NT, TILY>(ay, G + k0, hat_b + k0 * ay.out_cs, p0, p1, twy, min(TILY, L1 - k0),
+                                             static_cast<TC>(1));
+      DPROBE(2 + k0 / TILY);
     }
   } else {
     PassArgs ay;  // inverse level 2 over all ky, keep y < n2 -> G[y][kx]
-    ay.L = L2; ay.n_lo = L2; ay.n_hi = 0; ay.n_out = n2; ay.in_sa = static_cast<int64_t>(L1) * inner; ay.in_cs = inner;
-    ay.out_sa = Gs; ay.out_cs = 1; ay.sign = f.sign;
+    ay.L = L2; ay.n_lo = L2; ay.n_hi = 0; ay.n_out = n2; ay.in_sa = kHatT ? L1 : static_cast<int64_t>(L1) * inner;
+    ay.in_cs = kHatT ? 1 : inner; ay.out_sa = Gs; ay.out_cs = 1; ay.sign = f.sign;
+    const C<TI>* hat_b = static_cast<const C<TI>*>(f.in) + (kHatT ? b * L1 * L2 : b);
     for (int k0 = 0; k0 < L1; k0 += TILY) {
       if (k0) __syncthreads();
-      PY::template run<TI, TC, TC, k2dThreads, TILY>(ay, static_cast<const C<TI>*>(f.in) + k0 * inner + b, G + k0,
-                                                     b0, b1, twy, min(TILY, L1 - k0), static_cast<TC>(1));
+      PY::template run<TI, TC, TC, NT, TILY>(ay, hat_b + k0 * ay.in_cs, G + k0, b0, b1, twy, min(TILY, L1 - k0),
+                                             static_cast<TC>(1));
+      DPROBE(1 + k0 / TILY);
     }
     __syncthreads();
     PassArgs ax;  // inverse level 1, keep x < n1, 1/(l1 l2) -> v[y][x][b]
@@ -598,10 +635,14 @@ __device__ __forceinline__ bool fft2d_body(const Fft2dArgs& f, unsigned char* sm
     ax.out_cs = n1 * inner; ax.sign = f.sign;
     for (int y0 = 0; y0 < n2; y0 += TILX) {
       if (y0) __syncthreads();
-      PX::template run<TC, TC, TO, k2dThreads, TILX>(ax, G + y0 * Gs, static_cast<C<TO>*>(f.out) + y0 * n1 * inner + b,
-                                                     b0, b1, twx, min(TILX, n2 - y0),
+      PX::template run<TC, TC, TO, NT, TILX>(ax, G + y0 * Gs, static_cast<C<TO>*>(f.out) + y0 * n1 * inner + b,
+                                                     p0, p1, twx, min(TILX, n2 - y0),
                                                      static_cast<TC>(1.0 / (static_cast<double>(L1) * L2)));
     }
+#ifdef TOEP_ORTH_PROBE
+    __syncthreads();
+#endif
+    DPROBE(4);
   }
   return true;
 }
@@ -636,10 +677,16 @@ int launch2d(bool inverse, const Fft2dArgs& f, cudaStream_t s) {
 // In the product phase the ring grows to 6 stages (the DFT's shared memory is free by then).
 // Warps 0-15 run the DFTs; warps 0-7 consume and warp 16 produces in the product phase, exactly
 // as binprod_tma_kernel (csrc/binprod.cu): a bin's 128 x 128 block streams in 8 whole-row stages.
+#ifndef TOEP_FUSED_PF_MODE
+#define TOEP_FUSED_PF_MODE 1  // 0: L2 prefetch at kernel start; 1: after the forward level-1 pass (its u loads do not queue behind it)
+#endif
 #ifndef TOEP_FUSED_PF_MB
 #define TOEP_FUSED_PF_MB 48  // L2 prefetch of the first bins in hand-out order
 #endif
-constexpr int kFusedThreads = k2dThreads + 32;
+#ifndef TOEP_FUSED_THREADS
+#define TOEP_FUSED_THREADS 1024
+#endif
+constexpr int kFusedThreads = TOEP_FUSED_THREADS;  // every warp runs the DFTs; the last one produces in the product phase
 constexpr int kFusedN0 = 128;
 constexpr int kFusedRB = 16;                                 // rows per 32 KB stage
 constexpr int kFusedStageElems = kFusedRB * kFusedN0;
@@ -648,35 +695,29 @@ constexpr int kFusedEarly = 3;                               // stages filled du
 constexpr int kFusedConsumers = 8;
 using FusedPX = Plan<4, 3, 5>;
 using FusedPY = Plan<4, 3, 5>;
-constexpr int kFusedTILX = 32, kFusedTILY = 32;
-using FusedSmem = Fft2dSmem<double, kFusedTILX, kFusedTILY, FusedPX, FusedPY>;
+constexpr int kFusedTILX = 32, kFusedTILY = 60;  // one tile per pass (n2 <= 30, all 60 level-2 columns)
 
 struct FusedArgs {
   Fft2dArgs fwd, inv;
   const double2* DT;  // [K][n0][n0], DT[k][j][m] = D_k[m][j]
-  double2* hat;       // [K][n0] forward DFT output
-  double2* hat2;      // [K][n0] product output
+  double2* hat;       // [n0][K] forward DFT output (column-major: each DFT CTA writes one contiguous run)
+  double2* hat2;      // [n0][K] product output
   int64_t K;
   unsigned* bar;      // grid barrier arrival counter (monotonic, zeroed once)
   int* work;          // dynamic bin hand-out counter (zero between launches)
   int64_t pf_bytes;   // L2 prefetch budget of the first bins in hand-out order
 };
 
-__host__ __device__ constexpr size_t fused_dft_bytes(int n2) {
-  return ((sizeof(double2) * (FusedPX::L + FusedPY::L + 2 * (FusedPX::L * kFusedTILX > FusedPY::L * kFusedTILY
-                                                                 ? FusedPX::L * kFusedTILX
-                                                                 : FusedPY::L * kFusedTILY) +
-                              static_cast<size_t>(n2) * (FusedPX::L | 1)) +
-           127) / 128) * 128;
-}
-__host__ __device__ constexpr size_t fused_region0(int n2) {  // DFT workspace / late ring stages
-  return fused_dft_bytes(n2) > sizeof(double2) * 3 * kFusedStageElems ? fused_dft_bytes(n2)
-                                                                      : sizeof(double2) * 3 * kFusedStageElems;
-}
-__host__ __device__ constexpr size_t fused_smem_bytes(int n2) {
-  return fused_region0(n2) + sizeof(double2) * (3 * kFusedStageElems + kFusedN0 + kFusedConsumers * kFusedN0) +
-         2 * kFusedStages * sizeof(uint64_t);
-}
+// Shared memory: region 0 holds the DFT workspace (twiddles + two 60 x 60 ping-pong buffers, the
+// level-1 intermediate aliased into one of them) and, in the product phase, ring stages 3..5 plus
+// the consumers' vector / reduction buffers; region 1 holds ring stages 0..2 (filled during the
+// forward DFT).
+constexpr size_t kFusedDftBytes = sizeof(double2) * (FusedPX::L + FusedPY::L + 2 * FusedPY::L * kFusedTILY);
+constexpr size_t kFusedLateBytes = sizeof(double2) * (3 * kFusedStageElems + kFusedN0 + kFusedConsumers * kFusedN0);
+constexpr size_t kFusedRegion0 = ((kFusedDftBytes > kFusedLateBytes ? kFusedDftBytes : kFusedLateBytes) + 127) / 128 * 128;
+constexpr size_t kFusedSmem = kFusedRegion0 + sizeof(double2) * 3 * kFusedStageElems + 2 * kFusedStages * sizeof(uint64_t);
+static_assert(FusedPX::L * kFusedTILX <= FusedPY::L * kFusedTILY && 30 * (FusedPX::L | 1) <= FusedPY::L * kFusedTILY,
+              "fused DFT buffers");
 
 __device__ __forceinline__ void fused_grid_barrier(unsigned* bar) {
   __syncthreads();
@@ -715,12 +756,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
 #endif
   FPROBE(0);
   extern __shared__ __align__(128) unsigned char fsm[];
-  const int n2 = a.fwd.n2;
   unsigned char* region0 = fsm;                                      // DFT workspace, later stages 3..5
-  Z* ring0 = reinterpret_cast<Z*>(fsm + fused_region0(n2));           // stages 0..2
-  Z* us = ring0 + 3 * kFusedStageElems;
+  Z* ring0 = reinterpret_cast<Z*>(fsm + kFusedRegion0);               // stages 0..2
+  Z* us = reinterpret_cast<Z*>(region0) + 3 * kFusedStageElems;       // product phase only
   Z* red = us + kFusedN0;
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + kFusedConsumers * kFusedN0);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring0 + 3 * kFusedStageElems);
   uint64_t* empty = full + kFusedStages;
   auto stage_ptr = [&](int st) -> Z* {
     return st < 3 ? ring0 + st * kFusedStageElems : reinterpret_cast<Z*>(region0) + (st - 3) * kFusedStageElems;
@@ -758,13 +798,18 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
     const uint64_t pol = policy_evict_first();
     for (int64_t q = 0; q < early; ++q) issue(q, first, pol);
   }
-  if (warp == 1) {
-    const int64_t bin_bytes = sizeof(Z) * kFusedN0 * kFusedN0;
-    const int64_t pf_bins = std::min<int64_t>(a.K, a.pf_bytes / bin_bytes);
-    for (int64_t k = blockIdx.x; k < pf_bins; k += gridDim.x)
-      for (int64_t off = lane * 32768; off < bin_bytes; off += 32 * 32768)
-        bulk_prefetch_l2(reinterpret_cast<const char*>(a.DT + k * kFusedN0 * kFusedN0) + off, 32768);
-  }
+  auto prefetch_heads = [&]() {
+    if (warp == 1) {
+      const int64_t bin_bytes = sizeof(Z) * kFusedN0 * kFusedN0;
+      const int64_t pf_bins = std::min<int64_t>(a.K, a.pf_bytes / bin_bytes);
+      for (int64_t k = blockIdx.x; k < pf_bins; k += gridDim.x)
+        for (int64_t off = lane * 32768; off < bin_bytes; off += 32 * 32768)
+          bulk_prefetch_l2(reinterpret_cast<const char*>(a.DT + k * kFusedN0 * kFusedN0) + off, 32768);
+    }
+  };
+#if TOEP_FUSED_PF_MODE == 0
+  prefetch_heads();
+#endif
   pdl_wait();
   FPROBE(1);
   if (a.fwd.stop != nullptr && *a.fwd.stop != 0) {  // uniform across the grid: no barrier is reached
@@ -774,8 +819,16 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
   }
   // ---- phase 1: forward 2-D DFT of batch column b (CTAs beyond the batch only take the barriers)
   if (blockIdx.x < a.fwd.inner)
-    fft2d_body<double, double, double, kFusedTILX, kFusedTILY, FusedPX, FusedPY, false>(a.fwd, region0, blockIdx.x,
-                                                                                         false);
+    fft2d_body<double, double, double, kFusedTILX, kFusedTILY, FusedPX, FusedPY, false, true, kFusedThreads, true>(a.fwd, region0,
+                                                                                               blockIdx.x, false
+#if TOEP_FUSED_PF_MODE == 1
+                                                                                         , prefetch_heads
+#endif
+    );
+#if TOEP_FUSED_PF_MODE == 1
+  else
+    prefetch_heads();
+#endif
   FPROBE(2);
   fused_grid_barrier(a.bar);
   FPROBE(3);
@@ -806,8 +859,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
       mbar_wait(&full[st0], static_cast<uint32_t>((q / kFusedStages) & 1));
       const int it = item_of[st0];
       if (it < 0) break;
-      for (int t = threadIdx.x; t < kFusedN0; t += kFusedConsumers * 32)
-        us[t] = __ldcg(a.hat + static_cast<int64_t>(it) * kFusedN0 + t);
+      for (int t = threadIdx.x; t < kFusedN0; t += kFusedConsumers * 32)  // u_hat column-major: [b][k]
+        us[t] = __ldcg(a.hat + static_cast<int64_t>(t) * a.K + it);
       consumers_sync();
       Z acc[MPL];
 #pragma unroll
@@ -833,7 +886,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
         Z sum = red[t];
 #pragma unroll
         for (int ww = 1; ww < kFusedConsumers; ++ww) sum = cadd(sum, red[ww * kFusedN0 + t]);
-        a.hat2[static_cast<int64_t>(it) * kFusedN0 + t] = sum;
+        a.hat2[static_cast<int64_t>(t) * a.K + it] = sum;
       }
       consumers_sync();
     }
@@ -844,16 +897,23 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(a.work, 0);  // every CTA is past phase 2
   // ---- phase 3: inverse 2-D DFT, crop, 1/(l1 l2) of batch column b
   if (blockIdx.x < a.inv.inner)
-    fft2d_body<double, double, double, kFusedTILX, kFusedTILY, FusedPX, FusedPY, true>(a.inv, region0, blockIdx.x,
-                                                                                        false);
+    fft2d_body<double, double, double, kFusedTILX, kFusedTILY, FusedPX, FusedPY, true, true, kFusedThreads, true>(a.inv, region0,
+                                                                                              blockIdx.x, false);
 #ifdef TOEP_ORTH_PROBE
   FPROBE(6);
   __shared__ unsigned fcall;
   if (threadIdx.x == 0 && blockIdx.x == 0) fcall = atomicAdd(&g_fused_calls, 1);
   __syncthreads();
   if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 140) && (fcall % 200) == 150)
+  {
     printf("fused cta %d: start->pdl %lld dft %lld bar1 %lld product %lld bar2 %lld inv %lld ns\n", blockIdx.x,
            fpt[1] - fpt[0], fpt[2] - fpt[1], fpt[3] - fpt[2], fpt[4] - fpt[3], fpt[5] - fpt[4], fpt[6] - fpt[5]);
+    const long long* f0 = g_dft_ts[0][blockIdx.x];
+    const long long* f1 = g_dft_ts[1][blockIdx.x];
+    printf("  fwd cta %d: pdl->tw %lld lvl1 %lld lvl2a %lld lvl2b %lld | inv: tw %lld lvl2a %lld lvl2b %lld lvl1 %lld ns\n",
+           blockIdx.x, f0[0] - fpt[1], f0[1] - f0[0], f0[2] - f0[1], f0[3] - f0[2], f1[0] - fpt[5], f1[1] - f1[0],
+           f1[2] - f1[1], f1[4] - f1[2]);
+  }
 #endif
 }
 
@@ -1065,7 +1125,7 @@ int matvec_fused(const void* DT, int64_t K, int n2, int n1, int l2, int l1, int 
                  void* hat2, void* v, unsigned* bar, const double* in_scale, const int* stop, const L2Prefetch& pf,
                  cudaStream_t s) {
   if (n0 != kFusedN0 || l2 != 60 || l1 != 60 || n2 > 30 || n1 > 30 || bar == nullptr) return -1;
-  const size_t smem = fused_smem_bytes(n2);
+  const size_t smem = kFusedSmem;
   if (smem > 227 * 1024) return -1;
   static int sms = 0;
   if (sms == 0) {
