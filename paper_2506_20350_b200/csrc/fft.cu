@@ -564,27 +564,29 @@ struct NoHook {
 template <typename TI, typename TC, typename TO, int TILX, int TILY, typename PX, typename PY, bool INV,
           bool kAliasG = false, int NT = k2dThreads, bool kHatT = false, typename AfterL1 = NoHook>
 __device__ __forceinline__ bool fft2d_body(const Fft2dArgs& f, unsigned char* smem_raw, int64_t b, bool wait,
-                                           AfterL1 after_l1 = {}) {
+                                           AfterL1 after_l1 = {}, const C<TC>* tw_given = nullptr) {
   using Z = C<TC>;
   using S = Fft2dSmem<TC, TILX, TILY, PX, PY>;
   constexpr int L1 = PX::L, L2 = PY::L;
   static_assert(!kAliasG || (PX::kStages == 3 && PY::kStages == 3), "G aliasing assumes three-stage plans");
   static_assert(!kAliasG || TILY >= PX::L, "G aliasing needs single-tile level-2 passes (the caller keeps n2 <= TILX)");
-  Z* twx = reinterpret_cast<Z*>(smem_raw);
-  Z* twy = twx + L1;
-  Z* b0 = twy + L2;
+  // twiddles: computed here, or a table of the right sign the caller built earlier (L1 == L2)
+  Z* twx = tw_given != nullptr ? const_cast<Z*>(tw_given) : reinterpret_cast<Z*>(smem_raw);
+  Z* twy = tw_given != nullptr ? twx : twx + L1;
+  Z* b0 = reinterpret_cast<Z*>(smem_raw) + L1 + L2;
   Z* b1 = b0 + S::kBuf;
   Z* G = kAliasG ? b1 : b1 + S::kBuf;  // [n2][kGs]
   Z* p0 = kAliasG ? b1 : b0;  // ping-pong order of the second pass
   Z* p1 = kAliasG ? b0 : b1;
   constexpr int Gs = S::kGs;
-  for (int t = threadIdx.x; t < L1 + L2; t += NT) {
-    const int L = t < L1 ? L1 : L2;
-    const int tt = t < L1 ? t : t - L1;
-    TC s, c;
-    sincospi_t<TC>(static_cast<TC>(2.0 * tt / L), &s, &c);
-    (t < L1 ? twx[tt] : twy[tt]) = mk<TC>(c, f.sign * s);
-  }
+  if (tw_given == nullptr)
+    for (int t = threadIdx.x; t < L1 + L2; t += NT) {
+      const int L = t < L1 ? L1 : L2;
+      const int tt = t < L1 ? t : t - L1;
+      TC s, c;
+      sincospi_t<TC>(static_cast<TC>(2.0 * tt / L), &s, &c);
+      (t < L1 ? twx[tt] : twy[tt]) = mk<TC>(c, f.sign * s);
+    }
   if (wait) {
     pdl_wait();
     if (f.stop != nullptr && *f.stop != 0) return false;
@@ -677,9 +679,6 @@ int launch2d(bool inverse, const Fft2dArgs& f, cudaStream_t s) {
 // In the product phase the ring grows to 6 stages (the DFT's shared memory is free by then).
 // Warps 0-15 run the DFTs; warps 0-7 consume and warp 16 produces in the product phase, exactly
 // as binprod_tma_kernel (csrc/binprod.cu): a bin's 128 x 128 block streams in 8 whole-row stages.
-#ifndef TOEP_FUSED_PF_MODE
-#define TOEP_FUSED_PF_MODE 1  // 0: L2 prefetch at kernel start; 1: after the forward level-1 pass (its u loads do not queue behind it)
-#endif
 #ifndef TOEP_FUSED_PF_MB
 #define TOEP_FUSED_PF_MB 48  // L2 prefetch of the first bins in hand-out order
 #endif
@@ -798,6 +797,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
     const uint64_t pol = policy_evict_first();
     for (int64_t q = 0; q < early; ++q) issue(q, first, pol);
   }
+  // twiddle table of the inverse transform (L1 = L2 = 60), built by warps that idle in the product
+  // phase, so the inverse DFT after the second grid barrier starts at once
+  __shared__ Z tw_inv[60];
+  // The L2 prefetch of the first bins (in hand-out order, 48 MB) is issued by each DFT CTA after its
+  // forward level-1 pass, so that pass's vector loads do not queue behind it in HBM (CTAs without a
+  // batch column issue their share at once).  Issuing it from the 20 idle CTAs alone, once every
+  // level-1 pass is done, measured 10 us at the first grid barrier: the bulk prefetches back-pressure
+  // the issuing SM, so the stream must be spread over all of them.
   auto prefetch_heads = [&]() {
     if (warp == 1) {
       const int64_t bin_bytes = sizeof(Z) * kFusedN0 * kFusedN0;
@@ -807,9 +814,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
           bulk_prefetch_l2(reinterpret_cast<const char*>(a.DT + k * kFusedN0 * kFusedN0) + off, 32768);
     }
   };
-#if TOEP_FUSED_PF_MODE == 0
-  prefetch_heads();
-#endif
   pdl_wait();
   FPROBE(1);
   if (a.fwd.stop != nullptr && *a.fwd.stop != 0) {  // uniform across the grid: no barrier is reached
@@ -819,16 +823,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
   }
   // ---- phase 1: forward 2-D DFT of batch column b (CTAs beyond the batch only take the barriers)
   if (blockIdx.x < a.fwd.inner)
-    fft2d_body<double, double, double, kFusedTILX, kFusedTILY, FusedPX, FusedPY, false, true, kFusedThreads, true>(a.fwd, region0,
-                                                                                               blockIdx.x, false
-#if TOEP_FUSED_PF_MODE == 1
-                                                                                         , prefetch_heads
-#endif
-    );
-#if TOEP_FUSED_PF_MODE == 1
+    fft2d_body<double, double, double, kFusedTILX, kFusedTILY, FusedPX, FusedPY, false, true, kFusedThreads, true>(
+        a.fwd, region0, blockIdx.x, false, prefetch_heads);
   else
     prefetch_heads();
-#endif
   FPROBE(2);
   fused_grid_barrier(a.bar);
   FPROBE(3);
@@ -852,7 +850,13 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
         issue(q, k, pol);
       }
     }
-  } else if (warp < kFusedConsumers) {  // consumers: lane = output row m (4 per lane), warp = row slice
+  } else if (warp >= kFusedConsumers) {  // idle in this phase: the inverse DFT's twiddles
+    for (int t = threadIdx.x - kFusedConsumers * 32; t < 60; t += 32 * (kFusedThreads / 32 - 1 - kFusedConsumers)) {
+      double sn, cs;
+      sincospi(2.0 * t / 60, &sn, &cs);
+      tw_inv[t] = make_double2(cs, a.inv.sign * sn);
+    }
+  } else {  // consumers: lane = output row m (4 per lane), warp = row slice
     constexpr int MPL = kFusedN0 / 32;
     for (int64_t q = 0;; q += nrb) {
       const int st0 = static_cast<int>(q % kFusedStages);
@@ -897,8 +901,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(a.work, 0);  // every CTA is past phase 2
   // ---- phase 3: inverse 2-D DFT, crop, 1/(l1 l2) of batch column b
   if (blockIdx.x < a.inv.inner)
-    fft2d_body<double, double, double, kFusedTILX, kFusedTILY, FusedPX, FusedPY, true, true, kFusedThreads, true>(a.inv, region0,
-                                                                                              blockIdx.x, false);
+    fft2d_body<double, double, double, kFusedTILX, kFusedTILY, FusedPX, FusedPY, true, true, kFusedThreads, true>(
+        a.inv, region0, blockIdx.x, false, NoHook{}, tw_inv);
 #ifdef TOEP_ORTH_PROBE
   FPROBE(6);
   __shared__ unsigned fcall;
