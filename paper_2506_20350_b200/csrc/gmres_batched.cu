@@ -102,42 +102,78 @@ __global__ void __launch_bounds__(kCols) kb_dots_gram(const double2* const* __re
 }
 
 // h1[l][c] = sum_chunk partial; Gram column G[l][m-1] = sum_chunk partial2 (stored with its conjugate
-// row; gram[(k*ldr + l)*W + c] = G[l][k])
-__global__ void kb_reduce_gram(const double2* __restrict__ partial, const double2* __restrict__ partial2, int m,
-                               int nchunks, int W, double2* __restrict__ h1, double2* __restrict__ gram, int ldr,
-                               const int* __restrict__ stop) {
+// row; gram[(k*ldr + l)*W + c] = G[l][k]).  CTA (column tile of 32, l): warp g sums chunks g, g+8, ...
+// in order, then warp 0 adds the 8 group sums in order (fixed, run-to-run identical).  A thread per
+// (l, c) walking all row chunks serially was latency-bound: 1.5 ms per step at cfg3.
+constexpr int kRedGroups = 8;
+__global__ void __launch_bounds__(kRedGroups * 32) kb_reduce_gram(const double2* __restrict__ partial,
+                                                                  const double2* __restrict__ partial2, int m,
+                                                                  int nchunks, int W, double2* __restrict__ h1,
+                                                                  double2* __restrict__ gram, int ldr,
+                                                                  const int* __restrict__ stop) {
   pdl_wait();
   pdl_trigger();
-  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (t >= static_cast<int64_t>(m) * W) return;
-  const int l = static_cast<int>(t / W), c = static_cast<int>(t - static_cast<int64_t>(l) * W);
-  if (stop[c]) return;
+  __shared__ double2 r1[kRedGroups][32], r2[kRedGroups][32];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane, l = blockIdx.y;
   double2 s1 = make_double2(0, 0), s2 = make_double2(0, 0);
-  for (int ch = 0; ch < nchunks; ++ch) {
-    s1 = cadd(s1, partial[(static_cast<int64_t>(l) * nchunks + ch) * W + c]);
-    s2 = cadd(s2, partial2[(static_cast<int64_t>(l) * nchunks + ch) * W + c]);
+  if (c < W && !stop[c]) {
+    const double2* p1 = partial + static_cast<int64_t>(l) * nchunks * W + c;
+    const double2* p2 = partial2 + static_cast<int64_t>(l) * nchunks * W + c;
+    for (int ch = grp; ch < nchunks; ch += kRedGroups) {
+      s1 = cadd(s1, p1[static_cast<int64_t>(ch) * W]);
+      s2 = cadd(s2, p2[static_cast<int64_t>(ch) * W]);
+    }
+  }
+  r1[grp][lane] = s1;
+  r2[grp][lane] = s2;
+  __syncthreads();
+  if (grp != 0 || c >= W || stop[c]) return;
+#pragma unroll
+  for (int g = 1; g < kRedGroups; ++g) {
+    s1 = cadd(s1, r1[g][lane]);
+    s2 = cadd(s2, r2[g][lane]);
   }
   h1[static_cast<int64_t>(l) * W + c] = s1;
   gram[(static_cast<int64_t>(m - 1) * ldr + l) * W + c] = s2;
   gram[(static_cast<int64_t>(l) * ldr + (m - 1)) * W + c] = make_double2(s2.x, -s2.y);
 }
 
-// per column: h = h1 + (h1 - G h1) (the second CGS pass from the Gram matrix) -> h, Hessenberg column
+// nsum[c] = sum_chunk part[chunk][c] (squared-norm partials), same fixed-order two-level reduction;
+// the per-column kernels (init, cycle start, Givens) then read one value per column
+__global__ void __launch_bounds__(kRedGroups * 32) kb_norm_reduce(const double* __restrict__ part, int nchunks, int W,
+                                                                  double* __restrict__ nsum) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double r[kRedGroups][32];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  double sacc = 0.0;
+  if (c < W)
+    for (int ch = grp; ch < nchunks; ch += kRedGroups) sacc += part[static_cast<int64_t>(ch) * W + c];
+  r[grp][lane] = sacc;
+  __syncthreads();
+  if (grp != 0 || c >= W) return;
+#pragma unroll
+  for (int g = 1; g < kRedGroups; ++g) sacc += r[g][lane];
+  nsum[c] = sacc;
+}
+
+// per column: h = h1 + (h1 - G h1) (the second CGS pass from the Gram matrix) -> h, Hessenberg column;
+// one thread per (column, l)
 __global__ void kb_coef_gram(const double2* __restrict__ h1, const double2* __restrict__ gram, int m, int ldr, int W,
                              double2* __restrict__ h, double2* __restrict__ hcol, const int* __restrict__ stop) {
   pdl_wait();
   pdl_trigger();
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x, l = blockIdx.y;
   if (c >= W || stop[c]) return;
-  for (int l = 0; l < m; ++l) {
-    double2 t = make_double2(0, 0);
-    for (int k = 0; k < m; ++k)
-      cfma(t, gram[(static_cast<int64_t>(k) * ldr + l) * W + c], h1[static_cast<int64_t>(k) * W + c]);
-    const double2 a = h1[static_cast<int64_t>(l) * W + c];
-    const double2 hv = make_double2(2.0 * a.x - t.x, 2.0 * a.y - t.y);
-    h[static_cast<int64_t>(l) * W + c] = hv;
-    hcol[static_cast<int64_t>(l) * W + c] = hv;
-  }
+  double2 t = make_double2(0, 0);
+  for (int k = 0; k < m; ++k)
+    cfma(t, gram[(static_cast<int64_t>(k) * ldr + l) * W + c], h1[static_cast<int64_t>(k) * W + c]);
+  const double2 a = h1[static_cast<int64_t>(l) * W + c];
+  const double2 hv = make_double2(2.0 * a.x - t.x, 2.0 * a.y - t.y);
+  h[static_cast<int64_t>(l) * W + c] = hv;
+  hcol[static_cast<int64_t>(l) * W + c] = hv;
 }
 
 // w[:, c] -= sum_l V_l[:, c] h[l][c]  (active columns); mode 1: partial dots of the result,
@@ -455,6 +491,7 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
       std::max<int64_t>(1, std::min<int64_t>(n / 16, (chunk_mult * sms + ctiles - 1) / ctiles)));
   const int g1 = static_cast<int>(std::min<int64_t>((N + 255) / 256, 8 * sms));
   const int gc = (W + 127) / 128;
+  const int gr = (W + 31) / 32;  // column tiles of the partial reductions
   const bool per_step_pc = p->precond == TOEP_PC_BLOCK;
   const bool io64 = p->op->dtype == TOEP_C64;
 
@@ -462,7 +499,7 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
   double2 *w = nullptr, *tmp = nullptr, *pb = nullptr, *h1 = nullptr, *h2 = nullptr, *rcols = nullptr;
   double2 *sn = nullptr, *g = nullptr, *y = nullptr, *part = nullptr;
   double2 *part2 = nullptr, *gram = nullptr;  // one-sweep CGS2: Gram-column partials, per-column Gram matrices
-  double *cs = nullptr, *hist = nullptr, *inv = nullptr, *npart = nullptr;
+  double *cs = nullptr, *hist = nullptr, *inv = nullptr, *npart = nullptr, *nsum = nullptr;
   double2** Vp = nullptr;
   int *ran = nullptr, *active = nullptr;
   BCol st{};
@@ -471,7 +508,7 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
   auto cleanup = [&]() {
     for (auto v : Vh) cudaFreeAsync(v, s);
     for (void* q : {(void*)w, (void*)tmp, (void*)pb, (void*)h1, (void*)h2, (void*)rcols, (void*)sn, (void*)g, (void*)y,
-                    (void*)part, (void*)cs, (void*)hist, (void*)inv, (void*)npart, (void*)Vp, (void*)ran,
+                    (void*)part, (void*)cs, (void*)hist, (void*)inv, (void*)npart, (void*)nsum, (void*)Vp, (void*)ran,
                     (void*)part2, (void*)gram, (void*)active, (void*)st.beta0, (void*)st.stop, (void*)st.conv, (void*)st.brk, (void*)st.m,
                     (void*)st.total, (void*)st.nhist})
       if (q) cudaFreeAsync(q, s);
@@ -509,6 +546,7 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
   B_ALLOC(y, static_cast<int64_t>(ldr) * W);
   B_ALLOC(part, static_cast<int64_t>(ldr) * nchunks * W);
   B_ALLOC(npart, static_cast<int64_t>(nchunks) * W);
+  B_ALLOC(nsum, W);
   B_ALLOC(hist, (max_total + 2) * W);
   B_ALLOC(inv, W);
   B_ALLOC(ran, W);
@@ -554,7 +592,8 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
     zb = pb;
   }
   B_TRY(launch_k(kb_norm, gridc, dim3(kCols), 0, s, zb, n, W, nchunks, npart));
-  B_TRY(launch_k(kb_init, dim3(gc), dim3(128), 0, s, st, (const double*)npart, nchunks, W, hist));
+  B_TRY(launch_k(kb_norm_reduce, dim3(gr), dim3(kRedGroups * 32), 0, s, (const double*)npart, nchunks, W, nsum));
+  B_TRY(launch_k(kb_init, dim3(gc), dim3(128), 0, s, st, (const double*)nsum, 1, W, hist));
   TOEP_CUDA(cudaMemsetAsync(x, 0, N * sizeof(double2), s));
   B_TRY(ensure_basis(1));
 
@@ -576,7 +615,8 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
       z = w;
     }
     B_TRY(launch_k(kb_norm, gridc, dim3(kCols), 0, s, z, n, W, nchunks, npart));
-    B_TRY(launch_k(kb_cycle_start, dim3(gc), dim3(128), 0, s, st, (const double*)npart, nchunks, W, cfg->tol, g, inv,
+    B_TRY(launch_k(kb_norm_reduce, dim3(gr), dim3(kRedGroups * 32), 0, s, (const double*)npart, nchunks, W, nsum));
+    B_TRY(launch_k(kb_cycle_start, dim3(gc), dim3(128), 0, s, st, (const double*)nsum, 1, W, cfg->tol, g, inv,
                    first ? 1 : 0, active));
     B_TRY(launch_k(kb_mark_running, dim3(gc), dim3(128), 0, s, (const BCol)st, ran, W));
     B_TRY(launch_k(kb_scale, dim3(g1), dim3(256), 0, s, Vh[0], (const double*)inv, n, W, z));
@@ -594,16 +634,16 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
       } else {
         B_TRY(matvec_impl(p->op, Vh[j], w, W, false, io64, nullptr, s));
       }
-      const int rg = static_cast<int>((static_cast<int64_t>(m) * W + 255) / 256);
       B_TRY(launch_k(kb_dots_gram, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)w, n, W,
                      nchunks, part, part2));
-      B_TRY(launch_k(kb_reduce_gram, dim3(rg), dim3(256), 0, s, (const double2*)part, (const double2*)part2, m,
-                     nchunks, W, h1, gram, ldr, (const int*)st.stop));
-      B_TRY(launch_k(kb_coef_gram, dim3(gc), dim3(128), 0, s, (const double2*)h1, (const double2*)gram, m, ldr, W,
+      B_TRY(launch_k(kb_reduce_gram, dim3(gr, m), dim3(kRedGroups * 32), 0, s, (const double2*)part,
+                     (const double2*)part2, m, nchunks, W, h1, gram, ldr, (const int*)st.stop));
+      B_TRY(launch_k(kb_coef_gram, dim3(gc, m), dim3(128), 0, s, (const double2*)h1, (const double2*)gram, m, ldr, W,
                      h2, rcols + static_cast<int64_t>(j) * ldr * W, (const int*)st.stop));
       B_TRY(launch_k(kb_upd, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)h2, w, n,
                      W, nchunks, 2, (double2*)nullptr, npart, (const int*)st.stop));
-      B_TRY(launch_k(kb_givens, dim3(gc), dim3(128), 0, s, st, (const double*)npart, nchunks, W, rcols, ldr, cs, sn, g,
+      B_TRY(launch_k(kb_norm_reduce, dim3(gr), dim3(kRedGroups * 32), 0, s, (const double*)npart, nchunks, W, nsum));
+      B_TRY(launch_k(kb_givens, dim3(gc), dim3(128), 0, s, st, (const double*)nsum, 1, W, rcols, ldr, cs, sn, g,
                      hist, inv, cfg->tol, static_cast<int>(max_total), cycle_len, active));
       B_TRY(launch_k(kb_scale, dim3(g1), dim3(256), 0, s, Vh[j + 1], (const double*)inv, n, W, (const double2*)w));
       TOEP_CUDA(cudaMemcpyAsync(active_host, active, sizeof(int), cudaMemcpyDeviceToHost, s));
