@@ -742,6 +742,7 @@ __device__ __forceinline__ void fused_grid_barrier(unsigned* bar) {
 
 #ifdef TOEP_ORTH_PROBE
 __device__ unsigned g_fused_calls;
+__device__ long long g_fend[160];
 #define FPROBE(i) \
   if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fpt[i]))
 #else
@@ -816,6 +817,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
   };
   pdl_wait();
   FPROBE(1);
+#ifdef TOEP_ORTH_PROBE
+  long long prev_max = 0, prev_min = 0;
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    prev_min = 1ll << 62;
+    for (int i = 0; i < gridDim.x; ++i) {
+      const long long e = *(volatile long long*)&g_fend[i];
+      prev_max = e > prev_max ? e : prev_max;
+      prev_min = e < prev_min ? e : prev_min;
+    }
+  }
+#endif
   if (a.fwd.stop != nullptr && *a.fwd.stop != 0) {  // uniform across the grid: no barrier is reached
     if (threadIdx.x == 0)
       for (int64_t q = 0; q < early; ++q) mbar_wait(&full[q % kFusedStages], 0);  // no copy outlives the CTA
@@ -912,11 +924,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) mv_fused_kernel(FusedArgs a)
   {
     printf("fused cta %d: start->pdl %lld dft %lld bar1 %lld product %lld bar2 %lld inv %lld ns\n", blockIdx.x,
            fpt[1] - fpt[0], fpt[2] - fpt[1], fpt[3] - fpt[2], fpt[4] - fpt[3], fpt[5] - fpt[4], fpt[6] - fpt[5]);
+    if (blockIdx.x == 0)
+      printf("  previous launch: CTA exits spread %lld ns, last exit -> this CTA start %lld ns\n", prev_max - prev_min,
+             fpt[0] - prev_max);
     const long long* f0 = g_dft_ts[0][blockIdx.x];
     const long long* f1 = g_dft_ts[1][blockIdx.x];
     printf("  fwd cta %d: pdl->tw %lld lvl1 %lld lvl2a %lld lvl2b %lld | inv: tw %lld lvl2a %lld lvl2b %lld lvl1 %lld ns\n",
            blockIdx.x, f0[0] - fpt[1], f0[1] - f0[0], f0[2] - f0[1], f0[3] - f0[2], f1[0] - fpt[5], f1[1] - f1[0],
            f1[2] - f1[1], f1[4] - f1[2]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_fend[blockIdx.x] = t;
   }
 #endif
 }
