@@ -258,6 +258,16 @@ def count_launches(step, reps: int = 4) -> int:
     return round(n / reps)
 
 
+def _warm_calls(fn, n_min, seconds):
+    """Untimed warm-up: at least n_min calls and at least `seconds` of calls."""
+    t_end = time.perf_counter() + seconds
+    i = 0
+    while i < n_min or time.perf_counter() < t_end:
+        fn()
+        i += 1
+    return i
+
+
 def _percall(fn, n):
     """Per-call host wall times (each call ends with its own synchronisation) plus the total."""
     ts = []
@@ -497,8 +507,11 @@ def run_ours(args):
     # pinned blocks at 17-19 GB/s on these boxes, cudaHostAlloc blocks at 50 GB/s (tools/hostbuf_probe.py)
     u_host = pin(dense_rhs(DIM, seed=1)[:, None])
     out_host = pinned_empty(u_host.shape, u_host.dtype)
-    for _ in range(max(args.warmup, 50)):  # host path warm-up: page-locked blocks, driver state
-        matvec(spec, u_host, out=out_host)
+    # host path warm-up: page-locked blocks, driver state, and the host core's clock — the calling
+    # thread's core needs ~0.5-1 s of activity before a call settles at its steady cost (measured
+    # ~310 us per call for the first ~2 500 calls of a process, 235 us after; tools/e2e_warm.py), so
+    # the warm-up runs for at least 1 s of calls (and at least W calls)
+    _warm_calls(lambda: matvec(spec, u_host, out=out_host), args.warmup, 1.0)
     torch.cuda.synchronize()
     barrier()
     x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -514,8 +527,11 @@ def run_ours(args):
     # the reference's own calling convention: numpy in, numpy out (fresh result per call)
     u_np = dense_rhs(DIM, seed=1)
     r_np = None
-    for _ in range(args.warmup):
+
+    def np_warm():
+        nonlocal r_np
         r_np = matvec(spec, u_np)
+    _warm_calls(np_warm, args.warmup, 0.3)
     torch.cuda.synchronize()
     barrier()
 
