@@ -691,12 +691,13 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   if (fail_step) *fail_step = -1;
 
   double2 *g = nullptr, *h = nullptr, *gtmp = nullptr, *lu0 = nullptr, *lu12 = nullptr, *wide = nullptr;
+  double2 *d12 = nullptr, *num_save = nullptr;  // unfactored D1 / D2; copies of the step's H / G numerators
   int *piv0 = nullptr, *piv12 = nullptr, *info = nullptr;
   double *wplanes = nullptr, *scr = nullptr;  // 3M: planes of the wide blocks; per-stream B / T scratch
   // side stream: the block sums that do not depend on the step's LU factors run on it while the
   // (latency-bound, few-SM) cluster LU of D1/D2 runs on `st`
   cudaStream_t s2 = nullptr;
-  cudaEvent_t ev_step = nullptr, ev_sums = nullptr;
+  cudaEvent_t ev_step = nullptr, ev_sums = nullptr, ev_solved = nullptr;
   constexpr bool overlap = true;  // side stream for the LU-independent block sums (265 vs 287 ms at cfg5)
   auto cleanup = [&]() {
     if (s2 != nullptr) {
@@ -705,8 +706,9 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     }
     if (ev_step != nullptr) cudaEventDestroy(ev_step);
     if (ev_sums != nullptr) cudaEventDestroy(ev_sums);
+    if (ev_solved != nullptr) cudaEventDestroy(ev_solved);
     for (void* q : {(void*)g, (void*)h, (void*)gtmp, (void*)lu0, (void*)lu12, (void*)wide, (void*)piv0, (void*)piv12,
-                    (void*)info, (void*)wplanes, (void*)scr})
+                    (void*)info, (void*)wplanes, (void*)scr, (void*)d12, (void*)num_save})
       if (q) cudaFreeAsync(q, st);
     cudaStreamSynchronize(st);
   };
@@ -734,6 +736,8 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   R_ALLOC(gtmp, N * ss);
   R_ALLOC(lu0, ss);
   R_ALLOC(lu12, 2 * ss);  // D1, D2 factored together
+  R_ALLOC(d12, 2 * ss);
+  R_ALLOC(num_save, 4 * ss);  // two sets by step parity (the side stream fills the next while st reads this)
   R_ALLOC(piv0, s);
   R_ALLOC(piv12, 2 * s);
   R_ALLOC(info, 2);
@@ -808,19 +812,22 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     TOEP_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
     TOEP_CUDA(cudaEventCreateWithFlags(&ev_step, cudaEventDisableTiming));
     TOEP_CUDA(cudaEventCreateWithFlags(&ev_sums, cudaEventDisableTiming));
+    TOEP_CUDA(cudaEventCreateWithFlags(&ev_solved, cudaEventDisableTiming));
   }
   cudaStream_t ss2 = s2 != nullptr ? s2 : st;
   // C_b (+)= alpha * A_{m-1-b} @ B for b = 0..m-1 (A blocks s x s stacked, reversed), one batched GEMM
-  auto rev_batched = [&](const double2* Astack, int m, const double2* B, int64_t ncol, double2* C, int64_t c_bs) {
+  auto rev_batched = [&](const double2* Astack, int m, const double2* B, int64_t ncol, double2* C, int64_t c_bs,
+                         cudaStream_t sx) {
     if (use3m && ncol == s && c_bs == ss) {  // C stack -= reversed A stack x B, as 3 batched real GEMMs
-      TOEP_TRY(split3(Astack, static_cast<int64_t>(m) * s, s, s, bsc[0], st));       // A stack planes
-      const Planes bb = tsc[0].at(static_cast<int64_t>(m) * ss);                       // B planes after T
-      TOEP_TRY(split3(B, s, s, s, bb, st));
-      TOEP_TRY(gemm3(s, s, s, bsc[0].at(static_cast<int64_t>(m - 1) * ss), -ss, bb, 0, tsc[0], ss, m, st));
-      return combine3(tsc[0], static_cast<int64_t>(m) * s, s, C, s, -1.0, st);
+      const int k = sx == st ? 0 : 1;  // the stream's own scratch planes
+      TOEP_TRY(split3(Astack, static_cast<int64_t>(m) * s, s, s, bsc[k], sx));       // A stack planes
+      const Planes bb = tsc[k].at(static_cast<int64_t>(m) * ss);                       // B planes after T
+      TOEP_TRY(split3(B, s, s, s, bb, sx));
+      TOEP_TRY(gemm3(s, s, s, bsc[k].at(static_cast<int64_t>(m - 1) * ss), -ss, bb, 0, tsc[k], ss, m, sx));
+      return combine3(tsc[k], static_cast<int64_t>(m) * s, s, C, s, -1.0, sx);
     }
     return gemm(TOEP_C128, s, ncol, s, mone, Astack + static_cast<int64_t>(m - 1) * ss, s, 1, -ss, B, ncol, 1, 0, one,
-                C, ncol, 1, c_bs, m, st);
+                C, ncol, 1, c_bs, m, sx);
   };
 
   // base stage (rybicki.py:94-108)
@@ -839,19 +846,40 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   }
   R_TRY(stage_hook(1));
 
+  // Denominators.  The reference forms d1 = sum_{k<=m} R_k G_k - R_0 and d2 = sum_{k<=m} R_-k H_k - R_0
+  // afresh every step (rybicki.py:114,125), two block sums of depth m*s.  Substituting the step's
+  // cross-updates G_k' = G_k - H_{m+1-k} G_new, G_{m+1}' = G_new (and H_k' likewise) into the next
+  // step's sums gives, exactly in exact arithmetic,
+  //     d1(m+1) = d1(m) - hnum(m) G_new(m),    d2(m+1) = d2(m) - gnum(m) H_new(m),
+  // with hnum = sum_j R_{m+1-j} H_j - R_{m+1} and gnum = sum_j R_{j-m-1} G_j - R_-(m+1) the
+  // numerators this step already forms (rybicki.py:126-127): one s x s product each instead of a
+  // depth-m*s sum, a third fewer tensor-core flops over the solve.  It also takes the next LU off
+  // the cross-updates' path: D1 / D2 are ready as soon as the step's solves are, so the (few-SM,
+  // latency-bound) cluster LU of step m+1 runs on `st` while the side stream does step m's x and
+  // G / H cross-updates and step m+1's block sums.
+  double2 *D1 = d12, *D2 = d12 + ss;
+  if (N > 1) {
+    R_TRY(copy_neg(rb(0), D1, ss, -1.0, st));
+    R_TRY(wide_gemm(Wp, 0, 1, g, s, D1, st));
+    if (N > 2) {
+      R_TRY(copy_neg(rb(0), D2, ss, -1.0, st));
+      R_TRY(wide_gemm(Wn, 0, 1, h, s, D2, st));
+    }
+  }
   for (int m = 1; m < N; ++m) {
     const bool more = m < N - 1;
     double2* xn = x + m * sw;
     double2* gnew = gtmp + m * ss;  // slot m of the next G stack
     double2* hnew = h + m * ss;     // slot m of H
-    // Right-hand sides of this step's three solves (independent of the D1/D2 factors), on the
-    // side stream once the previous step's updates are done:
-    //   x_{m+1} <- sum_j R_{m+1-j} x_j - y_{m+1},  G_new <- sum_j R_{j-m-1} G_j - R_{-(m+1)},
-    //   H_new <- sum_j R_{m+1-j} H_j - R_{m+1}
-    if (s2 != nullptr) {
+    double2* hsave = num_save + (m & 1) * 2 * ss;  // this step's numerators, kept for the D updates
+    double2* gsave = hsave + ss;
+    if (m == 1 && s2 != nullptr) {  // the side stream starts after the base stage
       TOEP_CUDA(cudaEventRecord(ev_step, st));
       TOEP_CUDA(cudaStreamWaitEvent(s2, ev_step, 0));
     }
+    // side stream (after the previous step's cross-updates, queued there): the right-hand sides of
+    // this step's three solves, independent of the D1 / D2 factors —
+    //   x_{m+1} <- sum_j R_{m+1-j} x_j - y_{m+1},  G_new <- gnum,  H_new <- hnum
     R_TRY(copy_neg(y + m * sw, xn, sw, -1.0, ss2));
     R_TRY(wide_gemm(Wpr, N - 1 - m, m, x, w, xn, ss2));
     if (more) {
@@ -859,20 +887,18 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
       R_TRY(wide_gemm(Wnr, N - 1 - m, m, g, s, gnew, ss2));
       R_TRY(copy_neg(rb(m + 1), hnew, ss, -1.0, ss2));
       R_TRY(wide_gemm(Wpr, N - 1 - m, m, h, s, hnew, ss2));
+      if (m + 1 < N - 1)  // the numerators for the next step's D2 / D1 update
+        TOEP_CUDA(cudaMemcpyAsync(gsave, gnew, ss * sizeof(double2), cudaMemcpyDeviceToDevice, ss2));
+      TOEP_CUDA(cudaMemcpyAsync(hsave, hnew, ss * sizeof(double2), cudaMemcpyDeviceToDevice, ss2));
     }
     if (s2 != nullptr) TOEP_CUDA(cudaEventRecord(ev_sums, s2));
-    // d1 = sum_{k=1..m} R_k G_k - R_0 ;  d2 = sum_{k=1..m} R_{-k} H_k - R_0   (factored together)
-    R_TRY(copy_neg(rb(0), lu1, ss, -1.0, st));
-    R_TRY(wide_gemm(Wp, 0, m, g, s, lu1, st));
-    if (more) {
-      R_TRY(copy_neg(rb(0), lu2, ss, -1.0, st));
-      R_TRY(wide_gemm(Wn, 0, m, h, s, lu2, st));
-    }
+    // D1, D2 of this step, factored together (copies: the unfactored matrices take the next update)
+    TOEP_CUDA(cudaMemcpyAsync(lu12, d12, (more ? 2 : 1) * ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
     R_TRY(getrf_batched(lu12, ss, more ? 2 : 1, s, piv12, info, st));
-    if (s2 != nullptr) TOEP_CUDA(cudaStreamWaitEvent(st, ev_sums, 0));
     R_TRY(check_info(TOEP_ERR_SINGULAR_DENOM, m, more ? 2 : 1));
-    // G_new = D2^-1 (...) on the side stream (latency-bound blocked TRSM chain), concurrently with
-    // x_{m+1} = D1^-1 (...), the x update and H_new = D1^-1 (...) here
+    if (s2 != nullptr) TOEP_CUDA(cudaStreamWaitEvent(st, ev_sums, 0));
+    // G_new = D2^-1 gnum on the side stream (latency-bound blocked TRSM chain), concurrently with
+    // x_{m+1} = D1^-1 (...) and H_new = D1^-1 hnum here
     if (more && s2 != nullptr) {
       TOEP_CUDA(cudaEventRecord(ev_step, st));
       TOEP_CUDA(cudaStreamWaitEvent(s2, ev_step, 0));
@@ -880,19 +906,39 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
       TOEP_CUDA(cudaEventRecord(ev_sums, s2));
     }
     R_TRY(getrs(lu1, s, piv1, xn, static_cast<int>(w), static_cast<int>(w), st));
-    // x_j -= G_{m+1-j} x_{m+1}
-    R_TRY(rev_batched(g, m, xn, w, x, sw));
     if (more) {
       if (s2 == nullptr) R_TRY(getrs(lu2, s, piv2, gnew, s, s, st));
       R_TRY(getrs(lu1, s, piv1, hnew, s, s, st));
-      if (s2 != nullptr) TOEP_CUDA(cudaStreamWaitEvent(st, ev_sums, 0));
-      // G_j' = G_j - H_{m+1-j} G_new (old H, into the next stack);  H_j -= G_{m+1-j} H_new (old G)
-      TOEP_CUDA(cudaMemcpyAsync(gtmp, g, m * ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
-      R_TRY(rev_batched(h, m, gnew, s, gtmp, ss));
-      R_TRY(rev_batched(g, m, hnew, s, h, ss));
+      if (s2 != nullptr) {
+        TOEP_CUDA(cudaEventRecord(ev_solved, st));  // x_{m+1}, H_new
+        TOEP_CUDA(cudaStreamWaitEvent(st, ev_sums, 0));  // G_new
+      }
+      // next step's denominators (on st, ahead of its LU): D1 -= hnum G_new, D2 -= gnum H_new
+      if (m + 1 < N) {
+        R_TRY(gemm(TOEP_C128, s, s, s, mone, hsave, s, 1, 0, gnew, s, 1, 0, one, D1, s, 1, 0, 1, st, nullptr));
+        if (m + 1 < N - 1)
+          R_TRY(gemm(TOEP_C128, s, s, s, mone, gsave, s, 1, 0, hnew, s, 1, 0, one, D2, s, 1, 0, 1, st, nullptr));
+      }
+      // side stream: x_j -= G_{m+1-j} x_{m+1};  G_j' = G_j - H_{m+1-j} G_new (old H, into the next
+      // stack);  H_j -= G_{m+1-j} H_new (old G)
+      if (s2 != nullptr) TOEP_CUDA(cudaStreamWaitEvent(s2, ev_solved, 0));
+      R_TRY(rev_batched(g, m, xn, w, x, sw, ss2));
+      TOEP_CUDA(cudaMemcpyAsync(gtmp, g, m * ss * sizeof(double2), cudaMemcpyDeviceToDevice, ss2));
+      R_TRY(rev_batched(h, m, gnew, s, gtmp, ss, ss2));
+      R_TRY(rev_batched(g, m, hnew, s, h, ss, ss2));
       std::swap(g, gtmp);
+    } else {
+      R_TRY(rev_batched(g, m, xn, w, x, sw, st));  // last step: x_j -= G_{m+1-j} x_{m+1}
+    }
+    if (hook != nullptr && s2 != nullptr) {  // the hook sees the finished stage
+      TOEP_CUDA(cudaEventRecord(ev_step, s2));
+      TOEP_CUDA(cudaStreamWaitEvent(st, ev_step, 0));
     }
     R_TRY(stage_hook(m + 1));
+  }
+  if (s2 != nullptr) {  // everything queued on the side stream is ordered before the return
+    TOEP_CUDA(cudaEventRecord(ev_step, s2));
+    TOEP_CUDA(cudaStreamWaitEvent(st, ev_step, 0));
   }
   cleanup();
 #undef R_ALLOC
