@@ -680,7 +680,13 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   TOEP_NVTX("toep_rybicki");
   TOEP_REQUIRE(blocks_v != nullptr && y_v != nullptr && x_v != nullptr && N >= 1 && s >= 1 && w >= 1, TOEP_ERR_ARG,
                "bad rybicki arguments");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // The recursion runs on two library streams: `st` (highest priority) carries the latency-bound
+  // chain — the cluster LU of the denominators, the triangular solves, the denominator updates — and
+  // `s2` (lowest priority) the tensor-core block sums and cross-updates.  With equal priorities the
+  // GEMM CTAs held every SM and each LU panel launch waited for SMs to drain: the LU of a step grew
+  // from 3.7 to 12 ms as the block sums deepened.  The caller's stream `sc` is ordered before and after.
+  const cudaStream_t sc = static_cast<cudaStream_t>(stream);
+  cudaStream_t st = nullptr;
   keep_pool();
   const double2* blocks = static_cast<const double2*>(blocks_v);
   const double2* y = static_cast<const double2*>(y_v);
@@ -704,6 +710,7 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
       cudaStreamSynchronize(s2);
       cudaStreamDestroy(s2);
     }
+    if (st == nullptr) return;
     if (ev_step != nullptr) cudaEventDestroy(ev_step);
     if (ev_sums != nullptr) cudaEventDestroy(ev_sums);
     if (ev_solved != nullptr) cudaEventDestroy(ev_solved);
@@ -711,8 +718,19 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
                     (void*)info, (void*)wplanes, (void*)scr, (void*)d12, (void*)num_save})
       if (q) cudaFreeAsync(q, st);
     cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
   };
   int rc = TOEP_OK;
+  {
+    int lo = 0, hi = 0;
+    TOEP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    TOEP_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+    cudaEvent_t e0 = nullptr;
+    TOEP_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    cudaEventRecord(e0, sc);  // inputs were produced on the caller's stream
+    cudaStreamWaitEvent(st, e0, 0);
+    cudaEventDestroy(e0);
+  }
 #define R_ALLOC(ptr, count)                                                                                      \
   do {                                                                                                           \
     if (cudaMallocAsync(reinterpret_cast<void**>(&(ptr)), sizeof(*(ptr)) * (size_t)(count), st) != cudaSuccess) { \
@@ -791,6 +809,7 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   };
   auto stage_hook = [&](int stage) -> int {
     if (hook == nullptr) return TOEP_OK;
+    TOEP_CUDA(cudaStreamSynchronize(st));  // (the caller synchronised s2 into st first)
     TOEP_REQUIRE(hook(hook_ctx, stage, x, g, h, stream) == 0, TOEP_ERR_ARG, "rybicki step hook failed");
     return TOEP_OK;
   };
@@ -809,7 +828,11 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
                    ncol, sx);
   };
   if (overlap && N > 1) {
-    TOEP_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    {
+      int lo = 0, hi = 0;
+      TOEP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      TOEP_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, lo));
+    }
     TOEP_CUDA(cudaEventCreateWithFlags(&ev_step, cudaEventDisableTiming));
     TOEP_CUDA(cudaEventCreateWithFlags(&ev_sums, cudaEventDisableTiming));
     TOEP_CUDA(cudaEventCreateWithFlags(&ev_solved, cudaEventDisableTiming));
@@ -940,6 +963,7 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     TOEP_CUDA(cudaEventRecord(ev_step, s2));
     TOEP_CUDA(cudaStreamWaitEvent(st, ev_step, 0));
   }
+  TOEP_CUDA(cudaStreamSynchronize(st));  // x is complete before the caller's stream uses it
   cleanup();
 #undef R_ALLOC
 #undef R_TRY
