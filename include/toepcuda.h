@@ -109,6 +109,11 @@ TOEP_API int toep_matvec_host(toep_op_t op, const void* u_host, void* v_host, in
  * yields NULL.  No reference counterpart (the reference never leaves host memory). */
 TOEP_API int toep_host_alloc(uint64_t bytes, void** out);
 TOEP_API int toep_host_free(void* p);
+/* Pageable host -> device copy of `bytes` staged through the library's double-buffered page-locked
+ * chunks (the generator / level-1 block uploads behind precompute_spectral, toeplitz.py:248-253, and
+ * assemble_level1, rybicki.py:53-60): near the DMA rate instead of the driver's pageable 8-9 GB/s.
+ * The host source may be reused on return; the device data is ordered on `stream`. */
+TOEP_API int toep_h2d(const void* host, void* dev, uint64_t bytes, void* stream);
 
 /* Multi-GPU row / kx-slab decomposition (no reference counterpart:
  * the reference is single-process).  toep_op_slab: operator holding only the bins with

@@ -95,6 +95,7 @@ SIGNATURES = {
     "toep_matvec": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
     "toep_matvec_host": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
     "toep_host_alloc": (c_int, [ctypes.c_uint64, ctypes.POINTER(c_vp)]),
+    "toep_h2d": (c_int, [c_vp, c_vp, ctypes.c_uint64, c_vp]),
     "toep_host_free": (c_int, [c_vp]),
     "toep_op_slab": (c_int, [c_vp, c_int, c_int, c_vp, ctypes.POINTER(c_vp)]),
     "toep_op_create_slab": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
@@ -179,6 +180,18 @@ def stream_handle(stream=None) -> int:
     if _raw_stream is not None:  # skips building a torch.cuda.Stream object per call
         return int(_raw_stream(torch.cuda.current_device()))
     return int(torch.cuda.current_stream().cuda_stream)
+
+
+def upload(arr, dev) -> torch.Tensor:
+    """A C-contiguous numpy array copied to a new tensor on CUDA device ``dev`` through the
+    library's staged page-locked path (toep_h2d), ordered on torch's current stream."""
+    import numpy as np
+
+    a = np.ascontiguousarray(arr)
+    out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0].reshape(-1)).dtype, device=dev)
+    if a.nbytes:
+        check(lib().toep_h2d(a.ctypes.data, out.data_ptr(), a.nbytes, stream_handle()), "upload")
+    return out
 
 
 def last_error() -> str:

@@ -443,10 +443,8 @@ int toep_op_create_slab(const void* stacked4, int on_device, int n2, int n1, int
     gen = const_cast<void*>(stacked4);
   } else {
     TOEP_ALLOC(gen, gen_bytes);
-    if (cudaMemcpyAsync(gen, stacked4, gen_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) {
-      set_error("generator upload failed: %s", cudaGetErrorString(cudaGetLastError()));
-      return fail(TOEP_ERR_CUDA);
-    }
+    const int up = pipelined_h2d(stacked4, gen, gen_bytes, s);
+    if (up != TOEP_OK) return fail(up);
   }
   TOEP_ALLOC(x, x_bytes);
   // level-1 DFT of every (offset2) row of the generator, embedded at offset % l1
@@ -748,6 +746,14 @@ int toep_matvec_host(toep_op_t op, const void* u_host, void* v_host, int64_t w, 
     }
   }
   return TOEP_OK;
+}
+
+// host (pageable) -> device copy of `bytes`, staged through the library's page-locked buffers; the
+// host source may be reused when the call returns, the device data is ordered on `stream`
+int toep_h2d(const void* host, void* dev, uint64_t bytes, void* stream) {
+  TOEP_REQUIRE(bytes == 0 || (host != nullptr && dev != nullptr), TOEP_ERR_ARG, "null argument");
+  if (bytes == 0) return TOEP_OK;
+  return toep::pipelined_h2d(host, dev, bytes, static_cast<cudaStream_t>(stream));
 }
 
 int toep_op_spectral_apply(toep_op_t op, const void* hat_in, void* hat_out, int64_t w, int flags, void* stream) {

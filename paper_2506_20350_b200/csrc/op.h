@@ -60,6 +60,8 @@ void keep_pool();
 // hostio.cu: copy `bytes` from pageable `src` to page-locked `dst` with the library's copy threads
 // in chunks, enqueueing each chunk's H2D copy (dst -> dev) on `s` as soon as it is staged
 int staged_h2d(const void* src, void* dst_pinned, void* dev, size_t bytes, cudaStream_t s);
+// large pageable host -> device copy, staged through double-buffered page-locked chunks
+int pipelined_h2d(const void* src, void* dst, size_t bytes, cudaStream_t s);
 
 
 // the local stages of the slab-decomposed matvec (toep_matvec_stage / toep_matvec_stage_peer)
