@@ -330,9 +330,9 @@ def scale_legs(dev, world, rank, peer: bool = False):
     except Exception as exc:  # noqa: BLE001
         out["cfg3_columns"] = {"error": repr(exc)}
         ok = False
-    if not agreed(ok) or world == 1:
+    if not agreed(ok):
         return out
-    for exchange in (("collective", "peer") if peer else ("collective",)):
+    for exchange in (("collective", "peer") if peer and world > 1 else ("collective",)):
         try:
             out[f"cfg4_slab_{exchange}"] = _scale_cfg4(dev, world, rank, exchange, tmax, barrier)
             ok = True
@@ -410,6 +410,29 @@ def _scale_cfg4(dev, world, rank, exchange, tmax, barrier):
         k1.record()
         barrier()
         mv_us = tmax(k0.elapsed_time(k1) / 20) * 1e3
+        mv_native_us = None
+        if exchange == "collective":  # the library's own distributed matvec (NCCL all-to-alls in C)
+            import ctypes
+
+            from paper_2506_20350_b200 import _lib
+            from paper_2506_20350_b200.distributed import native_comm
+            comm = native_comm(None)
+            ctx = ctypes.c_void_p()
+            lib = _lib.lib()
+            _lib.check(lib.toep_slab_ctx_create(sop.stages.op.handle, comm.handle, 1, _lib.stream_handle(),
+                                                ctypes.byref(ctx)))
+            v = torch.empty_like(u.reshape(-1, 1))
+            uu = u.reshape(-1, 1).contiguous()
+            for _ in range(3):
+                _lib.check(lib.toep_slab_apply(ctx.value, uu.data_ptr(), v.data_ptr(), 1, _lib.stream_handle()))
+            barrier()
+            k0.record()
+            for _ in range(20):
+                lib.toep_slab_apply(ctx.value, uu.data_ptr(), v.data_ptr(), 1, _lib.stream_handle())
+            k1.record()
+            barrier()
+            mv_native_us = tmax(k0.elapsed_time(k1) / 20) * 1e3
+            lib.toep_slab_ctx_destroy(ctx.value)
         bl = b_full[y0 * 64 * 128:y1 * 64 * 128].contiguous()
         gmres_slab(sop, None, bl, GmresConfig(tol=1e-6, restart=50))
         barrier()
@@ -419,7 +442,10 @@ def _scale_cfg4(dev, world, rank, exchange, tmax, barrier):
         g1.record()
         barrier()
         res = {
-            "matvec_us_max_over_ranks": mv_us, "gmres_ms_max_over_ranks": tmax(g0.elapsed_time(g1)),
+            "matvec_us_max_over_ranks": mv_us, "matvec_native_us_max_over_ranks": mv_native_us,
+            "gmres_path": "native (toep_slab_apply + NCCL all-reduce called by the device engine)"
+            if exchange == "collective" else "python stage callbacks",
+            "gmres_ms_max_over_ranks": tmax(g0.elapsed_time(g1)),
             "gmres_iterations": rep.iterations, "reference_iterations": 28, "local_rows": n_loc // (64 * 128),
             "resident_spectral_bytes_per_rank": sop.stages.op.resident_bytes,
             "exchange_bytes_per_matvec_per_rank": 2 * 64 * 128 * 128 * 16 * (world - 1) // (world * world)}

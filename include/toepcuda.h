@@ -115,6 +115,25 @@ TOEP_API int toep_host_free(void* p);
  * The host source may be reused on return; the device data is ordered on `stream`. */
 TOEP_API int toep_h2d(const void* host, void* dev, uint64_t bytes, void* stream);
 
+/* Native multi-GPU plumbing for the slab decomposition (the reference is
+ * single-process, so no counterpart): an NCCL communicator owned by the library (NCCL bound with
+ * dlopen: the process's own libnccl.so.2 first), the distributed matvec of a slab operator with both
+ * all-to-all exchanges enqueued on the stream, and the all-reduce of GMRES's inner products.
+ * toep_slab_apply / toep_comm_allreduce have the toep_apply_fn / allreduce signatures of
+ * toep_gmres_problem_t (ctx = the slab context / the communicator), so toep_gmres runs a
+ * distributed solve with no host callback per Arnoldi step.  toep_comm_check reports an
+ * asynchronous NCCL error (ncclCommGetAsyncError) as TOEP_ERR_CUDA. */
+typedef struct toep_comm_s* toep_comm_t;
+typedef struct toep_slab_ctx_s* toep_slab_ctx_t;
+TOEP_API int toep_comm_unique_id(void* id /* 128 bytes */);
+TOEP_API int toep_comm_create(const void* id, int nranks, int rank, toep_comm_t* out);
+TOEP_API int toep_comm_destroy(toep_comm_t comm);
+TOEP_API int toep_comm_check(toep_comm_t comm);
+TOEP_API int toep_comm_allreduce(void* comm, void* buf, int64_t ndoubles, void* stream);
+TOEP_API int toep_slab_ctx_create(toep_op_t slab_op, toep_comm_t comm, int64_t w, void* stream, toep_slab_ctx_t* out);
+TOEP_API int toep_slab_ctx_destroy(toep_slab_ctx_t ctx);
+TOEP_API int toep_slab_apply(void* ctx, const void* x, void* y, int64_t w, void* stream);
+
 /* Multi-GPU row / kx-slab decomposition (no reference counterpart:
  * the reference is single-process).  toep_op_slab: operator holding only the bins with
  * level-1 frequency kx in [kx0, kx1).  toep_matvec_stage: the local steps of one distributed

@@ -96,6 +96,14 @@ SIGNATURES = {
     "toep_matvec_host": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
     "toep_host_alloc": (c_int, [ctypes.c_uint64, ctypes.POINTER(c_vp)]),
     "toep_h2d": (c_int, [c_vp, c_vp, ctypes.c_uint64, c_vp]),
+    "toep_comm_unique_id": (c_int, [c_vp]),
+    "toep_comm_create": (c_int, [c_vp, c_int, c_int, ctypes.POINTER(c_vp)]),
+    "toep_comm_destroy": (c_int, [c_vp]),
+    "toep_comm_check": (c_int, [c_vp]),
+    "toep_comm_allreduce": (c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "toep_slab_ctx_create": (c_int, [c_vp, c_vp, c_i64, c_vp, ctypes.POINTER(c_vp)]),
+    "toep_slab_ctx_destroy": (c_int, [c_vp]),
+    "toep_slab_apply": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "toep_host_free": (c_int, [c_vp]),
     "toep_op_slab": (c_int, [c_vp, c_int, c_int, c_vp, ctypes.POINTER(c_vp)]),
     "toep_op_create_slab": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,

@@ -242,16 +242,72 @@ class SlabOperator:
         return float(t.sqrt().item())
 
 
-def gmres_slab(op: SlabOperator, p, b_local, cfg):
+class NativeComm:
+    """An NCCL communicator owned by libtoepcuda over the ranks of a torch.distributed group
+    (toep_comm_create; the unique id travels through the group once).  Used by the native
+    distributed GMRES: the library enqueues the matvec's all-to-alls and the inner products'
+    all-reduce itself."""
+
+    def __init__(self, group=None):
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        lib = _lib.lib()
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _lib.check(lib.toep_comm_unique_id(uid), "comm_unique_id")
+        if self.world > 1:
+            box = [uid.raw if self.rank == 0 else None]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            ctypes.memmove(uid, box[0], 128)
+        h = ctypes.c_void_p()
+        _lib.check(lib.toep_comm_create(uid, self.world, self.rank, ctypes.byref(h)), "comm_create")
+        self.handle = h.value
+
+    def check(self):
+        """Raise CudaError if NCCL reported an asynchronous error on this communicator."""
+        _lib.check(_lib.lib().toep_comm_check(self.handle), "nccl")
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.lib().toep_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+_COMMS: dict = {}
+
+
+def native_comm(group=None) -> NativeComm:
+    """The library communicator of ``group`` (created once per group, collectively)."""
+    key = id(group)
+    c = _COMMS.get(key)
+    if c is None:
+        c = _COMMS[key] = NativeComm(group)
+    return c
+
+
+def gmres_slab(op: SlabOperator, p, b_local, cfg, native: bool | None = None):
     """GMRES (gmres.py:98-249 semantics) on row-distributed vectors of a SlabOperator.
 
     The device Arnoldi engine (toep_gmres) runs on every rank over the local rows; the
-    matvec is the distributed ``op.matvec_local`` (two all-to-alls), every inner product and
-    norm is all-reduced over the group on the device stream, so all ranks follow identical
-    scalar recurrences (same iterations, same stop step).  ``p``: None or an element-block
+    matvec is the distributed one (two all-to-alls), every inner product and norm is
+    all-reduced over the group on the device stream, so all ranks follow identical scalar
+    recurrences (same iterations, same stop step).  ``p``: None or an element-block
     preconditioner (P_K, local to each row block).  Returns this rank's rows of x.
+
+    ``native`` (default: on for the device slab operator with the collective exchange): the
+    engine calls the library's distributed matvec (toep_slab_apply: level-1 DFT, NCCL
+    all-to-all, slab step, all-to-all, inverse level-1 DFT) and NCCL all-reduce directly
+    through C function pointers — no Python callback per Arnoldi step.  Otherwise the matvec
+    and the all-reduce are Python callbacks (``op.matvec_local``, ``dist.all_reduce``).
     """
-    from .solvers.gmres import _run
+    from .solvers.gmres import NativeFn, _run
     from .errors import NoConvergence
     from ._tensor import to_columns, restore
 
@@ -260,6 +316,26 @@ def gmres_slab(op: SlabOperator, p, b_local, cfg):
         raise ShapeError(f"local rhs rows {b.shape[0]} != {op.local_dim}")
     group = op.group
     world = op.world
+    if native is None:
+        native = (op.exchange == "collective" and isinstance(op.stages, DeviceSlabStages)
+                  and (world == 1 or dist.get_backend(group) == "nccl"))
+    if native:
+        comm = native_comm(group)
+        ctx = ctypes.c_void_p()
+        _lib.check(_lib.lib().toep_slab_ctx_create(op.stages.op.handle, comm.handle, b.shape[1],
+                                                   _lib.stream_handle(), ctypes.byref(ctx)), "slab_ctx_create")
+        try:
+            x, report = _run(NativeFn("toep_slab_apply", ctx.value), p, b, cfg, prefer_numpy=False,
+                             allreduce=NativeFn("toep_comm_allreduce", comm.handle))
+        finally:
+            _lib.lib().toep_slab_ctx_destroy(ctx.value)
+        comm.check()
+        report.method = "gmres-slab"
+        xo = restore(x, origin)
+        if not report.converged:
+            raise NoConvergence(f"distributed GMRES stopped after {report.iterations} iterations", solution=xo,
+                                report=report)
+        return xo, report
 
     def allreduce(t):
         if world > 1:

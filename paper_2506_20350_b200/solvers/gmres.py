@@ -199,6 +199,16 @@ class _AllReduce:
             return 1
 
 
+class NativeFn:
+    """A library function (address) with its context pointer, passed to toep_gmres as the operator
+    (toep_apply_fn signature) or the all-reduce (e.g. toep_slab_apply / toep_comm_allreduce): the
+    engine calls it directly, no Python in the Arnoldi loop."""
+
+    def __init__(self, name: str, ctx: int):
+        self.addr = ctypes.cast(getattr(_lib.lib(), name), ctypes.c_void_p).value
+        self.ctx = ctx
+
+
 def _run(apply_op, precond, b: torch.Tensor, cfg: GmresConfig, prefer_numpy: bool, timings: bool = True,
          allreduce=None):
     """Run toep_gmres on a device (n, w) complex128 block; returns (x, SolveReport).
@@ -209,11 +219,14 @@ def _run(apply_op, precond, b: torch.Tensor, cfg: GmresConfig, prefer_numpy: boo
     n, w = b.shape
     prob = _lib.GmresProblem()
     keep = []  # keep ctypes callbacks / tensors alive for the call
-    if allreduce is not None:
+    if isinstance(allreduce, NativeFn):
+        prob.allreduce = _lib.ALLREDUCE_FN(allreduce.addr)
+        prob.allreduce_ctx = allreduce.ctx
+    elif allreduce is not None:
         ar = _AllReduce(allreduce)
         prob.allreduce = ar.cfunc
         keep.append(ar)
-    native = _native_op(apply_op)
+    native = None if isinstance(apply_op, NativeFn) else _native_op(apply_op)
     report = SolveReport()
     t_build = 0.0
     pc = precond
@@ -237,6 +250,10 @@ def _run(apply_op, precond, b: torch.Tensor, cfg: GmresConfig, prefer_numpy: boo
             pc = "done"
         else:
             prob.op = native.handle
+    elif isinstance(apply_op, NativeFn):
+        prob.op = None
+        prob.apply = _lib.APPLY_FN(apply_op.addr)
+        prob.apply_ctx = apply_op.ctx
     else:
         cb = _Callback(apply_op, n, w, prefer_numpy)
         prob.op = None

@@ -33,8 +33,9 @@ def test_device_slab_stages_match_matvec(dims, world):
     assert rel_err(got.cpu().numpy(), want.cpu().numpy()) <= 1e-12
 
 
+@pytest.mark.parametrize("native", [True, False])
 @pytest.mark.parametrize("tag", ["none", "pk"])
-def test_gmres_slab_world1_matches_native(tag):
+def test_gmres_slab_world1_matches_native(tag, native):
     from paper_2506_20350_b200.distributed import gmres_slab
     from paper_2506_20350_b200.problems import system_from_generator, unit_feed_rhs
     from paper_2506_20350_b200.solvers import BorderedOperator, GmresConfig, build_pk, solve_multi_rhs_vectorized
@@ -44,7 +45,7 @@ def test_gmres_slab_world1_matches_native(tag):
     p = build_pk(sys_) if tag == "pk" else None
     b = unit_feed_rhs(4, 4, 32)
     cfg = GmresConfig(tol=1e-8, restart=30)
-    x, rep = gmres_slab(SlabOperator.from_generator(gen), p, b, cfg)
+    x, rep = gmres_slab(SlabOperator.from_generator(gen), p, b, cfg, native=native)
     xn, rn = solve_multi_rhs_vectorized(BorderedOperator.from_system(sys_), p, b[:, None], cfg)
     assert abs(rep.iterations - rn.iterations) <= 1
     assert rel_err(x, xn[:, 0]) <= 1e-7
@@ -172,3 +173,33 @@ def test_slab_operator_built_without_full_operator(world):
         assert st.op.resident_bytes == full.resident_bytes * (k1 - k0) // full.l1
         got = st.op.diag_blocks.reshape(full.l2, k1 - k0, 8, 8)
         assert torch.equal(got, dfull[:, k0:k1])
+
+
+@pytest.mark.parametrize("dims,w", [((8, 8, 64), 3), ((30, 30, 128), 1)])
+def test_native_slab_apply_world1(dims, w):
+    """toep_slab_apply (level-1 DFT, NCCL all-to-all over a one-rank library communicator, slab
+    step, all-to-all back, inverse level-1 DFT) against the single-GPU matvec."""
+    import ctypes
+
+    from paper_2506_20350_b200 import _lib
+    from paper_2506_20350_b200.distributed import native_comm
+
+    ny, nx, nb = dims
+    gen = generator_from_stacked(seeded_stacked4(ny, nx, nb, seed=4))
+    op = SlabOperator.from_generator(gen)
+    comm = native_comm(None)
+    comm.check()
+    u = torch.from_numpy(dense_rhs(gen.dim, w, seed=2)).cuda()
+    want = matvec(precompute_spectral(gen), u)
+    ctx = ctypes.c_void_p()
+    lib = _lib.lib()
+    _lib.check(lib.toep_slab_ctx_create(op.stages.op.handle, comm.handle, w, _lib.stream_handle(), ctypes.byref(ctx)))
+    try:
+        got = torch.empty_like(u)
+        _lib.check(lib.toep_slab_apply(ctx.value, u.data_ptr(), got.data_ptr(), w, _lib.stream_handle()))
+    finally:
+        lib.toep_slab_ctx_destroy(ctx.value)
+    assert rel_err(got.cpu().numpy(), want.cpu().numpy()) <= 1e-12
+    t = torch.arange(5, dtype=torch.float64, device="cuda")
+    _lib.check(lib.toep_comm_allreduce(comm.handle, t.data_ptr(), 5, _lib.stream_handle()))
+    assert t.tolist() == [0.0, 1.0, 2.0, 3.0, 4.0]  # one rank: the sum is the value
