@@ -211,6 +211,12 @@ TOEP_API int toep_gemm(int dtype, int64_t m, int64_t n, int64_t k, const void* a
 /* Real FP64 C = alpha A B + beta C on the FP64 tensor cores (hand-written DMMA kernels, dmma.cu):
  * the real products of the 3M block products of rybicki.py:114-133.  Each operand needs a unit
  * stride in one dimension; batch strides may be negative. */
+/* Real FP64 GEMM on the int8 tensor cores (Ozaki scheme: 7 signed base-128 digits per value, per-row
+ * / per-column power-of-two scaling, exact int32 digit products in TMEM, FP64 recombination): the
+ * engine of the Rybicki block sums (rybicki.py:114-131).  Row-major A (M x K, M % 128 == 0),
+ * B (K x N), C (M x N); K % 32 == 0, K <= 19 000 (int32-exact digit sums).  ~1e-13 relative. */
+TOEP_API int toep_ozaki_dgemm(int M, int N, int64_t K, double alpha, const double* A, int64_t lda, const double* B,
+                              int64_t ldb, double beta, double* C, int64_t ldc, void* stream);
 TOEP_API int toep_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int64_t a_rs, int64_t a_cs,
                         int64_t a_bs, const double* b, int64_t b_rs, int64_t b_cs, int64_t b_bs, double beta,
                         double* c, int64_t c_rs, int64_t c_cs, int64_t c_bs, int64_t batch, void* stream);

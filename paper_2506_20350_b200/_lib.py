@@ -96,6 +96,8 @@ SIGNATURES = {
     "toep_matvec_host": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp]),
     "toep_host_alloc": (c_int, [ctypes.c_uint64, ctypes.POINTER(c_vp)]),
     "toep_h2d": (c_int, [c_vp, c_vp, ctypes.c_uint64, c_vp]),
+    "toep_ozaki_dgemm": (c_int, [c_int, c_int, c_i64, ctypes.c_double, c_vp, c_i64, c_vp, c_i64, ctypes.c_double, c_vp,
+                                 c_i64, c_vp]),
     "toep_comm_unique_id": (c_int, [c_vp]),
     "toep_comm_create": (c_int, [c_vp, c_int, c_int, ctypes.POINTER(c_vp)]),
     "toep_comm_destroy": (c_int, [c_vp]),

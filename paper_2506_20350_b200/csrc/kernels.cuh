@@ -126,6 +126,23 @@ bool fft_plan_has_planes(int L, int64_t inner);
 // Ozaki-scheme FP64 per-bin products on the int8 tensor cores (ozaki.cu): operator slices once,
 // then per chunk of bins: slice the (re, im) planes of U and write the (re, im) planes of D U
 bool ozaki_supported(int n0);
+// generic real GEMMs C_z (alpha*)= A_z B_z (+ beta C_z) on the int8 tensor cores (Ozaki scheme, 7 digits):
+// A row digits (M % 128 == 0, per-row exponents over the whole sliced row), B column digits
+struct OzGemm {
+  const int8_t* asl; const int32_t* aexp; int64_t a_kcs, a_k0, a_z0, a_zo, a_zp;
+  const int8_t* bsl; const int32_t* bexp; int64_t b_z0, b_zo, b_zp;
+  double* c; int64_t ldc, c_zo, c_zp;
+  double alpha, beta;
+  int M, N; int64_t K; int planes, zcount;
+};
+int64_t ozaki_rows_bytes(int64_t M, int64_t K);
+int64_t ozaki_cols_bytes(int64_t N, int64_t K);
+int64_t ozaki_cols_exps(int64_t N);
+int ozaki_slice_rows(const double* a, int64_t lda, int64_t a_bs, int64_t batch, int M, int64_t K, int8_t* asl,
+                     int32_t* aexp, cudaStream_t s);
+int ozaki_slice_cols(const double* b, int64_t ldb, int64_t b_bs, int64_t batch, int N, int64_t K, int8_t* bsl,
+                     int32_t* bexp, cudaStream_t s);
+int ozaki_gemm(const OzGemm& g, cudaStream_t s);
 int64_t ozaki_a_bytes(int n0, int64_t K);
 int64_t ozaki_b_bytes(int n0, int64_t bins, int64_t w);
 int64_t ozaki_b_exps(int64_t bins, int64_t w);

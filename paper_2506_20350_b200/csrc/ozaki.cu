@@ -25,6 +25,7 @@
 // stage is two contiguous bulk copies.
 #include <cstdlib>
 
+#include "../../include/toepcuda.h"
 #include "kernels.cuh"
 #include "launch.cuh"
 #include "tma.cuh"
@@ -400,6 +401,268 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ------------------------------------------------------------------------------------------
+// Generic real GEMM on the int8 tensor cores (Ozaki scheme), for the Rybicki block sums:
+// C_z (alpha *)= A_z B_z with A (M x K, row-major) cut into row digits [za][mt][kc] (per-row
+// exponents over the whole row, so a GEMM may use any 32-aligned K sub-range of a sliced matrix),
+// B (K x N, row-major) cut into column digits [zb][nt][kc] (per-column exponents over its K).
+// One CTA per (128-row tile, 128-column tile, batch z x K split): the same two-phase MMA / epilogue
+// as ozaki_tile_kernel.  Split partials go to `work` and are summed in a fixed order by
+// ozaki_split_reduce.
+
+// A digits: grid (M/128, kcs, batch); thread = row; 32 consecutive k of its row per CTA
+__global__ void __launch_bounds__(kBM) ozaki_rows_slice_kernel(const double* __restrict__ a, int64_t lda,
+                                                               int64_t a_bs, int M, int64_t kcs,
+                                                               const int32_t* __restrict__ aexp, int8_t* __restrict__ asl) {
+  const int mt = blockIdx.x, z = blockIdx.z;
+  const int64_t kc = blockIdx.y;
+  const int row = mt * kBM + threadIdx.x;
+  const double* src = a + z * a_bs + static_cast<int64_t>(row) * lda + kc * kBK;
+  const double sc = ldexp(1.0, 7 * kS - aexp[static_cast<int64_t>(z) * M + row]);
+  int8_t* t = asl + ((static_cast<int64_t>(z) * (M / kBM) + mt) * kcs + kc) * kATile;
+#pragma unroll
+  for (int h = 0; h < kBK / 16; ++h) {
+    double x[16];
+    const double2* s2 = reinterpret_cast<const double2*>(src + h * 16);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double2 v = __ldg(s2 + q);
+      x[2 * q] = v.x * sc;
+      x[2 * q + 1] = v.y * sc;
+    }
+    int4 sl[kS];
+    digits16(x, sl);
+#pragma unroll
+    for (int p = 0; p < kS; ++p)
+      *reinterpret_cast<int4*>(t + p * (kBM * kBK) + core_off(threadIdx.x, h * 16)) = sl[p];
+  }
+}
+
+// row exponents of A: one warp per row, max |a| over the row's K entries
+__global__ void ozaki_rows_exp_kernel(const double* __restrict__ a, int64_t lda, int64_t a_bs, int M, int64_t K,
+                                      int32_t* __restrict__ aexp) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int z = blockIdx.y;
+  if (warp >= M) return;
+  const double* src = a + z * a_bs + static_cast<int64_t>(warp) * lda;
+  double mx = 0.0;
+  for (int64_t k = lane; k < K; k += 32) mx = fmax(mx, fabs(__ldg(src + k)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) aexp[static_cast<int64_t>(z) * M + warp] = row_exponent(mx);
+}
+
+// column exponents of B (K x N row-major): grid (ntiles, kparts, batch), thread = column; the
+// exponent of the max is the max of the exponents, so parts combine with atomicMax (bexp zeroed)
+__global__ void __launch_bounds__(kBN) ozaki_cols_exp_kernel(const double* __restrict__ b, int64_t ldb, int64_t b_bs,
+                                                            int N, int64_t K, int ntiles, int64_t rows_per_part,
+                                                            int32_t* __restrict__ bexp) {
+  const int nt = blockIdx.x, z = blockIdx.z;
+  const int col = nt * kBN + threadIdx.x;
+  if (col >= N) return;
+  const int64_t k0 = blockIdx.y * rows_per_part, k1 = k0 + rows_per_part < K ? k0 + rows_per_part : K;
+  const double* src = b + z * b_bs + col;
+  double mx = 0.0;
+  for (int64_t k = k0; k < k1; ++k) mx = fmax(mx, fabs(__ldg(src + k * ldb)));
+  if (mx > 0.0) atomicMax(bexp + (static_cast<int64_t>(z) * ntiles + nt) * kBN + threadIdx.x, row_exponent(mx));
+}
+
+// B digits: grid (ntiles, kcs, batch); thread = column; 32 k of its column (coalesced across threads)
+__global__ void __launch_bounds__(kBN) ozaki_cols_slice_kernel(const double* __restrict__ b, int64_t ldb, int64_t b_bs,
+                                                              int N, int ntiles, int64_t kcs,
+                                                              const int32_t* __restrict__ bexp,
+                                                              int8_t* __restrict__ bsl) {
+  const int nt = blockIdx.x, z = blockIdx.z;
+  const int64_t kc = blockIdx.y;
+  const int col = nt * kBN + threadIdx.x;
+  const bool live = col < N;
+  const int32_t e = bexp[(static_cast<int64_t>(z) * ntiles + nt) * kBN + threadIdx.x];
+  const double sc = ldexp(1.0, 7 * kS - e);
+  const double* src = b + z * b_bs + kc * kBK * ldb + (live ? col : 0);
+  int8_t* t = bsl + ((static_cast<int64_t>(z) * ntiles + nt) * kcs + kc) * kBTile;
+#pragma unroll
+  for (int h = 0; h < kBK / 16; ++h) {
+    double x[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[q] = live ? __ldg(src + (h * 16 + q) * ldb) * sc : 0.0;
+    int4 sl[kS];
+    digits16(x, sl);
+#pragma unroll
+    for (int p = 0; p < kS; ++p)
+      *reinterpret_cast<int4*>(t + p * (kBN * kBK) + core_off(threadIdx.x, h * 16)) = sl[p];
+  }
+}
+
+struct OzGemmArgs {
+  const int8_t* asl;
+  const int32_t* aexp;
+  int64_t a_kcs, a_kc0;            // chunks per sliced A row; first chunk of this GEMM's K
+  int64_t a_z0, a_zo, a_zp;        // A batch = a_z0 + (z / planes) * a_zo + (z % planes) * a_zp
+  const int8_t* bsl;
+  const int32_t* bexp;
+  int64_t b_kcs, b_z0, b_zo, b_zp;
+  double* c;
+  int64_t ldc, c_zo, c_zp;         // C_z = c + (z / planes) * c_zo + (z % planes) * c_zp
+  double alpha, beta;
+  int M, N, mtiles, ntiles, planes, zcount;
+  int kcs, ksplit, kcs_per_split;  // this GEMM's K chunks and their split
+  double* work;                    // [split][z][M][N] partials when ksplit > 1
+};
+
+__global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(OzGemmArgs a) {
+  extern __shared__ __align__(1024) unsigned char oz_smem[];
+  int8_t* sA = reinterpret_cast<int8_t*>(oz_smem);
+  int8_t* sB = sA + kStages * kATile;
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull;
+  __shared__ uint32_t tmem_base;
+  __shared__ double scol[kBN];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int mt = blockIdx.x, nt = blockIdx.y;
+  const int z = blockIdx.z / a.ksplit, split = blockIdx.z % a.ksplit;
+  const int zo = z / a.planes, zp = z % a.planes;
+  const int64_t za = a.a_z0 + zo * a.a_zo + zp * a.a_zp, zb = a.b_z0 + zo * a.b_zo + zp * a.b_zp;
+  const int kc0 = split * a.kcs_per_split;
+  const int nk = max(0, min(a.kcs, kc0 + a.kcs_per_split) - kc0);
+  const int total = 2 * nk;  // steps: (phase, K chunk)
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull, 1);
+    mbar_init_fence();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
+  const int8_t* Ab = a.asl + ((za * a.mtiles + mt) * a.a_kcs + a.a_kc0 + kc0) * kATile;
+  const int8_t* Bb = a.bsl + ((zb * a.ntiles + nt) * a.b_kcs + kc0) * kBTile;
+  const int quarter = warp & 3, chalf = warp >> 2;
+  const int row = mt * kBM + quarter * 32 + lane;
+  const double srow = ldexp(1.0, a.aexp[za * a.M + row]);
+  if (tid < kBN) scol[tid] = ldexp(1.0, a.bexp[(zb * a.ntiles + nt) * kBN + tid]);
+  const uint64_t pol = policy_evict_last();
+  int issued = 0;
+  auto produce_until = [&](int limit) {
+    for (; issued < limit && issued < total; ++issued) {
+      const int st = issued % kStages;
+      if (issued >= kStages) mbar_wait(&empty[st], ((issued / kStages) - 1) & 1);
+      const int ph = issued / nk, kc = issued - ph * nk;
+      const uint32_t bytes = static_cast<uint32_t>(phase_slices(ph)) * (kBM * kBK);
+      mbar_expect_tx(&full[st], 2 * bytes);
+      bulk_g2s(sA + st * kATile, Ab + static_cast<int64_t>(kc) * kATile, bytes, &full[st], pol);
+      bulk_g2s(sB + st * kBTile, Bb + static_cast<int64_t>(kc) * kBTile, bytes, &full[st], pol);
+    }
+  };
+  const int64_t live = a.N - static_cast<int64_t>(nt) * kBN;
+  double part[kBN / 2];
+#pragma unroll
+  for (int i = 0; i < kBN / 2; ++i) part[i] = 0.0;
+  for (int ph = 0; ph < 2 && nk > 0; ++ph) {
+    if (warp == 0 && lane == 0) produce_until((ph + 1) * nk);
+    if (warp == 1 && lane == 0) {
+      const uint32_t idesc = idesc_n(live >= kBN ? kBN : static_cast<int>((live + 15) / 16) * 16);
+      for (int kc = 0; kc < nk; ++kc) {
+        const int step = ph * nk + kc, st = step % kStages;
+        mbar_wait(&full[st], (step / kStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
+        if (ph == 0) {
+#pragma unroll
+          for (int p = 1; p <= 4; ++p) {
+#pragma unroll
+            for (int q = 1; p + q <= 5; ++q)
+              mma_i8(tmem + static_cast<uint32_t>((p + q - 2) * kBN), umma_desc(a0 + (p - 1) * (kBM * kBK)),
+                     umma_desc(b0 + (q - 1) * (kBN * kBK)), (kc > 0 || p > 1) ? 1u : 0u, idesc);
+          }
+        } else {
+#pragma unroll
+          for (int p = 1; p <= kS; ++p) {
+#pragma unroll
+            for (int q = (6 - p > 1 ? 6 - p : 1); p + q <= kS + 1; ++q)
+              mma_i8(tmem + static_cast<uint32_t>((p + q - 6) * kBN), umma_desc(a0 + (p - 1) * (kBM * kBK)),
+                     umma_desc(b0 + (q - 1) * (kBN * kBK)), (kc > 0 || p > 1) ? 1u : 0u, idesc);
+          }
+        }
+        umma_commit(&empty[st]);
+      }
+      umma_commit(&tfull);
+    }
+    if (warp == 0 && lane == 0) produce_until((ph + 1) * nk + kStages);
+    __syncwarp();
+    mbar_wait(&tfull, ph & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    __syncthreads();
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll
+    for (int ci = 0; ci < kBN / 32; ++ci) {
+      const int cc = chalf * (kBN / 32) + ci;
+      if (cc * 16 >= live) break;
+      uint32_t v[4][16];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        if (ph == 1 && g == 3) break;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[g][0]), "=r"(v[g][1]), "=r"(v[g][2]), "=r"(v[g][3]), "=r"(v[g][4]), "=r"(v[g][5]),
+              "=r"(v[g][6]), "=r"(v[g][7]), "=r"(v[g][8]), "=r"(v[g][9]), "=r"(v[g][10]), "=r"(v[g][11]),
+              "=r"(v[g][12]), "=r"(v[g][13]), "=r"(v[g][14]), "=r"(v[g][15])
+            : "r"(lane_base + static_cast<uint32_t>(g * kBN + cc * 16)));
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        auto G = [&](int g) { return static_cast<int64_t>(static_cast<int32_t>(v[g][jj])); };
+        if (ph == 0)
+          part[ci * 16 + jj] = static_cast<double>((G(0) << 21) + (G(1) << 14) + (G(2) << 7) + G(3));
+        else
+          part[ci * 16 + jj] =
+              fma(part[ci * 16 + jj], 0x1p-35, static_cast<double>((G(0) << 14) + (G(1) << 7) + G(2)) * 0x1p-56);
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+  // epilogue: this thread's row, its 64 columns (phase-1 values are complete in `part`)
+  double* cz = a.c + zo * a.c_zo + zp * a.c_zp;
+#pragma unroll
+  for (int ci = 0; ci < kBN / 32; ++ci) {
+    const int cc = chalf * (kBN / 32) + ci;
+    const int64_t j0 = static_cast<int64_t>(nt) * kBN + cc * 16;
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      if (j0 + jj >= a.N) break;
+      const double o = nk > 0 ? part[ci * 16 + jj] * srow * scol[cc * 16 + jj] : 0.0;
+      if (a.work != nullptr) {
+        a.work[((static_cast<int64_t>(split) * a.zcount + z) * a.M + row) * a.N + j0 + jj] = o;
+      } else {
+        double* cp = cz + static_cast<int64_t>(row) * a.ldc + j0 + jj;
+        *cp = a.beta != 0.0 ? fma(a.beta, *cp, a.alpha * o) : a.alpha * o;
+      }
+    }
+  }
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+__global__ void ozaki_split_reduce(OzGemmArgs a) {
+  const int64_t mn = static_cast<int64_t>(a.M) * a.N, total = a.zcount * mn;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t z = e / mn, rc = e - z * mn;
+    double sum = 0.0;
+    for (int sp = 0; sp < a.ksplit; ++sp) sum += a.work[(sp * a.zcount + z) * mn + rc];  // fixed order
+    const int64_t r = rc / a.N, cidx = rc - r * a.N;
+    double* cp = a.c + (z / a.planes) * a.c_zo + (z % a.planes) * a.c_zp + r * a.ldc + cidx;
+    *cp = a.beta != 0.0 ? fma(a.beta, *cp, a.alpha * sum) : a.alpha * sum;
+  }
+}
+
 }  // namespace
 
 bool ozaki_supported(int n0) { return n0 >= 64 && (2 * n0) % kBM == 0 && 2 * n0 <= 1024; }
@@ -444,4 +707,113 @@ int ozaki_products(const int8_t* asl, const int32_t* aexp, const double* re, con
   return TOEP_OK;
 }
 
+void keep_pool();  // op.cu
+
+// ---- generic GEMM host side
+int64_t ozaki_rows_bytes(int64_t M, int64_t K) { return (M / kBM) * (K / kBK) * kATile; }
+int64_t ozaki_cols_bytes(int64_t N, int64_t K) { return ((N + kBN - 1) / kBN) * (K / kBK) * kBTile; }
+int64_t ozaki_cols_exps(int64_t N) { return ((N + kBN - 1) / kBN) * kBN; }
+
+int ozaki_slice_rows(const double* a, int64_t lda, int64_t a_bs, int64_t batch, int M, int64_t K, int8_t* asl,
+                     int32_t* aexp, cudaStream_t s) {
+  TOEP_REQUIRE(M % kBM == 0 && K % kBK == 0 && batch <= 65535, TOEP_ERR_ARG, "ozaki rows: M %% 128, K %% 32 required");
+  ozaki_rows_exp_kernel<<<dim3(static_cast<unsigned>((M * 32 + 255) / 256), static_cast<unsigned>(batch)), 256, 0, s>>>(
+      a, lda, a_bs, M, K, aexp);
+  TOEP_LAUNCHED();
+  ozaki_rows_slice_kernel<<<dim3(static_cast<unsigned>(M / kBM), static_cast<unsigned>(K / kBK),
+                                 static_cast<unsigned>(batch)),
+                            kBM, 0, s>>>(a, lda, a_bs, M, K / kBK, aexp, asl);
+  TOEP_LAUNCHED();
+  return TOEP_OK;
+}
+
+int ozaki_slice_cols(const double* b, int64_t ldb, int64_t b_bs, int64_t batch, int N, int64_t K, int8_t* bsl,
+                     int32_t* bexp, cudaStream_t s) {
+  TOEP_REQUIRE(K % kBK == 0 && batch <= 65535, TOEP_ERR_ARG, "ozaki cols: K %% 32 required");
+  const int ntiles = static_cast<int>((N + kBN - 1) / kBN);
+  TOEP_CUDA(cudaMemsetAsync(bexp, 0, sizeof(int32_t) * ntiles * kBN * batch, s));
+  const int64_t parts = std::max<int64_t>(1, std::min<int64_t>(K / 256, 64));
+  const int64_t rpp = (K + parts - 1) / parts;
+  ozaki_cols_exp_kernel<<<dim3(ntiles, static_cast<unsigned>(parts), static_cast<unsigned>(batch)), kBN, 0, s>>>(
+      b, ldb, b_bs, N, K, ntiles, rpp, bexp);
+  TOEP_LAUNCHED();
+  ozaki_cols_slice_kernel<<<dim3(ntiles, static_cast<unsigned>(K / kBK), static_cast<unsigned>(batch)), kBN, 0, s>>>(
+      b, ldb, b_bs, N, ntiles, K / kBK, bexp, bsl);
+  TOEP_LAUNCHED();
+  return TOEP_OK;
+}
+
+int ozaki_gemm(const OzGemm& g, cudaStream_t s) {
+  TOEP_REQUIRE(g.M % kBM == 0 && g.K % kBK == 0 && g.K <= 19000, TOEP_ERR_ARG, "ozaki gemm: bad shape");
+  OzGemmArgs a{};
+  a.asl = g.asl; a.aexp = g.aexp; a.a_kcs = g.a_kcs; a.a_kc0 = g.a_k0 / kBK;
+  a.a_z0 = g.a_z0; a.a_zo = g.a_zo; a.a_zp = g.a_zp;
+  a.bsl = g.bsl; a.bexp = g.bexp; a.b_kcs = g.K / kBK; a.b_z0 = g.b_z0; a.b_zo = g.b_zo; a.b_zp = g.b_zp;
+  a.c = g.c; a.ldc = g.ldc; a.c_zo = g.c_zo; a.c_zp = g.c_zp; a.alpha = g.alpha; a.beta = g.beta;
+  a.M = g.M; a.N = g.N; a.mtiles = g.M / kBM; a.ntiles = static_cast<int>((g.N + kBN - 1) / kBN);
+  a.planes = g.planes; a.zcount = g.zcount; a.kcs = static_cast<int>(g.K / kBK);
+  // split K so the grid covers the SMs about twice (the partials cost one write + one read of C)
+  const int64_t tiles = static_cast<int64_t>(a.mtiles) * a.ntiles * a.zcount;
+  int ks = 1;
+  while (tiles * ks < 2 * 148 && a.kcs / (ks * 2) >= 16) ks *= 2;
+  a.ksplit = ks;
+  a.kcs_per_split = (a.kcs + ks - 1) / ks;
+  a.work = nullptr;
+  const size_t smem = kStages * (kATile + kBTile);
+  TOEP_CUDA(ensure_smem(ozaki_gemm_kernel, smem));
+  if (ks > 1) {
+    keep_pool();
+    const size_t wbytes = static_cast<size_t>(ks) * a.zcount * a.M * a.N * sizeof(double);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&a.work), wbytes, s) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("out of device memory for the ozaki split-K partials");
+      return TOEP_ERR_OOM;
+    }
+  }
+  ozaki_gemm_kernel<<<dim3(a.mtiles, a.ntiles, static_cast<unsigned>(a.zcount * ks)), kOzThreads, smem, s>>>(a);
+  TOEP_LAUNCHED();
+  if (ks > 1) {
+    ozaki_split_reduce<<<148 * 8, 256, 0, s>>>(a);
+    TOEP_LAUNCHED();
+    cudaFreeAsync(a.work, s);
+  }
+  return TOEP_OK;
+}
+
 }  // namespace toep
+
+// Standalone entry (tests, tools): C = alpha A B + beta C for row-major real FP64 matrices on the
+// int8 tensor cores — A (M x K, M % 128 == 0), B (K x N), K % 32 == 0, K <= 19 000.
+extern "C" int toep_ozaki_dgemm(int M, int N, int64_t K, double alpha, const double* A, int64_t lda, const double* B,
+                                int64_t ldb, double beta, double* C, int64_t ldc, void* stream) {
+  using namespace toep;
+  TOEP_REQUIRE(A != nullptr && B != nullptr && C != nullptr && M > 0 && N > 0 && K > 0, TOEP_ERR_ARG,
+               "bad ozaki_dgemm arguments");
+  TOEP_REQUIRE(M % 128 == 0 && K % 32 == 0 && K <= 19000, TOEP_ERR_SHAPE, "ozaki_dgemm: M %% 128, K %% 32, K <= 19000");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  keep_pool();
+  int8_t *asl = nullptr, *bsl = nullptr;
+  int32_t *aexp = nullptr, *bexp = nullptr;
+  const size_t ab = ozaki_rows_bytes(M, K), bb = ozaki_cols_bytes(N, K);
+  if (cudaMallocAsync(reinterpret_cast<void**>(&asl), ab, s) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&bsl), bb, s) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&aexp), sizeof(int32_t) * M, s) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&bexp), sizeof(int32_t) * ozaki_cols_exps(N), s) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("out of device memory in ozaki_dgemm");
+    return TOEP_ERR_OOM;
+  }
+  int rc = ozaki_slice_rows(A, lda, 0, 1, M, K, asl, aexp, s);
+  if (rc == TOEP_OK) rc = ozaki_slice_cols(B, ldb, 0, 1, N, K, bsl, bexp, s);
+  if (rc == TOEP_OK) {
+    OzGemm g{};
+    g.asl = asl; g.aexp = aexp; g.a_kcs = K / 32; g.a_k0 = 0;
+    g.bsl = bsl; g.bexp = bexp;
+    g.c = C; g.ldc = ldc; g.alpha = alpha; g.beta = beta;
+    g.M = M; g.N = N; g.K = K; g.planes = 1; g.zcount = 1;
+    rc = ozaki_gemm(g, s);
+  }
+  for (void* p : {static_cast<void*>(asl), static_cast<void*>(bsl), static_cast<void*>(aexp), static_cast<void*>(bexp)})
+    cudaFreeAsync(p, s);
+  return rc;
+}

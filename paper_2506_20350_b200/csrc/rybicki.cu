@@ -700,6 +700,8 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   double2 *d12 = nullptr, *num_save = nullptr;  // unfactored D1 / D2; copies of the step's H / G numerators
   int *piv0 = nullptr, *piv12 = nullptr, *info = nullptr;
   double *wplanes = nullptr, *scr = nullptr;  // 3M: planes of the wide blocks; per-stream B / T scratch
+  int8_t *oz_a = nullptr, *oz_b = nullptr;    // Ozaki digits: wide planes (once), per-stream G / H stack planes
+  int32_t *oz_aexp = nullptr, *oz_bexp = nullptr;
   // side stream: the block sums that do not depend on the step's LU factors run on it while the
   // (latency-bound, few-SM) cluster LU of D1/D2 runs on `st`
   cudaStream_t s2 = nullptr;
@@ -715,7 +717,8 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     if (ev_sums != nullptr) cudaEventDestroy(ev_sums);
     if (ev_solved != nullptr) cudaEventDestroy(ev_solved);
     for (void* q : {(void*)g, (void*)h, (void*)gtmp, (void*)lu0, (void*)lu12, (void*)wide, (void*)piv0, (void*)piv12,
-                    (void*)info, (void*)wplanes, (void*)scr, (void*)d12, (void*)num_save})
+                    (void*)info, (void*)wplanes, (void*)scr, (void*)d12, (void*)num_save, (void*)oz_a, (void*)oz_b,
+                    (void*)oz_aexp, (void*)oz_bexp})
       if (q) cudaFreeAsync(q, st);
     cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
@@ -777,6 +780,15 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   // 3M (Gauss) products for the s x s block products: 3 real DMMA GEMMs instead of a complex one
   constexpr bool use3m = true;
   Planes wp[4];
+  // Block sums of depth >= kOzMinK on the int8 tensor cores (Ozaki, ozaki.cu): 1.8x the DMMA rate at
+  // depth 15 360, break-even near 4 096 (tools/ozaki_gemm_time.py); depth <= 19 000 keeps the digit
+  // sums exact in int32
+#ifndef TOEP_RYB_OZAKI
+#define TOEP_RYB_OZAKI 1
+#endif
+  constexpr int64_t kOzMinK = 4096;
+  const bool use_oz = TOEP_RYB_OZAKI != 0 && use3m && N > 1 && s % 128 == 0 && static_cast<int64_t>(N - 1) * s >= kOzMinK &&
+                      static_cast<int64_t>(N - 1) * s <= 19000;
   Planes bsc[2], tsc[2];  // per stream (st, s2): B planes (N s x s) and T planes (N s x s)
   if (use3m && N > 1) {
     R_ALLOC(wplanes, 12 * wsz);
@@ -790,6 +802,15 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
       double* base = scr + static_cast<int64_t>(k) * 6 * pl;
       bsc[k] = Planes{base, base + pl, base + 2 * pl, s};
       tsc[k] = Planes{base + 3 * pl, base + 4 * pl, base + 5 * pl, s};
+    }
+    if (use_oz) {  // row digits of the 12 wide planes, cut once per solve (exponents over whole rows)
+      R_ALLOC(oz_a, 12 * ozaki_rows_bytes(s, wld));
+      R_ALLOC(oz_aexp, 12 * static_cast<int64_t>(s));
+      R_ALLOC(oz_b, 2 * 3 * ozaki_cols_bytes(s, wld));
+      R_ALLOC(oz_bexp, 2 * 3 * ozaki_cols_exps(s));
+      for (int q = 0; q < 4; ++q)
+        R_TRY(ozaki_slice_rows(wp[q].re, wld, wsz, 3, s, wld, oz_a + 3 * q * ozaki_rows_bytes(s, wld),
+                               oz_aexp + 3 * q * static_cast<int64_t>(s), st));
     }
   }
   double2 *lu1 = lu12, *lu2 = lu12 + ss;
@@ -818,8 +839,26 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
                        cudaStream_t sx) {
     if (use3m && ncol == s) {  // G / H stacks: 3 real tensor-core GEMMs of depth m*s
       const int k = sx == st ? 0 : 1;
-      const Planes& a = wp[(W - wide) / wsz];
+      const int64_t q = (W - wide) / wsz;
+      const Planes& a = wp[q];
       TOEP_TRY(split3(B, static_cast<int64_t>(m) * s, s, s, bsc[k], sx));
+      const int64_t depth = static_cast<int64_t>(m) * s;
+      if (use_oz && depth >= kOzMinK) {
+        const int64_t pl = static_cast<int64_t>(N) * ss;
+        int8_t* bdig = oz_b + static_cast<int64_t>(k) * 3 * ozaki_cols_bytes(s, wld);
+        int32_t* bexp = oz_bexp + static_cast<int64_t>(k) * 3 * ozaki_cols_exps(s);
+        TOEP_TRY(ozaki_slice_cols(bsc[k].re, s, pl, 3, s, depth, bdig, bexp, sx));
+        OzGemm og{};
+        og.asl = oz_a + 3 * q * ozaki_rows_bytes(s, wld);
+        og.aexp = oz_aexp + 3 * q * static_cast<int64_t>(s);
+        og.a_kcs = wld / 32; og.a_k0 = static_cast<int64_t>(t0) * s; og.a_z0 = 0; og.a_zo = 0; og.a_zp = 1;
+        og.bsl = bdig; og.bexp = bexp; og.b_z0 = 0; og.b_zo = 0; og.b_zp = 1;
+        og.c = tsc[k].re; og.ldc = s; og.c_zo = 0; og.c_zp = pl;
+        og.alpha = 1.0; og.beta = 0.0;
+        og.M = s; og.N = s; og.K = depth; og.planes = 3; og.zcount = 3;
+        TOEP_TRY(ozaki_gemm(og, sx));
+        return combine3(tsc[k], s, s, C, s, 1.0, sx);
+      }
       TOEP_TRY(gemm3(s, s, static_cast<int64_t>(m) * s, a.at(static_cast<int64_t>(t0) * s), 0, bsc[k], 0, tsc[k], 0, 1,
                      sx));
       return combine3(tsc[k], s, s, C, s, 1.0, sx);
