@@ -756,11 +756,12 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   R_ALLOC(h, N * ss);
   R_ALLOC(gtmp, N * ss);
   R_ALLOC(lu0, ss);
-  R_ALLOC(lu12, 2 * ss);  // D1, D2 factored together
+  R_ALLOC(lu12, 4 * ss);  // D1, D2 factored together; two sets by step parity (the side stream still
+                          // solves with step m's factors while step m+1 is factored)
   R_ALLOC(d12, 2 * ss);
   R_ALLOC(num_save, 4 * ss);  // two sets by step parity (the side stream fills the next while st reads this)
   R_ALLOC(piv0, s);
-  R_ALLOC(piv12, 2 * s);
+  R_ALLOC(piv12, 4 * s);
   R_ALLOC(info, 2);
   // Block sums over k become single GEMMs of depth m*s against "wide" copies of the generator
   // blocks, s x (N-1)s row-major each:  Wp = [R_1 .. R_{N-1}],  Wpr = [R_{N-1} .. R_1],
@@ -815,6 +816,12 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   }
   double2 *lu1 = lu12, *lu2 = lu12 + ss;
   int *piv1 = piv12, *piv2 = piv12 + s;
+  auto use_factor_set = [&](int par) {
+    lu1 = lu12 + par * 2 * ss;
+    lu2 = lu1 + ss;
+    piv1 = piv12 + par * 2 * s;
+    piv2 = piv1 + s;
+  };
   const double2 one = make_double2(1, 0), mone = make_double2(-1, 0);
   auto check_info = [&](int code, int step, int count) -> int {
     int hinfo[2] = {0, 0};
@@ -955,8 +962,9 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     }
     if (s2 != nullptr) TOEP_CUDA(cudaEventRecord(ev_sums, s2));
     // D1, D2 of this step, factored together (copies: the unfactored matrices take the next update)
-    TOEP_CUDA(cudaMemcpyAsync(lu12, d12, (more ? 2 : 1) * ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
-    R_TRY(getrf_batched(lu12, ss, more ? 2 : 1, s, piv12, info, st));
+    use_factor_set(m & 1);
+    TOEP_CUDA(cudaMemcpyAsync(lu1, d12, (more ? 2 : 1) * ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+    R_TRY(getrf_batched(lu1, ss, more ? 2 : 1, s, piv1, info, st));
     R_TRY(check_info(TOEP_ERR_SINGULAR_DENOM, m, more ? 2 : 1));
     if (s2 != nullptr) TOEP_CUDA(cudaStreamWaitEvent(st, ev_sums, 0));
     // G_new = D2^-1 gnum on the side stream (latency-bound blocked TRSM chain), concurrently with
@@ -966,13 +974,16 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
       TOEP_CUDA(cudaStreamWaitEvent(s2, ev_step, 0));
       R_TRY(getrs(lu2, s, piv2, gnew, s, s, s2));
       TOEP_CUDA(cudaEventRecord(ev_sums, s2));
+      // x_{m+1} = D1^-1 (...) also here: nothing on the main stream's chain (the next LU) needs it
+      R_TRY(getrs(lu1, s, piv1, xn, static_cast<int>(w), static_cast<int>(w), s2));
+    } else {
+      R_TRY(getrs(lu1, s, piv1, xn, static_cast<int>(w), static_cast<int>(w), st));
     }
-    R_TRY(getrs(lu1, s, piv1, xn, static_cast<int>(w), static_cast<int>(w), st));
     if (more) {
       if (s2 == nullptr) R_TRY(getrs(lu2, s, piv2, gnew, s, s, st));
       R_TRY(getrs(lu1, s, piv1, hnew, s, s, st));
       if (s2 != nullptr) {
-        TOEP_CUDA(cudaEventRecord(ev_solved, st));  // x_{m+1}, H_new
+        TOEP_CUDA(cudaEventRecord(ev_solved, st));  // H_new
         TOEP_CUDA(cudaStreamWaitEvent(st, ev_sums, 0));  // G_new
       }
       // next step's denominators (on st, ahead of its LU): D1 -= hnum G_new, D2 -= gnum H_new
