@@ -762,7 +762,7 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   R_ALLOC(num_save, 4 * ss);  // two sets by step parity (the side stream fills the next while st reads this)
   R_ALLOC(piv0, s);
   R_ALLOC(piv12, 4 * s);
-  R_ALLOC(info, 2);
+  R_ALLOC(info, 2 * (N + 1));  // per step: checked at the end unless a step hook needs them at once
   // Block sums over k become single GEMMs of depth m*s against "wide" copies of the generator
   // blocks, s x (N-1)s row-major each:  Wp = [R_1 .. R_{N-1}],  Wpr = [R_{N-1} .. R_1],
   // Wn = [R_-1 .. R_-(N-1)],  Wnr = [R_-(N-1) .. R_-1].
@@ -825,7 +825,7 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
   const double2 one = make_double2(1, 0), mone = make_double2(-1, 0);
   auto check_info = [&](int code, int step, int count) -> int {
     int hinfo[2] = {0, 0};
-    TOEP_CUDA(cudaMemcpyAsync(hinfo, info, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+    TOEP_CUDA(cudaMemcpyAsync(hinfo, info + 2 * step, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
     TOEP_CUDA(cudaStreamSynchronize(st));
     if (hinfo[0] != 0 || (count > 1 && hinfo[1] != 0)) {
       if (fail_step) *fail_step = step;
@@ -964,8 +964,12 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     // D1, D2 of this step, factored together (copies: the unfactored matrices take the next update)
     use_factor_set(m & 1);
     TOEP_CUDA(cudaMemcpyAsync(lu1, d12, (more ? 2 : 1) * ss * sizeof(double2), cudaMemcpyDeviceToDevice, st));
-    R_TRY(getrf_batched(lu1, ss, more ? 2 : 1, s, piv1, info, st));
-    R_TRY(check_info(TOEP_ERR_SINGULAR_DENOM, m, more ? 2 : 1));
+    R_TRY(getrf_batched(lu1, ss, more ? 2 : 1, s, piv1, info + 2 * m, st));
+    // With a step hook the failure must surface before the next stage runs (rybicki.py raises
+    // SingularDenominator(m) at once); otherwise the host does not wait for each LU — every step's
+    // info is read back once at the end and the first failing step reported (a singular step's
+    // later results are discarded with x).
+    if (hook != nullptr) R_TRY(check_info(TOEP_ERR_SINGULAR_DENOM, m, more ? 2 : 1));
     if (s2 != nullptr) TOEP_CUDA(cudaStreamWaitEvent(st, ev_sums, 0));
     // G_new = D2^-1 gnum on the side stream (latency-bound blocked TRSM chain), concurrently with
     // x_{m+1} = D1^-1 (...) and H_new = D1^-1 hnum here
@@ -1014,6 +1018,17 @@ extern "C" int toep_rybicki(const void* blocks_v, int N, int s, const void* y_v,
     TOEP_CUDA(cudaStreamWaitEvent(st, ev_step, 0));
   }
   TOEP_CUDA(cudaStreamSynchronize(st));  // x is complete before the caller's stream uses it
+  if (hook == nullptr && N > 1) {  // deferred denominator checks, first failing step
+    std::vector<int> hinfo(2 * N, 0);
+    TOEP_CUDA(cudaMemcpy(hinfo.data(), info, sizeof(int) * 2 * N, cudaMemcpyDeviceToHost));
+    for (int m = 1; m < N; ++m)
+      if (hinfo[2 * m] != 0 || (m < N - 1 && hinfo[2 * m + 1] != 0)) {
+        if (fail_step) *fail_step = m;
+        set_error("singular denominator at bordering step %d", m);
+        cleanup();
+        return TOEP_ERR_SINGULAR_DENOM;
+      }
+  }
   cleanup();
 #undef R_ALLOC
 #undef R_TRY
