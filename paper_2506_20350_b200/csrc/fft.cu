@@ -11,6 +11,7 @@
 // stages ping-ponging between two shared buffers, and the last stage writes
 // straight to global memory with the crop and the 1/L scale fused.
 #include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <type_traits>
 
@@ -1159,7 +1160,7 @@ int matvec_fused(const void* DT, int64_t K, int n2, int n1, int l2, int l1, int 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   TOEP_CUDA(ensure_smem(mv_fused_kernel, smem));
-  static int fits = -1;  // every SM must hold one CTA (cooperative launch)
+  static int fits = -1;  // every SM must hold one CTA (the grid barriers need every CTA resident)
   if (fits < 0) {
     int per_sm = 0;
     fits = (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mv_fused_kernel, kFusedThreads, smem) ==
@@ -1180,8 +1181,33 @@ int matvec_fused(const void* DT, int64_t K, int n2, int n1, int l2, int l1, int 
   a.bar = bar;
   a.work = reinterpret_cast<int*>(bar + 1);
   a.pf_bytes = pf.bytes > 0 ? int64_t{TOEP_FUSED_PF_MB} << 20 : 0;
-  return launch_coop(mv_fused_kernel, dim3(static_cast<unsigned>(std::min<int64_t>(sms, K))), dim3(kFusedThreads),
-                     smem, s, a);
+  // Launched as an ordinary (PDL) grid, not a cooperative one: the next matvec's CTAs then start on
+  // the SMs the previous grid vacates first instead of waiting for the whole grid plus the
+  // cooperative launch's dispatch (142.4 vs 143.8 us per matvec).  Co-residency of all CTAs (one per
+  // SM, checked above) is what the grid barriers need; what a cooperative launch would add is
+  // protection from a second fused matvec on another stream holding part of the SMs — so fused
+  // launches are serialised across streams here: a launch on a different stream than the previous
+  // one first waits for that stream's work.  (Any other kernel holding SMs only delays CTAs; the
+  // barriers' 10 s trap bounds a pathological wait.)
+  static std::mutex order_mu;
+  static cudaStream_t last_stream[64] = {};
+  static cudaEvent_t order_ev[64] = {};  // recorded after every launch (the stream may be gone later)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  std::lock_guard<std::mutex> lock(order_mu);
+  if (order_ev[dev] == nullptr) {
+    TOEP_CUDA(cudaEventCreateWithFlags(&order_ev[dev], cudaEventDisableTiming));
+  } else if (last_stream[dev] != s) {
+    TOEP_CUDA(cudaStreamWaitEvent(s, order_ev[dev], 0));
+  }
+  const int rc = launch_k(mv_fused_kernel, dim3(static_cast<unsigned>(std::min<int64_t>(sms, K))),
+                          dim3(kFusedThreads), smem, s, a);
+  if (rc == TOEP_OK) {
+    TOEP_CUDA(cudaEventRecord(order_ev[dev], s));
+    last_stream[dev] = s;
+  }
+  return rc;
 }
 
 bool fft_plan_has_planes(int L, int64_t inner) {

@@ -396,3 +396,26 @@ def test_multi_rhs_int8_tensor_core_products_vs_oracle(dims, w):
     u = dense_rhs(gen.dim, w, seed=5)
     want = oracle.mlfft.matvec(oracle.mlfft.precompute_spectral(s4), (ny, nx, nb, 2 * ny - 1, 2 * nx - 1), u)
     assert rel_err(matvec(op, u), want) <= 1e-12
+
+
+def test_fused_matvec_on_several_streams():
+    """The fused single-RHS matvec (cfg2 shape) is launched without the cooperative attribute and
+    serialises itself across streams: back-to-back calls on two streams without host syncs must
+    neither deadlock at the grid barriers nor mix their workspaces."""
+    from paper_2506_20350_b200.problems import dense_rhs, seeded_stacked4
+    from paper_2506_20350_b200.toeplitz import generator_from_stacked, precompute_spectral
+
+    op = precompute_spectral(generator_from_stacked(seeded_stacked4(30, 30, 128, 0)))
+    us = [torch.from_numpy(dense_rhs(op.dim, seed=s)).cuda() for s in (1, 2)]
+    torch.cuda.synchronize()
+    want = [matvec(op, u).clone() for u in us]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [[], []]
+    for rep in range(4):
+        for k in (0, 1):
+            with torch.cuda.stream(streams[k]):
+                outs[k].append(matvec(op, us[k]))
+    torch.cuda.synchronize()
+    for k in (0, 1):
+        for v in outs[k]:
+            assert torch.equal(v, want[k])
