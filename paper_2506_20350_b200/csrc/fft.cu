@@ -1189,25 +1189,46 @@ int matvec_fused(const void* DT, int64_t K, int n2, int n1, int l2, int l1, int 
   // launches are serialised across streams here: a launch on a different stream than the previous
   // one first waits for that stream's work.  (Any other kernel holding SMs only delays CTAs; the
   // barriers' 10 s trap bounds a pathological wait.)
-  static std::mutex order_mu;
-  static cudaStream_t last_stream[64] = {};
-  static cudaEvent_t order_ev[64] = {};  // recorded after every launch (the stream may be gone later)
+  return launch_gridsync(mv_fused_kernel, dim3(static_cast<unsigned>(std::min<int64_t>(sms, K))),
+                         dim3(kFusedThreads), smem, s, a);
+}
+
+namespace {
+std::mutex g_gridsync_mu;
+cudaStream_t g_gridsync_last[64] = {};
+cudaEvent_t g_gridsync_ev[64] = {};
+}  // namespace
+
+// held from gridsync_order to gridsync_launched (same thread): the check, the launch and the record
+// are one step for concurrent host threads
+int gridsync_order(cudaStream_t s) {
+  g_gridsync_mu.lock();
   int dev = 0;
   cudaGetDevice(&dev);
   dev &= 63;
-  std::lock_guard<std::mutex> lock(order_mu);
-  if (order_ev[dev] == nullptr) {
-    TOEP_CUDA(cudaEventCreateWithFlags(&order_ev[dev], cudaEventDisableTiming));
-  } else if (last_stream[dev] != s) {
-    TOEP_CUDA(cudaStreamWaitEvent(s, order_ev[dev], 0));
+  if (g_gridsync_ev[dev] == nullptr) {
+    if (cudaEventCreateWithFlags(&g_gridsync_ev[dev], cudaEventDisableTiming) != cudaSuccess) {
+      g_gridsync_mu.unlock();
+      set_error("gridsync event creation failed");
+      return TOEP_ERR_CUDA;
+    }
+  } else if (g_gridsync_last[dev] != s && cudaStreamWaitEvent(s, g_gridsync_ev[dev], 0) != cudaSuccess) {
+    g_gridsync_mu.unlock();
+    set_error("gridsync stream wait failed");
+    return TOEP_ERR_CUDA;
   }
-  const int rc = launch_k(mv_fused_kernel, dim3(static_cast<unsigned>(std::min<int64_t>(sms, K))),
-                          dim3(kFusedThreads), smem, s, a);
-  if (rc == TOEP_OK) {
-    TOEP_CUDA(cudaEventRecord(order_ev[dev], s));
-    last_stream[dev] = s;
+  return TOEP_OK;
+}
+
+void gridsync_launched(cudaStream_t s, bool ok) {
+  if (ok) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev &= 63;
+    cudaEventRecord(g_gridsync_ev[dev], s);
+    g_gridsync_last[dev] = s;
   }
-  return rc;
+  g_gridsync_mu.unlock();
 }
 
 bool fft_plan_has_planes(int L, int64_t inner) {

@@ -1624,7 +1624,7 @@ int gmres_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg, const 
         OrthArgs oa{V, N, m, vs, w, part1, e.norm_partial, h1, st, rcols, ldr, cs, sn, g, hist, vs, cfg->tol,
                     static_cast<int>(max_total), cycle_len, hf_dev, bar, ts_dev, orth_pf, gram, part2,
                     gram_smem ? 1 : 0};
-        rc = launch_coop(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa, (const int*)stop_dev);
+        rc = launch_gridsync(k_orth_coop, dim3(coop_grid), dim3(kCoopThreads), coop_smem, s, oa, (const int*)stop_dev);
         if (rc != TOEP_OK) {  // cooperative launch unavailable: permanent fallback to the 4-kernel chain
           use_coop = false;
           rc = TOEP_OK;

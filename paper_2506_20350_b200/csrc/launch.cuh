@@ -44,6 +44,26 @@ int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStr
   return TOEP_OK;
 }
 
+// Grid-barrier kernels launched WITHOUT the cooperative attribute (one CTA per SM, the caller has
+// checked that every CTA fits): the next such grid's CTAs start on the SMs the previous grid
+// vacates first instead of waiting for the whole grid plus the cooperative dispatch.  What the
+// cooperative attribute guarded against — two grid-barrier grids on different streams each holding
+// part of the SMs — is excluded by serialising these launches across streams: a launch on another
+// stream than the previous one waits for the previous one (per-device event, recorded after every
+// launch because a stream may be destroyed later).  Other kernels holding SMs only delay CTAs; the
+// grid barriers trap after 10 s.
+int gridsync_order(cudaStream_t s);     // wait for the previous grid-barrier launch if on another stream
+void gridsync_launched(cudaStream_t s, bool ok);  // record this launch (if it went out); releases the order lock
+
+template <typename... KArgs, typename... Args>
+int launch_gridsync(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  const int o = gridsync_order(s);
+  if (o != TOEP_OK) return o;
+  const int rc = launch_k(kern, grid, block, smem, s, std::forward<Args>(args)...);
+  gridsync_launched(s, rc == TOEP_OK);
+  return rc;
+}
+
 // Cooperative (all CTAs co-resident, grid barriers allowed) + PDL launch.
 template <typename... KArgs, typename... Args>
 int launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
