@@ -15,8 +15,12 @@ if "notimings" in sys.argv[1:]:
     import importlib; G = importlib.import_module("paper_2506_20350_b200.solvers.gmres")
     _orig = G._run
     G._run = lambda *a, **k: _orig(*a, **{**k, "timings": False})
-for _ in range(2):
+for _ in range(0 if "fresh" in sys.argv[1:] else 2):  # fresh: profile the first solves (after one plain solve)
     solve_multi_rhs_vectorized(op, p, b, GmresConfig(tol=1e-8, restart=50))
+if "fresh" in sys.argv[1:]:
+    solve_multi_rhs_vectorized(op, None, b, GmresConfig(tol=1e-8, restart=50))
+    if p is not None:
+        solve_multi_rhs_vectorized(op, p, b, GmresConfig(tol=1e-8, restart=50))
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     x, rep = solve_multi_rhs_vectorized(op, p, b, GmresConfig(tol=1e-8, restart=50))
