@@ -316,11 +316,19 @@ def gmres_slab(op: SlabOperator, p, b_local, cfg, native: bool | None = None):
         raise ShapeError(f"local rhs rows {b.shape[0]} != {op.local_dim}")
     group = op.group
     world = op.world
-    if native is None:
+    auto = native is None
+    if auto:
         native = (op.exchange == "collective" and isinstance(op.stages, DeviceSlabStages)
                   and (world == 1 or dist.get_backend(group) == "nccl"))
+    comm = None
     if native:
-        comm = native_comm(group)
+        try:
+            comm = native_comm(group)
+        except Exception:  # noqa: BLE001 - no usable libnccl: the Python exchange path below
+            if not auto:
+                raise
+            native = False
+    if native:
         ctx = ctypes.c_void_p()
         _lib.check(_lib.lib().toep_slab_ctx_create(op.stages.op.handle, comm.handle, b.shape[1],
                                                    _lib.stream_handle(), ctypes.byref(ctx)), "slab_ctx_create")
