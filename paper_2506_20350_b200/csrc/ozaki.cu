@@ -12,12 +12,13 @@
 //     TMEM; one epilogue per output tile combines the seven groups in FP64.
 // The complex product D_k U_k is the real block product [Dr -Di; Di Dr] [Ur; Ui] (M = K = 2 n0).
 //
-// Kernel (ozaki_tile_kernel): one CTA per (bin, 128-row tile), walking the 64-column tiles of
-// the right-hand sides; warp 0 lane 0 streams the A / B slice tiles of each 64-deep K chunk
-// into a 2-stage shared-memory ring with bulk copies (TMA engine), warp 1 lane 0 issues the 56
-// tcgen05.mma.kind::i8 (M=128, N=64, K=32) of a chunk into the seven TMEM accumulators (7 x 64 of
-// the 512 columns), and all four warps run the epilogue (tcgen05.ld of the seven groups, FP64
-// combination, 2^(e_i + f_j) scaling, stores into the Re / Im output planes).
+// Kernel (ozaki_tile_kernel): one CTA per (bin, 128-row tile), walking the 128-column tiles of
+// the right-hand sides in two K phases each (groups t = 2..5, then 6..8: seven groups of 128
+// columns do not fit the 512 TMEM columns); warp 0 lane 0 streams the A / B digit tiles of each
+// 32-deep K step into a 3-stage shared-memory ring with bulk copies (TMA engine), warp 1 lane 0
+// issues the 10 / 18 tcgen05.mma.kind::i8 (M=128, N=128, K=32) of a step, and all 16 warps run
+// the two epilogues (tcgen05.ld of the phase's groups, exact integer combination -> FP64,
+// 2^(e_i + f_j) scaling, stores into the Re / Im output planes).
 //
 // Slice layouts are the no-swizzle K-major "core matrix" layout of the UMMA descriptors (8 rows x
 // 16 bytes per core matrix; adjacent K core matrices 128 B apart, adjacent 8-row groups
@@ -41,7 +42,11 @@ constexpr int kBK = 32;          // K bytes per stage
 constexpr int kATile = kS * kBM * kBK;  // 28 672 B
 constexpr int kBTile = kS * kBN * kBK;  // 28 672 B
 constexpr int kStages = 3;
-constexpr int kOzThreads = 256;  // 8 warps: warp w reads TMEM lane quarter w % 4, column half w / 4
+constexpr int kOzThreads = 256;  // generic GEMM: 8 warps, warp w reads TMEM lane quarter w % 4, column half w / 4
+// per-bin tile kernel: 16 warps (lane quarter w % 4, column quarter w / 4).  Its two epilogues per
+// column tile are not amortised over a deep K, and 8 warps left them latency-bound: cfg3 matvec
+// 45.0 ms with 256 threads, 43.4 ms with 512, 44.2-45.7 ms with 1024 (64-register cap, spills)
+constexpr int kOzTileThreads = 512;
 
 // element offset of (row, kk) inside one slice of a [g][c][r][16] tile (kk < kBK)
 __device__ __forceinline__ int core_off(int row, int kk) {
@@ -248,7 +253,17 @@ struct OzArgs {
 // N = 64 single-phase tile (the tensor core's smem bandwidth is what bounds N = 64).
 __device__ __forceinline__ int phase_slices(int ph) { return ph == 0 ? 4 : kS; }
 
-__global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
+// TMEM -> registers: 8 consecutive 32-bit columns of this warp's lane quarter
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(addr));
+}
+
+__global__ void __launch_bounds__(kOzTileThreads, 1) ozaki_tile_kernel(OzArgs a) {
+  constexpr int kCpt = kBN / (kOzTileThreads / 128);  // columns per thread (32)
+  constexpr int CW = 8;                               // columns per TMEM load
+  constexpr int kChunks = kCpt / CW;
   extern __shared__ __align__(1024) unsigned char oz_smem[];
   int8_t* sA = reinterpret_cast<int8_t*>(oz_smem);              // [kStages][kATile]
   int8_t* sB = sA + kStages * kATile;                            // [kStages][kBTile]
@@ -278,7 +293,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
   const uint32_t tmem = tmem_base;
   const int8_t* Ab = a.asl + (static_cast<int64_t>(b) * mtiles + mt) * kcs * kATile;
   const int8_t* Bb = a.bsl + static_cast<int64_t>(b) * nt_count * kcs * kBTile;
-  const int quarter = warp & 3, chalf = warp >> 2;
+  const int quarter = warp & 3, cgrp = warp >> 2;
   const int row = mt * kBM + quarter * 32 + lane;  // this thread's output row (epilogue)
   const double srow = ldexp(1.0, a.aexp[static_cast<int64_t>(b) * kdim + row]);
   double* orow = (row < a.n0 ? a.out_re + (static_cast<int64_t>(b) * a.n0 + row) * a.w
@@ -298,7 +313,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
     }
   };
   const bool vec = (a.w & 1) == 0;
-  double part[kBN / 2];  // per-thread partial sums of its 64 output columns (registers)
+  double part[kCpt];  // per-thread partial sums of its output columns (registers)
   for (int nt = 0; nt < nt_count; ++nt) {
     const int32_t* fe = a.bexp + (static_cast<int64_t>(b) * nt_count + nt) * kBN;
     if (tid < kBN) scol[tid] = ldexp(1.0, __ldg(fe + tid));  // read after the phase-0 barrier below
@@ -345,49 +360,44 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_tile_kernel(OzArgs a) {
       __syncthreads();  // scol visible
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
       {
-        // this thread's 64 columns: the phase-0 partial stays in registers until phase 1 completes it
+        // this thread's columns: the phase-0 partial stays in registers until phase 1 completes it
 #pragma unroll
-        for (int ci = 0; ci < kBN / 32; ++ci) {
-          const int cc = chalf * (kBN / 32) + ci;
-          if (static_cast<int64_t>(nt) * kBN + cc * 16 >= a.w) break;  // beyond the live columns (warp-uniform)
-          uint32_t v[4][16];
+        for (int ci = 0; ci < kChunks; ++ci) {
+          const int c0 = cgrp * kCpt + ci * CW;  // first column of the chunk inside the tile
+          if (static_cast<int64_t>(nt) * kBN + c0 >= a.w) break;  // beyond the live columns (warp-uniform)
+          uint32_t v[4][CW];
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             if (ph == 1 && g == 3) break;
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(v[g][0]), "=r"(v[g][1]), "=r"(v[g][2]), "=r"(v[g][3]), "=r"(v[g][4]), "=r"(v[g][5]),
-                  "=r"(v[g][6]), "=r"(v[g][7]), "=r"(v[g][8]), "=r"(v[g][9]), "=r"(v[g][10]), "=r"(v[g][11]),
-                  "=r"(v[g][12]), "=r"(v[g][13]), "=r"(v[g][14]), "=r"(v[g][15])
-                : "r"(lane_base + static_cast<uint32_t>(g * kBN + cc * 16)));
+            tmem_ld8(lane_base + static_cast<uint32_t>(g * kBN + c0), v[g]);
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
+          for (int jj = 0; jj < CW; ++jj) {
             auto G = [&](int g) { return static_cast<int64_t>(static_cast<int32_t>(v[g][jj])); };
             if (ph == 0) {
-              part[ci * 16 + jj] = static_cast<double>((G(0) << 21) + (G(1) << 14) + (G(2) << 7) + G(3));
+              part[ci * CW + jj] = static_cast<double>((G(0) << 21) + (G(1) << 14) + (G(2) << 7) + G(3));
             } else {
-              part[ci * 16 + jj] =
-                  fma(part[ci * 16 + jj], 0x1p-35, static_cast<double>((G(0) << 14) + (G(1) << 7) + G(2)) * 0x1p-56);
+              part[ci * CW + jj] =
+                  fma(part[ci * CW + jj], 0x1p-35, static_cast<double>((G(0) << 14) + (G(1) << 7) + G(2)) * 0x1p-56);
             }
           }
         }
         if (ph == 1) {
 #pragma unroll
-          for (int ci = 0; ci < kBN / 32; ++ci) {
-            const int cc = chalf * (kBN / 32) + ci;
-            const int64_t j0 = static_cast<int64_t>(nt) * kBN + cc * 16;
-            double o[16];
+          for (int ci = 0; ci < kChunks; ++ci) {
+            const int c0 = cgrp * kCpt + ci * CW;
+            const int64_t j0 = static_cast<int64_t>(nt) * kBN + c0;
+            double o[CW];
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) o[jj] = part[ci * 16 + jj] * srow * scol[cc * 16 + jj];
-            if (vec && j0 + 16 <= a.w) {
+            for (int jj = 0; jj < CW; ++jj) o[jj] = part[ci * CW + jj] * srow * scol[c0 + jj];
+            if (vec && j0 + CW <= a.w) {
 #pragma unroll
-              for (int jj = 0; jj < 16; jj += 2)
+              for (int jj = 0; jj < CW; jj += 2)
                 *reinterpret_cast<double2*>(orow + j0 + jj) = make_double2(o[jj], o[jj + 1]);
             } else {
 #pragma unroll
-              for (int jj = 0; jj < 16; ++jj)
+              for (int jj = 0; jj < CW; ++jj)
                 if (j0 + jj < a.w) orow[j0 + jj] = o[jj];
             }
           }
@@ -701,7 +711,7 @@ int ozaki_products(const int8_t* asl, const int32_t* aexp, const double* re, con
     TOEP_LAUNCHED();
     OzArgs oa{asl + b0 * a_bin, aexp + b0 * 2 * n0, bsl + b0 * b_bin, bexp + b0 * wpad, out_re + b0 * plane_bin,
               out_im + b0 * plane_bin, n0, w, ntiles};
-    ozaki_tile_kernel<<<dim3(static_cast<unsigned>(2 * n0 / kBM), nb), kOzThreads, smem, s>>>(oa);
+    ozaki_tile_kernel<<<dim3(static_cast<unsigned>(2 * n0 / kBM), nb), kOzTileThreads, smem, s>>>(oa);
     TOEP_LAUNCHED();
   }
   return TOEP_OK;
