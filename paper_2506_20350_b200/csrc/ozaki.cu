@@ -42,6 +42,7 @@ constexpr int kBK = 32;          // K bytes per stage
 constexpr int kATile = kS * kBM * kBK;  // 28 672 B
 constexpr int kBTile = kS * kBN * kBK;  // 28 672 B
 constexpr int kStages = 3;
+constexpr int kTileSlot = 65536;  // ozaki_tile_kernel ring slot: 32 KB per operand
 constexpr int kOzThreads = 256;  // generic GEMM: 8 warps, warp w reads TMEM lane quarter w % 4, column half w / 4
 // per-bin tile kernel: 16 warps (lane quarter w % 4, column quarter w / 4).  Its two epilogues per
 // column tile are not amortised over a deep K, and 8 warps left them latency-bound: cfg3 matvec
@@ -265,8 +266,8 @@ __global__ void __launch_bounds__(kOzTileThreads, 1) ozaki_tile_kernel(OzArgs a)
   constexpr int CW = 8;                               // columns per TMEM load
   constexpr int kChunks = kCpt / CW;
   extern __shared__ __align__(1024) unsigned char oz_smem[];
-  int8_t* sA = reinterpret_cast<int8_t*>(oz_smem);              // [kStages][kATile]
-  int8_t* sB = sA + kStages * kATile;                            // [kStages][kBTile]
+  int8_t* sA = reinterpret_cast<int8_t*>(oz_smem);              // [kStages][kTileSlot]: A half, then B half
+  int8_t* sB = sA + kTileSlot / 2;
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull;
   __shared__ uint32_t tmem_base;
   __shared__ double scol[kBN];
@@ -274,7 +275,11 @@ __global__ void __launch_bounds__(kOzTileThreads, 1) ozaki_tile_kernel(OzArgs a)
   const int b = blockIdx.y, mt = blockIdx.x;  // the row tiles of one bin run together (B tiles reused from L2)
   const int kdim = 2 * a.n0, kcs = kdim / kBK, mtiles = kdim / kBM;
   const int nt_count = a.ntiles;
-  const int total = nt_count * 2 * kcs;  // steps: (column tile, phase, K chunk)
+  // ring steps per column tile: phase 0 moves two K chunks per step (4 digits each: 2 x 16 KB per
+  // operand, so a step carries 64 KB like a phase-1 step's 56 KB -- with one chunk per step only
+  // 64 KB were in flight during phase 0 and its MMAs waited on L2), phase 1 one chunk per step
+  const int steps0 = kcs / 2, steps_tile = steps0 + kcs;
+  const int total = nt_count * steps_tile;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -304,12 +309,24 @@ __global__ void __launch_bounds__(kOzTileThreads, 1) ozaki_tile_kernel(OzArgs a)
     for (; issued < limit && issued < total; ++issued) {
       const int st = issued % kStages;
       if (issued >= kStages) mbar_wait(&empty[st], ((issued / kStages) - 1) & 1);
-      const int tp = issued / kcs, kc = issued - tp * kcs;  // tp = nt * 2 + phase
-      const int nt = tp >> 1;
-      const uint32_t bytes = static_cast<uint32_t>(phase_slices(tp & 1)) * (kBM * kBK);  // kBM == kBN
-      mbar_expect_tx(&full[st], 2 * bytes);
-      bulk_g2s(sA + st * kATile, Ab + static_cast<int64_t>(kc) * kATile, bytes, &full[st], pol);
-      bulk_g2s(sB + st * kBTile, Bb + (static_cast<int64_t>(nt) * kcs + kc) * kBTile, bytes, &full[st], pol);
+      const int nt = issued / steps_tile, r = issued - nt * steps_tile;
+      int8_t* da = sA + st * kTileSlot;
+      int8_t* db = sB + st * kTileSlot;
+      const int8_t* gb = Bb + static_cast<int64_t>(nt) * kcs * kBTile;
+      if (r < steps0) {
+        constexpr uint32_t bytes = 4 * (kBM * kBK);  // digits 1..4 of one K chunk
+        const int kc = 2 * r;
+        mbar_expect_tx(&full[st], 4 * bytes);
+        bulk_g2s(da, Ab + static_cast<int64_t>(kc) * kATile, bytes, &full[st], pol);
+        bulk_g2s(da + bytes, Ab + static_cast<int64_t>(kc + 1) * kATile, bytes, &full[st], pol);
+        bulk_g2s(db, gb + static_cast<int64_t>(kc) * kBTile, bytes, &full[st], pol);
+        bulk_g2s(db + bytes, gb + static_cast<int64_t>(kc + 1) * kBTile, bytes, &full[st], pol);
+      } else {
+        const int kc = r - steps0;
+        mbar_expect_tx(&full[st], kATile + kBTile);
+        bulk_g2s(da, Ab + static_cast<int64_t>(kc) * kATile, kATile, &full[st], pol);
+        bulk_g2s(db, gb + static_cast<int64_t>(kc) * kBTile, kBTile, &full[st], pol);
+      }
     }
   };
   const bool vec = (a.w & 1) == 0;
@@ -319,24 +336,28 @@ __global__ void __launch_bounds__(kOzTileThreads, 1) ozaki_tile_kernel(OzArgs a)
     if (tid < kBN) scol[tid] = ldexp(1.0, __ldg(fe + tid));  // read after the phase-0 barrier below
     for (int ph = 0; ph < 2; ++ph) {
       const int tp = nt * 2 + ph;
-      if (warp == 0 && lane == 0) produce_until((tp + 1) * kcs);
+      const int step0 = nt * steps_tile + (ph ? steps0 : 0), nsteps = ph ? kcs : steps0;
+      if (warp == 0 && lane == 0) produce_until(step0 + nsteps);
       if (warp == 1 && lane == 0) {
         // the last column tile runs the narrowest N (multiple of 16 for M = 128) covering its live columns
         const int64_t live = a.w - static_cast<int64_t>(nt) * kBN;
         const uint32_t idesc = idesc_n(live >= kBN ? kBN : static_cast<int>((live + 15) / 16) * 16);
-        for (int kc = 0; kc < kcs; ++kc) {
-          const int step = tp * kcs + kc, st = step % kStages;
+        for (int i = 0; i < nsteps; ++i) {
+          const int step = step0 + i, st = step % kStages;
           mbar_wait(&full[st], (step / kStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t a0 = smem_u32(sA + st * kATile), b0 = smem_u32(sB + st * kBTile);
+          const uint32_t a0 = smem_u32(sA + st * kTileSlot), b0 = smem_u32(sB + st * kTileSlot);
           if (ph == 0) {
 #pragma unroll
-            for (int p = 1; p <= 4; ++p) {
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t ah = a0 + h * 4 * (kBM * kBK), bh = b0 + h * 4 * (kBN * kBK);
 #pragma unroll
-              for (int q = 1; p + q <= 5; ++q)
-                mma_i8(tmem + static_cast<uint32_t>((p + q - 2) * kBN),
-                       umma_desc(a0 + (p - 1) * (kBM * kBK)), umma_desc(b0 + (q - 1) * (kBN * kBK)),
-                       (kc > 0 || p > 1) ? 1u : 0u, idesc);
+              for (int p = 1; p <= 4; ++p) {
+#pragma unroll
+                for (int q = 1; p + q <= 5; ++q)
+                  mma_i8(tmem + static_cast<uint32_t>((p + q - 2) * kBN), umma_desc(ah + (p - 1) * (kBM * kBK)),
+                         umma_desc(bh + (q - 1) * (kBN * kBK)), (i > 0 || h > 0 || p > 1) ? 1u : 0u, idesc);
+              }
             }
           } else {
 #pragma unroll
@@ -345,7 +366,7 @@ __global__ void __launch_bounds__(kOzTileThreads, 1) ozaki_tile_kernel(OzArgs a)
               for (int q = (6 - p > 1 ? 6 - p : 1); p + q <= kS + 1; ++q)
                 mma_i8(tmem + static_cast<uint32_t>((p + q - 6) * kBN),
                        umma_desc(a0 + (p - 1) * (kBM * kBK)), umma_desc(b0 + (q - 1) * (kBN * kBK)),
-                       (kc > 0 || p > 1) ? 1u : 0u, idesc);
+                       (i > 0 || p > 1) ? 1u : 0u, idesc);
             }
           }
           umma_commit(&empty[st]);  // smem slot free once these MMAs have read it
@@ -353,7 +374,7 @@ __global__ void __launch_bounds__(kOzTileThreads, 1) ozaki_tile_kernel(OzArgs a)
         umma_commit(&tfull);        // this phase's accumulators complete
       }
       // the producer runs ahead into the next phase before joining the epilogue
-      if (warp == 0 && lane == 0) produce_until((tp + 1) * kcs + kStages);
+      if (warp == 0 && lane == 0) produce_until(step0 + nsteps + kStages);
       __syncwarp();
       mbar_wait(&tfull, tp & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -698,7 +719,7 @@ int ozaki_products(const int8_t* asl, const int32_t* aexp, const double* re, con
   const int ntiles = static_cast<int>((w + kBN - 1) / kBN);
   const size_t tsm = static_cast<size_t>(2 * n0) * kSliceCols * sizeof(double);
   TOEP_CUDA(ensure_smem(ozaki_slice_b_kernel, tsm));
-  const size_t smem = kStages * (kATile + kBTile);
+  const size_t smem = kStages * kTileSlot;
   TOEP_CUDA(ensure_smem(ozaki_tile_kernel, smem));
   const int64_t wpad = static_cast<int64_t>(ntiles) * kBN;
   const int64_t a_bin = ozaki_a_bytes(n0, 1), b_bin = ozaki_b_bytes(n0, 1, w), plane_bin = static_cast<int64_t>(n0) * w;
