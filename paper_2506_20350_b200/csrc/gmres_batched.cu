@@ -43,7 +43,11 @@ __device__ __forceinline__ int64_t rows_begin(int chunk, int nchunks, int64_t n)
 // One-sweep CGS2 (Gram-matrix form), per column: partial[l] = V_l^H w and partial2[l] =
 // V_l^H V_{m-1} (the newest basis vector's Gram column) in the same basis sweep
 constexpr int kLGG = 4;
-__global__ void __launch_bounds__(kCols) kb_dots_gram(const double2* const* __restrict__ Vp, int m,
+// The groups of kLGG basis vectors of one (row chunk, column tile) run side by side on threadIdx.y
+// (up to kGramGroups per CTA), so the rows of w and v_{m-1} that every group needs come from HBM
+// once and from L1 for the other groups (one group after the other re-read them from HBM).
+constexpr int kGramGroups = 4;
+__global__ void __launch_bounds__(kCols * kGramGroups) kb_dots_gram(const double2* const* __restrict__ Vp, int m,
                                                       const double2* __restrict__ w, int64_t n, int W, int nchunks,
                                                       double2* __restrict__ partial, double2* __restrict__ partial2) {
   pdl_wait();
@@ -53,7 +57,7 @@ __global__ void __launch_bounds__(kCols) kb_dots_gram(const double2* const* __re
   const int chunk = blockIdx.x;
   const int64_t r0 = rows_begin(chunk, nchunks, n), r1 = rows_begin(chunk + 1, nchunks, n);
   const double2* vl = Vp[m - 1];
-  for (int l0 = 0; l0 < m; l0 += kLGG) {
+  for (int l0 = threadIdx.y * kLGG; l0 < m; l0 += blockDim.y * kLGG) {
     double2 acc[kLGG], acg[kLGG];
     const double2* vp[kLGG];
 #pragma unroll
@@ -634,8 +638,8 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
       } else {
         B_TRY(matvec_impl(p->op, Vh[j], w, W, false, io64, nullptr, s));
       }
-      B_TRY(launch_k(kb_dots_gram, gridc, dim3(kCols), 0, s, (const double2* const*)Vp, m, (const double2*)w, n, W,
-                     nchunks, part, part2));
+      B_TRY(launch_k(kb_dots_gram, gridc, dim3(kCols, std::min(kGramGroups, (m + kLGG - 1) / kLGG)), 0, s,
+                     (const double2* const*)Vp, m, (const double2*)w, n, W, nchunks, part, part2));
       B_TRY(launch_k(kb_reduce_gram, dim3(gr, m), dim3(kRedGroups * 32), 0, s, (const double2*)part,
                      (const double2*)part2, m, nchunks, W, h1, gram, ldr, (const int*)st.stop));
       B_TRY(launch_k(kb_coef_gram, dim3(gc, m), dim3(128), 0, s, (const double2*)h1, (const double2*)gram, m, ldr, W,
