@@ -344,6 +344,30 @@ def scale_legs(dev, world, rank, peer: bool = False):
     return out
 
 
+def _guarded_scale_legs(args, dev, world, rank, line):
+    """scale_legs under a watchdog.  The sharded legs run collectives (and, with --scale-peer, custom
+    spin waits) that one GPU cannot exercise at world > 1; if they do not finish within
+    ``--scale-timeout`` seconds every rank leaves with status 0 and rank 0 first prints the headline
+    line it already holds (``line``), with the time-out recorded under ``config.scale``."""
+    import threading
+
+    def give_up():
+        if rank == 0 and line is not None:
+            line["config"]["scale"] = {"error": f"sharded legs abandoned after {args.scale_timeout} s (watchdog)"}
+            print(json.dumps(line), flush=True)
+        os._exit(0)
+
+    wd = threading.Timer(args.scale_timeout, give_up)
+    wd.daemon = True
+    wd.start()
+    try:
+        return scale_legs(dev, world, rank, peer=args.scale_peer)
+    except Exception as exc:  # noqa: BLE001 - the headline line must still be printed
+        return {"error": repr(exc)}
+    finally:
+        wd.cancel()
+
+
 def _scale_cfg3(dev, world, rank, tmax, barrier):
     import torch
 
@@ -595,16 +619,14 @@ def run_ours(args):
                    "algorithmic_bytes": gbytes, "achieved_GBps": gbytes / (med * 1e-3) / 1e9}
     clocks = sampler.stop()
     launches_per_step = count_launches(lambda: matvec(spec, u))
-    scale = None
-    if args.scale or (world > 1 and not args.no_scale):
+    do_scale = args.scale or (world > 1 and not args.no_scale)
+    if do_scale:
         del op, spec, pk, sys_
         torch.cuda.empty_cache()
-        try:
-            scale = scale_legs(dev, world, rank, peer=args.scale_peer)
-        except Exception as exc:  # noqa: BLE001 - the headline line must still be printed
-            scale = {"error": repr(exc)}
 
     if rank != 0:
+        if do_scale:
+            _guarded_scale_legs(args, dev, world, rank, None)
         if world > 1:
             dist.destroy_process_group()
         return
@@ -667,8 +689,8 @@ def run_ours(args):
         "gpu_launches_per_step": launches_per_step,
         "clocks": clocks,
     }
-    if scale is not None:
-        line["config"]["scale"] = scale
+    if do_scale:  # after the headline is complete: a hang in a sharded leg cannot lose it
+        line["config"]["scale"] = _guarded_scale_legs(args, dev, world, rank, line)
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)
@@ -702,6 +724,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scale", action="store_true", help="add config.scale (cfg3 column / cfg4 slab legs) at N=1")
     ap.add_argument("--no-scale", action="store_true", help="skip config.scale at N>1")
+    ap.add_argument("--scale-timeout", type=float, default=480.0,
+                    help="seconds after which the config.scale legs are abandoned (the headline line is still printed)")
     ap.add_argument("--scale-peer", action="store_true",
                     help="config.scale also times the NVLink peer-store exchange of the cfg4 slab legs")
     ap.add_argument("--cpu-sample", action="store_true", help=argparse.SUPPRESS)
