@@ -42,6 +42,8 @@ __all__ = [
     "dense_rhs",
     "BorderedSystem",
     "system_from_generator",
+    "assemble_full",
+    "DEFAULT_ORACLE_CAP",
     "seeded_system",
 ]
 
@@ -357,3 +359,17 @@ def load(path) -> BorderedSystem:
     spec = ArrayProblemSpec(ny=ny, nx=nx, ne=ne, nb=nb, wavenumber=header["k"], pitch=header["pitch"],
                             regularization=header["a"], diagonal_shift=header["shift"], seed=header["seed"])
     return BorderedSystem(generator_from_stacked(stacked4), zb, zc, spec)
+
+
+DEFAULT_ORACLE_CAP = 20_000  # problems.py:50 of the reference
+
+
+def assemble_full(sys: BorderedSystem, cap: int = DEFAULT_ORACLE_CAP) -> np.ndarray:
+    """Dense ``[[Z_A, Z_B^T], [Z_B, Z_C]]`` on the host; refuses above the oracle cap (problems.py:200-205)."""
+    from .errors import TooLargeForOracle
+    from .toeplitz import assemble_dense
+
+    if sys.dim > cap:
+        raise TooLargeForOracle(f"dense assembly of dimension {sys.dim} exceeds cap {cap}")
+    za = assemble_dense(sys.gen)
+    return np.block([[za, sys.zb.T], [sys.zb, sys.zc]])
