@@ -384,10 +384,13 @@ def test_library_pinned_host_buffers():
     assert pinned_empty(u.shape).data_ptr() == addr  # cached block handed back
 
 
-@pytest.mark.parametrize("dims,w", [((16, 16, 64), 24), ((16, 16, 64), 70), ((16, 16, 64), 17), ((16, 16, 128), 16)])
+@pytest.mark.parametrize("dims,w", [((16, 16, 64), 24), ((16, 16, 64), 70), ((16, 16, 64), 17), ((16, 16, 128), 16),
+                                    ((16, 16, 64), 129), ((16, 16, 64), 136), ((16, 16, 64), 257)])
 def test_multi_rhs_int8_tensor_core_products_vs_oracle(dims, w):
     # W >= 16 on a grid with a compiled level-2 plan (l2 = 32) routes the per-bin products through
-    # the Ozaki-scheme int8 tensor-core kernel (ozaki.cu); partial column tiles (w % 64 != 0)
+    # the Ozaki-scheme int8 tensor-core kernel (ozaki.cu); partial column tiles (w % 128 != 0): a
+    # last tile of 1, 8 and 1 live columns after one or two full 128-column tiles exercises the
+    # epilogue warps whose column quarter is entirely / partly dead
     ny, nx, nb = dims
     s4 = seeded_stacked4(ny, nx, nb, seed=w)
     gen = generator_from_stacked(s4)
