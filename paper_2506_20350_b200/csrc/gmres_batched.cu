@@ -675,12 +675,16 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
     ax = pb;
   }
   B_TRY(launch_k(k_sub_b, dim3(g1), dim3(256), 0, s, b, (const double2*)ax, w, N));
-  std::vector<double> nr(static_cast<size_t>(nchunks) * W), nb(static_cast<size_t>(nchunks) * W);
+  // per-column sums on the device (the same fixed-order reduction as the in-cycle norms): two
+  // W-long read-backs instead of the nchunks x W partials (2 x 34 MB pageable at cfg3, ~20 ms)
+  std::vector<double> nr(W), nb(W);
   B_TRY(launch_k(kb_norm, gridc, dim3(kCols), 0, s, (const double2*)w, n, W, nchunks, npart));
-  TOEP_CUDA(cudaMemcpyAsync(nr.data(), npart, sizeof(double) * nchunks * W, cudaMemcpyDeviceToHost, s));
+  B_TRY(launch_k(kb_norm_reduce, dim3(gr), dim3(kRedGroups * 32), 0, s, (const double*)npart, nchunks, W, nsum));
+  TOEP_CUDA(cudaMemcpyAsync(nr.data(), nsum, sizeof(double) * W, cudaMemcpyDeviceToHost, s));
   TOEP_CUDA(cudaStreamSynchronize(s));
   B_TRY(launch_k(kb_norm, gridc, dim3(kCols), 0, s, b, n, W, nchunks, npart));
-  TOEP_CUDA(cudaMemcpyAsync(nb.data(), npart, sizeof(double) * nchunks * W, cudaMemcpyDeviceToHost, s));
+  B_TRY(launch_k(kb_norm_reduce, dim3(gr), dim3(kRedGroups * 32), 0, s, (const double*)npart, nchunks, W, nsum));
+  TOEP_CUDA(cudaMemcpyAsync(nb.data(), nsum, sizeof(double) * W, cudaMemcpyDeviceToHost, s));
   std::vector<int> it(W), cv(W), nh(W);
   TOEP_CUDA(cudaMemcpyAsync(it.data(), st.total, sizeof(int) * W, cudaMemcpyDeviceToHost, s));
   TOEP_CUDA(cudaMemcpyAsync(cv.data(), st.conv, sizeof(int) * W, cudaMemcpyDeviceToHost, s));
@@ -690,11 +694,7 @@ int gmres_batched_run(const toep_gmres_problem_t* p, const toep_gmres_cfg_t* cfg
     TOEP_CUDA(cudaMemcpyAsync(hist_host, hist, sizeof(double) * rows * W, cudaMemcpyDeviceToHost, s));
   TOEP_CUDA(cudaStreamSynchronize(s));
   for (int c = 0; c < W; ++c) {
-    double sr = 0.0, sb = 0.0;
-    for (int ch = 0; ch < nchunks; ++ch) {
-      sr += nr[static_cast<size_t>(ch) * W + c];
-      sb += nb[static_cast<size_t>(ch) * W + c];
-    }
+    const double sr = nr[c], sb = nb[c];
     rep_final[c] = sb > 0 ? std::sqrt(sr) / std::sqrt(sb) : 0.0;
     rep_iters[c] = it[c];
     rep_conv[c] = cv[c];
