@@ -106,10 +106,12 @@ __global__ void __launch_bounds__(kCols * kGramGroups) kb_dots_gram(const double
 }
 
 // h1[l][c] = sum_chunk partial; Gram column G[l][m-1] = sum_chunk partial2 (stored with its conjugate
-// row; gram[(k*ldr + l)*W + c] = G[l][k]).  CTA (column tile of 32, l): warp g sums chunks g, g+8, ...
-// in order, then warp 0 adds the 8 group sums in order (fixed, run-to-run identical).  A thread per
-// (l, c) walking all row chunks serially was latency-bound: 1.5 ms per step at cfg3.
-constexpr int kRedGroups = 8;
+// row; gram[(k*ldr + l)*W + c] = G[l][k]).  CTA (column tile of 32, l): warp g sums chunks g, g+32, ...
+// in two interleaved chains, then warp 0 adds the 32 group sums in order (fixed, run-to-run
+// identical).  A thread per (l, c) walking all row chunks serially was latency-bound: 1.5 ms per
+// step at cfg3; 8 warps with one chain each still were (one dependent 7 KB-strided load per ~1.2 us:
+// 450 us per Gram reduction, 755 us per norm reduction of the 4 736 x 900 partials).
+constexpr int kRedGroups = 32;
 __global__ void __launch_bounds__(kRedGroups * 32) kb_reduce_gram(const double2* __restrict__ partial,
                                                                   const double2* __restrict__ partial2, int m,
                                                                   int nchunks, int W, double2* __restrict__ h1,
@@ -124,10 +126,22 @@ __global__ void __launch_bounds__(kRedGroups * 32) kb_reduce_gram(const double2*
   if (c < W && !stop[c]) {
     const double2* p1 = partial + static_cast<int64_t>(l) * nchunks * W + c;
     const double2* p2 = partial2 + static_cast<int64_t>(l) * nchunks * W + c;
-    for (int ch = grp; ch < nchunks; ch += kRedGroups) {
+    double2 t1 = make_double2(0, 0), t2 = make_double2(0, 0);
+    int ch = grp;
+    for (; ch + kRedGroups < nchunks; ch += 2 * kRedGroups) {
+      const double2 a1 = p1[static_cast<int64_t>(ch) * W], b1 = p1[static_cast<int64_t>(ch + kRedGroups) * W];
+      const double2 a2 = p2[static_cast<int64_t>(ch) * W], b2 = p2[static_cast<int64_t>(ch + kRedGroups) * W];
+      s1 = cadd(s1, a1);
+      t1 = cadd(t1, b1);
+      s2 = cadd(s2, a2);
+      t2 = cadd(t2, b2);
+    }
+    if (ch < nchunks) {
       s1 = cadd(s1, p1[static_cast<int64_t>(ch) * W]);
       s2 = cadd(s2, p2[static_cast<int64_t>(ch) * W]);
     }
+    s1 = cadd(s1, t1);
+    s2 = cadd(s2, t2);
   }
   r1[grp][lane] = s1;
   r2[grp][lane] = s2;
@@ -153,8 +167,17 @@ __global__ void __launch_bounds__(kRedGroups * 32) kb_norm_reduce(const double* 
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   double sacc = 0.0;
-  if (c < W)
-    for (int ch = grp; ch < nchunks; ch += kRedGroups) sacc += part[static_cast<int64_t>(ch) * W + c];
+  if (c < W) {
+    double tacc = 0.0;
+    int ch = grp;
+    for (; ch + kRedGroups < nchunks; ch += 2 * kRedGroups) {
+      const double a = part[static_cast<int64_t>(ch) * W + c], b = part[static_cast<int64_t>(ch + kRedGroups) * W + c];
+      sacc += a;
+      tacc += b;
+    }
+    if (ch < nchunks) sacc += part[static_cast<int64_t>(ch) * W + c];
+    sacc += tacc;
+  }
   r[grp][lane] = sacc;
   __syncthreads();
   if (grp != 0 || c >= W) return;

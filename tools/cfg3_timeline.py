@@ -25,3 +25,14 @@ for e in ev:
 print(f"span {span / 1e3:.1f} ms  kernels {len(ev)}")
 for k, (c, busy) in sorted(tot.items(), key=lambda kv: -kv[1][1])[:20]:
     print(f"{c:6d}  {busy / 1e3:9.2f} ms  ({busy / c:9.1f} us/launch)  {k}")
+# idle gaps between consecutive device activities (host-side stalls show up here)
+gaps = []
+end = ev[0].time_range.end
+for a in ev[1:]:
+    g = a.time_range.start - end
+    if g > 200:
+        gaps.append((g, a.name[:60]))
+    end = max(end, a.time_range.end)
+print(f"gaps > 0.2 ms: {len(gaps)}, total {sum(g for g, _ in gaps) / 1e3:.1f} ms")
+for g, nm in sorted(gaps, reverse=True)[:12]:
+    print(f"  {g / 1e3:8.2f} ms before {nm}")
