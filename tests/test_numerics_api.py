@@ -73,3 +73,33 @@ def test_matmul_device_matches_host(m, n, k):
     assert n2.frobenius == pytest.approx(np.linalg.norm(a)) and n2.max_abs == pytest.approx(np.abs(a).max())
     with pytest.raises(DimensionMismatch):
         nm.matmul(ta, torch.zeros((k + 1, n), dtype=torch.complex128, device="cuda"))
+
+
+def test_block_inverse_and_lu_contract():
+    a = _rand((9, 9), 11) + 9 * np.eye(9)
+    f = nm.lu_factor(a)
+    np.testing.assert_allclose(nm.block_inverse(f) @ a, np.eye(9), rtol=0, atol=1e-13)
+    b = _rand((9, 3), 12)
+    np.testing.assert_allclose(a @ nm.lu_solve(f, b), b, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(a.conj().T @ nm.lu_solve(f, b, adjoint=True), b, rtol=0, atol=1e-12)
+    with pytest.raises(DimensionMismatch):
+        nm.lu_solve(f, b[:-1])
+
+
+def test_baseline_configs_table_matches_baseline_json():
+    import json
+    import os
+    import re
+
+    from paper_2506_20350_b200.problems import CONFIGS
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "BASELINE.json")
+    if not os.path.exists(path):
+        pytest.skip("BASELINE.json not shipped")
+    texts = json.load(open(path))["configs"]
+    assert len(texts) == len(CONFIGS) == 5
+    for spec, text in zip(CONFIGS.values(), texts):
+        grid = re.search(r"(\d+)\s*[×x]\s*(\d+)", text)
+        nb = re.search(r"N_b\s*=\s*(\d+)", text)
+        assert (int(grid.group(1)), int(grid.group(2)), int(nb.group(1))) == (spec.ny, spec.nx, spec.nb), text
+        assert spec.dim == spec.ny * spec.nx * spec.nb
