@@ -526,7 +526,12 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
 __device__ __forceinline__ double orth_update(const OrthArgs& a, const double2* coef, int64_t c0, int64_t c1) {
   constexpr int U = 8;  // basis loads issued together (latency-bound sweep over L2-resident vectors)
   double nrm = 0.0;
-  for (int64_t i = c0 + threadIdx.x; i < c1; i += kCoopThreads) {
+  // back to front: the dots sweep before it (and the next step's) run front to back, so when the
+  // basis outgrows L2 (cfg4 beyond ~13 vectors) each sweep starts on the lines the previous one
+  // touched last instead of the ones LRU has just evicted
+  const int64_t first = c0 + threadIdx.x;
+  const int64_t iters = first < c1 ? (c1 - first + kCoopThreads - 1) / kCoopThreads : 0;
+  for (int64_t i = first + (iters - 1) * kCoopThreads; i >= first; i -= kCoopThreads) {
     double2 acc = a.w[i];
     int l = 0;
     for (; l + U - 1 < a.m; l += U) {
